@@ -1,0 +1,180 @@
+/*
+ * pdm_b200.h -- C ABI of the B200-native distance-map update path
+ * (arXiv 2407.21552: partitioned occupancy / distance maps).
+ *
+ * Every entry point:
+ *   - takes caller-owned DEVICE pointers (plus plain sizes) and a CUDA stream
+ *     (`pdm_stream_t` is a cudaStream_t; NULL means the legacy default stream),
+ *   - enqueues its kernels on that stream and returns without synchronising,
+ *   - allocates nothing on the update path (scratch comes from the caller),
+ *   - returns PDM_OK (0) or an error code; pdm_last_error() then holds a
+ *     message for the calling thread.
+ *
+ * Layouts (same as the reference, volume.py:3-4,157-160): a volume is C-order
+ * [nx][ny][nz] (z contiguous) of uint8 (bits=8) or uint16 (bits=16); a block
+ * map is C-order [bx][by][bz] with bd = ceil(d / b).  A partitioned distance
+ * map set is partition-major [n][plane_pitch] uint8: map p starts at byte
+ * p * plane_pitch and holds bx*by*bz bytes; plane_pitch >= bx*by*bz.  A
+ * partition mask is [bx*by*bz][words] uint32, bit p of block c at
+ * mask[c*words + p/32] >> (p%32).
+ *
+ * Each function cites the reference interface it replaces (paths relative to
+ * /root/reference/pkg/src/pdmrender).  The reference "FFI" is numba functions
+ * over numpy arrays (_kernels.py) plus numpy ufunc loops.
+ */
+#ifndef PDM_B200_H
+#define PDM_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef void *pdm_stream_t;
+
+enum pdm_status {
+    PDM_OK = 0,
+    PDM_EINVAL = 1,      /* bad argument (maps to ValueError / reference error classes) */
+    PDM_ECUDA = 2,       /* CUDA launch or runtime failure (RuntimeError) */
+    PDM_EUNSUPPORTED = 3 /* shape outside what a kernel supports (RuntimeError) */
+};
+
+/* ---- library ------------------------------------------------------------ */
+int pdm_version(void);              /* ABI version, currently 1 */
+const char *pdm_last_error(void);   /* message of the last failing call (thread-local) */
+int pdm_device_sm_count(int device);
+
+/* volume.py:86-90 intensity_range of a device-resident volume: out[0] = min,
+ * out[1] = max over count voxels (out: device uint32[2]). */
+int pdm_volume_range(const void *vox, int bits, int64_t count, uint32_t *out,
+                     pdm_stream_t stream);
+
+/* ---- selection (K8) -------------------------------------------------------
+ * transfer.py:250-259 select_partitions: flags[pid[v]] = 1 for each intensity
+ * v < span with alpha[v * alpha_stride] > 0.0 (f64 compare: NaN transparent,
+ * denormals visible).  flags (device uint8[n]) is cleared first.
+ * pid: device int32[span], the scheme's pid_lut (transfer.py:168-171). */
+int pdm_select(const double *alpha, int64_t span, int64_t alpha_stride, const int32_t *pid,
+               int32_t n, uint8_t *flags, pdm_stream_t stream);
+
+/* transfer.py:250-259 on the LUT alone: nz[v] = alpha[v] > 0.0 and, when
+ * prefix != NULL, prefix[v+1] = #{u <= v : alpha[u] > 0} with prefix[0] = 0
+ * (the np.cumsum of acceleration.py:171).  prefix needs span+1 int32. */
+int pdm_alpha_support(const double *alpha, int64_t span, int64_t alpha_stride, uint8_t *nz,
+                      int32_t *prefix, pdm_stream_t stream);
+
+/* ---- TF-change merge (K7) -------------------------------------------------
+ * acceleration.py:244-276 combine: out[c] = min over the k selected maps of
+ * pdms[sel[i]][c] (sel = HOST array of 0-based partition indices, passed by
+ * value in kernel parameters); k == 0 writes the all-255 map. */
+int pdm_combine(const uint8_t *pdms, int64_t plane_pitch, int64_t map_bytes, int32_t n,
+                const int32_t *sel, int32_t k, uint8_t *out, pdm_stream_t stream);
+
+/* Same merge with the selection resident in device memory (flags from
+ * pdm_select): select + merge with no host round trip, graph-capturable. */
+int pdm_combine_flags(const uint8_t *pdms, int64_t plane_pitch, int64_t map_bytes, int32_t n,
+                      const uint8_t *flags, uint8_t *out, pdm_stream_t stream);
+
+/* ---- block reduction / occupancy (K1-K5) --------------------------------- */
+
+/* volume.py:289-300 block_min_max: per-block min/max over the block grown by a
+ * 1-voxel apron clipped to the volume; mins/maxs have the volume's dtype. */
+int pdm_block_min_max(const void *vox, int bits, int64_t nx, int64_t ny, int64_t nz, int32_t b,
+                      void *mins, void *maxs, pdm_stream_t stream);
+
+/* _kernels.py:137-149 partition_presence (build_pdm_set voxel branch,
+ * acceleration.py:219-222): bit p of block c set iff some in-bounds voxel v of
+ * the block has pid[v] == p.  mask is overwritten. */
+int pdm_partition_mask_voxel(const void *vox, int bits, int64_t nx, int64_t ny, int64_t nz,
+                             int32_t b, const int32_t *pid, int32_t n, uint32_t *mask,
+                             int32_t words, pdm_stream_t stream);
+
+/* acceleration.py:223-229 (build_pdm_set range_apron branch): bit p set iff
+ * pid[min] <= p <= pid[max] for the block's apron min/max -- equivalent to
+ * (min <= hi_p) & (max >= lo_p) for contiguous covering partitions.  Reads the
+ * volume directly (fused block_min_max).  mask is overwritten. */
+int pdm_partition_mask_range_apron(const void *vox, int bits, int64_t nx, int64_t ny, int64_t nz,
+                                   int32_t b, const int32_t *pid, int32_t n, uint32_t *mask,
+                                   int32_t words, pdm_stream_t stream);
+
+/* Same from precomputed min/max (the minmax= argument of the reference API). */
+int pdm_partition_mask_minmax(const void *mins, const void *maxs, int bits, int64_t nblocks,
+                              const int32_t *pid, int32_t n, uint32_t *mask, int32_t words,
+                              pdm_stream_t stream);
+
+/* _kernels.py:84-110 block_any_in_range and _kernels.py:113-134
+ * block_any_nonzero (voxel-mode occupancy_for_partition / occupancy_for_tf,
+ * acceleration.py:131-136,165-168): out[c] = 1 iff lut[v] != 0 for some
+ * in-bounds voxel v of block c.  lut: device uint8[2^bits]. */
+int pdm_block_any_lut(const void *vox, int bits, int64_t nx, int64_t ny, int64_t nz, int32_t b,
+                      const uint8_t *lut, uint8_t *out, pdm_stream_t stream);
+
+/* Slab-sharded range_apron: fold the apron min/max of a neighbour slab's
+ * boundary voxel plane (pdm_block_min_max of a 1 x ny x nz volume) into the
+ * slab's first/last block plane: mins = min(mins, plane_mins), maxs = max(...).
+ * count = by * bz. */
+int pdm_minmax_fold(void *mins, void *maxs, const void *plane_mins, const void *plane_maxs,
+                    int bits, int64_t count, pdm_stream_t stream);
+
+/* acceleration.py:138-141 (range_apron occupancy_for_partition):
+ * out[c] = (mins[c] <= hi) & (maxs[c] >= lo). */
+int pdm_occupancy_minmax_range(const void *mins, const void *maxs, int bits, int64_t nblocks,
+                               uint32_t lo, uint32_t hi, uint8_t *out, pdm_stream_t stream);
+
+/* acceleration.py:169-173 (range_apron occupancy_for_tf):
+ * out[c] = prefix[maxs[c]+1] - prefix[mins[c]] > 0. */
+int pdm_occupancy_minmax_prefix(const void *mins, const void *maxs, int bits, int64_t nblocks,
+                                const int32_t *prefix, uint8_t *out, pdm_stream_t stream);
+
+/* ---- Chebyshev distance transform (K6) ------------------------------------
+ * _kernels.py:17-81 chamfer_chebyshev + acceleration.py:177-181 clamp: exact
+ * chessboard distance (in blocks) to the nearest occupied block, clamped at
+ * 255, 255 everywhere when nothing is occupied.  Computed as three separable
+ * passes (1-D distance along x, then lower-envelope min-max passes along y and
+ * z), bit-identical to the reference's two raster passes. */
+
+/* One map from a uint8 occupancy [bx][by][bz] (nonzero = occupied). */
+int pdm_distance_transform(const uint8_t *occ, int64_t bx, int64_t by, int64_t bz, uint8_t *out,
+                           pdm_stream_t stream);
+
+/* All n partition maps of a mask (acceleration.py:230-233, the batched
+ * transforms of build_pdm_set) into pdms [n][plane_pitch]. */
+int pdm_distance_transform_mask(const uint32_t *mask, int32_t words, int32_t n, int64_t bx,
+                                int64_t by, int64_t bz, uint8_t *pdms, int64_t plane_pitch,
+                                pdm_stream_t stream);
+
+/* Slab-sharded pieces (multi-GPU, x split into contiguous slabs of block planes).
+ * pass_x: local 1-D distance along x of each partition inside the slab.
+ * slab_edges: edges[0][p][y][z] = g[p][0][y][z], edges[1][p][y][z] = g[p][bx-1][y][z].
+ * slab_fold: edges_all is the all-gathered [world][2][n][by][bz] edge planes
+ *   of every slab (its own included); slab_x0 is a HOST int64 [world+1] array of
+ *   slab start planes (slab r spans [slab_x0[r], slab_x0[r+1])).  For this
+ *   rank's slab it folds in the nearest occupied block of every other slab:
+ *   g[p][x] = min(g, below + x, above + bx-1-x) clamped at 255, with
+ *   below = min_{j<rank} hi_j + x0 - x1_j + 1 and
+ *   above = min_{j>rank} lo_j + x0_j - x1 + 1 (x0/x1 = this slab's bounds).
+ * pass_yz: the two min-max passes (y, then z). */
+int pdm_dt_pass_x_mask(const uint32_t *mask, int32_t words, int32_t n, int64_t bx, int64_t by,
+                       int64_t bz, uint8_t *pdms, int64_t plane_pitch, pdm_stream_t stream);
+int pdm_dt_slab_edges(const uint8_t *pdms, int64_t plane_pitch, int32_t n, int64_t bx,
+                      int64_t by, int64_t bz, uint8_t *edges, pdm_stream_t stream);
+int pdm_dt_slab_fold(uint8_t *pdms, int64_t plane_pitch, int32_t n, int64_t bx, int64_t by,
+                     int64_t bz, const uint8_t *edges_all, int32_t world, int32_t rank,
+                     const int64_t *slab_x0, pdm_stream_t stream);
+int pdm_dt_pass_yz(uint8_t *pdms, int64_t plane_pitch, int32_t n, int64_t bx, int64_t by,
+                   int64_t bz, pdm_stream_t stream);
+
+/* ---- synthetic volumes (bench / test inputs, not a reference function) ----
+ * Background 0 plus hashed-intensity boxes; boxes = HOST int64 [nbox][8]
+ * (x0 x1 y0 y1 z0 z1 band_lo band_hi).  Writes the x-slab [xs0, xs1).
+ * Bit-identical to oracle_synth_volume in oracle/pdm_oracle.c. */
+int pdm_synth_volume(int bits, int64_t nx, int64_t ny, int64_t nz, int64_t xs0, int64_t xs1,
+                     const int64_t *boxes, int32_t nbox, uint64_t seed, void *out,
+                     pdm_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PDM_B200_H */

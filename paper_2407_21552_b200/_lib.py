@@ -1,0 +1,108 @@
+"""ctypes binding of the C ABI in include/pdm_b200.h (lib/libpdm_b200.so).
+
+There is no CPU fallback: every compute entry point of the package goes
+through this library, and ``lib()`` raises if the shared library is missing
+or no CUDA device is visible.  Status codes map to Python exceptions the way
+the reference's callers expect: PDM_EINVAL -> ValueError,
+PDM_ECUDA / PDM_EUNSUPPORTED -> RuntimeError.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from pathlib import Path
+
+LIB_PATH = Path(__file__).resolve().parent / "lib" / "libpdm_b200.so"
+
+PDM_OK, PDM_EINVAL, PDM_ECUDA, PDM_EUNSUPPORTED = 0, 1, 2, 3
+
+_P = ctypes.c_void_p
+_I32 = ctypes.c_int32
+_I64 = ctypes.c_int64
+_INT = ctypes.c_int
+
+# name -> argtypes (all return int status unless listed in _RESTYPES)
+_SIGNATURES = {
+    "pdm_version": [],
+    "pdm_last_error": [],
+    "pdm_device_sm_count": [_INT],
+    "pdm_select": [_P, _I64, _I64, _P, _I32, _P, _P],
+    "pdm_alpha_support": [_P, _I64, _I64, _P, _P, _P],
+    "pdm_combine": [_P, _I64, _I64, _I32, _P, _I32, _P, _P],
+    "pdm_combine_flags": [_P, _I64, _I64, _I32, _P, _P, _P],
+    "pdm_block_min_max": [_P, _INT, _I64, _I64, _I64, _I32, _P, _P, _P],
+    "pdm_partition_mask_voxel": [_P, _INT, _I64, _I64, _I64, _I32, _P, _I32, _P, _I32, _P],
+    "pdm_partition_mask_range_apron": [_P, _INT, _I64, _I64, _I64, _I32, _P, _I32, _P, _I32, _P],
+    "pdm_partition_mask_minmax": [_P, _P, _INT, _I64, _P, _I32, _P, _I32, _P],
+    "pdm_block_any_lut": [_P, _INT, _I64, _I64, _I64, _I32, _P, _P, _P],
+    "pdm_occupancy_minmax_range": [_P, _P, _INT, _I64, ctypes.c_uint32, ctypes.c_uint32, _P, _P],
+    "pdm_occupancy_minmax_prefix": [_P, _P, _INT, _I64, _P, _P, _P],
+    "pdm_distance_transform": [_P, _I64, _I64, _I64, _P, _P],
+    "pdm_distance_transform_mask": [_P, _I32, _I32, _I64, _I64, _I64, _P, _I64, _P],
+    "pdm_dt_pass_x_mask": [_P, _I32, _I32, _I64, _I64, _I64, _P, _I64, _P],
+    "pdm_dt_slab_edges": [_P, _I64, _I32, _I64, _I64, _I64, _P, _P],
+    "pdm_dt_slab_fold": [_P, _I64, _I32, _I64, _I64, _I64, _P, _I32, _I32, _P, _P],
+    "pdm_dt_pass_yz": [_P, _I64, _I32, _I64, _I64, _I64, _P],
+    "pdm_volume_range": [_P, _INT, _I64, _P, _P],
+    "pdm_minmax_fold": [_P, _P, _P, _P, _INT, _I64, _P],
+    "pdm_synth_volume": [_INT, _I64, _I64, _I64, _I64, _I64, _P, _I32, ctypes.c_uint64, _P, _P],
+}
+_RESTYPES = {"pdm_last_error": ctypes.c_char_p}
+
+EXPORTED = tuple(_SIGNATURES)
+
+_lib = None
+
+
+class PdmCudaError(RuntimeError):
+    """A CUDA failure or unsupported shape inside libpdm_b200."""
+
+
+def load_library(path: Path | str = LIB_PATH) -> ctypes.CDLL:
+    """dlopen the library and bind every exported symbol (no GPU needed)."""
+    path = Path(path)
+    if not path.exists():
+        raise ImportError(
+            f"{path} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'`"
+        )
+    L = ctypes.CDLL(str(path))
+    for name, argtypes in _SIGNATURES.items():
+        fn = getattr(L, name)
+        fn.argtypes = argtypes
+        fn.restype = _RESTYPES.get(name, _INT)
+    return L
+
+
+def lib() -> ctypes.CDLL:
+    """The bound library; raises when there is no CUDA device (no CPU fallback)."""
+    global _lib
+    if _lib is None:
+        import torch
+
+        if not torch.cuda.is_available():
+            raise RuntimeError(
+                "paper_2407_21552_b200 runs on CUDA (sm_100a) only and no CUDA device is "
+                "visible; there is no CPU fallback"
+            )
+        _lib = load_library()
+    return _lib
+
+
+def check(status: int, what: str) -> None:
+    if status == PDM_OK:
+        return
+    msg = (_lib.pdm_last_error() or b"").decode(errors="replace") if _lib is not None else ""
+    if status == PDM_EINVAL:
+        raise ValueError(f"{what}: {msg}")
+    raise PdmCudaError(f"{what}: {msg} (status {status})")
+
+
+def stream_handle(stream=None) -> int:
+    import torch
+
+    s = torch.cuda.current_stream() if stream is None else stream
+    return int(s.cuda_stream)
+
+
+def ptr(t) -> int:
+    return int(t.data_ptr())

@@ -1,0 +1,403 @@
+"""Partitioned occupancy / distance maps on B200 -- the distance-map update path.
+
+Drop-in for /root/reference/pkg/src/pdmrender/acceleration.py: the same
+public names, signatures, defaults, validation order and exceptions
+(``OccupancyMap``/``DistanceMap``/``PdmSet`` :42-99, ``occupancy_for_partition``
+:114-142, ``occupancy_for_tf`` :145-174, ``distance_transform`` :177-181,
+``standard_distance_map`` :184-196, ``build_pdm_set`` :199-241, ``combine``
+:244-276, dumps :279-354).  Every computation runs in libpdm_b200 kernels:
+
+  K1/K2  pdm_partition_mask_voxel / pdm_partition_mask_range_apron  (POM build)
+  K3-K5  pdm_block_any_lut / pdm_occupancy_minmax_{range,prefix}   (occupancy)
+  K6     pdm_distance_transform[_mask]                              (Chebyshev DT)
+  K7     pdm_combine / pdm_combine_flags                            (TF-change merge)
+  K8     pdm_select                                                 (selection)
+
+Residency: maps live in HBM.  A ``PdmSet`` owns one partition-major
+[n][plane_pitch] uint8 allocation; ``DistanceMap``/``OccupancyMap`` hold a CUDA
+tensor and download ``.dist`` / ``.occupied`` to numpy on first access
+(cached), so callers that read them (raycast, CLI, service) see the reference
+types while the update itself never leaves the device.
+"""
+
+from __future__ import annotations
+
+import struct
+import time
+from pathlib import Path
+
+import numpy as np
+
+from . import _lib, device
+from .transfer import (
+    Partition,
+    PartitionScheme,
+    PartitionSelection,
+    SelectionError,
+    TransferFunction,
+    alpha_to_device,
+    select_partitions_device,
+)
+from .volume import BlockGrid, Volume, VolumeError, block_min_max_device, check_pair
+
+OCCUPANCY_MODES = ("voxel", "range_apron")
+DIST_CLAMP = 255
+_MAP_MAGIC = b"PDMD"
+_SET_MAGIC = b"PDMS"
+
+
+class OccupancyModeError(ValueError):
+    """Unknown occupancy mode string."""
+
+
+def _require_mode(mode: str) -> None:
+    if mode not in OCCUPANCY_MODES:
+        raise OccupancyModeError(
+            f"unknown occupancy mode {mode!r}; expected one of {OCCUPANCY_MODES}")
+
+
+class _BlockArray:
+    """A per-block array resident on the device, host copy materialised lazily."""
+
+    _np_dtype = np.uint8
+
+    def __init__(self, b, bdims, data, field):
+        self.b = int(b)
+        self.bdims = tuple(int(v) for v in bdims)
+        self._host = None
+        self._dev = None
+        shape = tuple(data.shape)
+        if shape != self.bdims:
+            raise ValueError(f"{field} array shape does not match bdims")
+        if isinstance(data, np.ndarray):
+            self._host = data
+        else:
+            self._dev = data
+
+    def _host_array(self):
+        if self._host is None:
+            self._host = device.to_host(self._dev, self._np_dtype)
+        return self._host
+
+    def device(self):
+        """uint8 CUDA tensor of shape bdims (uploaded on first use, then cached)."""
+        if self._dev is None:
+            self._dev = device.to_device(np.ascontiguousarray(self._host, dtype=np.uint8))
+        return self._dev
+
+
+class OccupancyMap(_BlockArray):
+    """One flag per block: True where the block can contribute opacity."""
+
+    _np_dtype = np.bool_
+
+    def __init__(self, b, bdims, occupied):
+        super().__init__(b, bdims, occupied, "occupancy")
+
+    @property
+    def occupied(self) -> np.ndarray:
+        return self._host_array()
+
+    @property
+    def occupied_fraction(self) -> float:
+        occ = self.occupied
+        return float(np.count_nonzero(occ)) / occ.size
+
+
+class DistanceMap(_BlockArray):
+    """Chessboard block distance to the nearest occupied block, clamped at 255
+    (0 = occupied, all 255 when nothing is occupied)."""
+
+    def __init__(self, b, bdims, dist):
+        super().__init__(b, bdims, dist, "distance")
+        if isinstance(dist, np.ndarray) and dist.dtype != np.uint8:
+            raise ValueError(f"distance array must be uint8, got {dist.dtype}")
+        if not isinstance(dist, np.ndarray) and dist.element_size() != 1:
+            raise ValueError("distance tensor must be uint8")
+
+    @property
+    def dist(self) -> np.ndarray:
+        return self._host_array()
+
+    @property
+    def occupied_fraction(self) -> float:
+        d = self.dist
+        return float(np.count_nonzero(d == 0)) / d.size
+
+
+class PdmSet:
+    """One distance map per partition of a scheme.
+
+    Device layout: ``storage`` is a uint8 CUDA tensor [n, plane_pitch]; map p
+    is ``storage[p, :num_blocks]`` viewed as bdims.  ``plane_pitch`` is
+    num_blocks rounded up to 256 bytes so every plane is 16-byte aligned for
+    the vectorised merge.
+    """
+
+    def __init__(self, grid: BlockGrid, scheme: PartitionScheme, pdms=None,
+                 occupancy_mode: str = "range_apron", init_seconds: float = 0.0, storage=None):
+        self.grid = grid
+        self.scheme = scheme
+        self.occupancy_mode = occupancy_mode
+        self.init_seconds = float(init_seconds)
+        self.plane_pitch = device.plane_pitch(grid.num_blocks)
+        self._storage = storage
+        if storage is not None:
+            nb = grid.num_blocks
+            self.pdms = tuple(
+                DistanceMap(b=grid.b, bdims=grid.bdims, dist=storage[p, :nb].view(grid.bdims))
+                for p in range(storage.shape[0]))
+        else:
+            self.pdms = tuple(pdms if pdms is not None else ())
+
+    @property
+    def n(self) -> int:
+        return len(self.pdms)
+
+    def memory_bytes(self) -> int:
+        """n * num_blocks (acceleration.py:96-99), excluding plane padding."""
+        return self.n * self.grid.num_blocks
+
+    @property
+    def storage(self):
+        """The [n, plane_pitch] device allocation (assembled on first use when
+        the set was built from individual maps)."""
+        if self._storage is None:
+            nb = self.grid.num_blocks
+            st = device.empty((self.n, self.plane_pitch), np.uint8)
+            for p, dm in enumerate(self.pdms):
+                st[p, :nb].copy_(dm.device().reshape(-1))
+            self._storage = st
+        return self._storage
+
+
+def _mask_words(n: int) -> int:
+    return (n + 31) // 32
+
+
+def occupancy_for_partition(volume: Volume, grid: BlockGrid, partition: Partition,
+                            mode: str = "voxel", minmax=None) -> OccupancyMap:
+    """Blocks containing (voxel) or possibly reaching (range_apron, 1-voxel
+    apron interval test) intensities inside the partition (acceleration.py:114-142)."""
+    _require_mode(mode)
+    check_pair(volume, grid)
+    L = _lib.lib()
+    out = device.empty(grid.bdims, np.uint8)
+    st = _lib.stream_handle()
+    if mode == "voxel":
+        lut = np.zeros(1 << volume.bits, dtype=np.uint8)
+        lut[partition.rho_lo: partition.rho_hi + 1] = 1
+        lut_dev = device.to_device(lut)
+        vox = volume.device_voxels()
+        _lib.check(L.pdm_block_any_lut(_lib.ptr(vox), volume.bits, *volume.dims, grid.b,
+                                       _lib.ptr(lut_dev), _lib.ptr(out), st), "pdm_block_any_lut")
+    else:
+        mins, maxs = _minmax_device(volume, grid, minmax)
+        _lib.check(L.pdm_occupancy_minmax_range(
+            _lib.ptr(mins), _lib.ptr(maxs), volume.bits, grid.num_blocks,
+            min(partition.rho_lo, 0xFFFFFFFF), min(partition.rho_hi, 0xFFFFFFFF),
+            _lib.ptr(out), st), "pdm_occupancy_minmax_range")
+    return OccupancyMap(b=grid.b, bdims=grid.bdims, occupied=out)
+
+
+def _minmax_device(volume, grid, minmax):
+    if minmax is None:
+        return block_min_max_device(volume, grid)
+    mins, maxs = minmax
+    if isinstance(mins, np.ndarray):
+        mins = device.to_device(np.ascontiguousarray(mins, dtype=volume.dtype))
+        maxs = device.to_device(np.ascontiguousarray(maxs, dtype=volume.dtype))
+    return mins.contiguous(), maxs.contiguous()
+
+
+def occupancy_for_tf(volume: Volume, grid: BlockGrid, tf: TransferFunction, mode: str = "voxel",
+                     minmax=None) -> OccupancyMap:
+    """Blocks that can contribute opacity under a TF (acceleration.py:145-174):
+    voxel = any voxel with alpha > 0; range_apron = alpha > 0 somewhere inside
+    the block's apron [min, max] (prefix count)."""
+    _require_mode(mode)
+    check_pair(volume, grid)
+    if tf.lut.shape[0] != (1 << volume.bits):
+        raise VolumeError(
+            f"tf covers {tf.lut.shape[0]} intensities, volume needs {1 << volume.bits}")
+    L = _lib.lib()
+    st = _lib.stream_handle()
+    span = 1 << volume.bits
+    alpha = alpha_to_device(tf)
+    nz = device.empty((span,), np.uint8)
+    prefix = device.empty((span + 1,), np.int32) if mode == "range_apron" else None
+    _lib.check(L.pdm_alpha_support(_lib.ptr(alpha), span, 1, _lib.ptr(nz),
+                                   _lib.ptr(prefix) if prefix is not None else None, st),
+               "pdm_alpha_support")
+    out = device.empty(grid.bdims, np.uint8)
+    if mode == "voxel":
+        vox = volume.device_voxels()
+        _lib.check(L.pdm_block_any_lut(_lib.ptr(vox), volume.bits, *volume.dims, grid.b,
+                                       _lib.ptr(nz), _lib.ptr(out), st), "pdm_block_any_lut")
+    else:
+        mins, maxs = _minmax_device(volume, grid, minmax)
+        _lib.check(L.pdm_occupancy_minmax_prefix(_lib.ptr(mins), _lib.ptr(maxs), volume.bits,
+                                                 grid.num_blocks, _lib.ptr(prefix),
+                                                 _lib.ptr(out), st),
+                   "pdm_occupancy_minmax_prefix")
+    return OccupancyMap(b=grid.b, bdims=grid.bdims, occupied=out)
+
+
+def distance_transform(occ: OccupancyMap) -> DistanceMap:
+    """Chessboard distance in blocks to the nearest occupied block, clamped at
+    255 (acceleration.py:177-181; exact, bit-identical to chamfer_chebyshev)."""
+    L = _lib.lib()
+    src = occ.device()
+    out = device.empty(occ.bdims, np.uint8)
+    _lib.check(L.pdm_distance_transform(_lib.ptr(src), *occ.bdims, _lib.ptr(out),
+                                        _lib.stream_handle()), "pdm_distance_transform")
+    return DistanceMap(b=occ.b, bdims=occ.bdims, dist=out)
+
+
+def standard_distance_map(volume: Volume, grid: BlockGrid, tf: TransferFunction,
+                          mode: str = "voxel", minmax=None) -> DistanceMap:
+    """Full recompute for one TF: occupancy scan + distance transform
+    (acceleration.py:184-196, the Deakin & Knackstedt baseline)."""
+    return distance_transform(occupancy_for_tf(volume, grid, tf, mode, minmax))
+
+
+def partition_mask(volume: Volume, grid: BlockGrid, scheme: PartitionScheme,
+                   mode: str = "range_apron"):
+    """Per-block partition bitmask [num_blocks, ceil(n/32)] uint32 on the device
+    (the POM of every partition at once; acceleration.py:218-229)."""
+    L = _lib.lib()
+    words = _mask_words(scheme.n)
+    mask = device.empty((grid.num_blocks, words), np.int32)
+    vox = volume.device_voxels()
+    pid = scheme.device_pid_lut()
+    fn = L.pdm_partition_mask_voxel if mode == "voxel" else L.pdm_partition_mask_range_apron
+    _lib.check(fn(_lib.ptr(vox), volume.bits, *volume.dims, grid.b, _lib.ptr(pid), scheme.n,
+                  _lib.ptr(mask), words, _lib.stream_handle()), f"partition mask ({mode})")
+    return mask
+
+
+def build_pdm_set(volume: Volume, grid: BlockGrid, scheme: PartitionScheme,
+                  mode: str = "range_apron") -> PdmSet:
+    """Every partition's occupancy and distance map in one shot
+    (acceleration.py:199-241).  init_seconds is measured to device completion."""
+    _require_mode(mode)
+    check_pair(volume, grid)
+    if scheme.intensity_span != (1 << volume.bits):
+        raise VolumeError(
+            f"scheme spans {scheme.intensity_span} intensities, volume needs {1 << volume.bits}")
+    L = _lib.lib()
+    torch = device.torch()
+    torch.cuda.synchronize()
+    start = time.perf_counter()
+    mask = partition_mask(volume, grid, scheme, mode)
+    pitch = device.plane_pitch(grid.num_blocks)
+    storage = device.empty((scheme.n, pitch), np.uint8)
+    _lib.check(L.pdm_distance_transform_mask(_lib.ptr(mask), mask.shape[1], scheme.n, *grid.bdims,
+                                             _lib.ptr(storage), pitch, _lib.stream_handle()),
+               "pdm_distance_transform_mask")
+    torch.cuda.synchronize()
+    elapsed = time.perf_counter() - start
+    return PdmSet(grid=grid, scheme=scheme, occupancy_mode=mode, init_seconds=elapsed,
+                  storage=storage)
+
+
+def combine(pdm_set: PdmSet, selection: PartitionSelection,
+            max_maps_per_pass: int | None = None) -> DistanceMap:
+    """Element-wise min of the selected partitions' maps, all-255 for an empty
+    selection (acceleration.py:244-276).  One kernel pass reads each selected
+    map once; max_maps_per_pass is validated like the reference and does not
+    change the result (the reference guarantees chunked == direct)."""
+    if selection.n != pdm_set.n:
+        raise SelectionError(
+            f"selection is over {selection.n} partitions, set holds {pdm_set.n}")
+    grid = pdm_set.grid
+    indices = selection.sorted
+    if indices and max_maps_per_pass is not None and max_maps_per_pass < 1:
+        raise ValueError(f"max_maps_per_pass must be >= 1, got {max_maps_per_pass}")
+    L = _lib.lib()
+    out = device.empty(grid.bdims, np.uint8)
+    sel = np.ascontiguousarray([i - 1 for i in indices], dtype=np.int32)
+    storage = pdm_set.storage if indices else None
+    _lib.check(L.pdm_combine(_lib.ptr(storage) if storage is not None else None,
+                             pdm_set.plane_pitch, grid.num_blocks, max(pdm_set.n, 1),
+                             sel.ctypes.data if sel.size else None, int(sel.size), _lib.ptr(out),
+                             _lib.stream_handle()), "pdm_combine")
+    return DistanceMap(b=grid.b, bdims=grid.bdims, dist=out)
+
+
+def update_from_tf(pdm_set: PdmSet, tf, out=None, flags=None) -> DistanceMap:
+    """Fused device-side TF-change update: selection (K8) + merge (K7) with the
+    selection kept in HBM -- two kernels, no host round trip.  ``tf`` is a
+    TransferFunction or a device-resident f64 alpha tensor of length 2^bits.
+    Equivalent to combine(pdm_set, select_partitions(tf, scheme))."""
+    alpha = alpha_to_device(tf) if isinstance(tf, TransferFunction) else tf
+    flags = select_partitions_device(alpha, pdm_set.scheme, flags)
+    return combine_flags_into(pdm_set, flags, out)
+
+
+def combine_flags_into(pdm_set: PdmSet, flags, out=None) -> DistanceMap:
+    """K7 with a device-resident selection (uint8 flags[n], e.g. from
+    select_partitions_device) writing into ``out`` (allocated if None)."""
+    L = _lib.lib()
+    grid = pdm_set.grid
+    if out is None:
+        out = device.empty(grid.bdims, np.uint8)
+    _lib.check(L.pdm_combine_flags(_lib.ptr(pdm_set.storage), pdm_set.plane_pitch,
+                                   grid.num_blocks, pdm_set.n, _lib.ptr(flags), _lib.ptr(out),
+                                   _lib.stream_handle()), "pdm_combine_flags")
+    return DistanceMap(b=grid.b, bdims=grid.bdims, dist=out)
+
+
+# --- persistence (acceleration.py:279-354 formats) -----------------------------
+
+def save_distance_map(dm: DistanceMap, path) -> None:
+    """'PDMD' + <4I (b, bx, by, bz) + raw uint8 payload."""
+    Path(path).write_bytes(_MAP_MAGIC + struct.pack("<4I", dm.b, *dm.bdims) + dm.dist.tobytes())
+
+
+def load_distance_map(path) -> DistanceMap:
+    raw = Path(path).read_bytes()
+    if raw[:4] != _MAP_MAGIC:
+        raise VolumeError(f"{path} is not a distance map dump")
+    b, bx, by, bz = struct.unpack_from("<4I", raw, 4)
+    payload = np.frombuffer(raw, dtype=np.uint8, offset=20)
+    if payload.size != bx * by * bz:
+        raise VolumeError(f"{path} payload size does not match header dims")
+    return DistanceMap(b=b, bdims=(bx, by, bz), dist=payload.reshape((bx, by, bz)).copy())
+
+
+def save_pdm_set(pdm_set: PdmSet, path) -> None:
+    """'PDMS' + <9I (b, dims, bdims, n, mode) + n x <2I bounds + n raw maps."""
+    g = pdm_set.grid
+    head = _SET_MAGIC + struct.pack("<9I", g.b, *g.dims, *g.bdims, pdm_set.n,
+                                    0 if pdm_set.occupancy_mode == "voxel" else 1)
+    bounds = b"".join(struct.pack("<2I", lo, hi) for lo, hi in pdm_set.scheme.bounds())
+    nb = g.num_blocks
+    maps = device.to_host(pdm_set.storage[:, :nb], np.uint8).tobytes()
+    Path(path).write_bytes(head + bounds + maps)
+
+
+def load_pdm_set(path) -> PdmSet:
+    """Reads a 'PDMS' dump straight into one device allocation."""
+    raw = Path(path).read_bytes()
+    if raw[:4] != _SET_MAGIC:
+        raise VolumeError(f"{path} is not a partition set dump")
+    vals = struct.unpack_from("<9I", raw, 4)
+    b, dims, bdims, n = vals[0], vals[1:4], tuple(vals[4:7]), vals[7]
+    mode = "voxel" if vals[8] == 0 else "range_apron"
+    grid = BlockGrid.for_dims(dims, b)
+    if grid.bdims != bdims:
+        raise VolumeError(f"{path} header block dims are inconsistent")
+    off = 40
+    bounds = [struct.unpack_from("<2I", raw, off + 8 * i) for i in range(n)]
+    off += 8 * n
+    nb = grid.num_blocks
+    if len(raw) - off != n * nb:
+        raise VolumeError(f"{path} payload size does not match header")
+    scheme = PartitionScheme(tuple(Partition(lo, hi) for lo, hi in bounds))
+    maps = np.frombuffer(raw, dtype=np.uint8, count=n * nb, offset=off).reshape(n, nb)
+    pitch = device.plane_pitch(nb)
+    storage = device.empty((n, pitch), np.uint8)
+    storage[:, :nb].copy_(device.torch().from_numpy(maps.copy()))
+    return PdmSet(grid=grid, scheme=scheme, occupancy_mode=mode, init_seconds=0.0,
+                  storage=storage)

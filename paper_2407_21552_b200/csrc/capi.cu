@@ -1,0 +1,342 @@
+// capi.cu -- library plumbing plus the TF-change update: selection (K8) and
+// the min-merge over the selected partition distance maps (K7).
+//
+// K7 is HBM-bound: it reads k uint8 maps and writes one, (k+1) * B bytes for
+// B blocks.  Each thread owns 16-byte chunks of the map; for every chunk it
+// issues the k selected maps' 128-bit loads in batches of 8 (all loads of a
+// batch in flight before the first min) and takes the byte-wise min with
+// __vminu4.  Loads bypass L1 (read once), the store is evict-first.
+#include <cuda_runtime.h>
+
+#include <cstring>
+#include <string>
+
+#include "pdm_common.cuh"
+
+namespace pdm {
+
+static thread_local char g_last_error[1024] = "";
+
+void set_error(const char *fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_last_error, sizeof(g_last_error), fmt, ap);
+    va_end(ap);
+}
+
+int cuda_status(const char *where) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        set_error("%s: %s", where, cudaGetErrorString(e));
+        return PDM_ECUDA;
+    }
+    return PDM_OK;
+}
+
+int sm_count() {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return 148;
+    static int cached[64] = {0};
+    if (dev >= 0 && dev < 64 && cached[dev]) return cached[dev];
+    int n = 0;
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0)
+        n = 148;
+    if (dev >= 0 && dev < 64) cached[dev] = n;
+    return n;
+}
+
+// ---------------------------------------------------------------------------
+// K8: selection.  transfer.py:250-259 -- flags[pid[v]] = 1 where alpha > 0.0.
+__global__ void select_kernel(const double *__restrict__ alpha, int64_t span, int64_t stride,
+                              const int32_t *__restrict__ pid, uint8_t *__restrict__ flags) {
+    int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (v < span && alpha[v * stride] > 0.0) flags[pid[v]] = 1;  // NaN compares false
+}
+
+// acceleration.py:166,171 -- nz = alpha > 0 and its exclusive prefix count.
+// One CTA: each thread counts a contiguous chunk, a block scan turns counts
+// into chunk offsets, then each thread writes its chunk of the prefix.
+__global__ void __launch_bounds__(1024)
+    alpha_support_kernel(const double *__restrict__ alpha, int64_t span, int64_t stride,
+                         uint8_t *__restrict__ nz, int32_t *__restrict__ prefix) {
+    __shared__ int32_t s_sum[1024];
+    const int t = threadIdx.x;
+    const int64_t per = (span + blockDim.x - 1) / blockDim.x;
+    const int64_t lo = t * per, hi = lo + per < span ? lo + per : span;
+    int32_t cnt = 0;
+    for (int64_t v = lo; v < hi; ++v) {
+        uint8_t on = alpha[v * stride] > 0.0;
+        nz[v] = on;
+        cnt += on;
+    }
+    s_sum[t] = cnt;
+    __syncthreads();
+    for (int off = 1; off < (int)blockDim.x; off <<= 1) {  // Hillis-Steele inclusive scan
+        int32_t add = t >= off ? s_sum[t - off] : 0;
+        __syncthreads();
+        s_sum[t] += add;
+        __syncthreads();
+    }
+    if (prefix) {
+        int32_t run = s_sum[t] - cnt;  // exclusive
+        if (t == 0) prefix[0] = 0;
+        for (int64_t v = lo; v < hi; ++v) {
+            run += nz[v];
+            prefix[v + 1] = run;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K7: merge.
+constexpr int kMaxSelParam = 240;  // indices carried in kernel parameters per launch
+constexpr int kMaxFlagsSmem = 4096;
+constexpr int kMergeThreads = 256;
+constexpr int kMergeBatch = 8;  // selected maps whose loads are in flight together
+
+struct SelParam {
+    int32_t k;
+    int32_t idx[kMaxSelParam];
+};
+
+template <bool kAccumulate>
+__device__ __forceinline__ void merge_chunks(const uint8_t *__restrict__ pdms, int64_t pitch,
+                                             int64_t nvec, const int32_t *idx, int k,
+                                             uint8_t *__restrict__ out) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < nvec; v += stride) {
+        const int64_t off = v * 16;
+        uint4 acc;
+        if (kAccumulate)
+            acc = *reinterpret_cast<const uint4 *>(out + off);
+        else
+            acc = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
+        int m = 0;
+        for (; m + kMergeBatch <= k; m += kMergeBatch) {
+            uint4 r[kMergeBatch];
+#pragma unroll
+            for (int j = 0; j < kMergeBatch; ++j)
+                r[j] = ld_stream_u4(pdms + (int64_t)idx[m + j] * pitch + off);
+#pragma unroll
+            for (int j = 0; j < kMergeBatch; ++j) acc = vmin_u8x16(acc, r[j]);
+        }
+        if (m < k) {  // remainder: up to kMergeBatch-1 maps, still issued together
+            uint4 r[kMergeBatch - 1];
+#pragma unroll
+            for (int j = 0; j < kMergeBatch - 1; ++j)
+                if (m + j < k) r[j] = ld_stream_u4(pdms + (int64_t)idx[m + j] * pitch + off);
+#pragma unroll
+            for (int j = 0; j < kMergeBatch - 1; ++j)
+                if (m + j < k) acc = vmin_u8x16(acc, r[j]);
+        }
+        st_stream_u4(out + off, acc);
+    }
+}
+
+// Bytes past the last full 16-byte chunk (map_bytes % 16), byte by byte.
+__device__ __forceinline__ void merge_tail(const uint8_t *__restrict__ pdms, int64_t pitch,
+                                           int64_t from, int64_t map_bytes, const int32_t *idx,
+                                           int k, bool accumulate, uint8_t *__restrict__ out) {
+    if (blockIdx.x != 0) return;
+    for (int64_t c = from + threadIdx.x; c < map_bytes; c += blockDim.x) {
+        uint32_t acc = accumulate ? out[c] : 255u;
+        for (int m = 0; m < k; ++m) {
+            uint32_t v = pdms[(int64_t)idx[m] * pitch + c];
+            acc = v < acc ? v : acc;
+        }
+        out[c] = (uint8_t)acc;
+    }
+}
+
+__global__ void __launch_bounds__(kMergeThreads)
+    combine_kernel(const uint8_t *__restrict__ pdms, int64_t pitch, int64_t map_bytes,
+                   const __grid_constant__ SelParam sel, uint8_t *__restrict__ out,
+                   int accumulate) {
+    const int64_t nvec = map_bytes / 16;
+    if (accumulate)
+        merge_chunks<true>(pdms, pitch, nvec, sel.idx, sel.k, out);
+    else
+        merge_chunks<false>(pdms, pitch, nvec, sel.idx, sel.k, out);
+    merge_tail(pdms, pitch, nvec * 16, map_bytes, sel.idx, sel.k, accumulate != 0, out);
+}
+
+// Misaligned layouts (pitch or pointers not 16-byte aligned): byte-wise.
+__global__ void combine_bytes_kernel(const uint8_t *__restrict__ pdms, int64_t pitch,
+                                     int64_t map_bytes, const __grid_constant__ SelParam sel,
+                                     uint8_t *__restrict__ out, int accumulate) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < map_bytes; c += stride) {
+        uint32_t acc = accumulate ? out[c] : 255u;
+        for (int m = 0; m < sel.k; ++m) {
+            uint32_t v = pdms[(int64_t)sel.idx[m] * pitch + c];
+            acc = v < acc ? v : acc;
+        }
+        out[c] = (uint8_t)acc;
+    }
+}
+
+// Selection resident on the device: every CTA compacts flags[0..n) into a
+// shared index list (warp 0, ballot + popc), then merges like combine_kernel.
+__global__ void __launch_bounds__(kMergeThreads)
+    combine_flags_kernel(const uint8_t *__restrict__ pdms, int64_t pitch, int64_t map_bytes,
+                         int n, const uint8_t *__restrict__ flags, uint8_t *__restrict__ out) {
+    __shared__ int32_t s_idx[kMaxFlagsSmem];
+    __shared__ int s_k;
+    if (threadIdx.x < 32) {
+        const unsigned lane = threadIdx.x;
+        int k = 0;
+        for (int base = 0; base < n; base += 32) {
+            const int p = base + (int)lane;
+            const bool on = p < n && flags[p] != 0;
+            const unsigned bal = __ballot_sync(0xFFFFFFFFu, on);
+            if (on) s_idx[k + __popc(bal & ((1u << lane) - 1u))] = p;
+            k += __popc(bal);
+        }
+        if (lane == 0) s_k = k;
+    }
+    __syncthreads();
+    const int k = s_k;
+    const int64_t nvec = map_bytes / 16;
+    merge_chunks<false>(pdms, pitch, nvec, s_idx, k, out);
+    merge_tail(pdms, pitch, nvec * 16, map_bytes, s_idx, k, false, out);
+}
+
+// Volume.intensity_range for device-born volumes (volume.py:86-90): out[0] =
+// min, out[1] = max over all voxels.  Grid-stride, warp shuffle, one atomic
+// per warp into out (pre-set to [UINT_MAX, 0] by the wrapper).
+template <typename T>
+__global__ void volume_range_kernel(const T *__restrict__ vox, int64_t count,
+                                    uint32_t *__restrict__ out) {
+    uint32_t mn = 0xFFFFFFFFu, mx = 0;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += stride) {
+        const uint32_t v = vox[i];
+        mn = v < mn ? v : mn;
+        mx = v > mx ? v : mx;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        mn = min(mn, __shfl_xor_sync(0xFFFFFFFFu, mn, o));
+        mx = max(mx, __shfl_xor_sync(0xFFFFFFFFu, mx, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicMin(&out[0], mn);
+        atomicMax(&out[1], mx);
+    }
+}
+
+__global__ void range_init_kernel(uint32_t *out) {
+    out[0] = 0xFFFFFFFFu;
+    out[1] = 0;
+}
+
+static int merge_grid(int64_t work_items) {
+    int64_t want = ceil_div(work_items, kMergeThreads);
+    int64_t cap = (int64_t)sm_count() * (2048 / kMergeThreads);
+    if (want > cap) want = cap;
+    return want < 1 ? 1 : (int)want;
+}
+
+}  // namespace pdm
+
+using namespace pdm;
+
+extern "C" int pdm_version(void) { return 1; }
+
+extern "C" const char *pdm_last_error(void) { return g_last_error; }
+
+extern "C" int pdm_device_sm_count(int device) {
+    int n = 0;
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) {
+        set_error("cudaDeviceGetAttribute failed for device %d", device);
+        return -1;
+    }
+    return n;
+}
+
+extern "C" int pdm_volume_range(const void *vox, int bits, int64_t count, uint32_t *out,
+                                pdm_stream_t stream) {
+    PDM_REQUIRE(vox && out, "pdm_volume_range: null pointer");
+    PDM_REQUIRE((bits == 8 || bits == 16) && count >= 1, "pdm_volume_range: bad args");
+    cudaStream_t s = as_stream(stream);
+    range_init_kernel<<<1, 1, 0, s>>>(out);
+    int64_t grid = ceil_div(count, 256);
+    const int64_t cap = (int64_t)sm_count() * 8;
+    if (grid > cap) grid = cap;
+    if (bits == 8)
+        volume_range_kernel<uint8_t><<<(unsigned)grid, 256, 0, s>>>((const uint8_t *)vox, count, out);
+    else
+        volume_range_kernel<uint16_t><<<(unsigned)grid, 256, 0, s>>>((const uint16_t *)vox, count,
+                                                                       out);
+    return cuda_status("volume_range_kernel");
+}
+
+extern "C" int pdm_select(const double *alpha, int64_t span, int64_t alpha_stride,
+                          const int32_t *pid, int32_t n, uint8_t *flags, pdm_stream_t stream) {
+    PDM_REQUIRE(alpha && pid && flags, "pdm_select: null pointer");
+    PDM_REQUIRE(span >= 1 && n >= 1 && alpha_stride >= 1, "pdm_select: bad sizes");
+    cudaStream_t s = as_stream(stream);
+    PDM_CUDA_TRY(cudaMemsetAsync(flags, 0, (size_t)n, s));
+    const int threads = 256;
+    select_kernel<<<(unsigned)ceil_div(span, threads), threads, 0, s>>>(alpha, span, alpha_stride,
+                                                                         pid, flags);
+    return cuda_status("select_kernel");
+}
+
+extern "C" int pdm_alpha_support(const double *alpha, int64_t span, int64_t alpha_stride,
+                                 uint8_t *nz, int32_t *prefix, pdm_stream_t stream) {
+    PDM_REQUIRE(alpha && nz, "pdm_alpha_support: null pointer");
+    PDM_REQUIRE(span >= 1 && span <= (1 << 16) && alpha_stride >= 1,
+                "pdm_alpha_support: span must be in [1, 65536]");
+    alpha_support_kernel<<<1, 1024, 0, as_stream(stream)>>>(alpha, span, alpha_stride, nz,
+                                                             prefix);
+    return cuda_status("alpha_support_kernel");
+}
+
+extern "C" int pdm_combine(const uint8_t *pdms, int64_t plane_pitch, int64_t map_bytes,
+                           int32_t n, const int32_t *sel, int32_t k, uint8_t *out,
+                           pdm_stream_t stream) {
+    PDM_REQUIRE(out && (k == 0 || (pdms && sel)), "pdm_combine: null pointer");
+    PDM_REQUIRE(map_bytes >= 1 && plane_pitch >= map_bytes && n >= 1 && k >= 0 && k <= n,
+                "pdm_combine: bad sizes (map_bytes=%lld pitch=%lld n=%d k=%d)",
+                (long long)map_bytes, (long long)plane_pitch, n, k);
+    for (int i = 0; i < k; ++i)
+        PDM_REQUIRE(sel[i] >= 0 && sel[i] < n, "pdm_combine: index %d outside [0, %d)", sel[i],
+                    n);
+    cudaStream_t s = as_stream(stream);
+    if (k == 0) {  // acceleration.py:261-263: the all-255 map
+        PDM_CUDA_TRY(cudaMemsetAsync(out, kDistClamp, (size_t)map_bytes, s));
+        return PDM_OK;
+    }
+    const bool vec = (plane_pitch % 16 == 0) && ((uintptr_t)pdms % 16 == 0) &&
+                     ((uintptr_t)out % 16 == 0);
+    SelParam p;
+    for (int base = 0; base < k; base += kMaxSelParam) {  // >240 maps: fold in passes
+        p.k = k - base < kMaxSelParam ? k - base : kMaxSelParam;
+        memcpy(p.idx, sel + base, sizeof(int32_t) * p.k);
+        const int acc = base > 0;
+        if (vec) {
+            combine_kernel<<<merge_grid(map_bytes / 16 > 0 ? map_bytes / 16 : 1), kMergeThreads, 0,
+                             s>>>(pdms, plane_pitch, map_bytes, p, out, acc);
+        } else {
+            combine_bytes_kernel<<<merge_grid(map_bytes), kMergeThreads, 0, s>>>(
+                pdms, plane_pitch, map_bytes, p, out, acc);
+        }
+        int st = cuda_status("combine_kernel");
+        if (st) return st;
+    }
+    return PDM_OK;
+}
+
+extern "C" int pdm_combine_flags(const uint8_t *pdms, int64_t plane_pitch, int64_t map_bytes,
+                                 int32_t n, const uint8_t *flags, uint8_t *out,
+                                 pdm_stream_t stream) {
+    PDM_REQUIRE(pdms && flags && out, "pdm_combine_flags: null pointer");
+    PDM_REQUIRE(map_bytes >= 1 && plane_pitch >= map_bytes && n >= 1,
+                "pdm_combine_flags: bad sizes");
+    PDM_REQUIRE(n <= kMaxFlagsSmem, "pdm_combine_flags: n=%d above %d", n, kMaxFlagsSmem);
+    PDM_REQUIRE(plane_pitch % 16 == 0 && (uintptr_t)pdms % 16 == 0 && (uintptr_t)out % 16 == 0,
+                "pdm_combine_flags: needs 16-byte aligned planes");
+    combine_flags_kernel<<<merge_grid(map_bytes / 16 > 0 ? map_bytes / 16 : 1), kMergeThreads, 0,
+                           as_stream(stream)>>>(pdms, plane_pitch, map_bytes, n, flags, out);
+    return cuda_status("combine_flags_kernel");
+}

@@ -1,0 +1,88 @@
+"""Device-memory plumbing: numpy <-> CUDA tensors through pinned staging.
+
+torch is used only as the allocator / stream / copy engine here; all compute
+goes through libpdm_b200 kernels.  Host<->device copies go through pinned
+(page-locked) buffers from torch's caching host allocator so they run at
+full PCIe/C2C rate and are stream-ordered.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+PLANE_ALIGN = 256  # bytes between partition planes are a multiple of this
+_PINNED_MIN = 1 << 16  # below this a plain pageable copy is cheaper
+
+
+def torch():
+    import torch as _torch
+
+    return _torch
+
+
+def device():
+    from . import _lib
+
+    _lib.lib()  # raises when no CUDA device / library: there is no CPU fallback
+    return torch().device("cuda", torch().cuda.current_device())
+
+
+_TORCH_DTYPE = {
+    np.dtype(np.uint8): "uint8",
+    np.dtype(np.uint16): "int16",  # reinterpreted: kernels only see raw bytes
+    np.dtype(np.int16): "int16",
+    np.dtype(np.int32): "int32",
+    np.dtype(np.uint32): "int32",
+    np.dtype(np.int64): "int64",
+    np.dtype(np.float64): "float64",
+    np.dtype(np.bool_): "uint8",
+}
+_VIEW_AS = {np.dtype(np.bool_): np.uint8, np.dtype(np.uint16): np.int16,
+            np.dtype(np.uint32): np.int32}
+
+
+def _torch_dtype(dt):
+    return getattr(torch(), _TORCH_DTYPE[np.dtype(dt)])
+
+
+def to_device(a: np.ndarray):
+    """Upload a host array as raw bytes of the same shape (stream-ordered)."""
+    t = torch()
+    dev = device()
+    a = np.ascontiguousarray(a)
+    dt = np.dtype(a.dtype)
+    src = t.from_numpy(a.view(_VIEW_AS[dt]) if dt in _VIEW_AS else a)
+    if a.nbytes >= _PINNED_MIN:
+        staged = t.empty(src.shape, dtype=src.dtype, pin_memory=True)
+        staged.copy_(src)
+        # non_blocking from pinned memory: torch's caching host allocator holds
+        # `staged` until the copy has completed on the current stream
+        return staged.to(dev, non_blocking=True)
+    return src.to(dev)
+
+
+def to_host(t_dev, np_dtype) -> np.ndarray:
+    """Download a device tensor into pinned host memory; reinterpret as np_dtype."""
+    t = torch()
+    np_dtype = np.dtype(np_dtype)
+    if t_dev.numel() * t_dev.element_size() >= _PINNED_MIN:
+        host_t = t.empty(t_dev.shape, dtype=t_dev.dtype, pin_memory=True)
+        host_t.copy_(t_dev, non_blocking=True)
+        t.cuda.current_stream().synchronize()
+    else:
+        host_t = t_dev.detach().to("cpu")
+    host = host_t.numpy()
+    if np_dtype == np.bool_:
+        return host.astype(bool)
+    if host.dtype.itemsize == np_dtype.itemsize:
+        return host.view(np_dtype)
+    return host.astype(np_dtype)
+
+
+def empty(shape, np_dtype):
+    return torch().empty(tuple(int(s) for s in shape), dtype=_torch_dtype(np_dtype),
+                         device=device())
+
+
+def plane_pitch(num_blocks: int) -> int:
+    return -(-int(num_blocks) // PLANE_ALIGN) * PLANE_ALIGN

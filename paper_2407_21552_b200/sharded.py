@@ -1,0 +1,208 @@
+"""Multi-GPU x-slab sharding of the PDM precompute.
+
+The volume is split into contiguous slabs of whole block planes along x, the
+slowest memory axis ([x][y][z] C-order, z contiguous) -- the north_star's
+"z-slabs" in memory terms.  One process per GPU; each rank holds its volume
+slab, its slab of every partition map and (after an update) its slab of D'.
+
+* TF-change update (select + merge): embarrassingly parallel, no collective.
+* POM build, voxel mode: local.  range_apron mode: a block's apron reaches one
+  voxel plane into each neighbour slab, so neighbours swap one boundary voxel
+  plane (send/recv over NCCL) and fold its apron min/max into their first/last
+  block plane (pdm_minmax_fold).
+* Distance transform: pass x runs along the shard axis, locally, then each
+  rank contributes its two edge planes per partition (the distance from its
+  first/last block plane to its nearest occupied block) to one all_gather of
+  2 * n * by * bz bytes per rank; pdm_dt_slab_fold folds every other slab's
+  nearest occupied block into the local 1-D distances, after which passes y
+  and z are local.  Bit-exact against the single-GPU transform (min over
+  slabs of clamped distances composes exactly).
+
+Collectives go through torch.distributed (NCCL on GPUs, gloo in CPU tests).
+The per-slab compute is an ``ops`` object: ``GpuOps`` (libpdm_b200 kernels)
+in the product; tests substitute a host implementation to exercise the
+collective logic on CPU with gloo.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from . import _lib, device
+from .acceleration import PdmSet, _require_mode
+from .transfer import PartitionScheme
+from .volume import BlockGrid, Volume, VolumeError
+
+
+class GpuOps:
+    """Per-slab compute on CUDA tensors via libpdm_b200."""
+
+    def empty(self, shape, np_dtype):
+        return device.empty(shape, np_dtype)
+
+    def voxels(self, volume):
+        return volume.device_voxels()
+
+    def plane(self, vol_t, x):
+        return vol_t[x: x + 1].contiguous()
+
+    def block_min_max(self, vol_t, bits, b):
+        L = _lib.lib()
+        dims = tuple(vol_t.shape)
+        bd = tuple(-(-d // b) for d in dims)
+        dt = np.uint8 if bits == 8 else np.uint16
+        mins, maxs = self.empty(bd, dt), self.empty(bd, dt)
+        _lib.check(L.pdm_block_min_max(_lib.ptr(vol_t), bits, *dims, b, _lib.ptr(mins),
+                                       _lib.ptr(maxs), _lib.stream_handle()), "pdm_block_min_max")
+        return mins, maxs
+
+    def fold_minmax(self, mins_plane, maxs_plane, pmins, pmaxs, bits):
+        L = _lib.lib()
+        _lib.check(L.pdm_minmax_fold(_lib.ptr(mins_plane), _lib.ptr(maxs_plane), _lib.ptr(pmins),
+                                     _lib.ptr(pmaxs), bits, mins_plane.numel(),
+                                     _lib.stream_handle()), "pdm_minmax_fold")
+
+    def mask_from_minmax(self, mins, maxs, bits, scheme):
+        L = _lib.lib()
+        words = (scheme.n + 31) // 32
+        mask = self.empty((mins.numel(), words), np.int32)
+        _lib.check(L.pdm_partition_mask_minmax(_lib.ptr(mins), _lib.ptr(maxs), bits, mins.numel(),
+                                               _lib.ptr(scheme.device_pid_lut()), scheme.n,
+                                               _lib.ptr(mask), words, _lib.stream_handle()),
+                   "pdm_partition_mask_minmax")
+        return mask
+
+    def mask_voxel(self, vol_t, bits, b, scheme):
+        L = _lib.lib()
+        dims = tuple(vol_t.shape)
+        nb = int(np.prod([-(-d // b) for d in dims]))
+        words = (scheme.n + 31) // 32
+        mask = self.empty((nb, words), np.int32)
+        _lib.check(L.pdm_partition_mask_voxel(_lib.ptr(vol_t), bits, *dims, b,
+                                              _lib.ptr(scheme.device_pid_lut()), scheme.n,
+                                              _lib.ptr(mask), words, _lib.stream_handle()),
+                   "pdm_partition_mask_voxel")
+        return mask
+
+    def pass_x(self, mask, n, bdims, storage, pitch):
+        L = _lib.lib()
+        _lib.check(L.pdm_dt_pass_x_mask(_lib.ptr(mask), mask.shape[1], n, *bdims,
+                                        _lib.ptr(storage), pitch, _lib.stream_handle()),
+                   "pdm_dt_pass_x_mask")
+
+    def edges(self, storage, pitch, n, bdims):
+        L = _lib.lib()
+        e = self.empty((2, n, bdims[1], bdims[2]), np.uint8)
+        _lib.check(L.pdm_dt_slab_edges(_lib.ptr(storage), pitch, n, *bdims, _lib.ptr(e),
+                                       _lib.stream_handle()), "pdm_dt_slab_edges")
+        return e
+
+    def fold(self, storage, pitch, n, bdims, edges_all, world, rank, slab_x0):
+        L = _lib.lib()
+        x0 = np.ascontiguousarray(slab_x0, dtype=np.int64)
+        _lib.check(L.pdm_dt_slab_fold(_lib.ptr(storage), pitch, n, *bdims, _lib.ptr(edges_all),
+                                      world, rank, x0.ctypes.data, _lib.stream_handle()),
+                   "pdm_dt_slab_fold")
+
+    def pass_yz(self, storage, pitch, n, bdims):
+        L = _lib.lib()
+        _lib.check(L.pdm_dt_pass_yz(_lib.ptr(storage), pitch, n, *bdims, _lib.stream_handle()),
+                   "pdm_dt_pass_yz")
+
+
+def slab_bounds(nx: int, b: int, world: int) -> list[int]:
+    """Voxel x0 of each slab (+ nx): whole block planes, as even as possible."""
+    bx = -(-nx // b)
+    per, rem = divmod(bx, world)
+    starts, acc = [], 0
+    for r in range(world):
+        starts.append(min(acc * b, nx))
+        acc += per + (r < rem)
+    return starts + [nx]
+
+
+def _exchange_planes(vol_t, ops, rank, world, group):
+    """Swap boundary voxel planes with the x-neighbours.  Returns (below, above):
+    the neighbour's plane at x0-1 and x1 (None at the volume ends)."""
+    import torch.distributed as dist
+
+    ops_list, below, above = [], None, None
+    nxl = vol_t.shape[0]
+    if rank > 0:
+        below = ops.empty((1,) + tuple(vol_t.shape[1:]), _np_dtype(vol_t))
+        ops_list.append(dist.P2POp(dist.isend, ops.plane(vol_t, 0), rank - 1, group))
+        ops_list.append(dist.P2POp(dist.irecv, below, rank - 1, group))
+    if rank < world - 1:
+        above = ops.empty((1,) + tuple(vol_t.shape[1:]), _np_dtype(vol_t))
+        ops_list.append(dist.P2POp(dist.isend, ops.plane(vol_t, nxl - 1), rank + 1, group))
+        ops_list.append(dist.P2POp(dist.irecv, above, rank + 1, group))
+    if ops_list:
+        for req in dist.batch_isend_irecv(ops_list):
+            req.wait()
+    return below, above
+
+
+def _np_dtype(t):
+    return np.uint8 if t.element_size() == 1 else np.uint16
+
+
+def build_pdm_set_sharded(volume: Volume, b: int, scheme: PartitionScheme,
+                          mode: str = "range_apron", bx0: int | None = None, group=None,
+                          ops=None) -> PdmSet:
+    """build_pdm_set over an x-slab of a volume split across the ranks of
+    ``group``.  ``volume`` is this rank's slab (its x0 must be a multiple of b
+    and every slab but the last must hold whole blocks); the result is this
+    rank's slab of every partition's distance map, bit-identical to the
+    corresponding planes of the single-device build_pdm_set."""
+    import torch
+    import torch.distributed as dist
+
+    _require_mode(mode)
+    if scheme.intensity_span != (1 << volume.bits):
+        raise VolumeError(
+            f"scheme spans {scheme.intensity_span} intensities, volume needs {1 << volume.bits}")
+    ops = ops or GpuOps()
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    vol_t = ops.voxels(volume)
+    grid = BlockGrid.for_dims(volume.dims, b)
+    bdims, n = grid.bdims, scheme.n
+
+    # slab table in block planes (every rank learns every slab's start)
+    mine = torch.tensor([bdims[0] if bx0 is None else bx0, bdims[0]], dtype=torch.int64)
+    if dist.get_backend(group) == "nccl":
+        mine = mine.cuda()
+    table = [torch.zeros_like(mine) for _ in range(world)]
+    dist.all_gather(table, mine, group=group)
+    sizes = [int(t[1]) for t in table]
+    starts = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+    if bx0 is not None and int(starts[rank]) != bx0:
+        raise VolumeError(f"rank {rank}: slab starts at block {bx0}, expected {starts[rank]}")
+
+    if mode == "voxel":
+        mask = ops.mask_voxel(vol_t, volume.bits, b, scheme)
+    else:
+        mins, maxs = ops.block_min_max(vol_t, volume.bits, b)
+        below, above = _exchange_planes(vol_t, ops, rank, world, group)
+        if below is not None:
+            pm, px = ops.block_min_max(below, volume.bits, b)
+            ops.fold_minmax(mins[0:1], maxs[0:1], pm, px, volume.bits)
+        if above is not None:
+            if volume.dims[0] % b:
+                raise VolumeError("only the last slab may end inside a block")
+            pm, px = ops.block_min_max(above, volume.bits, b)
+            ops.fold_minmax(mins[-1:], maxs[-1:], pm, px, volume.bits)
+        mask = ops.mask_from_minmax(mins, maxs, volume.bits, scheme)
+
+    pitch = device.plane_pitch(grid.num_blocks)
+    storage = ops.empty((n, pitch), np.uint8)
+    ops.pass_x(mask, n, bdims, storage, pitch)
+    edges = ops.edges(storage, pitch, n, bdims)
+    gathered = [torch.empty_like(edges) for _ in range(world)]
+    dist.all_gather(gathered, edges, group=group)
+    edges_all = torch.stack(gathered).contiguous()
+    ops.fold(storage, pitch, n, bdims, edges_all, world, rank, starts)
+    ops.pass_yz(storage, pitch, n, bdims)
+    pset = PdmSet(grid=grid, scheme=scheme, occupancy_mode=mode, storage=storage)
+    pset.slab = (int(starts[rank]), int(starts[rank + 1]), int(starts[-1]))
+    return pset

@@ -1,0 +1,251 @@
+"""GPU parity: the CUDA path (through the drop-in API, hence the C ABI) against
+the reference's golden vectors and the CPU oracle, bit-exact.  Needs a B200."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_2407_21552_b200 as pdm
+from conftest import (
+    GOLDEN,
+    bounds_of,
+    chebyshev_oracle,
+    golden_case_names,
+    load_case,
+    load_dt_cases,
+    lut_from_support,
+    random_structured_volume,
+    tf_names,
+)
+
+pytestmark = pytest.mark.gpu
+CASES = golden_case_names()
+
+
+def _scheme(bounds):
+    return pdm.PartitionScheme(tuple(pdm.Partition(lo, hi) for lo, hi in bounds))
+
+
+def _tf(alpha):
+    lut = np.zeros((alpha.size, 4))
+    lut[:, 3] = alpha
+    return pdm.TransferFunction(lut=lut)
+
+
+def _stack(pset):
+    return np.stack([d.dist for d in pset.pdms])
+
+
+# --- distance transform --------------------------------------------------------------
+
+def test_distance_transform_golden():
+    for occ, want in load_dt_cases():
+        dm = pdm.distance_transform(pdm.OccupancyMap(b=1, bdims=occ.shape, occupied=occ))
+        assert np.array_equal(dm.dist, want), occ.shape
+
+
+def test_distance_transform_brute_force():
+    rng = np.random.default_rng(404)
+    for case in range(200):
+        dims = tuple(int(rng.integers(1, 11)) for _ in range(3))
+        occ = (np.zeros(dims, bool) if case == 0 else np.ones(dims, bool) if case == 1
+               else rng.random(dims) < rng.uniform(0.0, 0.6))
+        dm = pdm.distance_transform(pdm.OccupancyMap(b=1, bdims=dims, occupied=occ))
+        assert np.array_equal(dm.dist.astype(np.int64), chebyshev_oracle(occ)), dims
+
+
+def test_distance_transform_clamp_far_field():
+    occ = np.zeros((300, 1, 1), bool)
+    occ[0] = True
+    d = pdm.distance_transform(pdm.OccupancyMap(b=4, bdims=occ.shape, occupied=occ)).dist
+    assert d[254, 0, 0] == 254 and d[255, 0, 0] == 255 and d[299, 0, 0] == 255
+    for shape, pt in (((2, 700, 3), (1, 3, 2)), ((3, 2, 1100), (0, 1, 1099)),
+                      ((5, 1300, 1), (4, 0, 0))):
+        occ = np.zeros(shape, bool)
+        occ[pt] = True
+        got = pdm.distance_transform(pdm.OccupancyMap(b=1, bdims=shape, occupied=occ)).dist
+        assert np.array_equal(got, oracle.distance_transform(occ)), shape
+
+
+def test_distance_transform_random_vs_oracle_medium():
+    rng = np.random.default_rng(9)
+    for dims, dens in (((64, 48, 80), 0.0005), ((33, 65, 17), 0.01), ((70, 70, 70), 0.00002),
+                       ((16, 300, 40), 0.001), ((128, 96, 260), 0.000005)):
+        occ = rng.random(dims) < dens
+        got = pdm.distance_transform(pdm.OccupancyMap(b=1, bdims=dims, occupied=occ)).dist
+        assert np.array_equal(got, oracle.distance_transform(occ)), dims
+
+
+# --- golden volume cases ---------------------------------------------------------------
+
+@pytest.fixture(scope="module", params=CASES)
+def case(request):
+    c = load_case(request.param)
+    vol = pdm.Volume.from_array(c["vox"])
+    grid = pdm.BlockGrid.for_dims(vol.dims, int(c["b"]))
+    return c, vol, grid, _scheme(bounds_of(c))
+
+
+def test_block_min_max(case):
+    c, vol, grid, _ = case
+    mins, maxs = pdm.block_min_max(vol, grid)
+    assert mins.dtype == c["mins"].dtype
+    assert np.array_equal(mins, c["mins"]) and np.array_equal(maxs, c["maxs"])
+
+
+@pytest.mark.parametrize("mode", ["voxel", "range_apron"])
+def test_occupancy_for_partition(case, mode):
+    c, vol, grid, scheme = case
+    mm = pdm.block_min_max_device(vol, grid) if mode == "range_apron" else None
+    for p, part in enumerate(scheme.partitions):
+        occ = pdm.occupancy_for_partition(vol, grid, part, mode, minmax=mm)
+        assert np.array_equal(occ.occupied, c[f"occ_part_{mode}"][p]), p
+
+
+@pytest.mark.parametrize("mode", ["voxel", "range_apron"])
+def test_build_pdm_set(case, mode):
+    c, vol, grid, scheme = case
+    pset = pdm.build_pdm_set(vol, grid, scheme, mode)
+    assert pset.n == scheme.n and pset.occupancy_mode == mode and pset.init_seconds > 0
+    assert np.array_equal(_stack(pset), c[f"pdms_{mode}"])
+
+
+@pytest.mark.parametrize("mode", ["voxel", "range_apron"])
+def test_select_combine_and_recompute(case, mode):
+    c, vol, grid, scheme = case
+    pset = pdm.build_pdm_set(vol, grid, scheme, mode)
+    for t in tf_names(c):
+        tf = _tf(c[f"tf_{t}_alpha"])
+        sel = pdm.select_partitions(tf, scheme)
+        assert sel.sorted == c[f"tf_{t}_sel"].tolist(), t
+        dp = pdm.combine(pset, sel)
+        assert np.array_equal(dp.dist, c[f"tf_{t}_dprime_{mode}"]), (t, mode)
+        fused = pdm.update_from_tf(pset, tf)
+        assert np.array_equal(fused.dist, c[f"tf_{t}_dprime_{mode}"]), (t, mode)
+        occ = pdm.occupancy_for_tf(vol, grid, tf, mode)
+        assert np.array_equal(occ.occupied, c[f"tf_{t}_occ_{mode}"]), (t, mode)
+        std = pdm.standard_distance_map(vol, grid, tf, mode)
+        assert np.array_equal(std.dist, c[f"tf_{t}_std_{mode}"]), (t, mode)
+
+
+def test_worked_example():
+    with np.load(GOLDEN / "worked_example.npz") as z:
+        scheme = _scheme([tuple(map(int, r)) for r in z["bounds"]])
+        vol = pdm.Volume.from_array(z["vox"])
+        grid = pdm.BlockGrid.for_dims(vol.dims, 1)
+        pset = pdm.build_pdm_set(vol, grid, scheme, "voxel")
+        assert np.array_equal(_stack(pset), z["pdms"])
+        sel = pdm.select_partitions(_tf(z["alpha"]), scheme)
+        assert sel.sorted == [2, 4]
+        assert np.array_equal(pdm.combine(pset, sel).dist, z["dprime"])
+
+
+# --- combine semantics (acceleration.py:244-276) ----------------------------------------
+
+@pytest.fixture(scope="module")
+def built16():
+    rng = np.random.default_rng(6)
+    vol = pdm.Volume.from_array(random_structured_volume(rng, (16, 16, 16)))
+    grid = pdm.BlockGrid.for_dims(vol.dims, 4)
+    scheme = pdm.scheme_uniform(16, 8)
+    return scheme, pdm.build_pdm_set(vol, grid, scheme, "voxel")
+
+
+def test_combine_empty_singleton_full(built16):
+    scheme, pset = built16
+    sel = lambda s: pdm.PartitionSelection(selected=frozenset(s), n=scheme.n)  # noqa: E731
+    assert np.all(pdm.combine(pset, sel(())).dist == 255)
+    single = pdm.combine(pset, sel({3}))
+    assert np.array_equal(single.dist, pset.pdms[2].dist)
+    assert single.device().data_ptr() != pset.pdms[2].device().data_ptr()
+    full = pdm.combine(pset, sel(range(1, 17)))
+    assert np.array_equal(full.dist, np.minimum.reduce([p.dist for p in pset.pdms]))
+    for chunk in (1, 2, 3, 100):
+        s = sel({1, 4, 7, 9, 15})
+        assert np.array_equal(pdm.combine(pset, s).dist,
+                              pdm.combine(pset, s, max_maps_per_pass=chunk).dist)
+    with pytest.raises(ValueError):
+        pdm.combine(pset, sel({1}), max_maps_per_pass=0)
+    small = pdm.combine(pset, sel({2, 5})).dist
+    large = pdm.combine(pset, sel({2, 5, 9, 12})).dist
+    assert np.all(large <= small)
+
+
+def test_combine_more_than_one_param_batch():
+    rng = np.random.default_rng(3)
+    vox = random_structured_volume(rng, (12, 10, 16), bits=8)
+    vol = pdm.Volume.from_array(vox)
+    grid = pdm.BlockGrid.for_dims(vol.dims, 2)
+    scheme = pdm.scheme_uniform(256, 8)
+    pset = pdm.build_pdm_set(vol, grid, scheme, "voxel")
+    want = oracle.build_pdm_set(vox, 2, scheme.bounds(), "voxel")
+    assert np.array_equal(_stack(pset), want)
+    for k in (239, 240, 241, 256):
+        s = sorted(rng.choice(np.arange(1, 257), size=k, replace=False).tolist())
+        got = pdm.combine(pset, pdm.PartitionSelection(selected=frozenset(s), n=256)).dist
+        assert np.array_equal(got, oracle.combine(want, s)), k
+
+
+def test_combine_rebuilt_from_host_maps(built16):
+    scheme, pset = built16
+    host = pdm.PdmSet(grid=pset.grid, scheme=scheme,
+                      pdms=tuple(pdm.DistanceMap(4, pset.grid.bdims, d.dist.copy())
+                                 for d in pset.pdms), occupancy_mode="voxel")
+    s = pdm.PartitionSelection(selected=frozenset({2, 9, 16}), n=16)
+    assert np.array_equal(pdm.combine(host, s).dist, pdm.combine(pset, s).dist)
+
+
+def test_pdm_set_round_trip(tmp_path, built16):
+    scheme, pset = built16
+    pdm.save_pdm_set(pset, tmp_path / "set.bin")
+    back = pdm.load_pdm_set(tmp_path / "set.bin")
+    assert back.n == pset.n and back.grid == pset.grid and back.scheme.bounds() == scheme.bounds()
+    assert np.array_equal(_stack(back), _stack(pset))
+
+
+# --- random fast-path shapes vs the oracle -----------------------------------------------
+
+@pytest.mark.parametrize("dims,bits,b,n", [
+    ((64, 64, 128), 16, 4, 32), ((48, 40, 64), 16, 8, 16), ((40, 36, 96), 8, 4, 64),
+    ((37, 29, 64), 16, 2, 33), ((31, 17, 48), 8, 16, 8), ((20, 20, 24), 16, 1, 4),
+    ((65, 33, 40), 16, 4, 64),
+])
+@pytest.mark.parametrize("mode", ["voxel", "range_apron"])
+def test_random_volumes_vs_oracle(dims, bits, b, n, mode):
+    rng = np.random.default_rng(sum(dims) + bits + b + n)
+    vox = random_structured_volume(rng, dims, bits)
+    vol = pdm.Volume.from_array(vox)
+    grid = pdm.BlockGrid.for_dims(dims, b)
+    scheme = pdm.scheme_uniform(n, bits)
+    pset = pdm.build_pdm_set(vol, grid, scheme, mode)
+    want = oracle.build_pdm_set(vox, b, scheme.bounds(), mode)
+    assert np.array_equal(_stack(pset), want)
+    mins, maxs = pdm.block_min_max(vol, grid)
+    omin, omax = oracle.block_min_max(vox, b)
+    assert np.array_equal(mins, omin) and np.array_equal(maxs, omax)
+    span = 1 << bits
+    for _ in range(3):
+        support = np.zeros(span, bool)
+        lo = int(rng.integers(0, span))
+        support[lo: lo + int(rng.integers(1, span // 3))] = True
+        lut = lut_from_support(support, rng)
+        tf = pdm.TransferFunction(lut=lut)
+        sel = pdm.select_partitions(tf, scheme)
+        assert sel.sorted == oracle.select(lut[:, 3], scheme.bounds())
+        assert np.array_equal(pdm.combine(pset, sel).dist, oracle.combine(want, sel.sorted))
+        assert np.array_equal(pdm.standard_distance_map(vol, grid, tf, mode).dist,
+                              oracle.standard_distance_map(vox, b, lut, mode))
+
+
+def test_device_born_volume_matches_oracle_synth():
+    from paper_2407_21552_b200 import synth
+
+    dims, bits = (40, 24, 64), 16
+    vol = synth.synth_volume_device(dims, bits, seed=11, nbox=8)
+    host = oracle.synth_volume(bits, dims, synth.synth_boxes(dims, bits, 11, 8), seed=11)
+    assert np.array_equal(vol.voxels, host)
+    assert vol.intensity_range == (int(host.min()), int(host.max()))
+    part = synth.synth_volume_device(dims, bits, seed=11, nbox=8, x_range=(8, 30))
+    assert np.array_equal(part.voxels, host[8:30])

@@ -1,0 +1,244 @@
+"""Host-side logic of the drop-in API (CPU only): geometry, schemes, TF
+validation, selection/error paths that are raised before any launch, RAW I/O,
+the C-ABI library's exports, and the no-CPU-fallback guarantee."""
+
+from __future__ import annotations
+
+import ctypes
+import json
+import re
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+import paper_2407_21552_b200 as pdm
+from paper_2407_21552_b200 import _lib
+
+ROOT = Path(__file__).resolve().parents[1]
+
+
+# --- C ABI -------------------------------------------------------------------------
+
+def _header_symbols() -> set[str]:
+    text = (ROOT / "include" / "pdm_b200.h").read_text()
+    return set(re.findall(r"^\s*(?:int|const char \*)\s*(pdm_\w+)\s*\(", text, re.M))
+
+
+def test_library_exports_every_header_symbol():
+    L = _lib.load_library()
+    declared = _header_symbols()
+    assert declared, "no declarations parsed from include/pdm_b200.h"
+    assert declared == set(_lib.EXPORTED), declared ^ set(_lib.EXPORTED)
+    for name in declared:
+        assert hasattr(L, name), name
+    assert L.pdm_version() == 1
+
+
+def test_library_rejects_bad_arguments_without_gpu():
+    L = _lib.load_library()
+    # null pointers / sizes are validated before any CUDA call
+    assert L.pdm_combine(None, 16, 16, 1, None, 1, None, None) == _lib.PDM_EINVAL
+    assert b"null" in L.pdm_last_error()
+    assert L.pdm_select(None, 0, 1, None, 0, None, None) == _lib.PDM_EINVAL
+    assert L.pdm_block_min_max(ctypes.c_void_p(16), 12, 4, 4, 4, 4, ctypes.c_void_p(16),
+                               ctypes.c_void_p(16), None) == _lib.PDM_EINVAL
+    assert b"bits" in L.pdm_last_error()
+
+
+def test_library_is_sm100a_only():
+    lib = ROOT / "paper_2407_21552_b200" / "lib" / "libpdm_b200.so"
+    import subprocess
+
+    out = subprocess.run(["cuobjdump", "--list-elf", str(lib)], capture_output=True, text=True)
+    archs = set(re.findall(r"sm_(\d+a?)", out.stdout))
+    assert archs == {"100a"}, out.stdout
+
+
+def test_no_cpu_fallback(monkeypatch):
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("has a GPU")
+    vol = pdm.Volume.from_array(np.zeros((8, 8, 8), dtype=np.uint8))
+    grid = pdm.BlockGrid.for_dims(vol.dims, 4)
+    with pytest.raises(RuntimeError, match="no CPU fallback"):
+        pdm.build_pdm_set(vol, grid, pdm.scheme_uniform(2, 8))
+    with pytest.raises(RuntimeError, match="no CPU fallback"):
+        pdm.select_partitions(pdm.tf_archetype("tf2"), pdm.scheme_uniform(4, 8))
+
+
+# --- geometry / volume ----------------------------------------------------------------
+
+def test_block_grid_ceil_division():
+    g = pdm.BlockGrid.for_dims((10, 8, 5), 4)
+    assert g.bdims == (3, 2, 2) and g.num_blocks == 12
+    assert g.block_of((9, 4, 0)) == (2, 1, 0)
+    with pytest.raises(ValueError):
+        pdm.BlockGrid.for_dims((8, 8, 8), 0)
+    with pytest.raises(ValueError):
+        pdm.BlockGrid.for_dims((8, 0, 8), 2)
+
+
+@pytest.mark.parametrize("dims", [(8, 8, 8), (9, 13, 4), (1, 1, 1), (17, 3, 100)])
+@pytest.mark.parametrize("b", [1, 2, 4, 7])
+def test_block_grid_bounds(dims, b):
+    g = pdm.BlockGrid.for_dims(dims, b)
+    for d, bd in zip(dims, g.bdims):
+        assert bd * b >= d > (bd - 1) * b
+
+
+def test_volume_validation():
+    with pytest.raises(pdm.BitDepthError):
+        pdm.Volume.from_array(np.zeros((2, 2, 2), dtype=np.int32))
+    with pytest.raises(pdm.VolumeError):
+        pdm.Volume(dims=(2, 2, 3), voxels=np.zeros((2, 2, 2), dtype=np.uint8))
+    with pytest.raises(pdm.VolumeError):
+        pdm.Volume.from_array(np.zeros((2, 2, 2), dtype=np.uint8), spacing=(1, 0, 1))
+    v = pdm.Volume.from_array(np.array([[[3, 9]]], dtype=np.uint16))
+    assert v.intensity_range == (3, 9) and v.bits == 16 and v.num_voxels == 2
+
+
+def _write_raw(tmp_path, payload: bytes, meta: dict):
+    d, m = tmp_path / "v.raw", tmp_path / "v.json"
+    d.write_bytes(payload)
+    m.write_text(json.dumps(meta))
+    return d, m
+
+
+def test_load_raw_layout_and_errors(tmp_path):
+    d, m = _write_raw(tmp_path, bytes(range(8)), {"dims": [2, 2, 2], "bits": 8})
+    v = pdm.load_raw(d, m)
+    assert v.voxels[1, 0, 0] == 1 and v.voxels[0, 1, 0] == 2 and v.voxels[0, 0, 1] == 4
+    d, m = _write_raw(tmp_path, np.array([300, 7, 0, 65535], ">u2").tobytes(),
+                      {"dims": [4, 1, 1], "bits": 16, "endianness": "be"})
+    assert pdm.load_raw(d, m).voxels[:, 0, 0].tolist() == [300, 7, 0, 65535]
+    d, m = _write_raw(tmp_path, bytes(10), {"dims": [2, 2, 2], "bits": 8})
+    with pytest.raises(pdm.SizeMismatchError):
+        pdm.load_raw(d, m)
+    d, m = _write_raw(tmp_path, bytes(8), {"dims": [2, 2, 2], "bits": 12})
+    with pytest.raises(pdm.BitDepthError):
+        pdm.load_raw(d, m)
+    d, m = _write_raw(tmp_path, bytes(8), {"dims": [2, 2, 2]})
+    with pytest.raises(pdm.VolumeError):
+        pdm.load_raw(d, m)
+
+
+def test_raw_round_trip(tmp_path):
+    rng = np.random.default_rng(11)
+    for bits, dt in ((8, np.uint8), (16, np.uint16)):
+        v = pdm.Volume.from_array(rng.integers(0, 1 << bits, (5, 6, 7)).astype(dt), (1, 2, .5))
+        pdm.save_raw(v, tmp_path / "a.raw", tmp_path / "a.json")
+        back = pdm.load_raw(tmp_path / "a.raw", tmp_path / "a.json")
+        assert np.array_equal(back.voxels, v.voxels) and back.spacing == v.spacing
+
+
+# --- schemes / TFs / selection errors ---------------------------------------------------
+
+def test_scheme_uniform_and_min_special():
+    s = pdm.scheme_uniform(3, 2)  # span 4 -> widths 2,1,1
+    assert s.bounds() == [(0, 1), (2, 2), (3, 3)]
+    assert pdm.scheme_uniform(4, 8).bounds()[1] == (64, 127)
+    assert s.pid_lut().tolist() == [0, 0, 1, 2]
+    assert s.partition_of(2) == 2
+    m = pdm.scheme_with_min_special(4, 8, 10)
+    assert m.bounds()[0] == (0, 10) and m.intensity_span == 256
+    with pytest.raises(pdm.SchemeError):
+        pdm.scheme_with_min_special(4, 8, 253)
+    with pytest.raises(pdm.SchemeError):
+        pdm.scheme_uniform(257, 8)
+    with pytest.raises(pdm.SchemeError):
+        pdm.PartitionScheme((pdm.Partition(0, 3), pdm.Partition(5, 7)))
+    with pytest.raises(pdm.SchemeError):
+        pdm.PartitionScheme((pdm.Partition(0, 5),))
+
+
+def test_scheme_matches_oracle_pid_lut():
+    import oracle
+
+    for n in (1, 7, 32, 100):
+        s = pdm.scheme_uniform(n, 16)
+        assert np.array_equal(s.pid_lut(), oracle.pid_lut(s.bounds()))
+
+
+def test_tf_validation_and_archetypes():
+    with pytest.raises(pdm.TransferFunctionError):
+        pdm.TransferFunction(lut=np.zeros((255, 4)))
+    with pytest.raises(pdm.TransferFunctionError):
+        pdm.TransferFunction(lut=np.full((256, 4), 1.5))
+    nan = np.zeros((256, 4))
+    nan[3, 3] = np.nan
+    pdm.TransferFunction(lut=nan)  # NaN passes validation like the reference
+    t3 = pdm.tf_archetype("tf3")
+    assert t3.nonzero_support().tolist() == list(range(128, 256))
+    t4 = pdm.tf_archetype("tf4", bits=4)
+    assert t4.nonzero_support().tolist() == [4, 5, 6, 7, 12, 13, 14, 15]
+    baked = pdm.bake_lut([(0, 0, 0, 0, 0), (255, 1, 1, 1, 1)], bits=8)
+    assert baked.lut[255, 3] == 1.0 and baked.lut[0, 3] == 0.0
+    assert pdm.tf_from_json(pdm.tf_to_json(baked)).lut.tolist() == baked.lut.tolist()
+
+
+def test_selection_errors_raised_before_launch():
+    s = pdm.scheme_uniform(4, 8)
+    with pytest.raises(pdm.SelectionError):
+        pdm.PartitionSelection(selected=frozenset({0}), n=4)
+    with pytest.raises(pdm.SelectionError):
+        pdm.PartitionSelection(selected=frozenset({5}), n=4)
+    tf4bit = pdm.bake_lut([(0, 0, 0, 0, 0), (15, 0, 0, 0, 1)], bits=4)
+    with pytest.raises(pdm.SelectionError):
+        pdm.select_partitions(tf4bit, s)
+
+
+def test_combine_and_mode_errors_raised_before_launch():
+    grid = pdm.BlockGrid.for_dims((8, 8, 8), 4)
+    pset = pdm.PdmSet(grid=grid, scheme=pdm.scheme_uniform(2, 8), pdms=(), occupancy_mode="voxel")
+    with pytest.raises(pdm.SelectionError):
+        pdm.combine(pset, pdm.PartitionSelection(selected=frozenset({1}), n=4))
+    vol = pdm.Volume.from_array(np.zeros((8, 8, 8), dtype=np.uint8))
+    with pytest.raises(pdm.OccupancyModeError):
+        pdm.occupancy_for_partition(vol, grid, pdm.Partition(0, 1), "apron")
+    with pytest.raises(pdm.OccupancyModeError):
+        pdm.build_pdm_set(vol, grid, pdm.scheme_uniform(2, 8), "apron")
+    with pytest.raises(pdm.VolumeError):
+        pdm.build_pdm_set(pdm.Volume.from_array(np.zeros((8, 8, 8), np.uint16)), grid,
+                          pdm.scheme_uniform(4, 8))
+    with pytest.raises(pdm.VolumeError):
+        pdm.occupancy_for_tf(pdm.Volume.from_array(np.zeros((8, 8, 8), np.uint16)), grid,
+                             pdm.tf_archetype("tf2", bits=8))
+    with pytest.raises(pdm.VolumeError):
+        pdm.occupancy_for_tf(vol, pdm.BlockGrid.for_dims((8, 8, 4), 4), pdm.tf_archetype("tf2"))
+
+
+def test_memory_accounting_and_pitch():
+    grid = pdm.BlockGrid.for_dims((16, 16, 16), 4)
+    pset = pdm.PdmSet(grid=grid, scheme=pdm.scheme_uniform(16, 8),
+                      pdms=tuple(pdm.DistanceMap(4, grid.bdims, np.zeros(grid.bdims, np.uint8))
+                                 for _ in range(16)), occupancy_mode="voxel")
+    assert pset.memory_bytes() == 16 * grid.num_blocks
+    assert pset.plane_pitch % 256 == 0 and pset.plane_pitch >= grid.num_blocks
+
+
+def test_host_maps_keep_reference_types():
+    dm = pdm.DistanceMap(b=4, bdims=(2, 2, 2), dist=np.arange(8, dtype=np.uint8).reshape(2, 2, 2))
+    assert dm.dist.dtype == np.uint8 and dm.occupied_fraction == 1 / 8
+    with pytest.raises(ValueError):
+        pdm.DistanceMap(b=4, bdims=(2, 2, 2), dist=np.zeros((2, 2, 2), np.int32))
+    with pytest.raises(ValueError):
+        pdm.OccupancyMap(b=4, bdims=(2, 2, 3), occupied=np.zeros((2, 2, 2), bool))
+    occ = pdm.OccupancyMap(b=4, bdims=(2, 2, 2), occupied=np.eye(2, dtype=bool)[:, :, None]
+                           .repeat(2, axis=2))
+    assert occ.occupied_fraction == 0.5
+
+
+def test_distance_map_dump_format(tmp_path):
+    dm = pdm.DistanceMap(b=4, bdims=(2, 3, 1), dist=np.arange(6, dtype=np.uint8).reshape(2, 3, 1))
+    pdm.save_distance_map(dm, tmp_path / "d.bin")
+    raw = (tmp_path / "d.bin").read_bytes()
+    assert raw[:4] == b"PDMD" and len(raw) == 20 + 6
+    back = pdm.load_distance_map(tmp_path / "d.bin")
+    assert back.b == 4 and back.bdims == (2, 3, 1) and np.array_equal(back.dist, dm.dist)
+    (tmp_path / "junk.bin").write_bytes(b"NOPE" + bytes(64))
+    with pytest.raises(pdm.VolumeError):
+        pdm.load_distance_map(tmp_path / "junk.bin")
+    with pytest.raises(pdm.VolumeError):
+        pdm.load_pdm_set(tmp_path / "junk.bin")
