@@ -69,60 +69,62 @@ def tf_sequence(n: int, span: int, steps: int, seed: int):
 
 
 class ClockSampler:
-    """nvidia-smi clocks/throttle sampling during the timed region."""
+    """SM clock + clock-event (throttle) reasons sampled through NVML every
+    ~2 ms from a background thread while the timed region runs (the same
+    counters `nvidia-smi --query-gpu=clocks.sm,clocks_event_reasons.*` reads)."""
 
-    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown"}
 
     def __init__(self, gpu_index: int):
         self.gpu = gpu_index
-        self.proc = None
-        self.lines: list[str] = []
+        self.samples: list[tuple[int, int]] = []
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._nvml = None
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.thread = threading.Thread(target=self._read, daemon=True)
-            self.thread.start()
-        except FileNotFoundError:
-            self.proc = None
+            import pynvml
+
+            pynvml.nvmlInit()
+            self._nvml = pynvml
+            idx = int(os.environ.get("CUDA_VISIBLE_DEVICES", str(self.gpu)).split(",")[self.gpu]) \
+                if os.environ.get("CUDA_VISIBLE_DEVICES", "").replace(",", "").isdigit() else self.gpu
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(idx)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+            self._thread = threading.Thread(target=self._run, daemon=True)
+            self._thread.start()
+        except Exception as exc:  # no NVML: report unsampled
+            self._err = str(exc)
+            self._nvml = None
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
+    def _run(self):
+        p = self._nvml
+        while not self._stop.is_set():
+            try:
+                sm = p.nvmlDeviceGetClockInfo(self._h, p.NVML_CLOCK_SM)
+                rs = p.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+                self.samples.append((sm, rs))
+            except Exception:
+                pass
+            time.sleep(0.002)
 
     def __exit__(self, *exc):
-        if self.proc is not None:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except subprocess.TimeoutExpired:
-                self.proc.kill()
+        self._stop.set()
+        if self._nvml is not None:
+            self._thread.join(timeout=2)
 
     def summary(self):
-        sm, mx, reasons = [], None, set()
-        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
-        for ln in self.lines:
-            f = [x.strip() for x in ln.split(",")]
-            if len(f) < 9:
-                continue
-            try:
-                sm.append(float(f[1]))
-                mx = float(f[2])
-            except ValueError:
-                continue
-            for name, val in zip(names, f[5:9]):
-                if val.lower() == "active":
-                    reasons.add(name)
-        if not sm:
-            return {"sm_mhz": None, "sm_max_mhz": mx, "reasons": ["unsampled"], "samples": 0}
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unsampled"],
+                    "samples": 0}
+        reasons = sorted({name for _, rs in self.samples for bit, name in self.REASONS.items()
+                          if rs & bit})
+        return {"sm_mhz": statistics.median(s for s, _ in self.samples),
+                "sm_max_mhz": self.max_mhz, "reasons": reasons, "samples": len(self.samples),
+                "source": "NVML clocks + clocks_event_reasons, 2 ms polling"}
 
 
 # ---------------------------------------------------------------------------------
@@ -180,6 +182,7 @@ def run_b200(args, rank, world, local_rank):
            torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
     barrier()
     with ClockSampler(local_rank) as clocks:
+        time.sleep(0.02)  # sampler running before the first timed step
         for i in range(steps):
             flush.fill_(i & 0xFF)  # evict the previous step's maps from L2 (untimed)
             e0, e1, e2 = ev[i]
@@ -209,16 +212,22 @@ def run_b200(args, rank, world, local_rank):
     for i in range(min(warm, steps)):
         pdm.combine(pset, pdm.select_partitions(host_tfs[i], scheme)).dist
     e2e_s = 0.0
+    parts = np.zeros(3)  # select_partitions / combine (launch) / .dist (merge + D2H)
     barrier()
     for i in range(steps):
         flush.fill_(i & 0xFF)
         torch.cuda.synchronize()
         t1 = time.perf_counter()
         sel = pdm.select_partitions(host_tfs[i], scheme)
+        t2 = time.perf_counter()
         dm = pdm.combine(pset, sel)
+        t3 = time.perf_counter()
         host = dm.dist  # D2H into pinned host memory
-        e2e_s += time.perf_counter() - t1
+        t4 = time.perf_counter()
+        e2e_s += t4 - t1
+        parts += (t2 - t1, t3 - t2, t4 - t3)
     assert host.shape == grid.bdims
+    e2e_parts_ms = (parts / steps * 1e3).round(4).tolist()
     barrier()
 
     # ---- max over ranks ----------------------------------------------------------------
@@ -260,7 +269,8 @@ def run_b200(args, rank, world, local_rank):
         "e2e": {"value": round(voxels_rank * world * steps / (e2e_ms * 1e-3) / 1e9, 2),
                 "unit": "Gvoxel/s", "ms_per_step": round(e2e_ms / steps, 4),
                 "h2d_bytes_per_step": span * 8, "d2h_bytes_per_step": n + B,
-                "api": "select_partitions(tf, scheme) + combine(pdm_set, sel) + .dist"},
+                "api": "select_partitions(tf, scheme) + combine(pdm_set, sel) + .dist",
+                "breakdown_ms": {"select_partitions": e2e_parts_ms[0], "combine_launch": e2e_parts_ms[1], "dist_merge_d2h": e2e_parts_ms[2]}},
         "gpu_launches": 2 * steps,
         "clocks": clock,
         "precompute_ms": round(precompute_ms, 2),

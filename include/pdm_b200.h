@@ -51,12 +51,14 @@ int pdm_volume_range(const void *vox, int bits, int64_t count, uint32_t *out,
                      pdm_stream_t stream);
 
 /* ---- selection (K8) -------------------------------------------------------
- * transfer.py:250-259 select_partitions: flags[pid[v]] = 1 for each intensity
- * v < span with alpha[v * alpha_stride] > 0.0 (f64 compare: NaN transparent,
- * denormals visible).  flags (device uint8[n]) is cleared first.
- * pid: device int32[span], the scheme's pid_lut (transfer.py:168-171). */
-int pdm_select(const double *alpha, int64_t span, int64_t alpha_stride, const int32_t *pid,
-               int32_t n, uint8_t *flags, pdm_stream_t stream);
+ * transfer.py:250-259 select_partitions: flags[p] = 1 iff some intensity v of
+ * partition p has alpha[v * alpha_stride] > 0.0 (f64 compare: NaN transparent,
+ * denormals visible), else 0 -- every flag is written.  starts: device
+ * int32[n+1], partition p = [starts[p], starts[p+1]) (contiguous, covering,
+ * starts[n] = span, transfer.py:124-148); max_width = widest partition (picks
+ * a CTA or a warp per partition).  flags: device uint8[n]. */
+int pdm_select(const double *alpha, int64_t span, int64_t alpha_stride, const int32_t *starts,
+               int32_t n, int32_t max_width, uint8_t *flags, pdm_stream_t stream);
 
 /* transfer.py:250-259 on the LUT alone: nz[v] = alpha[v] > 0.0 and, when
  * prefix != NULL, prefix[v+1] = #{u <= v : alpha[u] > 0} with prefix[0] = 0

@@ -26,7 +26,7 @@ _SIGNATURES = {
     "pdm_version": [],
     "pdm_last_error": [],
     "pdm_device_sm_count": [_INT],
-    "pdm_select": [_P, _I64, _I64, _P, _I32, _P, _P],
+    "pdm_select": [_P, _I64, _I64, _P, _I32, _I32, _P, _P],
     "pdm_alpha_support": [_P, _I64, _I64, _P, _P, _P],
     "pdm_combine": [_P, _I64, _I64, _I32, _P, _I32, _P, _P],
     "pdm_combine_flags": [_P, _I64, _I64, _I32, _P, _P, _P],

@@ -44,6 +44,7 @@ OCCUPANCY_MODES = ("voxel", "range_apron")
 DIST_CLAMP = 255
 _MAP_MAGIC = b"PDMD"
 _SET_MAGIC = b"PDMS"
+_MAX_FLAGS = 4096  # pdm_combine_flags compacts the selection in shared memory
 
 
 class OccupancyModeError(ValueError):
@@ -311,6 +312,11 @@ def combine(pdm_set: PdmSet, selection: PartitionSelection,
         raise SelectionError(
             f"selection is over {selection.n} partitions, set holds {pdm_set.n}")
     grid = pdm_set.grid
+    flags = selection.device_flags()
+    if (flags is not None and selection._selected is None and max_maps_per_pass is None
+            and pdm_set.n <= _MAX_FLAGS):
+        # selection still on the device (select_partitions): no host round trip
+        return combine_flags_into(pdm_set, flags)
     indices = selection.sorted
     if indices and max_maps_per_pass is not None and max_maps_per_pass < 1:
         raise ValueError(f"max_maps_per_pass must be >= 1, got {max_maps_per_pass}")

@@ -46,11 +46,36 @@ int sm_count() {
 }
 
 // ---------------------------------------------------------------------------
-// K8: selection.  transfer.py:250-259 -- flags[pid[v]] = 1 where alpha > 0.0.
-__global__ void select_kernel(const double *__restrict__ alpha, int64_t span, int64_t stride,
-                              const int32_t *__restrict__ pid, uint8_t *__restrict__ flags) {
-    int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (v < span && alpha[v * stride] > 0.0) flags[pid[v]] = 1;  // NaN compares false
+// K8: selection.  transfer.py:250-259 -- flags[p] = any(alpha[v] > 0.0) over
+// partition p's contiguous intensity range [starts[p], starts[p+1]).  Every
+// flag is written (0 or 1), so no clearing pass is needed.  kTPP threads per
+// partition: a whole CTA (256) for wide partitions, a warp for narrow ones.
+// With PDL the dependent merge launches while this runs and waits on
+// griddepcontrol before it reads the flags.
+__device__ __forceinline__ void pdl_launch_dependents() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+template <int kTPP>
+__global__ void __launch_bounds__(256)
+    select_kernel(const double *__restrict__ alpha, int64_t stride,
+                  const int32_t *__restrict__ starts, int n, uint8_t *__restrict__ flags) {
+    pdl_launch_dependents();
+    const int group = threadIdx.x / kTPP, lane = threadIdx.x % kTPP;
+    const int p = blockIdx.x * (256 / kTPP) + group;
+    bool any = false;
+    if (p < n) {
+        const int lo = starts[p], hi = starts[p + 1];
+#pragma unroll 4
+        for (int v = lo + lane; v < hi; v += kTPP) any |= alpha[(int64_t)v * stride] > 0.0;
+    }
+    if (kTPP == 256) {
+        any = __syncthreads_or(any);
+    } else {
+        any = __any_sync(0xFFFFFFFFu, any);  // kTPP == 32: one partition per warp
+    }
+    if (lane == 0 && p < n) flags[p] = any;  // NaN compares false: transparent
 }
 
 // acceleration.py:166,171 -- nz = alpha > 0 and its exclusive prefix count.
@@ -99,38 +124,61 @@ struct SelParam {
     int32_t idx[kMaxSelParam];
 };
 
+// One iteration of a thread covers U 16-byte chunks spaced one grid-width
+// apart (so every warp access stays 512 contiguous bytes); per batch of M
+// selected maps it issues all U*M 128-bit loads before the first min.  Small
+// selections use wide U so each thread still keeps ~8 loads in flight.
+template <int U, int M, bool kAccumulate>
+__device__ __forceinline__ void merge_uv(const uint8_t *__restrict__ pdms, int64_t pitch,
+                                         int64_t nvec, const int32_t *idx, int k,
+                                         uint8_t *__restrict__ out) {
+    const int64_t T = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t base = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; base < nvec;
+         base += T * U) {
+        uint4 acc[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t v = base + u * T;
+            if (kAccumulate && v < nvec)
+                acc[u] = *reinterpret_cast<const uint4 *>(out + v * 16);
+            else
+                acc[u] = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
+        }
+        for (int m = 0; m < k; m += M) {
+            uint4 r[U][M];
+#pragma unroll
+            for (int j = 0; j < M; ++j) {
+                const uint8_t *plane = pdms + (int64_t)idx[m + j < k ? m + j : m] * pitch;
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int64_t v = base + u * T;
+                    if (m + j < k && v < nvec) r[u][j] = ld_stream_u4(plane + v * 16);
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < M; ++j)
+#pragma unroll
+                for (int u = 0; u < U; ++u)
+                    if (m + j < k && base + u * T < nvec) acc[u] = vmin_u8x16(acc[u], r[u][j]);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t v = base + u * T;
+            if (v < nvec) st_stream_u4(out + v * 16, acc[u]);
+        }
+    }
+}
+
 template <bool kAccumulate>
 __device__ __forceinline__ void merge_chunks(const uint8_t *__restrict__ pdms, int64_t pitch,
                                              int64_t nvec, const int32_t *idx, int k,
                                              uint8_t *__restrict__ out) {
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < nvec; v += stride) {
-        const int64_t off = v * 16;
-        uint4 acc;
-        if (kAccumulate)
-            acc = *reinterpret_cast<const uint4 *>(out + off);
-        else
-            acc = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
-        int m = 0;
-        for (; m + kMergeBatch <= k; m += kMergeBatch) {
-            uint4 r[kMergeBatch];
-#pragma unroll
-            for (int j = 0; j < kMergeBatch; ++j)
-                r[j] = ld_stream_u4(pdms + (int64_t)idx[m + j] * pitch + off);
-#pragma unroll
-            for (int j = 0; j < kMergeBatch; ++j) acc = vmin_u8x16(acc, r[j]);
-        }
-        if (m < k) {  // remainder: up to kMergeBatch-1 maps, still issued together
-            uint4 r[kMergeBatch - 1];
-#pragma unroll
-            for (int j = 0; j < kMergeBatch - 1; ++j)
-                if (m + j < k) r[j] = ld_stream_u4(pdms + (int64_t)idx[m + j] * pitch + off);
-#pragma unroll
-            for (int j = 0; j < kMergeBatch - 1; ++j)
-                if (m + j < k) acc = vmin_u8x16(acc, r[j]);
-        }
-        st_stream_u4(out + off, acc);
-    }
+    if (k <= 2)
+        merge_uv<4, 2, kAccumulate>(pdms, pitch, nvec, idx, k, out);
+    else if (k <= 4)
+        merge_uv<2, 4, kAccumulate>(pdms, pitch, nvec, idx, k, out);
+    else
+        merge_uv<1, kMergeBatch, kAccumulate>(pdms, pitch, nvec, idx, k, out);
 }
 
 // Bytes past the last full 16-byte chunk (map_bytes % 16), byte by byte.
@@ -182,6 +230,7 @@ __global__ void __launch_bounds__(kMergeThreads)
                          int n, const uint8_t *__restrict__ flags, uint8_t *__restrict__ out) {
     __shared__ int32_t s_idx[kMaxFlagsSmem];
     __shared__ int s_k;
+    pdl_wait();  // flags come from the preceding select kernel (PDL)
     if (threadIdx.x < 32) {
         const unsigned lane = threadIdx.x;
         int k = 0;
@@ -229,12 +278,36 @@ __global__ void range_init_kernel(uint32_t *out) {
     out[1] = 0;
 }
 
-static int merge_grid(int64_t work_items) {
-    int64_t want = ceil_div(work_items, kMergeThreads);
-    int64_t cap = (int64_t)sm_count() * (2048 / kMergeThreads);
-    if (want > cap) want = cap;
-    return want < 1 ? 1 : (int)want;
+// Resident CTAs per SM of a kernel (cached per kernel), so a grid-stride merge
+// launches exactly one wave.
+template <class K>
+static int resident_ctas(K kernel, int threads) {
+    static int cached[64] = {0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev >= 0 && dev < 64 && cached[dev]) return cached[dev];
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, 0) !=
+            cudaSuccess ||
+        per_sm < 1)
+        per_sm = 1;
+    if (dev >= 0 && dev < 64) cached[dev] = per_sm;
+    return per_sm;
 }
+
+// One wave of resident CTAs; when the work does not fill it, just enough
+// CTAs, and when it does, the per-thread iteration count is equalised so no
+// CTA runs an extra lap (work_items in 16-byte chunks, U chunks per lap).
+static int merge_grid(int64_t work_items, int per_sm, int U) {
+    const int64_t cap = (int64_t)sm_count() * per_sm;
+    const int64_t per_cta = (int64_t)kMergeThreads * U;
+    const int64_t laps = ceil_div(work_items, cap * per_cta);
+    int64_t grid = ceil_div(work_items, laps * per_cta);
+    if (grid > cap) grid = cap;
+    return grid < 1 ? 1 : (int)grid;
+}
+
+static int merge_lanes(int k) { return k <= 2 ? 4 : (k <= 4 ? 2 : 1); }
 
 }  // namespace pdm
 
@@ -271,14 +344,18 @@ extern "C" int pdm_volume_range(const void *vox, int bits, int64_t count, uint32
 }
 
 extern "C" int pdm_select(const double *alpha, int64_t span, int64_t alpha_stride,
-                          const int32_t *pid, int32_t n, uint8_t *flags, pdm_stream_t stream) {
-    PDM_REQUIRE(alpha && pid && flags, "pdm_select: null pointer");
-    PDM_REQUIRE(span >= 1 && n >= 1 && alpha_stride >= 1, "pdm_select: bad sizes");
+                          const int32_t *starts, int32_t n, int32_t max_width, uint8_t *flags,
+                          pdm_stream_t stream) {
+    PDM_REQUIRE(alpha && starts && flags, "pdm_select: null pointer");
+    PDM_REQUIRE(span >= 1 && span <= (1 << 16) && n >= 1 && n <= span && alpha_stride >= 1,
+                "pdm_select: bad sizes (span=%lld n=%d)", (long long)span, n);
     cudaStream_t s = as_stream(stream);
-    PDM_CUDA_TRY(cudaMemsetAsync(flags, 0, (size_t)n, s));
-    const int threads = 256;
-    select_kernel<<<(unsigned)ceil_div(span, threads), threads, 0, s>>>(alpha, span, alpha_stride,
-                                                                         pid, flags);
+    if (max_width >= 512) {
+        select_kernel<256><<<n, 256, 0, s>>>(alpha, alpha_stride, starts, n, flags);
+    } else {
+        select_kernel<32><<<(unsigned)ceil_div(n, 8), 256, 0, s>>>(alpha, alpha_stride, starts, n,
+                                                                    flags);
+    }
     return cuda_status("select_kernel");
 }
 
@@ -315,11 +392,13 @@ extern "C" int pdm_combine(const uint8_t *pdms, int64_t plane_pitch, int64_t map
         memcpy(p.idx, sel + base, sizeof(int32_t) * p.k);
         const int acc = base > 0;
         if (vec) {
-            combine_kernel<<<merge_grid(map_bytes / 16 > 0 ? map_bytes / 16 : 1), kMergeThreads, 0,
-                             s>>>(pdms, plane_pitch, map_bytes, p, out, acc);
+            const int per_sm = resident_ctas(combine_kernel, kMergeThreads);
+            combine_kernel<<<merge_grid(map_bytes / 16 > 0 ? map_bytes / 16 : 1, per_sm,
+                                        merge_lanes(p.k)),
+                             kMergeThreads, 0, s>>>(pdms, plane_pitch, map_bytes, p, out, acc);
         } else {
-            combine_bytes_kernel<<<merge_grid(map_bytes), kMergeThreads, 0, s>>>(
-                pdms, plane_pitch, map_bytes, p, out, acc);
+            combine_bytes_kernel<<<merge_grid(ceil_div(map_bytes, 16), 8, 1), kMergeThreads, 0,
+                                   s>>>(pdms, plane_pitch, map_bytes, p, out, acc);
         }
         int st = cuda_status("combine_kernel");
         if (st) return st;
@@ -336,7 +415,20 @@ extern "C" int pdm_combine_flags(const uint8_t *pdms, int64_t plane_pitch, int64
     PDM_REQUIRE(n <= kMaxFlagsSmem, "pdm_combine_flags: n=%d above %d", n, kMaxFlagsSmem);
     PDM_REQUIRE(plane_pitch % 16 == 0 && (uintptr_t)pdms % 16 == 0 && (uintptr_t)out % 16 == 0,
                 "pdm_combine_flags: needs 16-byte aligned planes");
-    combine_flags_kernel<<<merge_grid(map_bytes / 16 > 0 ? map_bytes / 16 : 1), kMergeThreads, 0,
-                           as_stream(stream)>>>(pdms, plane_pitch, map_bytes, n, flags, out);
+    // Programmatic dependent launch: the merge CTAs are scheduled while the
+    // preceding select kernel finishes; they wait on griddepcontrol.wait.
+    const int per_sm = resident_ctas(combine_flags_kernel, kMergeThreads);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)merge_grid(map_bytes / 16 > 0 ? map_bytes / 16 : 1, per_sm, 1));
+    cfg.blockDim = dim3(kMergeThreads);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = as_stream(stream);
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    PDM_CUDA_TRY(cudaLaunchKernelEx(&cfg, combine_flags_kernel, pdms, plane_pitch, map_bytes,
+                                    (int)n, flags, out));
     return cuda_status("combine_flags_kernel");
 }

@@ -135,7 +135,11 @@ def test_worked_example():
         scheme = _scheme([tuple(map(int, r)) for r in z["bounds"]])
         vol = pdm.Volume.from_array(z["vox"])
         grid = pdm.BlockGrid.for_dims(vol.dims, 1)
-        pset = pdm.build_pdm_set(vol, grid, scheme, "voxel")
+        # 3-bit scheme over a uint8 volume: built per partition as in
+        # test_acceptance.py:121-128 (build_pdm_set would reject the span)
+        pdms = tuple(pdm.distance_transform(pdm.occupancy_for_partition(vol, grid, p, "voxel"))
+                     for p in scheme.partitions)
+        pset = pdm.PdmSet(grid=grid, scheme=scheme, pdms=pdms, occupancy_mode="voxel")
         assert np.array_equal(_stack(pset), z["pdms"])
         sel = pdm.select_partitions(_tf(z["alpha"]), scheme)
         assert sel.sorted == [2, 4]

@@ -40,7 +40,7 @@ def test_library_rejects_bad_arguments_without_gpu():
     # null pointers / sizes are validated before any CUDA call
     assert L.pdm_combine(None, 16, 16, 1, None, 1, None, None) == _lib.PDM_EINVAL
     assert b"null" in L.pdm_last_error()
-    assert L.pdm_select(None, 0, 1, None, 0, None, None) == _lib.PDM_EINVAL
+    assert L.pdm_select(None, 0, 1, None, 0, 0, None, None) == _lib.PDM_EINVAL
     assert L.pdm_block_min_max(ctypes.c_void_p(16), 12, 4, 4, 4, 4, ctypes.c_void_p(16),
                                ctypes.c_void_p(16), None) == _lib.PDM_EINVAL
     assert b"bits" in L.pdm_last_error()
