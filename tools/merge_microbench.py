@@ -28,6 +28,8 @@ def main():
     ap.add_argument("--blocks", type=int, default=256 ** 3)
     ap.add_argument("--n", type=int, default=32)
     ap.add_argument("--reps", type=int, default=20)
+    ap.add_argument("--ks", type=int, nargs="+", default=[1, 2, 4, 8, 16, 24, 32])
+    ap.add_argument("--no-host", action="store_true", help="skip the D' to host section")
     args = ap.parse_args()
     L = _lib.lib()
     nb, n = args.blocks, args.n
@@ -37,7 +39,7 @@ def main():
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     st = _lib.stream_handle()
     res = {}
-    for k in (1, 2, 4, 8, 16, 24, 32):
+    for k in args.ks:
         if k > n:
             break
         sel = np.ascontiguousarray(np.arange(k), dtype=np.int32)
@@ -57,7 +59,45 @@ def main():
         res[k] = {"ms": round(ms, 5), "GB/s": round(gbs, 1)}
         want = pdms[:k, :nb].min(dim=0).values
         assert torch.equal(out, want)
-    print(json.dumps({"blocks": nb, "n": n, "merge": res}))
+    # floor for the same bytes as k=1: a plain device copy of one map
+    ts = []
+    for r in range(args.reps + 3):
+        flush.fill_(r & 0xFF)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        out.copy_(pdms[1, :nb])
+        e1.record()
+        torch.cuda.synchronize()
+        if r >= 3:
+            ts.append(e0.elapsed_time(e1))
+    ms = float(np.median(ts))
+    res["torch_copy_1map"] = {"ms": round(ms, 5), "GB/s": round(2 * nb / (ms * 1e-3) / 1e9, 1)}
+    # D' to host: merge into HBM + D2H copy, vs the merge writing pinned host
+    # memory directly (zero-copy over PCIe)
+    to_host = {}
+    host = torch.empty(nb, dtype=torch.uint8, pin_memory=True)
+    for k in (() if args.no_host else (1, 16, 32)):
+        sel = np.ascontiguousarray(np.arange(k), dtype=np.int32)
+        for mode in ("hbm+d2h", "zero-copy"):
+            ts = []
+            for r in range(8):
+                flush.fill_(r & 0xFF)
+                torch.cuda.synchronize()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                dst = out if mode == "hbm+d2h" else host
+                _lib.check(L.pdm_combine(_lib.ptr(pdms), pitch, nb, n, sel.ctypes.data, k,
+                                         _lib.ptr(dst), st), "pdm_combine")
+                if mode == "hbm+d2h":
+                    host.copy_(out, non_blocking=True)
+                e1.record()
+                torch.cuda.synchronize()
+                if r >= 3:
+                    ts.append(e0.elapsed_time(e1))
+            ms = float(np.median(ts))
+            to_host[f"{mode} k={k}"] = {"ms": round(ms, 4), "PCIe GB/s": round(nb / ms / 1e6, 1)}
+            assert torch.equal(host.cuda(), pdms[:k, :nb].min(dim=0).values)
+    print(json.dumps({"blocks": nb, "n": n, "merge": res, "to_host": to_host}))
 
 
 if __name__ == "__main__":
