@@ -1,10 +1,11 @@
 // dt.cu -- exact clamped Chebyshev distance transform of block occupancy (K6).
 //
 // Replaces _kernels.py:17-81 chamfer_chebyshev (two sequential raster passes
-// over the 26-neighbourhood) + the clamp of acceleration.py:180 with three
-// separable, embarrassingly parallel passes over the partition-major map set
+// over the 26-neighbourhood) + the clamp of acceleration.py:180 with separable,
+// embarrassingly parallel passes over the partition-major map set
 // pdms[p][x][y][z] (z contiguous), all in place:
 //
+//   expand:  g0 = 0 where partition p occupies the block, else 255
 //   pass x:  g1[x] = 1-D distance along x to the nearest occupied block
 //            (forward + backward run-length sweeps, clamped at 255);
 //   pass y:  g2[y] = min_j max(|y - j|, g1[j])     (lower envelope)
@@ -12,22 +13,26 @@
 //
 // min(C, max(a, b)) = max(min(C, a), min(C, b)) makes uint8-clamped
 // intermediates exact, and the chessboard metric is the max of the per-axis
-// distances, so g3 == min(255, chamfer_chebyshev) cell for cell (verified
-// against the reference in tests/test_gpu_parity.py and the golden vectors).
+// distances, so g3 == min(255, chamfer_chebyshev) cell for cell (pinned
+// against the reference's golden vectors and the C oracle in tests/).
 //
 // The lower-envelope passes use Meijster et al.'s linear-time scan with the
-// L-infinity separator (one thread per line, stack in local memory):
+// L-infinity separator (one lane per line, stack in local memory):
 //   f(x, i)  = max(|x - i|, g(i))
 //   Sep(i,u) = g(i) <= g(u) ? max(i + g(u), (i + u) / 2) : min(u - g(i), (i + u) / 2)
-// Pass x and pass y read lines whose elements are bz bytes apart; consecutive
-// threads take consecutive z so every step is a coalesced warp access.  Pass z
-// runs along the contiguous axis, so a CTA stages a tile of rows in shared
-// memory (coalesced in, Meijster from shared memory, coalesced out).
+// Every pass works on warp tiles of 32 lines staged in shared memory: the
+// warp loads the tile with coalesced 32-bit accesses, each lane runs its line
+// from shared memory (the per-element dependency chain sees shared-memory
+// latency, not DRAM latency), and the warp writes the tile back.  Lines along
+// x and y are strided in memory (a tile is 32 consecutive z of one line
+// family); lines along z are contiguous rows (a tile is 32 consecutive rows).
 #include <cuda_runtime.h>
 
 #include "pdm_common.cuh"
 
 namespace pdm {
+
+// ---- per-line operations -----------------------------------------------------------
 
 // Stack entry: s (12 bits) | t (12 bits) << 12 | g(s) (8 bits) << 24.
 __device__ __forceinline__ uint32_t pack_entry(int s, int t, int g) {
@@ -39,135 +44,246 @@ __device__ __forceinline__ int ent_g(uint32_t e) { return (int)(e >> 24); }
 
 // Meijster lower envelope of one line of m <= LMAX values (LMAX <= 4096):
 // out[u] = min(255, min_i max(|u - i|, g[i])).  Ld/St access element u.
+// The top of the envelope stack lives in a register (`top`); only entries
+// below it are in the local-memory array, so an element that neither pops nor
+// pushes touches no memory but its own input, and the next input is loaded
+// one element ahead.
 template <int LMAX, class Ld, class St>
 __device__ __forceinline__ void cone_line(int m, Ld ld, St st) {
     uint32_t stk[LMAX];
-    int q = 0;
-    stk[0] = pack_entry(0, 0, ld(0));
+    int q = 0;  // entries stored below the top
+    uint32_t top = pack_entry(0, 0, ld(0));
+    int gnext = m > 1 ? ld(1) : 0;
     for (int u = 1; u < m; ++u) {
-        const int gu = ld(u);
-        while (q >= 0) {
-            const uint32_t e = stk[q];
-            const int t = ent_t(e), s = ent_s(e);
-            const int fs = max(abs(t - s), ent_g(e));
+        const int gu = gnext;
+        if (u + 1 < m) gnext = ld(u + 1);
+        bool empty = false;
+        for (;;) {  // pop while the top's cone is above u's at the top's threshold
+            const int t = ent_t(top);
+            const int fs = max(abs(t - ent_s(top)), ent_g(top));
             const int fu = max(abs(t - u), gu);
-            if (fs > fu)
-                --q;
-            else
+            if (fs <= fu) break;
+            if (q == 0) {
+                empty = true;
                 break;
+            }
+            top = stk[--q];
         }
-        if (q < 0) {
-            q = 0;
-            stk[0] = pack_entry(u, 0, gu);
+        if (empty) {
+            top = pack_entry(u, 0, gu);
         } else {
-            const uint32_t e = stk[q];
-            const int s = ent_s(e), gs = ent_g(e);
+            const int s = ent_s(top), gs = ent_g(top);
             const int mid = (s + u) >> 1;
             const int sep = gs <= gu ? max(s + gu, mid) : min(u - gs, mid);
             const int w = 1 + sep;
             if (w < m) {
-                ++q;
-                stk[q] = pack_entry(u, w, gu);
+                stk[q++] = top;
+                top = pack_entry(u, w, gu);
             }
         }
     }
     for (int u = m - 1; u >= 0; --u) {
-        const uint32_t e = stk[q];
-        const int d = max(abs(u - ent_s(e)), ent_g(e));
+        const int d = max(abs(u - ent_s(top)), ent_g(top));
         st(u, d < kDistClamp ? d : kDistClamp);
-        if (u == ent_t(e)) --q;
+        if (u == ent_t(top) && q > 0) top = stk[--q];
     }
 }
 
-// ---- pass x -----------------------------------------------------------------------
-// Source of occupancy: a mask (bit p of words) or a plain uint8 map (n == 1).
+// 1-D distance of a {0 = occupied, else not} line: forward then backward
+// run-length sweep, clamped at 255.
+template <class Ld, class St>
+__device__ __forceinline__ void dist1d_line(int m, Ld ld, St st) {
+    int run = kDistClamp;
+    for (int u = 0; u < m; ++u) {
+        run = ld(u) == 0 ? 0 : min(run + 1, kDistClamp);
+        st(u, run);
+    }
+    run = kDistClamp;
+    for (int u = m - 1; u >= 0; --u) {
+        const int fwd = ld(u);
+        run = fwd == 0 ? 0 : min(run + 1, kDistClamp);
+        st(u, min(fwd, run));
+    }
+}
+
+// ---- expand: partition occupancy -> {0, 255} planes ---------------------------------
+// Thread = 16 consecutive blocks: it reads their mask words once and writes a
+// 16-byte vector to every partition plane (coalesced 512 B per warp store).
 struct MaskSrc {
     const uint32_t *mask;
     int words;
-    __device__ __forceinline__ bool occ(int64_t c, int p) const {
-        return (mask[c * words + (p >> 5)] >> (p & 31)) & 1u;
-    }
-};
-struct OccSrc {
-    const uint8_t *occ8;
-    __device__ __forceinline__ bool occ(int64_t c, int) const { return occ8[c] != 0; }
 };
 
-// Thread = (p, y, z); sweeps x forward then backward.  Writes pdms[p][x][y][z].
-template <class Src>
-__global__ void dt_pass_x_kernel(Src src, int n, int64_t bx, int64_t by, int64_t bz,
-                                 uint8_t *__restrict__ pdms, int64_t pitch) {
-    const int64_t plane = by * bz;
-    const int64_t lines = (int64_t)n * plane;
+__global__ void __launch_bounds__(256)
+    dt_expand_mask_kernel(MaskSrc src, int n, int64_t nb, uint8_t *__restrict__ pdms,
+                          int64_t pitch) {
+    const int64_t nchunks = ceil_div(nb, 16);
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; l < lines; l += stride) {
-        const int p = (int)(l / plane);
-        const int64_t yz = l % plane;
-        uint8_t *dst = pdms + (int64_t)p * pitch + yz;
-        int run = kDistClamp;
-        for (int64_t x = 0; x < bx; ++x) {
-            run = src.occ(x * plane + yz, p) ? 0 : min(run + 1, kDistClamp);
-            dst[x * plane] = (uint8_t)run;
-        }
-        run = kDistClamp;
-        for (int64_t x = bx - 1; x >= 0; --x) {
-            run = src.occ(x * plane + yz, p) ? 0 : min(run + 1, kDistClamp);
-            const int fwd = dst[x * plane];
-            dst[x * plane] = (uint8_t)min(fwd, run);
+    for (int64_t ch = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; ch < nchunks; ch += stride) {
+        const int64_t c0 = ch * 16;
+        const int cnt = (int)min((int64_t)16, nb - c0);
+        for (int w = 0; w < src.words; ++w) {
+            uint32_t m[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) m[i] = i < cnt ? src.mask[(c0 + i) * src.words + w] : 0u;
+            const int pend = min(32, n - w * 32);
+            for (int pp = 0; pp < pend; ++pp) {
+                uint32_t q[4];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    uint32_t v = 0;
+#pragma unroll
+                    for (int b = 0; b < 4; ++b)
+                        v |= (((m[4 * k + b] >> pp) & 1u) ? 0u : 0xFFu) << (8 * b);
+                    q[k] = v;
+                }
+                uint8_t *dst = pdms + (int64_t)(w * 32 + pp) * pitch + c0;
+                if (cnt == 16) {
+                    *reinterpret_cast<uint4 *>(dst) = make_uint4(q[0], q[1], q[2], q[3]);
+                } else {
+                    for (int i = 0; i < cnt; ++i) dst[i] = (uint8_t)(q[i >> 2] >> (8 * (i & 3)));
+                }
+            }
         }
     }
 }
 
-// ---- pass y: strided lines ---------------------------------------------------------
-// Line = (p, x, z): elements pdms[p][x][u][z], u in [0, by).
-template <int LMAX>
-__global__ void __launch_bounds__(128) dt_cone_y_kernel(int n, int64_t bx, int64_t by, int64_t bz,
-                                                        uint8_t *__restrict__ pdms,
-                                                        int64_t pitch) {
-    const int64_t lines = (int64_t)n * bx * bz;
+// Single map from a uint8 occupancy: byte == 0 -> 255, nonzero -> 0.
+__global__ void __launch_bounds__(256)
+    dt_expand_occ_kernel(const uint8_t *__restrict__ occ, int64_t nb, uint8_t *__restrict__ out) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; l < lines; l += stride) {
-        const int64_t z = l % bz;
-        const int64_t px = l / bz;
-        const int64_t x = px % bx;
-        const int p = (int)(px / bx);
-        uint8_t *base = pdms + (int64_t)p * pitch + x * by * bz + z;
-        cone_line<LMAX>(
-            (int)by, [&](int u) -> int { return base[(int64_t)u * bz]; },
-            [&](int u, int v) { base[(int64_t)u * bz] = (uint8_t)v; });
+    for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < nb; c += stride)
+        out[c] = occ[c] ? 0 : 255;
+}
+
+// ---- warp-tile passes ----------------------------------------------------------------
+enum { kAxisX = 0, kAxisY = 1, kAxisZ = 2 };
+
+template <int LMAX, int AXIS, bool kDist1D>
+__global__ void __launch_bounds__(128)
+    dt_tile_kernel(int n, int64_t bx, int64_t by, int64_t bz, uint8_t *__restrict__ pdms,
+                   int64_t pitch, int sstride, int64_t tiles) {
+    extern __shared__ __align__(16) uint8_t s_tiles[];
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    const int wpc = blockDim.x >> 5;
+    constexpr bool kRows = AXIS == kAxisZ;  // contiguous lines
+    const int L = (int)(AXIS == kAxisX ? bx : (AXIS == kAxisY ? by : bz));
+    const int64_t S = AXIS == kAxisX ? by * bz : bz;  // element stride of strided lines
+    uint8_t *s = s_tiles + (size_t)warp * (kRows ? 32 * (size_t)sstride : 32 * (size_t)L);
+    const int64_t zblocks = ceil_div(bz, 32);
+    const bool vec = (bz & 3) == 0;
+    for (int64_t t = (int64_t)blockIdx.x * wpc + warp; t < tiles; t += (int64_t)gridDim.x * wpc) {
+        uint8_t *g;
+        int nlines;
+        if (kRows) {  // tile = 32 consecutive (x, y) rows of partition p
+            const int64_t rows = bx * by, per_p = ceil_div(rows, 32);
+            const int p = (int)(t / per_p);
+            const int64_t r0 = (t % per_p) * 32;
+            nlines = (int)min((int64_t)32, rows - r0);
+            g = pdms + (int64_t)p * pitch + r0 * bz;
+            if (vec) {
+                const int words = L >> 2;
+                for (int i = lane; i < nlines * words; i += 32) {
+                    const int r = i / words, w = i - r * words;
+                    *reinterpret_cast<uint32_t *>(s + r * sstride + 4 * w) =
+                        *reinterpret_cast<const uint32_t *>(g + (int64_t)r * bz + 4 * w);
+                }
+            } else {
+                for (int i = lane; i < nlines * L; i += 32) {
+                    const int r = i / L, u = i - r * L;
+                    s[r * sstride + u] = g[(int64_t)r * bz + u];
+                }
+            }
+        } else {  // tile = 32 consecutive z of one line family (p, outer)
+            const int64_t outer_n = AXIS == kAxisX ? by : bx;
+            const int64_t po = t / zblocks;
+            const int64_t z0 = (t % zblocks) * 32;
+            const int p = (int)(po / outer_n);
+            const int64_t o = po % outer_n;
+            nlines = (int)min((int64_t)32, bz - z0);
+            g = pdms + (int64_t)p * pitch + (AXIS == kAxisX ? o * bz : o * by * bz) + z0;
+            if (nlines == 32 && vec) {  // 8 lanes per 32-byte row, 4 rows per access
+                for (int i = lane; i < L * 8; i += 32) {
+                    const int u = i >> 3, w = i & 7;
+                    *reinterpret_cast<uint32_t *>(s + u * 32 + 4 * w) =
+                        *reinterpret_cast<const uint32_t *>(g + (int64_t)u * S + 4 * w);
+                }
+            } else {
+                for (int u = 0; u < L; ++u)
+                    if (lane < nlines) s[u * 32 + lane] = g[(int64_t)u * S + lane];
+            }
+        }
+        __syncwarp();
+        if (lane < nlines) {
+            uint8_t *line = kRows ? s + lane * sstride : s + lane;
+            const int es = kRows ? 1 : 32;
+            auto ld = [&](int u) -> int { return line[u * es]; };
+            auto st = [&](int u, int v) { line[u * es] = (uint8_t)v; };
+            if (kDist1D)
+                dist1d_line(L, ld, st);
+            else
+                cone_line<LMAX>(L, ld, st);
+        }
+        __syncwarp();
+        if (kRows) {
+            if (vec) {
+                const int words = L >> 2;
+                for (int i = lane; i < nlines * words; i += 32) {
+                    const int r = i / words, w = i - r * words;
+                    *reinterpret_cast<uint32_t *>(g + (int64_t)r * bz + 4 * w) =
+                        *reinterpret_cast<const uint32_t *>(s + r * sstride + 4 * w);
+                }
+            } else {
+                for (int i = lane; i < nlines * L; i += 32) {
+                    const int r = i / L, u = i - r * L;
+                    g[(int64_t)r * bz + u] = s[r * sstride + u];
+                }
+            }
+        } else {
+            if (nlines == 32 && vec) {
+                for (int i = lane; i < L * 8; i += 32) {
+                    const int u = i >> 3, w = i & 7;
+                    *reinterpret_cast<uint32_t *>(g + (int64_t)u * S + 4 * w) =
+                        *reinterpret_cast<const uint32_t *>(s + u * 32 + 4 * w);
+                }
+            } else {
+                for (int u = 0; u < L; ++u)
+                    if (lane < nlines) g[(int64_t)u * S + lane] = s[u * 32 + lane];
+            }
+        }
+        __syncwarp();
     }
 }
 
-// ---- pass z: contiguous rows through shared memory --------------------------------
-// Row = (p, x, y): pdms[p][x][y][0..bz).  A CTA of R threads owns R consecutive
-// rows of one partition; row stride in shared memory is an odd number of
-// 32-bit words so the R threads reading element u hit distinct banks.
-template <int LMAX>
-__global__ void __launch_bounds__(64) dt_cone_z_kernel(int n, int64_t rows_per_p, int64_t bz,
-                                                       uint8_t *__restrict__ pdms, int64_t pitch,
-                                                       int sstride) {
-    extern __shared__ uint8_t s_tile[];
-    const int R = blockDim.x;
-    const int64_t tiles_per_p = ceil_div(rows_per_p, R);
-    const int64_t tiles = tiles_per_p * n;
-    for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
-        const int p = (int)(tile / tiles_per_p);
-        const int64_t r0 = (tile % tiles_per_p) * R;
-        const int rows = (int)min((int64_t)R, rows_per_p - r0);
-        uint8_t *g = pdms + (int64_t)p * pitch + r0 * bz;
-        __syncthreads();
-        for (int r = 0; r < rows; ++r)
-            for (int64_t z = threadIdx.x; z < bz; z += R) s_tile[r * sstride + z] = g[r * bz + z];
-        __syncthreads();
-        if ((int)threadIdx.x < rows) {
-            uint8_t *row = s_tile + threadIdx.x * sstride;
-            cone_line<LMAX>(
-                (int)bz, [&](int u) -> int { return row[u]; },
-                [&](int u, int v) { row[u] = (uint8_t)v; });
-        }
-        __syncthreads();
-        for (int r = 0; r < rows; ++r)
-            for (int64_t z = threadIdx.x; z < bz; z += R) g[r * bz + z] = s_tile[r * sstride + z];
+// Lines longer than 1024 blocks: one thread per line straight from global
+// memory (correct for any length up to 4095, slower).
+template <int AXIS, bool kDist1D>
+__global__ void __launch_bounds__(128)
+    dt_line_kernel(int n, int64_t bx, int64_t by, int64_t bz, uint8_t *__restrict__ pdms,
+                   int64_t pitch) {
+    const int L = (int)(AXIS == kAxisX ? bx : (AXIS == kAxisY ? by : bz));
+    const int64_t S = AXIS == kAxisX ? by * bz : (AXIS == kAxisY ? bz : 1);
+    const int64_t per_p = bx * by * bz / L;
+    const int64_t lines = (int64_t)n * per_p;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; l < lines; l += stride) {
+        const int p = (int)(l / per_p);
+        const int64_t r = l % per_p;
+        int64_t base;
+        if (AXIS == kAxisX)
+            base = r;  // r = y * bz + z
+        else if (AXIS == kAxisY)
+            base = (r / bz) * by * bz + (r % bz);  // r = x * bz + z
+        else
+            base = r * bz;  // r = x * by + y
+        uint8_t *line = pdms + (int64_t)p * pitch + base;
+        auto ld = [&](int u) -> int { return line[(int64_t)u * S]; };
+        auto st = [&](int u, int v) { line[(int64_t)u * S] = (uint8_t)v; };
+        if (kDist1D)
+            dist1d_line(L, ld, st);
+        else
+            cone_line<4096>(L, ld, st);
     }
 }
 
@@ -221,78 +337,78 @@ __global__ void slab_fold_kernel(uint8_t *__restrict__ pdms, int64_t pitch, int 
     }
 }
 
-static int grid_lines(int64_t lines, int threads, int per_sm) {
-    int64_t want = ceil_div(lines, threads);
+// ---- host launchers ---------------------------------------------------------------------
+
+static int grid_for(int64_t items, int threads, int per_sm) {
+    int64_t want = ceil_div(items, threads);
     int64_t cap = (int64_t)sm_count() * per_sm;
     if (want > cap) want = cap;
     return want < 1 ? 1 : (int)want;
 }
 
-template <class Src>
-static int pass_x(Src src, int n, int64_t bx, int64_t by, int64_t bz, uint8_t *pdms,
-                  int64_t pitch, cudaStream_t s) {
-    const int64_t lines = (int64_t)n * by * bz;
-    dt_pass_x_kernel<Src><<<grid_lines(lines, 256, 8), 256, 0, s>>>(src, n, bx, by, bz, pdms,
-                                                                    pitch);
-    return cuda_status("dt_pass_x_kernel");
-}
-
-template <int LMAX>
-static int cone_y(int n, int64_t bx, int64_t by, int64_t bz, uint8_t *pdms, int64_t pitch,
-                  cudaStream_t s) {
-    const int64_t lines = (int64_t)n * bx * bz;
-    dt_cone_y_kernel<LMAX><<<grid_lines(lines, 128, 16), 128, 0, s>>>(n, bx, by, bz, pdms, pitch);
-    return cuda_status("dt_cone_y_kernel");
-}
-
-template <int LMAX>
-static int cone_z(int n, int64_t bx, int64_t by, int64_t bz, uint8_t *pdms, int64_t pitch,
-                  cudaStream_t s) {
-    const int R = 64;
-    int sw = (int)ceil_div(bz, 4);
+template <int LMAX, int AXIS, bool kDist1D>
+static int tile_pass(int n, int64_t bx, int64_t by, int64_t bz, uint8_t *pdms, int64_t pitch,
+                     cudaStream_t s) {
+    const int64_t L = AXIS == kAxisX ? bx : (AXIS == kAxisY ? by : bz);
+    int sw = (int)ceil_div(L, 4);
     if (sw % 2 == 0) sw += 1;
     const int sstride = 4 * sw;
-    const size_t smem = (size_t)R * sstride;
-    auto kern = dt_cone_z_kernel<LMAX>;
-    if (smem > 48 * 1024)
-        PDM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          (int)smem));
-    const int64_t rows_per_p = bx * by;
-    const int64_t tiles = ceil_div(rows_per_p, R) * n;
-    kern<<<grid_lines(tiles, 1, 16), R, smem, s>>>(n, rows_per_p, bz, pdms, pitch, sstride);
-    return cuda_status("dt_cone_z_kernel");
+    const size_t per_warp = AXIS == kAxisZ ? (size_t)32 * sstride : (size_t)32 * L;
+    int wpc = (int)(65536 / per_warp);
+    wpc = wpc < 1 ? 1 : (wpc > 4 ? 4 : wpc);
+    const size_t smem = per_warp * wpc;
+    auto kern = dt_tile_kernel<LMAX, AXIS, kDist1D>;
+    PDM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)smem));
+    const int64_t tiles = AXIS == kAxisZ ? (int64_t)n * ceil_div(bx * by, 32)
+                                         : (int64_t)n * (AXIS == kAxisX ? by : bx) *
+                                               ceil_div(bz, 32);
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * wpc, smem) !=
+            cudaSuccess ||
+        per_sm < 1)
+        per_sm = 1;
+    int64_t grid = ceil_div(tiles, wpc);
+    const int64_t cap = (int64_t)sm_count() * per_sm;
+    if (grid > cap) grid = cap;
+    kern<<<(unsigned)grid, 32 * wpc, smem, s>>>(n, bx, by, bz, pdms, pitch, sstride, tiles);
+    return cuda_status("dt_tile_kernel");
+}
+
+template <int AXIS, bool kDist1D>
+static int axis_pass(int n, int64_t bx, int64_t by, int64_t bz, uint8_t *pdms, int64_t pitch,
+                     cudaStream_t s) {
+    const int64_t L = AXIS == kAxisX ? bx : (AXIS == kAxisY ? by : bz);
+    if (L <= 1) return PDM_OK;  // a 1-long line is already final
+    if (kDist1D || L <= 64) {
+        if (L <= 64) return tile_pass<64, AXIS, kDist1D>(n, bx, by, bz, pdms, pitch, s);
+        if (L <= 1024) return tile_pass<64, AXIS, kDist1D>(n, bx, by, bz, pdms, pitch, s);
+    } else {
+        if (L <= 256) return tile_pass<256, AXIS, kDist1D>(n, bx, by, bz, pdms, pitch, s);
+        if (L <= 512) return tile_pass<512, AXIS, kDist1D>(n, bx, by, bz, pdms, pitch, s);
+        if (L <= 1024) return tile_pass<1024, AXIS, kDist1D>(n, bx, by, bz, pdms, pitch, s);
+    }
+    const int64_t lines = (int64_t)n * bx * by * bz / L;
+    dt_line_kernel<AXIS, kDist1D><<<grid_for(lines, 128, 16), 128, 0, s>>>(n, bx, by, bz, pdms,
+                                                                           pitch);
+    return cuda_status("dt_line_kernel");
+}
+
+static int pass_x_mask(const uint32_t *mask, int words, int n, int64_t bx, int64_t by,
+                       int64_t bz, uint8_t *pdms, int64_t pitch, cudaStream_t s) {
+    const int64_t nb = bx * by * bz;
+    dt_expand_mask_kernel<<<grid_for(ceil_div(nb, 16), 256, 8), 256, 0, s>>>(
+        MaskSrc{mask, words}, n, nb, pdms, pitch);
+    int st = cuda_status("dt_expand_mask_kernel");
+    if (st) return st;
+    return axis_pass<kAxisX, true>(n, bx, by, bz, pdms, pitch, s);
 }
 
 static int pass_yz(int n, int64_t bx, int64_t by, int64_t bz, uint8_t *pdms, int64_t pitch,
                    cudaStream_t s) {
-    int st;
-    if (by > 1) {
-        if (by <= 64)
-            st = cone_y<64>(n, bx, by, bz, pdms, pitch, s);
-        else if (by <= 256)
-            st = cone_y<256>(n, bx, by, bz, pdms, pitch, s);
-        else if (by <= 512)
-            st = cone_y<512>(n, bx, by, bz, pdms, pitch, s);
-        else if (by <= 1024)
-            st = cone_y<1024>(n, bx, by, bz, pdms, pitch, s);
-        else
-            st = cone_y<4096>(n, bx, by, bz, pdms, pitch, s);
-        if (st) return st;
-    }
-    if (bz > 1) {
-        if (bz <= 64)
-            st = cone_z<64>(n, bx, by, bz, pdms, pitch, s);
-        else if (bz <= 256)
-            st = cone_z<256>(n, bx, by, bz, pdms, pitch, s);
-        else if (bz <= 512)
-            st = cone_z<512>(n, bx, by, bz, pdms, pitch, s);
-        else if (bz <= 1024)
-            st = cone_z<1024>(n, bx, by, bz, pdms, pitch, s);
-        else
-            st = cone_z<4096>(n, bx, by, bz, pdms, pitch, s);
-        if (st) return st;
-    }
-    return PDM_OK;
+    int st = axis_pass<kAxisY, false>(n, bx, by, bz, pdms, pitch, s);
+    if (st) return st;
+    return axis_pass<kAxisZ, false>(n, bx, by, bz, pdms, pitch, s);
 }
 
 static int check_grid(const char *fn, int n, int64_t bx, int64_t by, int64_t bz, int64_t pitch) {
@@ -317,7 +433,10 @@ extern "C" int pdm_distance_transform(const uint8_t *occ, int64_t bx, int64_t by
     int st = check_grid("pdm_distance_transform", 1, bx, by, bz, nb);
     if (st) return st;
     cudaStream_t s = as_stream(stream);
-    st = pass_x(OccSrc{occ}, 1, bx, by, bz, out, nb, s);
+    dt_expand_occ_kernel<<<grid_for(nb, 256, 8), 256, 0, s>>>(occ, nb, out);
+    st = cuda_status("dt_expand_occ_kernel");
+    if (st) return st;
+    st = axis_pass<kAxisX, true>(1, bx, by, bz, out, nb, s);
     if (st) return st;
     return pass_yz(1, bx, by, bz, out, nb, s);
 }
@@ -330,7 +449,7 @@ extern "C" int pdm_distance_transform_mask(const uint32_t *mask, int32_t words, 
     int st = check_grid("pdm_distance_transform_mask", n, bx, by, bz, plane_pitch);
     if (st) return st;
     cudaStream_t s = as_stream(stream);
-    st = pass_x(MaskSrc{mask, words}, n, bx, by, bz, pdms, plane_pitch, s);
+    st = pass_x_mask(mask, words, n, bx, by, bz, pdms, plane_pitch, s);
     if (st) return st;
     return pass_yz(n, bx, by, bz, pdms, plane_pitch, s);
 }
@@ -342,7 +461,7 @@ extern "C" int pdm_dt_pass_x_mask(const uint32_t *mask, int32_t words, int32_t n
     PDM_REQUIRE(words == (n + 31) / 32, "pdm_dt_pass_x_mask: words");
     int st = check_grid("pdm_dt_pass_x_mask", n, bx, by, bz, plane_pitch);
     if (st) return st;
-    return pass_x(MaskSrc{mask, words}, n, bx, by, bz, pdms, plane_pitch, as_stream(stream));
+    return pass_x_mask(mask, words, n, bx, by, bz, pdms, plane_pitch, as_stream(stream));
 }
 
 extern "C" int pdm_dt_slab_edges(const uint8_t *pdms, int64_t plane_pitch, int32_t n, int64_t bx,
@@ -351,7 +470,7 @@ extern "C" int pdm_dt_slab_edges(const uint8_t *pdms, int64_t plane_pitch, int32
     int st = check_grid("pdm_dt_slab_edges", n, bx, by, bz, plane_pitch);
     if (st) return st;
     const int64_t plane = by * bz;
-    slab_edges_kernel<<<grid_lines((int64_t)n * plane, 256, 8), 256, 0, as_stream(stream)>>>(
+    slab_edges_kernel<<<grid_for((int64_t)n * plane, 256, 8), 256, 0, as_stream(stream)>>>(
         pdms, plane_pitch, n, bx, plane, edges);
     return cuda_status("slab_edges_kernel");
 }
@@ -368,7 +487,7 @@ extern "C" int pdm_dt_slab_fold(uint8_t *pdms, int64_t plane_pitch, int32_t n, i
     SlabBounds sb;
     for (int r = 0; r <= world; ++r) sb.x0[r] = slab_x0[r];
     const int64_t plane = by * bz;
-    slab_fold_kernel<<<grid_lines((int64_t)n * plane, 256, 8), 256, 0, as_stream(stream)>>>(
+    slab_fold_kernel<<<grid_for((int64_t)n * plane, 256, 8), 256, 0, as_stream(stream)>>>(
         pdms, plane_pitch, n, bx, plane, edges_all, world, rank, sb);
     return cuda_status("slab_fold_kernel");
 }

@@ -39,6 +39,13 @@ inline cudaStream_t as_stream(pdm_stream_t s) { return reinterpret_cast<cudaStre
 
 int sm_count();  // cached SM count of the current device
 
+// apron.cu: streaming apron min/max (+ mask) when b divides a 16-byte voxel
+// chunk; returns PDM_EUNSUPPORTED without launching otherwise.  outs: bit 0 =
+// write mins/maxs, bit 1 = write the partition mask.
+int apron_fast_launch(const void *vox, int bits, int64_t nx, int64_t ny, int64_t nz, int b,
+                      int outs, void *mins, void *maxs, const int32_t *pid, uint32_t *mask,
+                      int words, cudaStream_t s);
+
 __host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
 // ---- memory access helpers ------------------------------------------------------

@@ -357,6 +357,9 @@ extern "C" int pdm_block_any_lut(const void *vox, int bits, int64_t nx, int64_t 
 static int apron_launch(const void *vox, int bits, const Dims &d, int b, int outs, void *mins,
                         void *maxs, const int32_t *pid, uint32_t *mask, int words,
                         cudaStream_t s) {
+    const int fast = apron_fast_launch(vox, bits, d.nx, d.ny, d.nz, b, outs, mins, maxs, pid,
+                                       mask, words, s);
+    if (fast != PDM_EUNSUPPORTED) return fast;
     const int64_t nb = d.bx * d.by * d.bz;
     const int threads = 256;
     const int grid = grid_for(nb, threads, 8);
