@@ -179,30 +179,52 @@ def build_pdm_set_sharded(volume: Volume, b: int, scheme: PartitionScheme,
     if bx0 is not None and int(starts[rank]) != bx0:
         raise VolumeError(f"rank {rank}: slab starts at block {bx0}, expected {starts[rank]}")
 
-    if mode == "voxel":
-        mask = ops.mask_voxel(vol_t, volume.bits, b, scheme)
-    else:
-        mins, maxs = ops.block_min_max(vol_t, volume.bits, b)
+    below = above = None
+    if mode == "range_apron":
+        if rank < world - 1 and volume.dims[0] % b:
+            raise VolumeError("only the last slab may end inside a block")
         below, above = _exchange_planes(vol_t, ops, rank, world, group)
-        if below is not None:
-            pm, px = ops.block_min_max(below, volume.bits, b)
-            ops.fold_minmax(mins[0:1], maxs[0:1], pm, px, volume.bits)
-        if above is not None:
-            if volume.dims[0] % b:
-                raise VolumeError("only the last slab may end inside a block")
-            pm, px = ops.block_min_max(above, volume.bits, b)
-            ops.fold_minmax(mins[-1:], maxs[-1:], pm, px, volume.bits)
-        mask = ops.mask_from_minmax(mins, maxs, volume.bits, scheme)
-
-    pitch = device.plane_pitch(grid.num_blocks)
-    storage = ops.empty((n, pitch), np.uint8)
-    ops.pass_x(mask, n, bdims, storage, pitch)
-    edges = ops.edges(storage, pitch, n, bdims)
+    storage, pitch, edges = slab_phase_local(vol_t, volume.bits, b, scheme, mode, below, above,
+                                             ops)
     gathered = [torch.empty_like(edges) for _ in range(world)]
     dist.all_gather(gathered, edges, group=group)
     edges_all = torch.stack(gathered).contiguous()
-    ops.fold(storage, pitch, n, bdims, edges_all, world, rank, starts)
-    ops.pass_yz(storage, pitch, n, bdims)
+    slab_phase_fold(storage, pitch, n, bdims, edges_all, world, rank, starts, ops)
     pset = PdmSet(grid=grid, scheme=scheme, occupancy_mode=mode, storage=storage)
     pset.slab = (int(starts[rank]), int(starts[rank + 1]), int(starts[-1]))
     return pset
+
+
+def slab_phase_local(vol_t, bits: int, b: int, scheme: PartitionScheme, mode: str, below, above,
+                     ops):
+    """Everything a rank does before the exchange: its POM (folding in the
+    neighbours' boundary voxel planes ``below``/``above`` in range_apron mode),
+    the local 1-D distance along x, and its edge planes.  Returns
+    (storage [n, pitch], pitch, edges [2, n, by, bz])."""
+    dims = tuple(vol_t.shape)
+    bdims = tuple(-(-d // b) for d in dims)
+    n = scheme.n
+    if mode == "voxel":
+        mask = ops.mask_voxel(vol_t, bits, b, scheme)
+    else:
+        mins, maxs = ops.block_min_max(vol_t, bits, b)
+        if below is not None:
+            pm, px = ops.block_min_max(below, bits, b)
+            ops.fold_minmax(mins[0:1], maxs[0:1], pm, px, bits)
+        if above is not None:
+            pm, px = ops.block_min_max(above, bits, b)
+            ops.fold_minmax(mins[-1:], maxs[-1:], pm, px, bits)
+        mask = ops.mask_from_minmax(mins, maxs, bits, scheme)
+    nb = bdims[0] * bdims[1] * bdims[2]
+    pitch = device.plane_pitch(nb)
+    storage = ops.empty((n, pitch), np.uint8)
+    ops.pass_x(mask, n, bdims, storage, pitch)
+    return storage, pitch, ops.edges(storage, pitch, n, bdims)
+
+
+def slab_phase_fold(storage, pitch: int, n: int, bdims, edges_all, world: int, rank: int,
+                    slab_x0, ops) -> None:
+    """After the exchange: fold the other slabs' nearest occupied blocks into
+    the local 1-D distances, then the local y and z passes."""
+    ops.fold(storage, pitch, n, bdims, edges_all, world, rank, slab_x0)
+    ops.pass_yz(storage, pitch, n, bdims)

@@ -1,0 +1,145 @@
+"""Multi-rank x-slab sharding of the PDM precompute (paper_2407_21552_b200.sharded).
+
+* CPU: world_size 2 and 3 over gloo, per-slab compute by the host ops
+  (tests/sharded_host_ops.py), every rank's slab of every PDM compared with
+  the oracle's single-volume build_pdm_set -- exercises the slab table, the
+  boundary-plane send/recv (range_apron) and the edge all_gather + fold.
+* GPU: the same decomposition emulated on one device with the CUDA slab
+  kernels (slab_phase_local on each slab, stacked edges, slab_phase_fold):
+  bit-identical to the single-GPU build.  No kernel waits on another.
+"""
+
+from __future__ import annotations
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import oracle
+import paper_2407_21552_b200 as pdm
+from conftest import random_structured_volume
+from paper_2407_21552_b200 import sharded
+
+CASES = [
+    # dims, bits, b, n, block planes per slab (None = even split)
+    ((24, 10, 12), 8, 4, 8, None),
+    ((22, 9, 14), 16, 2, 5, None),   # last slab ends inside a block (22 / 2 = 11 planes)
+    ((30, 7, 9), 8, 3, 40, None),    # n > 32: two mask words
+    ((40, 6, 5), 8, 1, 4, [3, 30, 7]),
+]
+
+
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _slab_planes(bx, world, planes):
+    if planes is not None:
+        return planes
+    per, rem = divmod(bx, world)
+    return [per + (r < rem) for r in range(world)]
+
+
+def _worker(rank, world, port, case, mode, seed):
+    from sharded_host_ops import HostOps
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        dims, bits, b, n, planes = case
+        rng = np.random.default_rng(seed)
+        vox = random_structured_volume(rng, dims, bits)
+        scheme = pdm.scheme_uniform(n, bits)
+        bx = -(-dims[0] // b)
+        planes = _slab_planes(bx, world, planes)[:world]
+        starts = np.concatenate([[0], np.cumsum(planes)])
+        x0, x1 = int(starts[rank]) * b, min(int(starts[rank + 1]) * b, dims[0])
+        slab = pdm.Volume.from_array(vox[x0:x1])
+        pset = sharded.build_pdm_set_sharded(slab, b, scheme, mode, bx0=int(starts[rank]),
+                                             ops=HostOps())
+        nb = pset.grid.num_blocks
+        got = pset.storage[:, :nb].numpy().reshape((n,) + pset.grid.bdims)
+        want = oracle.build_pdm_set(vox, b, scheme.bounds(), mode)[:, starts[rank]:starts[rank + 1]]
+        assert pset.slab == (int(starts[rank]), int(starts[rank + 1]), bx)
+        assert np.array_equal(got, want), f"rank {rank} slab mismatch ({mode})"
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("case", CASES)
+@pytest.mark.parametrize("mode", ["voxel", "range_apron"])
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_build_gloo(case, mode, world):
+    if case[4] is not None and len(case[4]) != world:
+        pytest.skip("explicit slab layout is for world=3")
+    mp.spawn(_worker, args=(world, _free_port(), case, mode, 1234 + world), nprocs=world,
+             join=True)
+
+
+def test_fold_restatement_matches_full_transform():
+    """The numpy fold (mirror of slab_fold_kernel) composes to the full DT."""
+    from sharded_host_ops import HostOps, cone_axis, dist1d_axis0
+
+    rng = np.random.default_rng(5)
+    occ = rng.random((4, 37, 6, 5)) < 0.01
+    occ[0, 2, 3, 1] = True
+    full = np.stack([oracle.distance_transform(o) for o in occ])
+    starts = np.array([0, 5, 6, 20, 37])
+    slabs = [dist1d_axis0(occ[:, a:c].transpose(1, 0, 2, 3)).transpose(1, 0, 2, 3)
+             for a, c in zip(starts[:-1], starts[1:])]
+    edges = torch.from_numpy(np.stack([np.stack([s[:, 0], s[:, -1]]) for s in slabs])
+                             .astype(np.uint8))
+    ops = HostOps()
+    for r, (a, c) in enumerate(zip(starts[:-1], starts[1:])):
+        bd = (c - a, 6, 5)
+        nb = int(np.prod(bd))
+        st = torch.from_numpy(np.ascontiguousarray(slabs[r].reshape(4, nb).astype(np.uint8)))
+        ops.fold(st, nb, 4, bd, edges, len(slabs), r, starts)
+        g = st.numpy().reshape((4,) + bd)
+        g = cone_axis(cone_axis(g, 2), 3)
+        assert np.array_equal(g, full[:, a:c]), r
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("mode", ["voxel", "range_apron"])
+@pytest.mark.parametrize("dims,bits,b,n,planes", [
+    ((64, 40, 64), 16, 4, 32, [5, 1, 7, 3]),
+    ((48, 20, 48), 8, 2, 12, [10, 14]),
+    ((33, 16, 32), 16, 4, 40, [2, 3, 4]),  # last slab partial, two mask words
+])
+def test_sharded_emulated_on_one_gpu(mode, dims, bits, b, n, planes):
+    rng = np.random.default_rng(sum(dims) + n)
+    vox = random_structured_volume(rng, dims, bits)
+    scheme = pdm.scheme_uniform(n, bits)
+    full = pdm.build_pdm_set(pdm.Volume.from_array(vox), pdm.BlockGrid.for_dims(dims, b), scheme,
+                             mode)
+    want = np.stack([d.dist for d in full.pdms])
+    ops = sharded.GpuOps()
+    starts = np.concatenate([[0], np.cumsum(planes)]).astype(np.int64)
+    assert starts[-1] == -(-dims[0] // b)
+    world = len(planes)
+    vols, outs = [], []
+    for r in range(world):
+        x0, x1 = int(starts[r]) * b, min(int(starts[r + 1]) * b, dims[0])
+        vt = pdm.Volume.from_array(vox[x0:x1]).device_voxels()
+        below = vt.new_tensor(vox[x0 - 1:x0].view(np.int16) if bits == 16 else vox[x0 - 1:x0]) \
+            if (mode == "range_apron" and r > 0) else None
+        above = vt.new_tensor(vox[x1:x1 + 1].view(np.int16) if bits == 16 else vox[x1:x1 + 1]) \
+            if (mode == "range_apron" and r < world - 1) else None
+        outs.append(sharded.slab_phase_local(vt, bits, b, scheme, mode, below, above, ops))
+        vols.append(vt)
+    edges_all = torch.stack([e for _, _, e in outs]).contiguous()
+    for r, (storage, pitch, _) in enumerate(outs):
+        bd = (int(starts[r + 1] - starts[r]),) + full.grid.bdims[1:]
+        sharded.slab_phase_fold(storage, pitch, n, bd, edges_all, world, r, starts, ops)
+        nb = int(np.prod(bd))
+        got = storage[:, :nb].cpu().numpy().reshape((n,) + bd)
+        assert np.array_equal(got, want[:, starts[r]:starts[r + 1]]), r
