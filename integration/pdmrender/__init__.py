@@ -1,0 +1,21 @@
+"""Drop-in overlay for the reference package.
+
+With ``integration/`` first on ``sys.path``, ``import pdmrender`` executes the
+reference's own ``__init__.py`` but resolves ``pdmrender.acceleration``,
+``pdmrender.volume`` and ``pdmrender.transfer`` to the B200 modules of
+``paper_2407_21552_b200`` (via the overlay modules in this directory), while
+every other module -- ``raycast``, ``bench``, ``cli``, ``service``, ``_kernels``
+-- still comes from the reference tree at ``$PDMRENDER_REF``.  Because the
+reference imports its hot modules relatively (``from .acceleration import``
+in bench.py:24, cli.py:19, raycast.py:20, service/session.py:17), those
+callers bind to the GPU implementation too.
+"""
+
+import os
+
+_REF = os.environ.get("PDMRENDER_REF", "/root/reference/pkg/src/pdmrender")
+__path__ = [os.path.dirname(os.path.abspath(__file__)), _REF]
+
+_init = os.path.join(_REF, "__init__.py")
+with open(_init) as _f:
+    exec(compile(_f.read(), _init, "exec"))
