@@ -47,8 +47,37 @@ __device__ __forceinline__ void write_range_bits(uint32_t *mask, int64_t c, int 
     }
 }
 
+// Planes prefetched per warp (cp.async ring depth) and the ring footprint.
+template <int B>
+__host__ __device__ constexpr int apron_ring() {
+    return B <= 4 ? 4 : 3;
+}
+template <int B>
+constexpr size_t apron_smem_per_warp() {
+    return (size_t)apron_ring<B>() * (B + 2) * (32 * 16 + 2 * 4);
+}
+constexpr int kApronWarps = 4;
+
+__device__ __forceinline__ void cp_async16_apron(void *smem, const void *gmem) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(tma::smem_u32(smem)),
+                 "l"(gmem)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async4_apron(void *smem, const void *gmem) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(tma::smem_u32(smem)),
+                 "l"(gmem)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit_apron() {
+    asm volatile("cp.async.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait_apron() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
 template <int BITS, int B, int OUTS>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(32 * kApronWarps)
     apron_fast_kernel(const typename VoxT<BITS>::type *__restrict__ vox, int64_t nx, int64_t ny,
                       int64_t nz, int64_t bx, int64_t by, int64_t bz, int XB,
                       typename VoxT<BITS>::type *__restrict__ mins,
@@ -57,9 +86,18 @@ __global__ void __launch_bounds__(256)
     using T = typename VoxT<BITS>::type;
     constexpr int VPC = 16 / (BITS / 8);
     constexpr int ZB = VPC / B;
+    constexpr int kRows = B + 2;
+    constexpr int kRing = apron_ring<B>();
     constexpr uint32_t kHi = 0xFFFFFFFFu;
     const unsigned FULL = 0xFFFFFFFFu;
     const int lane = threadIdx.x & 31;
+    extern __shared__ __align__(16) uint8_t s_apron[];
+    uint4 *ring_main = reinterpret_cast<uint4 *>(s_apron) +
+                       (size_t)(threadIdx.x >> 5) * kRing * kRows * 32;
+    uint32_t *ring_edge = reinterpret_cast<uint32_t *>(
+                              reinterpret_cast<uint4 *>(s_apron) +
+                              (size_t)(blockDim.x >> 5) * kRing * kRows * 32) +
+                          (size_t)(threadIdx.x >> 5) * kRing * kRows * 2;
     const int64_t strip = 32 * VPC;
     const int64_t nstrips = ceil_div(nz, strip);
     const int64_t xchunks = ceil_div(bx, XB);
@@ -84,6 +122,27 @@ __global__ void __launch_bounds__(256)
             pmn[t] = cmn[t] = nmn[t] = kHi;
             pmx[t] = cmx[t] = nmx[t] = 0;
         }
+        // plane prefetch: rows y0..y1 of plane px into ring slot `slot` (16 B
+        // per lane + the strip-edge words of lanes 0/31), one commit group per
+        // plane (empty past the run, so group counting stays uniform)
+        const int nrows = (int)(y1 - y0 + 1);
+        auto issue_plane = [&](int64_t px, int slot) {
+            if (px <= xe) {
+                const T *plane = vox + px * ny * nz + y0 * nz;
+                for (int yy = 0; yy < nrows; ++yy) {
+                    const T *row = plane + (int64_t)yy * nz;
+                    if (active) cp_async16_apron(&ring_main[(slot * kRows + yy) * 32 + lane], row + zl);
+                    if (lane == 0 && has_left)
+                        cp_async4_apron(&ring_edge[(slot * kRows + yy) * 2],
+                                        row + zs - (BITS == 8 ? 4 : 2));
+                    if (lane == 31 && has_right)
+                        cp_async4_apron(&ring_edge[(slot * kRows + yy) * 2 + 1], row + zs + strip);
+                }
+            }
+            cp_async_commit_apron();
+        };
+        for (int d = 0; d < kRing; ++d) issue_plane(xs + d, d);
+
         auto emit = [&](int64_t i, const uint32_t(&mn)[ZB], const uint32_t(&mx)[ZB]) {
             if (!active) return;
             const int64_t c0 = (i * by + j) * bz + zl / B;
@@ -111,7 +170,9 @@ __global__ void __launch_bounds__(256)
                     nmx[t] = 0;
                 }
             }
-            // y-apron reduction of this plane, per voxel
+            // y-apron reduction of this plane, per voxel, from the prefetched slot
+            const int slot = (int)((x - xs) % kRing);
+            cp_async_wait_apron<kRing - 1>();
             uint32_t vmn[VPC], vmx[VPC];
 #pragma unroll
             for (int e = 0; e < VPC; ++e) {
@@ -119,29 +180,30 @@ __global__ void __launch_bounds__(256)
                 vmx[e] = 0;
             }
             uint32_t lmn = kHi, lmx = 0, rmn = kHi, rmx = 0;  // strip-edge voxels
-            const T *plane = vox + x * ny * nz;
-            for (int64_t y = y0; y <= y1; ++y) {
-                const T *row = plane + y * nz;
+            for (int yy = 0; yy < nrows; ++yy) {
                 if (active) {
                     uint32_t v[VPC];
-                    unpack16<BITS>(ld_stream_u4(row + zl), v);
+                    unpack16<BITS>(ring_main[(slot * kRows + yy) * 32 + lane], v);
 #pragma unroll
                     for (int e = 0; e < VPC; ++e) {
                         vmn[e] = min(vmn[e], v[e]);
                         vmx[e] = max(vmx[e], v[e]);
                     }
                 }
-                if (lane == 0 && has_left) {
-                    const uint32_t e = row[zs - 1];
+                if (lane == 0 && has_left) {  // voxel zs-1: top of its aligned word
+                    const uint32_t w = ring_edge[(slot * kRows + yy) * 2];
+                    const uint32_t e = BITS == 8 ? w >> 24 : w >> 16;
                     lmn = min(lmn, e);
                     lmx = max(lmx, e);
                 }
-                if (lane == 31 && has_right) {
-                    const uint32_t e = row[zs + strip];
+                if (lane == 31 && has_right) {  // voxel zs+strip: bottom of its word
+                    const uint32_t w = ring_edge[(slot * kRows + yy) * 2 + 1];
+                    const uint32_t e = BITS == 8 ? w & 0xFFu : w & 0xFFFFu;
                     rmn = min(rmn, e);
                     rmx = max(rmx, e);
                 }
             }
+            issue_plane(x + kRing, slot);  // refill the slot just consumed
             // neighbouring voxels across lanes (inactive lanes hold the identity)
             const uint32_t umn = __shfl_up_sync(FULL, vmn[VPC - 1], 1);
             const uint32_t umx = __shfl_up_sync(FULL, vmx[VPC - 1], 1);
@@ -180,6 +242,7 @@ __global__ void __launch_bounds__(256)
             if (r == 0 && i - 1 >= i0) emit(i - 1, pmn, pmx);
         }
         if (xe < i1 * B) emit(i1 - 1, cmn, cmx);
+        cp_async_wait_apron<0>();  // the ring is reused by the next item
     }
 }
 
@@ -191,20 +254,26 @@ static int launch_b(const void *vox, int64_t nx, int64_t ny, int64_t nz, int64_t
     constexpr int VPC = 16 / (BITS / 8);
     const int XB = 32;
     const int64_t items = by * ceil_div(nz, 32 * VPC) * ceil_div(bx, XB);
-    int64_t grid = ceil_div(items * 32, 256);
-    const int64_t cap = (int64_t)sm_count() * 8;
+    const size_t smem = kApronWarps * apron_smem_per_warp<B>();
+    const int threads = 32 * kApronWarps;
+    auto pick = [&]() {
+        if (outs == kOutMinMax) return apron_fast_kernel<BITS, B, kOutMinMax>;
+        if (outs == kOutMask) return apron_fast_kernel<BITS, B, kOutMask>;
+        return apron_fast_kernel<BITS, B, kOutMinMax | kOutMask>;
+    };
+    auto kern = pick();
+    PDM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)smem));
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem) !=
+            cudaSuccess ||
+        per_sm < 1)
+        per_sm = 1;
+    int64_t grid = ceil_div(items, kApronWarps);
+    const int64_t cap = (int64_t)sm_count() * per_sm;
     if (grid > cap) grid = cap;
-    const T *v = (const T *)vox;
-    T *mn = (T *)mins, *mx = (T *)maxs;
-    if (outs == kOutMinMax)
-        apron_fast_kernel<BITS, B, kOutMinMax><<<(unsigned)grid, 256, 0, s>>>(
-            v, nx, ny, nz, bx, by, bz, XB, mn, mx, pid, mask, words);
-    else if (outs == kOutMask)
-        apron_fast_kernel<BITS, B, kOutMask><<<(unsigned)grid, 256, 0, s>>>(
-            v, nx, ny, nz, bx, by, bz, XB, mn, mx, pid, mask, words);
-    else
-        apron_fast_kernel<BITS, B, kOutMinMax | kOutMask><<<(unsigned)grid, 256, 0, s>>>(
-            v, nx, ny, nz, bx, by, bz, XB, mn, mx, pid, mask, words);
+    kern<<<(unsigned)grid, threads, smem, s>>>((const T *)vox, nx, ny, nz, bx, by, bz, XB,
+                                              (T *)mins, (T *)maxs, pid, mask, words);
     return cuda_status("apron_fast_kernel");
 }
 
