@@ -151,14 +151,19 @@ def run_b200(args, rank, world, local_rank):
                                     x_range=(x0, x1))
     scheme = pdm.scheme_uniform(n, bits)
     grid = pdm.BlockGrid.for_dims(vol.dims, b)
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    if world > 1:
-        pset = sharded.build_pdm_set_sharded(vol, b, scheme, CFG["mode"], x0 // b)
-    else:
-        pset = pdm.build_pdm_set(vol, grid, scheme, CFG["mode"])
-    torch.cuda.synchronize()
-    precompute_ms = (time.perf_counter() - t0) * 1e3
+    def precompute():
+        if world > 1:
+            return sharded.build_pdm_set_sharded(vol, b, scheme, CFG["mode"], x0 // b)
+        return pdm.build_pdm_set(vol, grid, scheme, CFG["mode"])
+
+    build_ms = []
+    for _ in range(2):  # first call pays one-time costs (kernel attributes, local memory)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        pset = precompute()
+        torch.cuda.synchronize()
+        build_ms.append((time.perf_counter() - t0) * 1e3)
+    precompute_ms = build_ms[1]
     B = grid.num_blocks
     voxels_rank = vol.num_voxels
 
@@ -282,6 +287,7 @@ def run_b200(args, rank, world, local_rank):
         "gpu_launches": 2 * steps,
         "clocks": clock,
         "precompute_ms": round(precompute_ms, 2),
+        "precompute_first_call_ms": round(build_ms[0], 2),
         "sweep_ms": {str(k): round(t, 5) for k, t in sorted(zip(ks, step_ms))[:: max(1, steps // 8)]},
     }
     if world == 1 and not args.no_cpu_baseline:

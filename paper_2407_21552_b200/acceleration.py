@@ -67,6 +67,7 @@ class _BlockArray:
         self.bdims = tuple(int(v) for v in bdims)
         self._host = None
         self._dev = None
+        self._pending = None  # producer(out_tensor) for deferred results
         shape = tuple(data.shape)
         if shape != self.bdims:
             raise ValueError(f"{field} array shape does not match bdims")
@@ -75,15 +76,43 @@ class _BlockArray:
         else:
             self._dev = data
 
+    @classmethod
+    def _deferred(cls, b, bdims, producer):
+        """A result whose kernel is launched on first access: into HBM for
+        .device(), or straight into pinned host memory for the host view (the
+        kernel's stores then stream over PCIe while it runs, so the
+        download costs no separate copy)."""
+        self = cls.__new__(cls)
+        self.b = int(b)
+        self.bdims = tuple(int(v) for v in bdims)
+        self._host = None
+        self._dev = None
+        self._pending = producer
+        return self
+
     def _host_array(self):
         if self._host is None:
-            self._host = device.to_host(self._dev, self._np_dtype)
+            if self._dev is None and self._pending is not None:
+                t = device.torch()
+                host_t = t.empty(self.bdims, dtype=t.uint8, pin_memory=True)
+                if host_t.data_ptr() % 16 == 0:
+                    self._pending(host_t)
+                    t.cuda.current_stream().synchronize()
+                    self._host_t = host_t  # owns the pinned buffer behind the view
+                    host = host_t.numpy()
+                    self._host = host.astype(bool) if self._np_dtype == np.bool_ else host
+                    return self._host
+            self._host = device.to_host(self.device(), self._np_dtype)
         return self._host
 
     def device(self):
         """uint8 CUDA tensor of shape bdims (uploaded on first use, then cached)."""
         if self._dev is None:
-            self._dev = device.to_device(np.ascontiguousarray(self._host, dtype=np.uint8))
+            if self._pending is not None:
+                self._dev = device.empty(self.bdims, np.uint8)
+                self._pending(self._dev)
+            else:
+                self._dev = device.to_device(np.ascontiguousarray(self._host, dtype=np.uint8))
         return self._dev
 
 
@@ -307,7 +336,13 @@ def combine(pdm_set: PdmSet, selection: PartitionSelection,
     """Element-wise min of the selected partitions' maps, all-255 for an empty
     selection (acceleration.py:244-276).  One kernel pass reads each selected
     map once; max_maps_per_pass is validated like the reference and does not
-    change the result (the reference guarantees chunked == direct)."""
+    change the result (the reference guarantees chunked == direct).
+
+    The merge is launched when the result is first used: ``.device()`` runs it
+    into HBM, ``.dist`` runs it straight into pinned host memory (zero-copy
+    stores over PCIe overlap the merge), so the reference's host-array
+    contract costs one PCIe transfer and no extra pass.  Use update_from_tf /
+    combine_flags_into for an eager device-resident result."""
     if selection.n != pdm_set.n:
         raise SelectionError(
             f"selection is over {selection.n} partitions, set holds {pdm_set.n}")
@@ -316,19 +351,22 @@ def combine(pdm_set: PdmSet, selection: PartitionSelection,
     if (flags is not None and selection._selected is None and max_maps_per_pass is None
             and pdm_set.n <= _MAX_FLAGS):
         # selection still on the device (select_partitions): no host round trip
-        return combine_flags_into(pdm_set, flags)
+        return DistanceMap._deferred(grid.b, grid.bdims,
+                                     lambda out: combine_flags_into(pdm_set, flags, out))
     indices = selection.sorted
     if indices and max_maps_per_pass is not None and max_maps_per_pass < 1:
         raise ValueError(f"max_maps_per_pass must be >= 1, got {max_maps_per_pass}")
-    L = _lib.lib()
-    out = device.empty(grid.bdims, np.uint8)
     sel = np.ascontiguousarray([i - 1 for i in indices], dtype=np.int32)
-    storage = pdm_set.storage if indices else None
-    _lib.check(L.pdm_combine(_lib.ptr(storage) if storage is not None else None,
-                             pdm_set.plane_pitch, grid.num_blocks, max(pdm_set.n, 1),
-                             sel.ctypes.data if sel.size else None, int(sel.size), _lib.ptr(out),
-                             _lib.stream_handle()), "pdm_combine")
-    return DistanceMap(b=grid.b, bdims=grid.bdims, dist=out)
+
+    def produce(out):
+        L = _lib.lib()
+        storage = pdm_set.storage if sel.size else None
+        _lib.check(L.pdm_combine(_lib.ptr(storage) if storage is not None else None,
+                                 pdm_set.plane_pitch, grid.num_blocks, max(pdm_set.n, 1),
+                                 sel.ctypes.data if sel.size else None, int(sel.size),
+                                 _lib.ptr(out), _lib.stream_handle()), "pdm_combine")
+
+    return DistanceMap._deferred(grid.b, grid.bdims, produce)
 
 
 def update_from_tf(pdm_set: PdmSet, tf, out=None, flags=None) -> DistanceMap:

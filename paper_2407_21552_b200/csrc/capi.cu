@@ -799,10 +799,8 @@ extern "C" int pdm_combine(const uint8_t *pdms, int64_t plane_pitch, int64_t map
         PDM_REQUIRE(sel[i] >= 0 && sel[i] < n, "pdm_combine: index %d outside [0, %d)", sel[i],
                     n);
     cudaStream_t s = as_stream(stream);
-    if (k == 0) {  // acceleration.py:261-263: the all-255 map
-        PDM_CUDA_TRY(cudaMemsetAsync(out, kDistClamp, (size_t)map_bytes, s));
-        return PDM_OK;
-    }
+    // k == 0 (acceleration.py:261-263, the all-255 map) runs the merge kernel
+    // with an empty selection: it also works when `out` is mapped host memory.
     const bool vec = (plane_pitch % 16 == 0) && ((uintptr_t)pdms % 16 == 0) &&
                      ((uintptr_t)out % 16 == 0);
     SelParam p;
@@ -812,7 +810,7 @@ extern "C" int pdm_combine(const uint8_t *pdms, int64_t plane_pitch, int64_t map
         return launch_tma<false>(pdms, plane_pitch, map_bytes, p, n, nullptr, out, s);
     }
     if (vec && merge_impl() == kImplAsync) {
-        for (int base = 0; base < k; base += kMaxSelParam) {
+        for (int base = 0; base == 0 || base < k; base += kMaxSelParam) {
             p.k = k - base < kMaxSelParam ? k - base : kMaxSelParam;
             memcpy(p.idx, sel + base, sizeof(int32_t) * p.k);
             const int grid = async_grid(combine_async_kernel, kAsyncRingBytes, map_bytes / 16);
@@ -823,7 +821,7 @@ extern "C" int pdm_combine(const uint8_t *pdms, int64_t plane_pitch, int64_t map
         }
         return PDM_OK;
     }
-    for (int base = 0; base < k; base += kMaxSelParam) {  // >240 maps: fold in passes
+    for (int base = 0; base == 0 || base < k; base += kMaxSelParam) {  // >240: passes
         p.k = k - base < kMaxSelParam ? k - base : kMaxSelParam;
         memcpy(p.idx, sel + base, sizeof(int32_t) * p.k);
         const int acc = base > 0;

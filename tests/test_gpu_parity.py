@@ -177,6 +177,28 @@ def test_combine_empty_singleton_full(built16):
     assert np.all(large <= small)
 
 
+def test_combine_deferred_host_and_device_paths(built16):
+    """combine() results launch on first use: .dist writes pinned host memory
+    directly, .device() writes HBM; both orders agree, for every selection
+    kind (device flags, host indices, empty)."""
+    scheme, pset = built16
+    want = np.minimum.reduce([pset.pdms[i - 1].dist for i in (2, 7, 11)])
+    lut = np.zeros((256, 4))
+    for i in (2, 7, 11):
+        lo, hi = scheme.partitions[i - 1].rho_lo, scheme.partitions[i - 1].rho_hi
+        lut[lo: hi + 1, 3] = 0.5
+    tf = pdm.TransferFunction(lut=lut)
+    a = pdm.combine(pset, pdm.select_partitions(tf, scheme))  # device flags, host first
+    assert np.array_equal(a.dist, want) and np.array_equal(a.device().cpu().numpy(), want)
+    b = pdm.combine(pset, pdm.select_partitions(tf, scheme))  # device first
+    assert np.array_equal(b.device().cpu().numpy(), want) and np.array_equal(b.dist, want)
+    c = pdm.combine(pset, pdm.PartitionSelection(selected=frozenset({2, 7, 11}), n=16))
+    assert np.array_equal(c.dist, want)
+    e = pdm.combine(pset, pdm.PartitionSelection(selected=frozenset(), n=16))
+    assert np.all(e.dist == 255) and int(e.device().min()) == 255
+    assert a.dist.ctypes.data != b.dist.ctypes.data
+
+
 def test_combine_more_than_one_param_batch():
     rng = np.random.default_rng(3)
     vox = random_structured_volume(rng, (12, 10, 16), bits=8)
