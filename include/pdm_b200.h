@@ -50,6 +50,12 @@ int pdm_device_sm_count(int device);
 int pdm_volume_range(const void *vox, int bits, int64_t count, uint32_t *out,
                      pdm_stream_t stream);
 
+/* acceleration.py:77-79 DistanceMap.occupied_fraction on the device:
+ * *count = number of bytes of data[0..bytes) equal to value (device
+ * unsigned long long, cleared first). */
+int pdm_count_value(const uint8_t *data, int64_t bytes, uint32_t value,
+                    unsigned long long *count, pdm_stream_t stream);
+
 /* ---- selection (K8) -------------------------------------------------------
  * transfer.py:250-259 select_partitions: flags[p] = 1 iff some intensity v of
  * partition p has alpha[v * alpha_stride] > 0.0 (f64 compare: NaN transparent,

@@ -44,6 +44,7 @@ _SIGNATURES = {
     "pdm_dt_slab_fold": [_P, _I64, _I32, _I64, _I64, _I64, _P, _I32, _I32, _P, _P],
     "pdm_dt_pass_yz": [_P, _I64, _I32, _I64, _I64, _I64, _P],
     "pdm_volume_range": [_P, _INT, _I64, _P, _P],
+    "pdm_count_value": [_P, _I64, ctypes.c_uint32, _P, _P],
     "pdm_minmax_fold": [_P, _P, _P, _P, _INT, _I64, _P],
     "pdm_synth_volume": [_INT, _I64, _I64, _I64, _I64, _I64, _P, _I32, ctypes.c_uint64, _P, _P],
 }

@@ -151,8 +151,21 @@ class DistanceMap(_BlockArray):
 
     @property
     def occupied_fraction(self) -> float:
-        d = self.dist
-        return float(np.count_nonzero(d == 0)) / d.size
+        """Share of blocks at distance 0 (acceleration.py:77-79); counted on
+        the device (8 bytes back) unless the host copy already exists."""
+        if self._host is not None:
+            d = self._host
+            return float(np.count_nonzero(d == 0)) / d.size
+        return count_value(self.device(), 0) / float(np.prod(self.bdims))
+
+
+def count_value(t_dev, value: int) -> int:
+    """Number of bytes of a uint8 CUDA tensor equal to value (pdm_count_value)."""
+    L = _lib.lib()
+    cnt = device.empty((1,), np.int64)
+    _lib.check(L.pdm_count_value(_lib.ptr(t_dev), t_dev.numel(), int(value), _lib.ptr(cnt),
+                                 _lib.stream_handle()), "pdm_count_value")
+    return int(cnt.item())
 
 
 class PdmSet:

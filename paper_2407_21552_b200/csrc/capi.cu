@@ -622,6 +622,29 @@ __global__ void volume_range_kernel(const T *__restrict__ vox, int64_t count,
     }
 }
 
+// DistanceMap.occupied_fraction (acceleration.py:77-79) on the device:
+// count[0] += #bytes == value.  16-byte loads, __vcmpeq4 + popc, one atomic
+// per warp.  count must be zeroed by the caller.
+__global__ void count_value_kernel(const uint8_t *__restrict__ data, int64_t bytes,
+                                   uint32_t value, unsigned long long *__restrict__ count) {
+    const uint32_t rep = value * 0x01010101u;
+    unsigned long long c = 0;
+    const int64_t nvec = bytes / 16;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const bool aligned = ((uintptr_t)data & 15) == 0;
+    if (aligned) {
+        for (int64_t v = t0; v < nvec; v += stride) {
+            const uint4 q = ld_stream_u4(data + v * 16);
+            c += __popc(__vcmpeq4(q.x, rep) & 0x01010101u) + __popc(__vcmpeq4(q.y, rep) & 0x01010101u) +
+                 __popc(__vcmpeq4(q.z, rep) & 0x01010101u) + __popc(__vcmpeq4(q.w, rep) & 0x01010101u);
+        }
+    }
+    for (int64_t i = (aligned ? nvec * 16 : 0) + t0; i < bytes; i += stride) c += data[i] == value;
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xFFFFFFFFu, c, o);
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd(count, c);
+}
+
 __global__ void range_init_kernel(uint32_t *out) {
     out[0] = 0xFFFFFFFFu;
     out[1] = 0;
@@ -760,6 +783,19 @@ extern "C" int pdm_volume_range(const void *vox, int bits, int64_t count, uint32
         volume_range_kernel<uint16_t><<<(unsigned)grid, 256, 0, s>>>((const uint16_t *)vox, count,
                                                                        out);
     return cuda_status("volume_range_kernel");
+}
+
+extern "C" int pdm_count_value(const uint8_t *data, int64_t bytes, uint32_t value,
+                               unsigned long long *count, pdm_stream_t stream) {
+    PDM_REQUIRE(data && count, "pdm_count_value: null pointer");
+    PDM_REQUIRE(bytes >= 1 && value <= 255, "pdm_count_value: bad args");
+    cudaStream_t s = as_stream(stream);
+    PDM_CUDA_TRY(cudaMemsetAsync(count, 0, sizeof(unsigned long long), s));
+    int64_t grid = ceil_div(ceil_div(bytes, 16), 256);
+    const int64_t cap = (int64_t)sm_count() * 8;
+    if (grid > cap) grid = cap;
+    count_value_kernel<<<(unsigned)(grid < 1 ? 1 : grid), 256, 0, s>>>(data, bytes, value, count);
+    return cuda_status("count_value_kernel");
 }
 
 extern "C" int pdm_select(const double *alpha, int64_t span, int64_t alpha_stride,
