@@ -89,6 +89,73 @@ __device__ __forceinline__ void cone_line(int m, Ld ld, St st) {
     }
 }
 
+// Same scan for lines of m <= 256 with a compact stack: entries are 16 bits
+// (s | g << 8) in a caller-provided shared-memory column, the top two entries
+// stay in registers, and thresholds are recomputed from adjacent entries
+// (t(entry q) = 1 + Sep(entry q-1, entry q), t(bottom) = 0) instead of stored.
+__device__ __forceinline__ int sep16(uint32_t i, uint32_t u) {
+    const int si = (int)(i & 0xFFu), gi = (int)(i >> 8);
+    const int su = (int)(u & 0xFFu), gu = (int)(u >> 8);
+    const int mid = (si + su) >> 1;
+    return gi <= gu ? max(si + gu, mid) : min(su - gi, mid);
+}
+
+template <class Ld, class St, class Stk>
+__device__ __forceinline__ void cone_line16(int m, Ld ld, St st, Stk stk) {
+    // q = entries on the stack; top = entry q-1, below = entry q-2, stk(i)
+    // holds entries 0..q-3.
+    int q = 1;
+    uint32_t top = (uint32_t)ld(0) << 8, below = 0;
+    int t_top = 0;
+    int gnext = m > 1 ? ld(1) : 0;
+    for (int u = 1; u < m; ++u) {
+        const int gu = gnext;
+        if (u + 1 < m) gnext = ld(u + 1);
+        for (;;) {  // pop while the top's cone is above u's at the top's threshold
+            const int fs = max(abs(t_top - (int)(top & 0xFFu)), (int)(top >> 8));
+            const int fu = max(abs(t_top - u), gu);
+            if (fs <= fu) break;
+            if (--q == 0) break;
+            top = below;
+            if (q >= 2) {
+                below = stk(q - 2);
+                t_top = 1 + sep16(below, top);
+            } else {
+                t_top = 0;
+            }
+        }
+        const uint32_t cand = (uint32_t)u | ((uint32_t)gu << 8);
+        if (q == 0) {
+            q = 1;
+            top = cand;
+            t_top = 0;
+        } else {
+            const int w = 1 + sep16(top, cand);
+            if (w < m) {
+                if (q >= 2) stk(q - 2) = (uint16_t)below;
+                below = top;
+                top = cand;
+                t_top = w;
+                ++q;
+            }
+        }
+    }
+    for (int u = m - 1; u >= 0; --u) {
+        const int d = max(abs(u - (int)(top & 0xFFu)), (int)(top >> 8));
+        st(u, d < kDistClamp ? d : kDistClamp);
+        if (u == t_top && q > 1) {
+            --q;
+            top = below;
+            if (q >= 2) {
+                below = stk(q - 2);
+                t_top = 1 + sep16(below, top);
+            } else {
+                t_top = 0;
+            }
+        }
+    }
+}
+
 // 1-D distance of a {0 = occupied, else not} line: forward then backward
 // run-length sweep, clamped at 255.
 template <class Ld, class St>
@@ -170,7 +237,15 @@ __global__ void __launch_bounds__(128)
     constexpr bool kRows = AXIS == kAxisZ;  // contiguous lines
     const int L = (int)(AXIS == kAxisX ? bx : (AXIS == kAxisY ? by : bz));
     const int64_t S = AXIS == kAxisX ? by * bz : bz;  // element stride of strided lines
-    uint8_t *s = s_tiles + (size_t)warp * (kRows ? 32 * (size_t)sstride : 32 * (size_t)L);
+    const size_t tile_bytes = kRows ? 32 * (size_t)sstride : 32 * (size_t)L;
+    uint8_t *s = s_tiles + (size_t)warp * tile_bytes;
+    // 16-bit envelope stacks for short lines, [depth][lane] after all tiles.
+    // (For 256-long lines the 16 KB/warp of stack halves the resident warps
+    // and measured slower than the local-memory stack: 7.5 vs 4.8 ms at
+    // config c.)
+    constexpr bool kSmemStack = !kDist1D && LMAX <= 64;
+    uint16_t *stk16 = reinterpret_cast<uint16_t *>(s_tiles + (size_t)wpc * tile_bytes) +
+                      (size_t)warp * 32 * L + lane;
     const int64_t zblocks = ceil_div(bz, 32);
     const bool vec = (bz & 3) == 0;
     for (int64_t t = (int64_t)blockIdx.x * wpc + warp; t < tiles; t += (int64_t)gridDim.x * wpc) {
@@ -222,6 +297,8 @@ __global__ void __launch_bounds__(128)
             auto st = [&](int u, int v) { line[u * es] = (uint8_t)v; };
             if (kDist1D)
                 dist1d_line(L, ld, st);
+            else if (kSmemStack)
+                cone_line16(L, ld, st, [&](int i) -> uint16_t & { return stk16[i * 32]; });
             else
                 cone_line<LMAX>(L, ld, st);
         }
@@ -353,7 +430,8 @@ static int tile_pass(int n, int64_t bx, int64_t by, int64_t bz, uint8_t *pdms, i
     int sw = (int)ceil_div(L, 4);
     if (sw % 2 == 0) sw += 1;
     const int sstride = 4 * sw;
-    const size_t per_warp = AXIS == kAxisZ ? (size_t)32 * sstride : (size_t)32 * L;
+    const size_t per_warp = (AXIS == kAxisZ ? (size_t)32 * sstride : (size_t)32 * L) +
+                            (!kDist1D && LMAX <= 64 ? (size_t)64 * L : 0);
     int wpc = (int)(65536 / per_warp);
     wpc = wpc < 1 ? 1 : (wpc > 4 ? 4 : wpc);
     const size_t smem = per_warp * wpc;
