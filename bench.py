@@ -172,7 +172,16 @@ def run_b200(args, rank, world, local_rank):
     alphas = [torch.from_numpy(a).to(dev) for _, a in seq]
     out = torch.empty(grid.bdims, dtype=torch.uint8, device=dev)
     flags = torch.empty(n, dtype=torch.uint8, device=dev)
-    flush = torch.empty(FLUSH_BYTES, dtype=torch.uint8, device=dev)
+    flush_w = torch.empty(FLUSH_BYTES, dtype=torch.uint8, device=dev)
+    flush_r = torch.zeros(FLUSH_BYTES // 8, dtype=torch.int64, device=dev)
+
+    def flush_l2(i):
+        """Untimed L2 flush between steps: write 256 MB (> 126 MB L2), then read
+        another 256 MB so the dirty lines are written back now rather than
+        inside the next timed step."""
+        flush_w.fill_(i & 0xFF)
+        flush_r.sum()
+
     stream = torch.cuda.current_stream()
 
     def barrier():
@@ -190,8 +199,11 @@ def run_b200(args, rank, world, local_rank):
         the merge kernel alone (the roofline's per-launch duration)."""
         ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
               for _ in range(steps)]
+        if args.gpu_lead_ms > 0:
+            # keep the GPU busy while the host enqueues, so no step waits on a launch
+            torch.cuda._sleep(int(args.gpu_lead_ms * 1e-3 * 1.9e9))
         for i in range(steps):
-            flush.fill_(i & 0xFF)  # evict the previous step's maps from L2 (untimed)
+            flush_l2(i)  # evict the previous step's maps from L2 (untimed)
             if merge_only:
                 pdm.select_partitions_device(alphas[warm + i], scheme, flags)
             ev[i][0].record(stream)
@@ -228,7 +240,7 @@ def run_b200(args, rank, world, local_rank):
     parts = np.zeros(3)  # select_partitions / combine (launch) / .dist (merge + D2H)
     barrier()
     for i in range(steps):
-        flush.fill_(i & 0xFF)
+        flush_l2(i)
         torch.cuda.synchronize()
         t1 = time.perf_counter()
         sel = pdm.select_partitions(host_tfs[i], scheme)
@@ -271,7 +283,8 @@ def run_b200(args, rank, world, local_rank):
         "config": {"workload": WORKLOAD, "dims_per_gpu": list(CFG["dims"]),
                    "global_dims": list(gdims), "bits": bits, "b": b, "n": n,
                    "occupancy_mode": CFG["mode"], "k_sweep": "1..32",
-                   "l2": "inputs > L2 (PDM set 537 MB/GPU) and 256 MB L2 flush between steps",
+                   "l2": "inputs > L2 (PDM set 537 MB/GPU); untimed L2 flush between steps "
+                         "(256 MB write, then 256 MB read to drain dirty lines)",
                    "parallelism": f"x-slab x{world}, no collective on the update"},
         "roofline": {"bound": "hbm", "kernel": "combine_flags_kernel (K7 merge)",
                      "achieved": round(achieved, 1), "peak": peak, "peak_kind": peak_kind,
@@ -399,6 +412,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=4)
     ap.add_argument("--impl", choices=("b200", "reference"), default="b200")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--gpu-lead-ms", type=float, default=0.0,
+                    help="GPU spin before each timed pass so host enqueue never gates a step")
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")

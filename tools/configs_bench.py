@@ -38,7 +38,14 @@ def main():
     ap.add_argument("--reps", type=int, default=9)
     ap.add_argument("--cpu", action="store_true", help="also time the C oracle")
     args = ap.parse_args()
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    flush_w = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    flush_r = torch.zeros(32 << 20, dtype=torch.int64, device="cuda")
+
+    class flush:  # write 256 MB then read 256 MB: L2 emptied, dirty lines drained
+        @staticmethod
+        def fill_(v):
+            flush_w.fill_(v)
+            flush_r.sum()
 
     def dev_ms(fn):
         ts = []
