@@ -109,6 +109,30 @@ def test_fold_restatement_matches_full_transform():
 
 
 @pytest.mark.gpu
+def test_sharded_build_nccl_world1():
+    """The NCCL plumbing of build_pdm_set_sharded (slab table and edge
+    all_gathers on CUDA tensors) on a one-rank process group."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(_free_port())
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1)
+    try:
+        rng = np.random.default_rng(77)
+        dims, b, n = (32, 24, 48), 4, 12
+        vox = random_structured_volume(rng, dims, 16)
+        vol = pdm.Volume.from_array(vox)
+        scheme = pdm.scheme_uniform(n, 16)
+        for mode in ("voxel", "range_apron"):
+            got = sharded.build_pdm_set_sharded(vol, b, scheme, mode, bx0=0)
+            want = pdm.build_pdm_set(vol, pdm.BlockGrid.for_dims(dims, b), scheme, mode)
+            assert got.slab == (0, 8, 8)
+            assert np.array_equal(np.stack([d.dist for d in got.pdms]),
+                                  np.stack([d.dist for d in want.pdms])), mode
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
 @pytest.mark.parametrize("mode", ["voxel", "range_apron"])
 @pytest.mark.parametrize("dims,bits,b,n,planes", [
     ((64, 40, 64), 16, 4, 32, [5, 1, 7, 3]),
