@@ -258,12 +258,11 @@ __global__ void __launch_bounds__(128)
             nlines = (int)min((int64_t)32, rows - r0);
             g = pdms + (int64_t)p * pitch + r0 * bz;
             if (vec) {
-                const int words = L >> 2;
-                for (int i = lane; i < nlines * words; i += 32) {
-                    const int r = i / words, w = i - r * words;
-                    *reinterpret_cast<uint32_t *>(s + r * sstride + 4 * w) =
-                        *reinterpret_cast<const uint32_t *>(g + (int64_t)r * bz + 4 * w);
-                }
+                const int words = L >> 2;  // rows outer: no division per word
+                for (int r = 0; r < nlines; ++r)
+                    for (int w = lane; w < words; w += 32)
+                        *reinterpret_cast<uint32_t *>(s + r * sstride + 4 * w) =
+                            *reinterpret_cast<const uint32_t *>(g + (int64_t)r * bz + 4 * w);
             } else {
                 for (int i = lane; i < nlines * L; i += 32) {
                     const int r = i / L, u = i - r * L;
@@ -306,11 +305,10 @@ __global__ void __launch_bounds__(128)
         if (kRows) {
             if (vec) {
                 const int words = L >> 2;
-                for (int i = lane; i < nlines * words; i += 32) {
-                    const int r = i / words, w = i - r * words;
-                    *reinterpret_cast<uint32_t *>(g + (int64_t)r * bz + 4 * w) =
-                        *reinterpret_cast<const uint32_t *>(s + r * sstride + 4 * w);
-                }
+                for (int r = 0; r < nlines; ++r)
+                    for (int w = lane; w < words; w += 32)
+                        *reinterpret_cast<uint32_t *>(g + (int64_t)r * bz + 4 * w) =
+                            *reinterpret_cast<const uint32_t *>(s + r * sstride + 4 * w);
             } else {
                 for (int i = lane; i < nlines * L; i += 32) {
                     const int r = i / L, u = i - r * L;
