@@ -331,6 +331,110 @@ __global__ void __launch_bounds__(128)
     }
 }
 
+// Envelope along a strided axis (x or y) for lines <= 256: the warp's tile of
+// 32 lines stays intact in shared memory ([u][32]), each lane's stack holds
+// 8-bit positions only ([depth][32] bytes, g(s) is re-read from the tile and
+// thresholds are recomputed from adjacent entries), and outputs go straight
+// to global memory -- all lanes store element u together, a coalesced 32-byte
+// access.  16 KB of shared memory per warp, no local memory.
+__device__ __forceinline__ int sep_pos(int si, int gi, int su, int gu) {
+    const int mid = (si + su) >> 1;
+    return gi <= gu ? max(si + gu, mid) : min(su - gi, mid);
+}
+
+template <int AXIS>
+__global__ void __launch_bounds__(128)
+    dt_env_strided_kernel(int n, int64_t bx, int64_t by, int64_t bz, uint8_t *__restrict__ pdms,
+                          int64_t pitch, int64_t tiles) {
+    extern __shared__ __align__(16) uint8_t s_env[];
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    const int wpc = blockDim.x >> 5;
+    const int L = (int)(AXIS == kAxisX ? bx : by);
+    const int64_t S = AXIS == kAxisX ? by * bz : bz;
+    uint8_t *tile = s_env + (size_t)warp * 32 * L;
+    uint8_t *stack = s_env + (size_t)wpc * 32 * L + (size_t)warp * 32 * L;
+    const int64_t zblocks = ceil_div(bz, 32);
+    const int64_t outer_n = AXIS == kAxisX ? by : bx;
+    for (int64_t t = (int64_t)blockIdx.x * wpc + warp; t < tiles; t += (int64_t)gridDim.x * wpc) {
+        const int64_t po = t / zblocks;
+        const int64_t z0 = (t % zblocks) * 32;
+        const int p = (int)(po / outer_n);
+        const int64_t o = po % outer_n;
+        const int nlines = (int)min((int64_t)32, bz - z0);
+        uint8_t *g = pdms + (int64_t)p * pitch + (AXIS == kAxisX ? o * bz : o * by * bz) + z0;
+        if (nlines == 32 && (bz & 3) == 0) {
+            for (int i = lane; i < L * 8; i += 32) {
+                const int u = i >> 3, w = i & 7;
+                *reinterpret_cast<uint32_t *>(tile + u * 32 + 4 * w) =
+                    *reinterpret_cast<const uint32_t *>(g + (int64_t)u * S + 4 * w);
+            }
+        } else {
+            for (int u = 0; u < L; ++u)
+                if (lane < nlines) tile[u * 32 + lane] = g[(int64_t)u * S + lane];
+        }
+        __syncwarp();
+        if (lane < nlines) {
+            const uint8_t *col = tile + lane;
+            uint8_t *stk = stack + lane;
+            uint8_t *outp = g + lane;
+            int q = 1, top = 0, below = 0, gtop = col[0], gbelow = 0, t_top = 0;
+            for (int u = 1; u < L; ++u) {
+                const int gu = col[u * 32];
+                for (;;) {
+                    const int fs = max(abs(t_top - top), gtop);
+                    const int fu = max(abs(t_top - u), gu);
+                    if (fs <= fu) break;
+                    if (--q == 0) break;
+                    top = below;
+                    gtop = gbelow;
+                    if (q >= 2) {
+                        below = stk[(q - 2) * 32];
+                        gbelow = col[below * 32];
+                        t_top = 1 + sep_pos(below, gbelow, top, gtop);
+                    } else {
+                        t_top = 0;
+                    }
+                }
+                if (q == 0) {
+                    q = 1;
+                    top = u;
+                    gtop = gu;
+                    t_top = 0;
+                } else {
+                    const int w = 1 + sep_pos(top, gtop, u, gu);
+                    if (w < L) {
+                        if (q >= 2) stk[(q - 2) * 32] = (uint8_t)below;
+                        below = top;
+                        gbelow = gtop;
+                        top = u;
+                        gtop = gu;
+                        t_top = w;
+                        ++q;
+                    }
+                }
+            }
+            for (int u = L - 1; u >= 0; --u) {
+                const int d = max(abs(u - top), gtop);
+                outp[(int64_t)u * S] = (uint8_t)(d < kDistClamp ? d : kDistClamp);
+                if (u == t_top && q > 1) {
+                    --q;
+                    top = below;
+                    gtop = gbelow;
+                    if (q >= 2) {
+                        below = stk[(q - 2) * 32];
+                        gbelow = col[below * 32];
+                        t_top = 1 + sep_pos(below, gbelow, top, gtop);
+                    } else {
+                        t_top = 0;
+                    }
+                }
+            }
+        }
+        __syncwarp();
+    }
+}
+
 // Lines longer than 1024 blocks: one thread per line straight from global
 // memory (correct for any length up to 4095, slower).
 template <int AXIS, bool kDist1D>
@@ -451,6 +555,40 @@ static int tile_pass(int n, int64_t bx, int64_t by, int64_t bz, uint8_t *pdms, i
     return cuda_status("dt_tile_kernel");
 }
 
+static bool env_strided_enabled() {
+    static int on = -1;
+    if (on < 0) {
+        // PDM_DT_ENV=1 selects the shared-stack strided envelope kernel.  Off by
+        // default: at config c it measured 5.14 ms for passes y+z vs 4.90 ms for
+        // the warp-tile kernel with local-memory stacks (fewer resident warps).
+        const char *e = getenv("PDM_DT_ENV");
+        on = (e && e[0] == '1') ? 1 : 0;
+    }
+    return on == 1;
+}
+
+template <int AXIS>
+static int env_strided_pass(int n, int64_t bx, int64_t by, int64_t bz, uint8_t *pdms,
+                            int64_t pitch, cudaStream_t s) {
+    const int64_t L = AXIS == kAxisX ? bx : by;
+    const int wpc = 4;
+    const size_t smem = (size_t)wpc * 64 * L;
+    auto kern = dt_env_strided_kernel<AXIS>;
+    PDM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)smem));
+    const int64_t tiles = (int64_t)n * (AXIS == kAxisX ? by : bx) * ceil_div(bz, 32);
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * wpc, smem) !=
+            cudaSuccess ||
+        per_sm < 1)
+        per_sm = 1;
+    int64_t grid = ceil_div(tiles, wpc);
+    const int64_t cap = (int64_t)sm_count() * per_sm;
+    if (grid > cap) grid = cap;
+    kern<<<(unsigned)grid, 32 * wpc, smem, s>>>(n, bx, by, bz, pdms, pitch, tiles);
+    return cuda_status("dt_env_strided_kernel");
+}
+
 template <int AXIS, bool kDist1D>
 static int axis_pass(int n, int64_t bx, int64_t by, int64_t bz, uint8_t *pdms, int64_t pitch,
                      cudaStream_t s) {
@@ -459,6 +597,8 @@ static int axis_pass(int n, int64_t bx, int64_t by, int64_t bz, uint8_t *pdms, i
     if (kDist1D || L <= 64) {
         if (L <= 64) return tile_pass<64, AXIS, kDist1D>(n, bx, by, bz, pdms, pitch, s);
         if (L <= 1024) return tile_pass<64, AXIS, kDist1D>(n, bx, by, bz, pdms, pitch, s);
+    } else if (AXIS != kAxisZ && L <= 256 && env_strided_enabled()) {
+        return env_strided_pass<AXIS == kAxisZ ? kAxisY : AXIS>(n, bx, by, bz, pdms, pitch, s);
     } else {
         if (L <= 256) return tile_pass<256, AXIS, kDist1D>(n, bx, by, bz, pdms, pitch, s);
         if (L <= 512) return tile_pass<512, AXIS, kDist1D>(n, bx, by, bz, pdms, pitch, s);
