@@ -58,24 +58,6 @@ constexpr size_t apron_smem_per_warp() {
 }
 constexpr int kApronWarps = 4;
 
-__device__ __forceinline__ void cp_async16_apron(void *smem, const void *gmem) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(tma::smem_u32(smem)),
-                 "l"(gmem)
-                 : "memory");
-}
-__device__ __forceinline__ void cp_async4_apron(void *smem, const void *gmem) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(tma::smem_u32(smem)),
-                 "l"(gmem)
-                 : "memory");
-}
-__device__ __forceinline__ void cp_async_commit_apron() {
-    asm volatile("cp.async.commit_group;" ::: "memory");
-}
-template <int N>
-__device__ __forceinline__ void cp_async_wait_apron() {
-    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
-
 template <int BITS, int B, int OUTS>
 __global__ void __launch_bounds__(32 * kApronWarps)
     apron_fast_kernel(const typename VoxT<BITS>::type *__restrict__ vox, int64_t nx, int64_t ny,
@@ -131,15 +113,15 @@ __global__ void __launch_bounds__(32 * kApronWarps)
                 const T *plane = vox + px * ny * nz + y0 * nz;
                 for (int yy = 0; yy < nrows; ++yy) {
                     const T *row = plane + (int64_t)yy * nz;
-                    if (active) cp_async16_apron(&ring_main[(slot * kRows + yy) * 32 + lane], row + zl);
+                    if (active) cpa::copy16(&ring_main[(slot * kRows + yy) * 32 + lane], row + zl);
                     if (lane == 0 && has_left)
-                        cp_async4_apron(&ring_edge[(slot * kRows + yy) * 2],
+                        cpa::copy4(&ring_edge[(slot * kRows + yy) * 2],
                                         row + zs - (BITS == 8 ? 4 : 2));
                     if (lane == 31 && has_right)
-                        cp_async4_apron(&ring_edge[(slot * kRows + yy) * 2 + 1], row + zs + strip);
+                        cpa::copy4(&ring_edge[(slot * kRows + yy) * 2 + 1], row + zs + strip);
                 }
             }
-            cp_async_commit_apron();
+            cpa::commit();
         };
         for (int d = 0; d < kRing; ++d) issue_plane(xs + d, d);
 
@@ -172,7 +154,7 @@ __global__ void __launch_bounds__(32 * kApronWarps)
             }
             // y-apron reduction of this plane, per voxel, from the prefetched slot
             const int slot = (int)((x - xs) % kRing);
-            cp_async_wait_apron<kRing - 1>();
+            cpa::wait<kRing - 1>();
             uint32_t vmn[VPC], vmx[VPC];
 #pragma unroll
             for (int e = 0; e < VPC; ++e) {
@@ -242,7 +224,7 @@ __global__ void __launch_bounds__(32 * kApronWarps)
             if (r == 0 && i - 1 >= i0) emit(i - 1, pmn, pmx);
         }
         if (xe < i1 * B) emit(i1 - 1, cmn, cmx);
-        cp_async_wait_apron<0>();  // the ring is reused by the next item
+        cpa::wait<0>();  // the ring is reused by the next item
     }
 }
 

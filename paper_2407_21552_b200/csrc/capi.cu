@@ -236,19 +236,6 @@ __device__ __forceinline__ void merge_large_k(const uint8_t *__restrict__ pdms, 
 // shared accesses are 512 contiguous bytes (conflict-free).
 constexpr int kAsyncDepth = 12;
 
-__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(tma::smem_u32(smem)),
-                 "l"(gmem)
-                 : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() {
-    asm volatile("cp.async.commit_group;" ::: "memory");
-}
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
-
 template <bool kAccumulate>
 __device__ __forceinline__ void merge_async(const uint8_t *__restrict__ pdms, int64_t pitch,
                                             int64_t nvec, const int32_t *idx, int k,
@@ -269,13 +256,13 @@ __device__ __forceinline__ void merge_async(const uint8_t *__restrict__ pdms, in
 #pragma unroll
     for (int d = 0; d < kAsyncDepth; ++d) {
         if (d < items) {
-            cp_async16(slot0 + d * B, pdms + (int64_t)idx[load_m] * pitch + load_off);
+            cpa::copy16(slot0 + d * B, pdms + (int64_t)idx[load_m] * pitch + load_off);
             if (++load_m == k) {
                 load_m = 0;
                 load_off += T * 16;
             }
         }
-        cp_async_commit();
+        cpa::commit();
     }
     int64_t store_off = v0 * 16;
     int fold_m = 0, d = 0;
@@ -283,16 +270,16 @@ __device__ __forceinline__ void merge_async(const uint8_t *__restrict__ pdms, in
     acc.init_ff();
     if (kAccumulate) acc.fold(*reinterpret_cast<const uint4 *>(out + store_off));
     for (int64_t i = 0; i < items; ++i) {
-        cp_async_wait<kAsyncDepth - 1>();
+        cpa::wait<kAsyncDepth - 1>();
         acc.fold(slot0[d * B]);
         if (i + kAsyncDepth < items) {
-            cp_async16(slot0 + d * B, pdms + (int64_t)idx[load_m] * pitch + load_off);
+            cpa::copy16(slot0 + d * B, pdms + (int64_t)idx[load_m] * pitch + load_off);
             if (++load_m == k) {
                 load_m = 0;
                 load_off += T * 16;
             }
         }
-        cp_async_commit();
+        cpa::commit();
         if (++d == kAsyncDepth) d = 0;
         if (++fold_m == k) {
             st_stream_u4(out + store_off, acc.result());
@@ -303,7 +290,7 @@ __device__ __forceinline__ void merge_async(const uint8_t *__restrict__ pdms, in
                 acc.fold(*reinterpret_cast<const uint4 *>(out + store_off));
         }
     }
-    cp_async_wait<0>();
+    cpa::wait<0>();
 }
 
 constexpr int kAsyncThreads = 256;

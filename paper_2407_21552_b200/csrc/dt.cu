@@ -173,6 +173,135 @@ __device__ __forceinline__ void dist1d_line(int m, Ld ld, St st) {
     }
 }
 
+// Lower envelope of a line of len <= 256 values by two running sweeps, no
+// stack.  Forward: L[u] = min_{i<=u} max(u - i, g[i]).  Given m = L[u-1],
+// every i in [u-m, u-1] has g[i] >= m, so
+//   L[u] = g[u]                        if g[u] <= m
+//        = m    if the last i < u with g[i] == m lies in [u-m, u-1]
+//        = m+1  otherwise,
+// and one table `last[v]` (latest position holding value v) decides it.
+// Backward: the same sweep over L reversed gives the full envelope
+// (env(L) == env(g), and L is its own left envelope), written in place.
+// Positions fit a byte; a cleared table entry reads as position 0, which is
+// only consulted when a real entry for m exists (m >= u implies g[i*] == m
+// for the minimiser i* < u) or when position 0 is outside the window.
+// `tab` is the lane's column of a [256][32] byte table; the caller clears it
+// before each sweep.  Values are clamped at 255 by construction (m + 1 is
+// only taken when g[u] > m, so m < 255).
+// One step at sweep position j with input g; m is the running value.
+// nm = min(g, m + [last[m] + m < j]) is the case split above (g <= m gives g
+// either way); both candidates are formed while last[m] is in flight, so the
+// loop-carried chain is load -> compare -> select.
+// The table is addressed with 32-bit shared-window addresses and the
+// select is written in PTX so the compiler keeps it a select between the two
+// precomputed addresses (left to itself it re-derives the address from
+// min(g, m + up), four dependent ALU ops instead of two).
+__device__ __forceinline__ int lds_u8(uint32_t a) {
+    uint32_t v;
+    asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+    return (int)v;
+}
+__device__ __forceinline__ void sts_u8(uint32_t a, int v) {
+    asm volatile("st.shared.u8 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ uint32_t sweep_step(int &m, uint32_t &am, int g, int j,
+                                               uint32_t tab) {
+    const int lp = lds_u8(am);  // last[m]; am == tab + 32 * m
+    const int a0 = min(g, m), a1 = min(g, m + 1);
+    const uint32_t o0 = tab + 32u * (uint32_t)a0, o1 = tab + 32u * (uint32_t)a1;
+    int nm;
+    asm("{\n\t.reg .pred p;\n\t"
+        "setp.lt.s32 p, %2, %3;\n\t"
+        "selp.b32 %0, %4, %5, p;\n\t"
+        "selp.b32 %1, %6, %7, p;\n\t}"
+        : "=r"(am), "=r"(nm)
+        : "r"(lp), "r"(j - m), "r"(o1), "r"(o0), "r"(a1), "r"(a0));
+    sts_u8(tab + 32u * (uint32_t)g, j);
+    m = nm;
+    return (uint32_t)nm;
+}
+
+// A line in a shared-memory tile: contiguous (row tiles) or strided by the
+// 32 lines of a [u][32] tile.  ld4/st4 move 4 consecutive elements as one
+// word (u % 4 == 0).
+template <bool kContig>
+struct TileLine {
+    uint8_t *p;
+    __device__ __forceinline__ int ld(int u) const { return p[kContig ? u : u * 32]; }
+    __device__ __forceinline__ void st(int u, uint32_t v) const {
+        p[kContig ? u : u * 32] = (uint8_t)v;
+    }
+    __device__ __forceinline__ uint32_t ld4(int u) const {
+        if (kContig) return *reinterpret_cast<const uint32_t *>(p + u);
+        return (uint32_t)p[u * 32] | (uint32_t)p[(u + 1) * 32] << 8 |
+               (uint32_t)p[(u + 2) * 32] << 16 | (uint32_t)p[(u + 3) * 32] << 24;
+    }
+    __device__ __forceinline__ void st4(int u, uint32_t v) const {
+        if (kContig) {
+            *reinterpret_cast<uint32_t *>(p + u) = v;
+        } else {
+            p[u * 32] = (uint8_t)v;
+            p[(u + 1) * 32] = (uint8_t)(v >> 8);
+            p[(u + 2) * 32] = (uint8_t)(v >> 16);
+            p[(u + 3) * 32] = (uint8_t)(v >> 24);
+        }
+    }
+};
+
+// Forward sweep in place.  Lengths divisible by 4 go a word at a time with
+// the next word loaded before this word's results are stored.
+template <bool kContig>
+__device__ __forceinline__ void sweep_forward(int len, TileLine<kContig> line, uint32_t tab) {
+    int m = kDistClamp;
+    uint32_t pm = tab + 32u * kDistClamp;
+    if ((len & 3) == 0) {
+        uint32_t w = line.ld4(0);
+        for (int u = 0; u < len; u += 4) {
+            const uint32_t wn = u + 4 < len ? line.ld4(u + 4) : 0u;
+            uint32_t o = sweep_step(m, pm, (int)(w & 0xFFu), u, tab);
+            o |= sweep_step(m, pm, (int)((w >> 8) & 0xFFu), u + 1, tab) << 8;
+            o |= sweep_step(m, pm, (int)((w >> 16) & 0xFFu), u + 2, tab) << 16;
+            o |= sweep_step(m, pm, (int)(w >> 24), u + 3, tab) << 24;
+            line.st4(u, o);
+            w = wn;
+        }
+        return;
+    }
+    for (int u = 0; u < len; ++u) line.st(u, sweep_step(m, pm, line.ld(u), u, tab));
+}
+
+// Backward sweep in place: sweep position j = len - 1 - u.
+template <bool kContig>
+__device__ __forceinline__ void sweep_backward(int len, TileLine<kContig> line, uint32_t tab) {
+    int m = kDistClamp;
+    uint32_t pm = tab + 32u * kDistClamp;
+    if ((len & 3) == 0) {
+        uint32_t w = line.ld4(len - 4);
+        for (int u0 = len - 4, j = 0; u0 >= 0; u0 -= 4, j += 4) {
+            const uint32_t wn = u0 >= 4 ? line.ld4(u0 - 4) : 0u;
+            uint32_t o = sweep_step(m, pm, (int)(w >> 24), j, tab) << 24;
+            o |= sweep_step(m, pm, (int)((w >> 16) & 0xFFu), j + 1, tab) << 16;
+            o |= sweep_step(m, pm, (int)((w >> 8) & 0xFFu), j + 2, tab) << 8;
+            o |= sweep_step(m, pm, (int)(w & 0xFFu), j + 3, tab);
+            line.st4(u0, o);
+            w = wn;
+        }
+        return;
+    }
+    for (int j = 0; j < len; ++j) {
+        const int u = len - 1 - j;
+        line.st(u, sweep_step(m, pm, line.ld(u), j, tab));
+    }
+}
+
+// Warp-collective clear of a [256][32] byte table (16 B per lane x 16).
+__device__ __forceinline__ void clear_table(uint8_t *tab_warp, int lane) {
+    uint4 *t = reinterpret_cast<uint4 *>(tab_warp);
+#pragma unroll
+    for (int i = 0; i < 16; ++i) t[i * 32 + lane] = make_uint4(0u, 0u, 0u, 0u);
+}
+
 // ---- expand: partition occupancy -> {0, 255} planes ---------------------------------
 // Thread = 16 consecutive blocks: it reads their mask words once and writes a
 // 16-byte vector to every partition plane (coalesced 512 B per warp store).
@@ -226,10 +355,11 @@ __global__ void __launch_bounds__(256)
 // ---- warp-tile passes ----------------------------------------------------------------
 enum { kAxisX = 0, kAxisY = 1, kAxisZ = 2 };
 
-template <int LMAX, int AXIS, bool kDist1D>
+template <int LMAX, int AXIS, bool kDist1D, bool kSweep>
 __global__ void __launch_bounds__(128)
     dt_tile_kernel(int n, int64_t bx, int64_t by, int64_t bz, uint8_t *__restrict__ pdms,
                    int64_t pitch, int sstride, int64_t tiles) {
+    static_assert(!kSweep || (LMAX <= 256 && !kDist1D), "sweep envelope: lines <= 256");
     extern __shared__ __align__(16) uint8_t s_tiles[];
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
@@ -239,11 +369,12 @@ __global__ void __launch_bounds__(128)
     const int64_t S = AXIS == kAxisX ? by * bz : bz;  // element stride of strided lines
     const size_t tile_bytes = kRows ? 32 * (size_t)sstride : 32 * (size_t)L;
     uint8_t *s = s_tiles + (size_t)warp * tile_bytes;
-    // 16-bit envelope stacks for short lines, [depth][lane] after all tiles.
-    // (For 256-long lines the 16 KB/warp of stack halves the resident warps
-    // and measured slower than the local-memory stack: 7.5 vs 4.8 ms at
-    // config c.)
-    constexpr bool kSmemStack = !kDist1D && LMAX <= 64;
+    // Per-warp scratch after all tiles: the sweep's [256][32] position table,
+    // or 16-bit envelope stacks [depth][lane] for short lines.  (For 256-long
+    // lines a 16 KB/warp stack halves the resident warps and measured slower
+    // than the local-memory stack: 7.5 vs 4.8 ms at config c.)
+    constexpr bool kSmemStack = !kDist1D && !kSweep && LMAX <= 64;
+    uint8_t *tab_warp = s_tiles + (size_t)wpc * tile_bytes + (size_t)warp * 8192;
     uint16_t *stk16 = reinterpret_cast<uint16_t *>(s_tiles + (size_t)wpc * tile_bytes) +
                       (size_t)warp * 32 * L + lane;
     const int64_t zblocks = ceil_div(bz, 32);
@@ -261,8 +392,7 @@ __global__ void __launch_bounds__(128)
                 const int words = L >> 2;  // rows outer: no division per word
                 for (int r = 0; r < nlines; ++r)
                     for (int w = lane; w < words; w += 32)
-                        *reinterpret_cast<uint32_t *>(s + r * sstride + 4 * w) =
-                            *reinterpret_cast<const uint32_t *>(g + (int64_t)r * bz + 4 * w);
+                        cpa::copy4(s + r * sstride + 4 * w, g + (int64_t)r * bz + 4 * w);
             } else {
                 for (int i = lane; i < nlines * L; i += 32) {
                     const int r = i / L, u = i - r * L;
@@ -277,23 +407,39 @@ __global__ void __launch_bounds__(128)
             const int64_t o = po % outer_n;
             nlines = (int)min((int64_t)32, bz - z0);
             g = pdms + (int64_t)p * pitch + (AXIS == kAxisX ? o * bz : o * by * bz) + z0;
-            if (nlines == 32 && vec) {  // 8 lanes per 32-byte row, 4 rows per access
+            if (nlines == 32 && (bz & 15) == 0) {  // 2 lanes per 32-byte row
+                for (int i = lane; i < L * 2; i += 32) {
+                    const int u = i >> 1, w = i & 1;
+                    cpa::copy16(s + u * 32 + 16 * w, g + (int64_t)u * S + 16 * w);
+                }
+            } else if (nlines == 32 && vec) {  // 8 lanes per 32-byte row
                 for (int i = lane; i < L * 8; i += 32) {
                     const int u = i >> 3, w = i & 7;
-                    *reinterpret_cast<uint32_t *>(s + u * 32 + 4 * w) =
-                        *reinterpret_cast<const uint32_t *>(g + (int64_t)u * S + 4 * w);
+                    cpa::copy4(s + u * 32 + 4 * w, g + (int64_t)u * S + 4 * w);
                 }
             } else {
                 for (int u = 0; u < L; ++u)
                     if (lane < nlines) s[u * 32 + lane] = g[(int64_t)u * S + lane];
             }
         }
+        // Tile loads are cp.async (no register staging), so every load of the
+        // tile is in flight at once instead of a few per dependent wait.
+        cpa::commit();
+        cpa::wait<0>();
         __syncwarp();
-        if (lane < nlines) {
-            uint8_t *line = kRows ? s + lane * sstride : s + lane;
-            const int es = kRows ? 1 : 32;
-            auto ld = [&](int u) -> int { return line[u * es]; };
-            auto st = [&](int u, int v) { line[u * es] = (uint8_t)v; };
+        uint8_t *line = kRows ? s + lane * sstride : s + lane;
+        const int es = kRows ? 1 : 32;
+        auto ld = [&](int u) -> int { return line[u * es]; };
+        auto st = [&](int u, int v) { line[u * es] = (uint8_t)v; };
+        if (kSweep) {
+            clear_table(tab_warp, lane);
+            __syncwarp();
+            if (lane < nlines) sweep_forward(L, TileLine<kRows>{line}, tma::smem_u32(tab_warp + lane));
+            __syncwarp();
+            clear_table(tab_warp, lane);
+            __syncwarp();
+            if (lane < nlines) sweep_backward(L, TileLine<kRows>{line}, tma::smem_u32(tab_warp + lane));
+        } else if (lane < nlines) {
             if (kDist1D)
                 dist1d_line(L, ld, st);
             else if (kSmemStack)
@@ -525,7 +671,7 @@ static int grid_for(int64_t items, int threads, int per_sm) {
     return want < 1 ? 1 : (int)want;
 }
 
-template <int LMAX, int AXIS, bool kDist1D>
+template <int LMAX, int AXIS, bool kDist1D, bool kSweep = false>
 static int tile_pass(int n, int64_t bx, int64_t by, int64_t bz, uint8_t *pdms, int64_t pitch,
                      cudaStream_t s) {
     const int64_t L = AXIS == kAxisX ? bx : (AXIS == kAxisY ? by : bz);
@@ -533,11 +679,11 @@ static int tile_pass(int n, int64_t bx, int64_t by, int64_t bz, uint8_t *pdms, i
     if (sw % 2 == 0) sw += 1;
     const int sstride = 4 * sw;
     const size_t per_warp = (AXIS == kAxisZ ? (size_t)32 * sstride : (size_t)32 * L) +
-                            (!kDist1D && LMAX <= 64 ? (size_t)64 * L : 0);
+                            (kSweep ? (size_t)8192 : (!kDist1D && LMAX <= 64 ? (size_t)64 * L : 0));
     int wpc = (int)(65536 / per_warp);
     wpc = wpc < 1 ? 1 : (wpc > 4 ? 4 : wpc);
     const size_t smem = per_warp * wpc;
-    auto kern = dt_tile_kernel<LMAX, AXIS, kDist1D>;
+    auto kern = dt_tile_kernel<LMAX, AXIS, kDist1D, kSweep>;
     PDM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)smem));
     const int64_t tiles = AXIS == kAxisZ ? (int64_t)n * ceil_div(bx * by, 32)
@@ -553,6 +699,16 @@ static int tile_pass(int n, int64_t bx, int64_t by, int64_t bz, uint8_t *pdms, i
     if (grid > cap) grid = cap;
     kern<<<(unsigned)grid, 32 * wpc, smem, s>>>(n, bx, by, bz, pdms, pitch, sstride, tiles);
     return cuda_status("dt_tile_kernel");
+}
+
+static bool sweep_enabled() {
+    static int on = -1;
+    if (on < 0) {
+        // PDM_DT_SWEEP=0 falls back to the Meijster stack scan (A/B only).
+        const char *e = getenv("PDM_DT_SWEEP");
+        on = (e && e[0] == '0') ? 0 : 1;
+    }
+    return on == 1;
 }
 
 static bool env_strided_enabled() {
@@ -594,6 +750,10 @@ static int axis_pass(int n, int64_t bx, int64_t by, int64_t bz, uint8_t *pdms, i
                      cudaStream_t s) {
     const int64_t L = AXIS == kAxisX ? bx : (AXIS == kAxisY ? by : bz);
     if (L <= 1) return PDM_OK;  // a 1-long line is already final
+    if constexpr (!kDist1D) {
+        if (L <= 256 && sweep_enabled())
+            return tile_pass<256, AXIS, false, true>(n, bx, by, bz, pdms, pitch, s);
+    }
     if (kDist1D || L <= 64) {
         if (L <= 64) return tile_pass<64, AXIS, kDist1D>(n, bx, by, bz, pdms, pitch, s);
         if (L <= 1024) return tile_pass<64, AXIS, kDist1D>(n, bx, by, bz, pdms, pitch, s);

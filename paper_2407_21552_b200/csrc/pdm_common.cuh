@@ -122,6 +122,28 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
 
 }  // namespace tma
 
+// LDGSTS (cp.async): global -> shared without register staging; completion
+// is tracked per thread in commit groups.
+namespace cpa {
+
+__device__ __forceinline__ void copy16(void *smem, const void *gmem) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(tma::smem_u32(smem)),
+                 "l"(gmem)
+                 : "memory");
+}
+__device__ __forceinline__ void copy4(void *smem, const void *gmem) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(tma::smem_u32(smem)),
+                 "l"(gmem)
+                 : "memory");
+}
+__device__ __forceinline__ void commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+}  // namespace cpa
+
 template <int BITS>
 struct VoxT;
 template <>
