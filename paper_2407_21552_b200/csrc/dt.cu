@@ -178,24 +178,21 @@ __device__ __forceinline__ void dist1d_line(int m, Ld ld, St st) {
 // every i in [u-m, u-1] has g[i] >= m, so
 //   L[u] = g[u]                        if g[u] <= m
 //        = m    if the last i < u with g[i] == m lies in [u-m, u-1]
-//        = m+1  otherwise,
-// and one table `last[v]` (latest position holding value v) decides it.
-// Backward: the same sweep over L reversed gives the full envelope
-// (env(L) == env(g), and L is its own left envelope), written in place.
-// Positions fit a byte; a cleared table entry reads as position 0, which is
-// only consulted when a real entry for m exists (m >= u implies g[i*] == m
-// for the minimiser i* < u) or when position 0 is outside the window.
-// `tab` is the lane's column of a [256][32] byte table; the caller clears it
-// before each sweep.  Values are clamped at 255 by construction (m + 1 is
-// only taken when g[u] > m, so m < 255).
-// One step at sweep position j with input g; m is the running value.
-// nm = min(g, m + [last[m] + m < j]) is the case split above (g <= m gives g
-// either way); both candidates are formed while last[m] is in flight, so the
-// loop-carried chain is load -> compare -> select.
-// The table is addressed with 32-bit shared-window addresses and the
-// select is written in PTX so the compiler keeps it a select between the two
-// precomputed addresses (left to itself it re-derives the address from
-// min(g, m + up), four dependent ALU ops instead of two).
+//        = m+1  otherwise
+// (= min(g[u], m + [miss]), g[u] <= m giving g[u] either way), and one
+// table indexed by value decides it.  Backward: the same sweep over L
+// reversed gives the full envelope (env(L) == env(g), and L is its own left
+// envelope), written in place.  Values stay <= 255 (m + 1 is only taken when
+// g[u] > m).  `tab` is the lane's column of a [256][32] byte table (32-bit
+// shared-window address); the caller clears it before each sweep.
+//
+// Table entry of value v: min(255, last position of v + v).  The window test
+// last[m] + m >= u is then entry >= u (u <= 255, so saturation keeps it
+// exact), and a cleared entry (0) fails it for every u >= 1 -- correct, since
+// m >= u implies the minimiser i* < u has g[i*] == m, i.e. a real entry.
+// Table accesses are PTX with the select written out so the compiler keeps
+// the loop-carried chain at load -> compare -> select (left to itself it
+// re-derives the next address from min(g, m + miss): four dependent ops).
 __device__ __forceinline__ int lds_u8(uint32_t a) {
     uint32_t v;
     asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
@@ -205,93 +202,168 @@ __device__ __forceinline__ void sts_u8(uint32_t a, int v) {
     asm volatile("st.shared.u8 [%0], %1;" ::"r"(a), "r"(v) : "memory");
 }
 
-__device__ __forceinline__ uint32_t sweep_step(int &m, uint32_t &am, int g, int j,
-                                               uint32_t tab) {
-    const int lp = lds_u8(am);  // last[m]; am == tab + 32 * m
-    const int a0 = min(g, m), a1 = min(g, m + 1);
-    const uint32_t o0 = tab + 32u * (uint32_t)a0, o1 = tab + 32u * (uint32_t)a1;
-    int nm;
+// One step in "address space": M = tab + 32 m is the table entry of the
+// running value and G = tab + 32 g; min() commutes with that map, so the two
+// candidates are min(G, M) and min(G, M + 32).  Returns 32 * m.
+__device__ __forceinline__ uint32_t step_scaled(uint32_t &M, int g, int j, uint32_t tab) {
+    const uint32_t G = tab + 32u * (uint32_t)g;
+    const uint32_t a0 = min(G, M), a1 = min(G, M + 32u);
+    const int e = lds_u8(M);
+    uint32_t nM;
     asm("{\n\t.reg .pred p;\n\t"
-        "setp.lt.s32 p, %2, %3;\n\t"
-        "selp.b32 %0, %4, %5, p;\n\t"
-        "selp.b32 %1, %6, %7, p;\n\t}"
-        : "=r"(am), "=r"(nm)
-        : "r"(lp), "r"(j - m), "r"(o1), "r"(o0), "r"(a1), "r"(a0));
-    sts_u8(tab + 32u * (uint32_t)g, j);
-    m = nm;
-    return (uint32_t)nm;
+        "setp.lt.s32 p, %1, %2;\n\t"
+        "selp.b32 %0, %3, %4, p;\n\t}"
+        : "=r"(nM)
+        : "r"(e), "r"(j), "r"(a1), "r"(a0));
+    sts_u8(G, min(g + j, kDistClamp));
+    M = nM;
+    return M - tab;
 }
 
-// A line in a shared-memory tile: contiguous (row tiles) or strided by the
-// 32 lines of a [u][32] tile.  ld4/st4 move 4 consecutive elements as one
-// word (u % 4 == 0).
-template <bool kContig>
+// Four steps on one word of 4 consecutive elements (one PRMT per byte).
+// kRev walks the bytes high to low (backward sweep); j0 is the sweep position
+// of the first element handled.
+template <bool kRev>
+__device__ __forceinline__ uint32_t sweep_word(uint32_t &M, uint32_t w, int j0, uint32_t tab) {
+    uint32_t d[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const int byte = kRev ? 3 - k : k;
+        d[byte] = step_scaled(M, (int)__byte_perm(w, 0u, 0x4440u + byte), j0 + k, tab);
+    }
+    return (d[0] >> 5) | (d[1] << 3) | (d[2] << 11) | (d[3] << 19);
+}
+
+__device__ __forceinline__ uint4 sweep_chunk_fwd(uint32_t &M, uint4 c, int j0, uint32_t tab) {
+    uint4 o;
+    o.x = sweep_word<false>(M, c.x, j0, tab);
+    o.y = sweep_word<false>(M, c.y, j0 + 4, tab);
+    o.z = sweep_word<false>(M, c.z, j0 + 8, tab);
+    o.w = sweep_word<false>(M, c.w, j0 + 12, tab);
+    return o;
+}
+__device__ __forceinline__ uint4 sweep_chunk_bwd(uint32_t &M, uint4 c, int j0, uint32_t tab) {
+    uint4 o;
+    o.w = sweep_word<true>(M, c.w, j0, tab);
+    o.z = sweep_word<true>(M, c.z, j0 + 4, tab);
+    o.y = sweep_word<true>(M, c.y, j0 + 8, tab);
+    o.x = sweep_word<true>(M, c.x, j0 + 12, tab);
+    return o;
+}
+
+// Line layouts in a warp's shared-memory tile:
+//   kStrided: element u of lane l at tile[u * 32 + l] ([u][32] tile of lines
+//             along x or y);
+//   kRow:     contiguous row (sstride = 4 x odd, conflict-free 32-bit access);
+//   kRowSwz:  256 B-aligned rows of L % 128 == 0, 16-byte chunk c of row r
+//             stored at chunk c ^ (r & 7): each quarter-warp's 16-byte
+//             accesses hit 8 distinct bank groups.
+enum { kStrided = 0, kRow = 1, kRowSwz = 2 };
+
+template <int LAYOUT>
 struct TileLine {
-    uint8_t *p;
-    __device__ __forceinline__ int ld(int u) const { return p[kContig ? u : u * 32]; }
+    uint8_t *p;  // kStrided: tile + lane; rows: the lane's row
+    int lane;
+    __device__ __forceinline__ int ld(int u) const { return p[LAYOUT == kStrided ? u * 32 : u]; }
     __device__ __forceinline__ void st(int u, uint32_t v) const {
-        p[kContig ? u : u * 32] = (uint8_t)v;
+        p[LAYOUT == kStrided ? u * 32 : u] = (uint8_t)v;
     }
     __device__ __forceinline__ uint32_t ld4(int u) const {
-        if (kContig) return *reinterpret_cast<const uint32_t *>(p + u);
-        return (uint32_t)p[u * 32] | (uint32_t)p[(u + 1) * 32] << 8 |
-               (uint32_t)p[(u + 2) * 32] << 16 | (uint32_t)p[(u + 3) * 32] << 24;
+        return *reinterpret_cast<const uint32_t *>(p + u);
     }
     __device__ __forceinline__ void st4(int u, uint32_t v) const {
-        if (kContig) {
-            *reinterpret_cast<uint32_t *>(p + u) = v;
-        } else {
-            p[u * 32] = (uint8_t)v;
-            p[(u + 1) * 32] = (uint8_t)(v >> 8);
-            p[(u + 2) * 32] = (uint8_t)(v >> 16);
-            p[(u + 3) * 32] = (uint8_t)(v >> 24);
-        }
+        *reinterpret_cast<uint32_t *>(p + u) = v;
+    }
+    __device__ __forceinline__ uint4 *chunk(int c) const {
+        return reinterpret_cast<uint4 *>(p) + (c ^ (lane & 7));
     }
 };
 
-// Forward sweep in place.  Lengths divisible by 4 go a word at a time with
-// the next word loaded before this word's results are stored.
-template <bool kContig>
-__device__ __forceinline__ void sweep_forward(int len, TileLine<kContig> line, uint32_t tab) {
-    int m = kDistClamp;
-    uint32_t pm = tab + 32u * kDistClamp;
-    if ((len & 3) == 0) {
+// Forward sweep in place.  Every layout loads the next group of elements
+// before the current group's results are stored (the table accesses are
+// ordered PTX, so the compiler cannot hoist loads across them by itself).
+template <int LAYOUT>
+__device__ __forceinline__ void sweep_forward(int len, TileLine<LAYOUT> line, uint32_t tab) {
+    uint32_t M = tab + 32u * kDistClamp;
+    if (LAYOUT == kRowSwz) {
+        const int nc = len >> 4;
+        uint4 c = *line.chunk(0);
+        for (int cc = 0; cc < nc; ++cc) {
+            const uint4 nx = cc + 1 < nc ? *line.chunk(cc + 1) : make_uint4(0u, 0u, 0u, 0u);
+            *line.chunk(cc) = sweep_chunk_fwd(M, c, 16 * cc, tab);
+            c = nx;
+        }
+        return;
+    }
+    if (LAYOUT == kRow && (len & 3) == 0) {
         uint32_t w = line.ld4(0);
         for (int u = 0; u < len; u += 4) {
             const uint32_t wn = u + 4 < len ? line.ld4(u + 4) : 0u;
-            uint32_t o = sweep_step(m, pm, (int)(w & 0xFFu), u, tab);
-            o |= sweep_step(m, pm, (int)((w >> 8) & 0xFFu), u + 1, tab) << 8;
-            o |= sweep_step(m, pm, (int)((w >> 16) & 0xFFu), u + 2, tab) << 16;
-            o |= sweep_step(m, pm, (int)(w >> 24), u + 3, tab) << 24;
-            line.st4(u, o);
+            line.st4(u, sweep_word<false>(M, w, u, tab));
             w = wn;
         }
         return;
     }
-    for (int u = 0; u < len; ++u) line.st(u, sweep_step(m, pm, line.ld(u), u, tab));
+    if (LAYOUT == kStrided && (len & 3) == 0) {
+        int q0 = line.ld(0), q1 = line.ld(1), q2 = line.ld(2), q3 = line.ld(3);
+        for (int u = 0; u < len; u += 4) {
+            int n0 = 0, n1 = 0, n2 = 0, n3 = 0;
+            if (u + 4 < len) {
+                n0 = line.ld(u + 4), n1 = line.ld(u + 5), n2 = line.ld(u + 6), n3 = line.ld(u + 7);
+            }
+            line.st(u, step_scaled(M, q0, u, tab) >> 5);
+            line.st(u + 1, step_scaled(M, q1, u + 1, tab) >> 5);
+            line.st(u + 2, step_scaled(M, q2, u + 2, tab) >> 5);
+            line.st(u + 3, step_scaled(M, q3, u + 3, tab) >> 5);
+            q0 = n0, q1 = n1, q2 = n2, q3 = n3;
+        }
+        return;
+    }
+    for (int u = 0; u < len; ++u) line.st(u, step_scaled(M, line.ld(u), u, tab) >> 5);
 }
 
 // Backward sweep in place: sweep position j = len - 1 - u.
-template <bool kContig>
-__device__ __forceinline__ void sweep_backward(int len, TileLine<kContig> line, uint32_t tab) {
-    int m = kDistClamp;
-    uint32_t pm = tab + 32u * kDistClamp;
-    if ((len & 3) == 0) {
+template <int LAYOUT>
+__device__ __forceinline__ void sweep_backward(int len, TileLine<LAYOUT> line, uint32_t tab) {
+    uint32_t M = tab + 32u * kDistClamp;
+    if (LAYOUT == kRowSwz) {
+        const int nc = len >> 4;
+        uint4 c = *line.chunk(nc - 1);
+        for (int cc = nc - 1, j = 0; cc >= 0; --cc, j += 16) {
+            const uint4 nx = cc > 0 ? *line.chunk(cc - 1) : make_uint4(0u, 0u, 0u, 0u);
+            *line.chunk(cc) = sweep_chunk_bwd(M, c, j, tab);
+            c = nx;
+        }
+        return;
+    }
+    if (LAYOUT == kRow && (len & 3) == 0) {
         uint32_t w = line.ld4(len - 4);
         for (int u0 = len - 4, j = 0; u0 >= 0; u0 -= 4, j += 4) {
             const uint32_t wn = u0 >= 4 ? line.ld4(u0 - 4) : 0u;
-            uint32_t o = sweep_step(m, pm, (int)(w >> 24), j, tab) << 24;
-            o |= sweep_step(m, pm, (int)((w >> 16) & 0xFFu), j + 1, tab) << 16;
-            o |= sweep_step(m, pm, (int)((w >> 8) & 0xFFu), j + 2, tab) << 8;
-            o |= sweep_step(m, pm, (int)(w & 0xFFu), j + 3, tab);
-            line.st4(u0, o);
+            line.st4(u0, sweep_word<true>(M, w, j, tab));
             w = wn;
+        }
+        return;
+    }
+    if (LAYOUT == kStrided && (len & 3) == 0) {
+        int q0 = line.ld(len - 1), q1 = line.ld(len - 2), q2 = line.ld(len - 3),
+            q3 = line.ld(len - 4);
+        for (int u = len - 1, j = 0; u >= 0; u -= 4, j += 4) {
+            int n0 = 0, n1 = 0, n2 = 0, n3 = 0;
+            if (u >= 4) {
+                n0 = line.ld(u - 4), n1 = line.ld(u - 5), n2 = line.ld(u - 6), n3 = line.ld(u - 7);
+            }
+            line.st(u, step_scaled(M, q0, j, tab) >> 5);
+            line.st(u - 1, step_scaled(M, q1, j + 1, tab) >> 5);
+            line.st(u - 2, step_scaled(M, q2, j + 2, tab) >> 5);
+            line.st(u - 3, step_scaled(M, q3, j + 3, tab) >> 5);
+            q0 = n0, q1 = n1, q2 = n2, q3 = n3;
         }
         return;
     }
     for (int j = 0; j < len; ++j) {
         const int u = len - 1 - j;
-        line.st(u, sweep_step(m, pm, line.ld(u), j, tab));
+        line.st(u, step_scaled(M, line.ld(u), j, tab) >> 5);
     }
 }
 
@@ -379,6 +451,10 @@ __global__ void __launch_bounds__(128)
                       (size_t)warp * 32 * L + lane;
     const int64_t zblocks = ceil_div(bz, 32);
     const bool vec = (bz & 3) == 0;
+    // Swizzled 16-byte row tiles (the host sets sstride == L only when
+    // L % 128 == 0 and rows are 16-byte aligned).
+    const bool swz = kSweep && kRows && sstride == L && (L & 127) == 0;
+    const int cpr = L >> 4, csh = __ffs(cpr) - 1;  // chunks per row (power of 2 if swz)
     for (int64_t t = (int64_t)blockIdx.x * wpc + warp; t < tiles; t += (int64_t)gridDim.x * wpc) {
         uint8_t *g;
         int nlines;
@@ -388,7 +464,12 @@ __global__ void __launch_bounds__(128)
             const int64_t r0 = (t % per_p) * 32;
             nlines = (int)min((int64_t)32, rows - r0);
             g = pdms + (int64_t)p * pitch + r0 * bz;
-            if (vec) {
+            if (swz) {
+                for (int i = lane; i < nlines << csh; i += 32) {
+                    const int r = i >> csh, c = i & (cpr - 1);
+                    cpa::copy16(s + r * L + ((c ^ (r & 7)) << 4), g + (int64_t)r * bz + 16 * c);
+                }
+            } else if (vec) {
                 const int words = L >> 2;  // rows outer: no division per word
                 for (int r = 0; r < nlines; ++r)
                     for (int w = lane; w < words; w += 32)
@@ -432,13 +513,24 @@ __global__ void __launch_bounds__(128)
         auto ld = [&](int u) -> int { return line[u * es]; };
         auto st = [&](int u, int v) { line[u * es] = (uint8_t)v; };
         if (kSweep) {
-            clear_table(tab_warp, lane);
-            __syncwarp();
-            if (lane < nlines) sweep_forward(L, TileLine<kRows>{line}, tma::smem_u32(tab_warp + lane));
-            __syncwarp();
-            clear_table(tab_warp, lane);
-            __syncwarp();
-            if (lane < nlines) sweep_backward(L, TileLine<kRows>{line}, tma::smem_u32(tab_warp + lane));
+            const uint32_t tab = tma::smem_u32(tab_warp + lane);
+            for (int dir = 0; dir < 2; ++dir) {
+                clear_table(tab_warp, lane);
+                __syncwarp();
+                if (lane < nlines) {
+                    if (!kRows) {
+                        const TileLine<kStrided> tl{line, lane};
+                        dir == 0 ? sweep_forward(L, tl, tab) : sweep_backward(L, tl, tab);
+                    } else if (swz) {
+                        const TileLine<kRowSwz> tl{line, lane};
+                        dir == 0 ? sweep_forward(L, tl, tab) : sweep_backward(L, tl, tab);
+                    } else {
+                        const TileLine<kRow> tl{line, lane};
+                        dir == 0 ? sweep_forward(L, tl, tab) : sweep_backward(L, tl, tab);
+                    }
+                }
+                __syncwarp();
+            }
         } else if (lane < nlines) {
             if (kDist1D)
                 dist1d_line(L, ld, st);
@@ -449,7 +541,13 @@ __global__ void __launch_bounds__(128)
         }
         __syncwarp();
         if (kRows) {
-            if (vec) {
+            if (swz) {
+                for (int i = lane; i < nlines << csh; i += 32) {
+                    const int r = i >> csh, c = i & (cpr - 1);
+                    *reinterpret_cast<uint4 *>(g + (int64_t)r * bz + 16 * c) =
+                        *reinterpret_cast<const uint4 *>(s + r * L + ((c ^ (r & 7)) << 4));
+                }
+            } else if (vec) {
                 const int words = L >> 2;
                 for (int r = 0; r < nlines; ++r)
                     for (int w = lane; w < words; w += 32)
@@ -462,7 +560,13 @@ __global__ void __launch_bounds__(128)
                 }
             }
         } else {
-            if (nlines == 32 && vec) {
+            if (nlines == 32 && (bz & 15) == 0) {
+                for (int i = lane; i < L * 2; i += 32) {
+                    const int u = i >> 1, w = i & 1;
+                    *reinterpret_cast<uint4 *>(g + (int64_t)u * S + 16 * w) =
+                        *reinterpret_cast<const uint4 *>(s + u * 32 + 16 * w);
+                }
+            } else if (nlines == 32 && vec) {
                 for (int i = lane; i < L * 8; i += 32) {
                     const int u = i >> 3, w = i & 7;
                     *reinterpret_cast<uint32_t *>(g + (int64_t)u * S + 4 * w) =
@@ -677,7 +781,11 @@ static int tile_pass(int n, int64_t bx, int64_t by, int64_t bz, uint8_t *pdms, i
     const int64_t L = AXIS == kAxisX ? bx : (AXIS == kAxisY ? by : bz);
     int sw = (int)ceil_div(L, 4);
     if (sw % 2 == 0) sw += 1;
-    const int sstride = 4 * sw;
+    // Row tiles for the sweep with L % 128 == 0 and 16-byte aligned rows use
+    // unpadded 16-byte-swizzled rows (sstride == L); otherwise rows are
+    // padded to 4 x odd bytes.
+    const bool swz = kSweep && AXIS == kAxisZ && L % 128 == 0 && bz % 16 == 0;
+    const int sstride = swz ? (int)L : 4 * sw;
     const size_t per_warp = (AXIS == kAxisZ ? (size_t)32 * sstride : (size_t)32 * L) +
                             (kSweep ? (size_t)8192 : (!kDist1D && LMAX <= 64 ? (size_t)64 * L : 0));
     int wpc = (int)(65536 / per_warp);

@@ -78,6 +78,26 @@ def test_distance_transform_random_vs_oracle_medium():
         assert np.array_equal(got, oracle.distance_transform(occ)), dims
 
 
+@pytest.mark.parametrize("dims", [
+    (12, 128, 256),  # y strided with 16-byte tile copies, z swizzled 16-byte rows
+    (9, 256, 128),   # swizzled rows of 128
+    (7, 100, 48),    # 16-byte strided copies, padded rows (48 % 128 != 0)
+    (6, 61, 20),     # 4-byte copies, odd line length
+    (5, 30, 13),     # scalar tile copies, partial warp tiles
+    (300, 3, 256),   # x lines > 256 blocks (dist1d) with swizzled z rows
+])
+def test_distance_transform_tile_layouts(dims):
+    """Every shared-memory tile layout of the sweep envelope kernel against
+    the oracle, with far fields (values reaching the 255 clamp) and clusters."""
+    rng = np.random.default_rng(sum(dims))
+    for dens in (0.0, 0.00003, 0.002, 0.05):
+        occ = rng.random(dims) < dens
+        if dens == 0.0:
+            occ[tuple(int(rng.integers(0, d)) for d in dims)] = True
+        got = pdm.distance_transform(pdm.OccupancyMap(b=1, bdims=dims, occupied=occ)).dist
+        assert np.array_equal(got, oracle.distance_transform(occ)), (dims, dens)
+
+
 # --- golden volume cases ---------------------------------------------------------------
 
 @pytest.fixture(scope="module", params=CASES)
