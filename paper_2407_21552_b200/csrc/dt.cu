@@ -455,15 +455,25 @@ __global__ void __launch_bounds__(128)
     // L % 128 == 0 and rows are 16-byte aligned).
     const bool swz = kSweep && kRows && sstride == L && (L & 127) == 0;
     const int cpr = L >> 4, csh = __ffs(cpr) - 1;  // chunks per row (power of 2 if swz)
-    for (int64_t t = (int64_t)blockIdx.x * wpc + warp; t < tiles; t += (int64_t)gridDim.x * wpc) {
-        uint8_t *g;
-        int nlines;
-        if (kRows) {  // tile = 32 consecutive (x, y) rows of partition p
+    // Tile t: rows -> 32 consecutive (x, y) rows of partition p; strided ->
+    // 32 consecutive z of one line family (p, outer).
+    auto tile_at = [&](int64_t tt, int &nl) -> uint8_t * {
+        if (kRows) {
             const int64_t rows = bx * by, per_p = ceil_div(rows, 32);
-            const int p = (int)(t / per_p);
-            const int64_t r0 = (t % per_p) * 32;
-            nlines = (int)min((int64_t)32, rows - r0);
-            g = pdms + (int64_t)p * pitch + r0 * bz;
+            const int64_t r0 = (tt % per_p) * 32;
+            nl = (int)min((int64_t)32, rows - r0);
+            return pdms + (tt / per_p) * pitch + r0 * bz;
+        }
+        const int64_t outer_n = AXIS == kAxisX ? by : bx;
+        const int64_t po = tt / zblocks, z0 = (tt % zblocks) * 32;
+        const int64_t o = po % outer_n;
+        nl = (int)min((int64_t)32, bz - z0);
+        return pdms + (po / outer_n) * pitch + (AXIS == kAxisX ? o * bz : o * by * bz) + z0;
+    };
+    for (int64_t t = (int64_t)blockIdx.x * wpc + warp; t < tiles; t += (int64_t)gridDim.x * wpc) {
+        int nlines;
+        uint8_t *g = tile_at(t, nlines);
+        if (kRows) {
             if (swz) {
                 for (int i = lane; i < nlines << csh; i += 32) {
                     const int r = i >> csh, c = i & (cpr - 1);
@@ -480,14 +490,7 @@ __global__ void __launch_bounds__(128)
                     s[r * sstride + u] = g[(int64_t)r * bz + u];
                 }
             }
-        } else {  // tile = 32 consecutive z of one line family (p, outer)
-            const int64_t outer_n = AXIS == kAxisX ? by : bx;
-            const int64_t po = t / zblocks;
-            const int64_t z0 = (t % zblocks) * 32;
-            const int p = (int)(po / outer_n);
-            const int64_t o = po % outer_n;
-            nlines = (int)min((int64_t)32, bz - z0);
-            g = pdms + (int64_t)p * pitch + (AXIS == kAxisX ? o * bz : o * by * bz) + z0;
+        } else {
             if (nlines == 32 && (bz & 15) == 0) {  // 2 lanes per 32-byte row
                 for (int i = lane; i < L * 2; i += 32) {
                     const int u = i >> 1, w = i & 1;
@@ -716,6 +719,230 @@ __global__ void __launch_bounds__(128)
     }
 }
 
+// ---- streaming sweep: 4 lines per lane, only the tables in shared memory ----------
+// The tile kernels hold a 256-byte tile row and a 256-byte table per line
+// (16 KB per warp, 12 resident warps): the envelope's load -> compare ->
+// select chain then leaves the SM half idle.  Here the lines stay in global
+// memory -- the forward sweep reads g and writes L in place, the backward
+// sweep reads L back (an L2 hit: a warp's 32 KB of lines is revisited within
+// microseconds) and writes the result -- so shared memory holds only the
+// tables, [256 values][32 lanes][4 lines] bytes = 32 KB per warp, and an SM
+// keeps 7 warps x 128 lines in flight.  Each lane owns one bank of every
+// table row, so table accesses never conflict, and its 4 lines are 4
+// independent chains to interleave.  Register rings keep the loads of the
+// next elements in flight ahead of the chain.
+//   AXIS 1 (y lines): a warp = 128 consecutive z of one (p, x) plane; lane l
+//     has z0 + 4l .. +3, one 32-bit load/store per y (coalesced 512 B).
+//   AXIS 2 (z rows): a warp = 128 consecutive rows; lane l has rows
+//     r0 + 32t + l (t < 4), 16-byte loads/stores along each row.
+constexpr int kStreamTableBytes = 256 * 128;
+
+__device__ __forceinline__ uint32_t step_lane4(uint32_t &M, int g, int j, uint32_t tabt) {
+    const uint32_t G = tabt + 128u * (uint32_t)g;
+    const uint32_t a0 = min(G, M), a1 = min(G, M + 128u);
+    const int e = lds_u8(M);
+    uint32_t nM;
+    asm("{\n\t.reg .pred p;\n\t"
+        "setp.lt.s32 p, %1, %2;\n\t"
+        "selp.b32 %0, %3, %4, p;\n\t}"
+        : "=r"(nM)
+        : "r"(e), "r"(j), "r"(a1), "r"(a0));
+    sts_u8(G, min(g + j, kDistClamp));
+    M = nM;
+    return M - tabt;  // 128 * m
+}
+
+__device__ __forceinline__ void clear_stream_table(uint8_t *tab, int lane) {
+    uint4 *t = reinterpret_cast<uint4 *>(tab);
+#pragma unroll 8
+    for (int i = 0; i < kStreamTableBytes / 512; ++i) t[i * 32 + lane] = make_uint4(0u, 0u, 0u, 0u);
+}
+
+// One y position of the 4 lines of a lane: bytes of w are lines t = 0..3.
+__device__ __forceinline__ uint32_t step_word4(uint32_t (&M)[4], uint32_t w, int j, uint32_t tab) {
+    const uint32_t d0 = step_lane4(M[0], (int)__byte_perm(w, 0u, 0x4440u), j, tab);
+    const uint32_t d1 = step_lane4(M[1], (int)__byte_perm(w, 0u, 0x4441u), j, tab + 1);
+    const uint32_t d2 = step_lane4(M[2], (int)__byte_perm(w, 0u, 0x4442u), j, tab + 2);
+    const uint32_t d3 = step_lane4(M[3], (int)__byte_perm(w, 0u, 0x4443u), j, tab + 3);
+    return (d0 >> 7) | (d1 << 1) | (d2 << 9) | (d3 << 17);
+}
+
+template <bool kBackward>
+__device__ __forceinline__ void stream_y_sweep(uint8_t *base, int64_t bz, int L, bool act,
+                                               uint32_t tab) {
+    constexpr int R = 16;  // loads in flight ahead of the chain
+    uint32_t M[4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) M[t] = tab + t + 128u * kDistClamp;
+    auto addr = [&](int j) { return base + (int64_t)(kBackward ? L - 1 - j : j) * bz; };
+    // Loads are unconditional (clamped position; an inactive lane's base is
+    // lane 0's column): a predicated load into a ring slot makes the compiler
+    // merge old and new values with a move that waits on the load.
+    auto ld = [&](int j) {
+        const int jj = j < L ? j : L - 1;
+        return *reinterpret_cast<const uint32_t *>(base + (int64_t)(kBackward ? L - 1 - jj : jj) * bz);
+    };
+    uint32_t ring[R];
+#pragma unroll
+    for (int i = 0; i < R; ++i) ring[i] = ld(i);
+    for (int j0 = 0; j0 < L; j0 += R) {
+#pragma unroll
+        for (int i = 0; i < R; ++i) {
+            const int j = j0 + i;
+            if (j < L) {
+                const uint32_t w = ring[i];
+                ring[i] = ld(j + R);
+                const uint32_t o = step_word4(M, w, j, tab);
+                if (act) *reinterpret_cast<uint32_t *>(addr(j)) = o;
+            }
+        }
+    }
+}
+
+// 16 elements of each of the lane's 4 rows (chunk c of every row).
+template <bool kBackward>
+__device__ __forceinline__ void stream_z_chunk(uint32_t (&M)[4], const uint4 (&in)[4],
+                                               uint4 (&out)[4], int j0, uint32_t tab) {
+    uint32_t iw[4][4], ow[4][4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+        iw[t][0] = in[t].x, iw[t][1] = in[t].y, iw[t][2] = in[t].z, iw[t][3] = in[t].w;
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {  // word of the chunk, in sweep order
+        const int word = kBackward ? 3 - q : q;
+        uint32_t d[4][4];
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {  // byte of the word, in sweep order
+            const int byte = kBackward ? 3 - b : b;
+            const int j = j0 + 4 * q + b;
+#pragma unroll
+            for (int t = 0; t < 4; ++t)
+                d[t][byte] = step_lane4(M[t], (int)__byte_perm(iw[t][word], 0u, 0x4440u + byte), j,
+                                        tab + t);
+        }
+#pragma unroll
+        for (int t = 0; t < 4; ++t)
+            ow[t][word] = (d[t][0] >> 7) | (d[t][1] << 1) | (d[t][2] << 9) | (d[t][3] << 17);
+    }
+#pragma unroll
+    for (int t = 0; t < 4; ++t) out[t] = make_uint4(ow[t][0], ow[t][1], ow[t][2], ow[t][3]);
+}
+
+template <bool kBackward>
+__device__ __forceinline__ void stream_z_sweep(uint8_t *const (&row)[4], const bool (&act)[4],
+                                               int L, uint32_t tab) {
+    const int nc = L >> 4;
+    uint32_t M[4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) M[t] = tab + t + 128u * kDistClamp;
+    auto chunk = [&](int t, int c) {
+        return reinterpret_cast<uint4 *>(row[t]) + (kBackward ? nc - 1 - c : c);
+    };
+    // Unconditional loads (clamped chunk; inactive rows alias row 0 of the
+    // tile, which always exists): see stream_y_sweep.
+    uint4 cur[4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) cur[t] = *chunk(t, 0);
+    for (int c = 0; c < nc; ++c) {
+        uint4 nxt[4], out[4];
+        const int cn = c + 1 < nc ? c + 1 : c;
+#pragma unroll
+        for (int t = 0; t < 4; ++t) nxt[t] = *chunk(t, cn);
+        stream_z_chunk<kBackward>(M, cur, out, 16 * c, tab);
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            if (act[t]) *chunk(t, c) = out[t];
+            cur[t] = nxt[t];
+        }
+    }
+}
+
+constexpr int kStreamWarps = 7;  // 7 x 32 KB of tables: one CTA per SM
+
+// Tile geometry: AXIS 1 -> (p, x, 128 z) with `base` at z of lane 0;
+// AXIS 2 -> (p, 128 rows) with `base` at row 0.
+template <int AXIS>
+struct StreamTile {
+    uint8_t *base;
+    int64_t count;  // z (AXIS 1) or rows (AXIS 2) in the tile, <= 128
+};
+
+template <int AXIS>
+__device__ __forceinline__ StreamTile<AXIS> stream_tile(int64_t t, int64_t bx, int64_t by,
+                                                         int64_t bz, uint8_t *pdms,
+                                                         int64_t pitch) {
+    if (AXIS == kAxisY) {
+        const int64_t zt = ceil_div(bz, 128);
+        const int64_t px = t / zt, z0 = (t % zt) * 128;
+        return {pdms + (px / bx) * pitch + (px % bx) * by * bz + z0, min((int64_t)128, bz - z0)};
+    }
+    const int64_t rows = bx * by, rt = ceil_div(rows, 128);
+    const int64_t p = t / rt, r0 = (t % rt) * 128;
+    return {pdms + p * pitch + r0 * bz, min((int64_t)128, rows - r0)};
+}
+
+// Pull a tile's bytes into L2 ahead of its sweeps (the register rings then
+// wait on L2, not DRAM): y tiles are L rows of 128 B at stride bz, one
+// prefetch per row; z tiles are one contiguous span.
+template <int AXIS>
+__device__ __forceinline__ void stream_prefetch(const StreamTile<AXIS> &tl, int64_t bz, int L,
+                                                int lane) {
+    if (AXIS == kAxisY) {
+        for (int u = lane; u < L; u += 32)
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(tl.base + (int64_t)u * bz));
+    } else if (lane == 0) {
+        const uint32_t bytes = (uint32_t)(tl.count * bz);  // multiple of 16 (bz % 16 == 0)
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(tl.base), "r"(bytes)
+                     : "memory");
+    }
+}
+
+template <int AXIS>
+__global__ void __launch_bounds__(32 * kStreamWarps)
+    dt_stream_kernel(int n, int64_t bx, int64_t by, int64_t bz, uint8_t *__restrict__ pdms,
+                     int64_t pitch, int64_t tiles) {
+    extern __shared__ __align__(16) uint8_t s_tab[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint8_t *wtab = s_tab + (size_t)warp * kStreamTableBytes;
+    const uint32_t tab = tma::smem_u32(wtab) + 4u * lane;
+    const int L = (int)(AXIS == kAxisY ? by : bz);
+    const int64_t stride = (int64_t)gridDim.x * kStreamWarps;
+    int64_t t = (int64_t)blockIdx.x * kStreamWarps + warp;
+    if (t < tiles) stream_prefetch<AXIS>(stream_tile<AXIS>(t, bx, by, bz, pdms, pitch), bz, L, lane);
+    for (; t < tiles; t += stride) {
+        const StreamTile<AXIS> tl = stream_tile<AXIS>(t, bx, by, bz, pdms, pitch);
+        if (t + stride < tiles)
+            stream_prefetch<AXIS>(stream_tile<AXIS>(t + stride, bx, by, bz, pdms, pitch), bz, L,
+                                  lane);
+        uint8_t *row[4];
+        bool ract[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            ract[k] = 32 * k + lane < tl.count;
+            row[k] = tl.base + (ract[k] ? (int64_t)(32 * k + lane) * bz : 0);
+        }
+        const bool yact = 4 * lane < tl.count;
+        uint8_t *ybase = tl.base + (yact ? 4 * lane : 0);
+        for (int dir = 0; dir < 2; ++dir) {
+            clear_stream_table(wtab, lane);
+            __syncwarp();
+            if (AXIS == kAxisY) {
+                if (dir == 0)
+                    stream_y_sweep<false>(ybase, bz, L, yact, tab);
+                else
+                    stream_y_sweep<true>(ybase, bz, L, yact, tab);
+            } else {
+                if (dir == 0)
+                    stream_z_sweep<false>(row, ract, L, tab);
+                else
+                    stream_z_sweep<true>(row, ract, L, tab);
+            }
+            __syncwarp();
+        }
+    }
+}
+
 // ---- slab pieces --------------------------------------------------------------------
 __global__ void slab_edges_kernel(const uint8_t *__restrict__ pdms, int64_t pitch, int n,
                                   int64_t bx, int64_t plane, uint8_t *__restrict__ edges) {
@@ -809,6 +1036,35 @@ static int tile_pass(int n, int64_t bx, int64_t by, int64_t bz, uint8_t *pdms, i
     return cuda_status("dt_tile_kernel");
 }
 
+// Streaming sweep for lines <= 256: y lines need 4-byte aligned z runs, z
+// rows 16-byte aligned rows.  One warp per CTA, 32 KB of tables each.
+template <int AXIS>
+static int stream_pass(int n, int64_t bx, int64_t by, int64_t bz, uint8_t *pdms, int64_t pitch,
+                       cudaStream_t s) {
+    auto kern = dt_stream_kernel<AXIS>;
+    const int smem = kStreamWarps * kStreamTableBytes;
+    PDM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    const int64_t tiles = AXIS == kAxisY ? (int64_t)n * bx * ceil_div(bz, 128)
+                                         : (int64_t)n * ceil_div(bx * by, 128);
+    int64_t grid = ceil_div(tiles, kStreamWarps);
+    if (grid > sm_count()) grid = sm_count();
+    kern<<<(unsigned)grid, 32 * kStreamWarps, smem, s>>>(n, bx, by, bz, pdms, pitch, tiles);
+    return cuda_status("dt_stream_kernel");
+}
+
+static bool stream_enabled() {
+    static int on = -1;
+    if (on < 0) {
+        // PDM_DT_STREAM=1 selects the streaming sweep (A/B only).  Off by
+        // default: at config c passes y+z took 6.1 ms vs 1.53 ms for the tile
+        // kernels -- with only 7 warps per SM the register rings cannot cover
+        // the global load latency (long-scoreboard stalls ~5 per issue).
+        const char *e = getenv("PDM_DT_STREAM");
+        on = (e && e[0] == '1') ? 1 : 0;
+    }
+    return on == 1;
+}
+
 static bool sweep_enabled() {
     static int on = -1;
     if (on < 0) {
@@ -858,6 +1114,11 @@ static int axis_pass(int n, int64_t bx, int64_t by, int64_t bz, uint8_t *pdms, i
                      cudaStream_t s) {
     const int64_t L = AXIS == kAxisX ? bx : (AXIS == kAxisY ? by : bz);
     if (L <= 1) return PDM_OK;  // a 1-long line is already final
+    if constexpr (!kDist1D && AXIS != kAxisX) {
+        if (L <= 256 && stream_enabled() &&
+            (AXIS == kAxisY ? bz % 4 == 0 : bz % 16 == 0))
+            return stream_pass<AXIS>(n, bx, by, bz, pdms, pitch, s);
+    }
     if constexpr (!kDist1D) {
         if (L <= 256 && sweep_enabled())
             return tile_pass<256, AXIS, false, true>(n, bx, by, bz, pdms, pitch, s);
