@@ -719,6 +719,70 @@ __global__ void __launch_bounds__(128)
     }
 }
 
+// ---- x pass, wide tiles: 1-D distance of 4 lines per lane in 16-bit lanes -------
+// The 1-D distance has no lookup in its chain (run = nonzero ? run + 1 : 0),
+// so it is instruction bound; here each lane runs 4 adjacent z lines at once
+// as two u16x2 registers (even and odd bytes of a 32-bit word).  Runs are not
+// clamped while sweeping (they stay <= 255 + L <= 511, inside the 9-bit lane
+// mask) and are clamped with one VIMNMX.U16x2 on output.  Tile: [u][128 z]
+// bytes per warp, lane l owns z0 + 4l .. z0 + 4l + 3; lines <= 256.
+__device__ __forceinline__ uint32_t nonzero16(uint32_t x) {  // u16x2 lanes <= 255
+    return (((x + 0x00FF00FFu) >> 8) & 0x00010001u) * 0x1FFu;  // 0x1FF where x != 0
+}
+
+__global__ void __launch_bounds__(256)
+    dt_dist1d_wide_kernel(int n, int64_t bx, int64_t by, int64_t bz, uint8_t *__restrict__ pdms,
+                          int64_t pitch, int64_t tiles) {
+    extern __shared__ __align__(16) uint8_t s_wide[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, wpc = blockDim.x >> 5;
+    const int L = (int)bx;
+    const int64_t S = by * bz;
+    uint8_t *s = s_wide + (size_t)warp * 128 * L;
+    uint32_t *col = reinterpret_cast<uint32_t *>(s) + lane;  // word u at col[32 u]
+    const int64_t zq = ceil_div(bz, 128);
+    for (int64_t t = (int64_t)blockIdx.x * wpc + warp; t < tiles; t += (int64_t)gridDim.x * wpc) {
+        const int64_t py = t / zq, z0 = (t % zq) * 128;
+        const int nz = (int)min((int64_t)128, bz - z0);  // multiple of 16 (bz % 16 == 0)
+        uint8_t *g = pdms + (py / by) * pitch + (py % by) * bz + z0;
+        for (int i = lane; i < L * 8; i += 32) {
+            const int u = i >> 3, c = i & 7;
+            if (16 * c < nz) cpa::copy16(s + u * 128 + 16 * c, g + (int64_t)u * S + 16 * c);
+        }
+        cpa::commit();
+        cpa::wait<0>();
+        __syncwarp();
+        if (4 * lane < nz) {
+            uint32_t re = 0x00FF00FFu, ro = 0x00FF00FFu;  // "no occupied block yet" = 255
+            uint32_t w = col[0];
+            for (int u = 0; u < L; ++u) {
+                const uint32_t wn = u + 1 < L ? col[32 * (u + 1)] : 0u;
+                re = (re + 0x00010001u) & nonzero16(w & 0x00FF00FFu);
+                ro = (ro + 0x00010001u) & nonzero16((w >> 8) & 0x00FF00FFu);
+                col[32 * u] = __vminu2(re, 0x00FF00FFu) | (__vminu2(ro, 0x00FF00FFu) << 8);
+                w = wn;
+            }
+            re = ro = 0x00FF00FFu;
+            w = col[32 * (L - 1)];
+            for (int u = L - 1; u >= 0; --u) {
+                const uint32_t wn = u > 0 ? col[32 * (u - 1)] : 0u;
+                const uint32_t fe = w & 0x00FF00FFu, fo = (w >> 8) & 0x00FF00FFu;
+                re = (re + 0x00010001u) & nonzero16(fe);
+                ro = (ro + 0x00010001u) & nonzero16(fo);
+                col[32 * u] = __vminu2(re, fe) | (__vminu2(ro, fo) << 8);
+                w = wn;
+            }
+        }
+        __syncwarp();
+        for (int i = lane; i < L * 8; i += 32) {
+            const int u = i >> 3, c = i & 7;
+            if (16 * c < nz)
+                *reinterpret_cast<uint4 *>(g + (int64_t)u * S + 16 * c) =
+                    *reinterpret_cast<const uint4 *>(s + u * 128 + 16 * c);
+        }
+        __syncwarp();
+    }
+}
+
 // ---- streaming sweep: 4 lines per lane, only the tables in shared memory ----------
 // The tile kernels hold a 256-byte tile row and a 256-byte table per line
 // (16 KB per warp, 12 resident warps): the envelope's load -> compare ->
@@ -1052,6 +1116,39 @@ static int stream_pass(int n, int64_t bx, int64_t by, int64_t bz, uint8_t *pdms,
     return cuda_status("dt_stream_kernel");
 }
 
+static bool wide_enabled() {
+    static int on = -1;
+    if (on < 0) {
+        // PDM_DT_WIDE=0 keeps the per-lane x pass (A/B only).
+        const char *e = getenv("PDM_DT_WIDE");
+        on = (e && e[0] == '0') ? 0 : 1;
+    }
+    return on == 1;
+}
+
+// x pass (1-D distance along x) with 128-z tiles, 4 lines per lane.
+static int wide_x_pass(int n, int64_t bx, int64_t by, int64_t bz, uint8_t *pdms, int64_t pitch,
+                       cudaStream_t s) {
+    const size_t per_warp = (size_t)128 * bx;
+    int wpc = (int)((227 * 1024) / per_warp);
+    wpc = wpc < 1 ? 1 : (wpc > 8 ? 8 : wpc);
+    const size_t smem = per_warp * wpc;
+    PDM_CUDA_TRY(cudaFuncSetAttribute(dt_dist1d_wide_kernel,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const int64_t tiles = (int64_t)n * by * ceil_div(bz, 128);
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dt_dist1d_wide_kernel, 32 * wpc,
+                                                      smem) != cudaSuccess ||
+        per_sm < 1)
+        per_sm = 1;
+    int64_t grid = ceil_div(tiles, wpc);
+    const int64_t cap = (int64_t)sm_count() * per_sm;
+    if (grid > cap) grid = cap;
+    dt_dist1d_wide_kernel<<<(unsigned)grid, 32 * wpc, smem, s>>>(n, bx, by, bz, pdms, pitch,
+                                                                  tiles);
+    return cuda_status("dt_dist1d_wide_kernel");
+}
+
 static bool stream_enabled() {
     static int on = -1;
     if (on < 0) {
@@ -1114,6 +1211,9 @@ static int axis_pass(int n, int64_t bx, int64_t by, int64_t bz, uint8_t *pdms, i
                      cudaStream_t s) {
     const int64_t L = AXIS == kAxisX ? bx : (AXIS == kAxisY ? by : bz);
     if (L <= 1) return PDM_OK;  // a 1-long line is already final
+    if constexpr (kDist1D && AXIS == kAxisX) {
+        if (L <= 256 && bz % 16 == 0 && wide_enabled()) return wide_x_pass(n, bx, by, bz, pdms, pitch, s);
+    }
     if constexpr (!kDist1D && AXIS != kAxisX) {
         if (L <= 256 && stream_enabled() &&
             (AXIS == kAxisY ? bz % 4 == 0 : bz % 16 == 0))
