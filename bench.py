@@ -221,7 +221,13 @@ def run_b200(args, rank, world, local_rank):
     merge_ms = timed_pass(merge_only=True)
     ks = [k for k, _ in seq[warm:warm + steps]]
     total_ms = sum(step_ms)
-    merge_bytes = sum((k + 1) * B for k in ks)
+    merge_bytes = sum((k + 1) * B for k in ks)  # SURVEY.md §8(d) algorithmic bytes
+    packed = pset.packed()
+    if packed is not None:  # bytes the packed merge actually moves: nibbles + bases + D'
+        per_plane = -(-B // 32) * 2 * 9
+        moved_bytes = sum(k * per_plane + B for k in ks)
+    else:
+        moved_bytes = merge_bytes
 
     # parity spot check of the last step against the host-API path (untimed)
     last = pdm.PartitionSelection(
@@ -286,10 +292,15 @@ def run_b200(args, rank, world, local_rank):
                    "l2": "inputs > L2 (PDM set 537 MB/GPU); untimed L2 flush between steps "
                          "(256 MB write, then 256 MB read to drain dirty lines)",
                    "parallelism": f"x-slab x{world}, no collective on the update"},
-        "roofline": {"bound": "hbm", "kernel": "combine_flags_kernel (K7 merge)",
+        "roofline": {"bound": "hbm",
+                     "kernel": ("combine_packed_flags_kernel (K7 merge over nibble-packed planes)"
+                                if packed is not None else "combine_flags_kernel (K7 merge)"),
                      "achieved": round(achieved, 1), "peak": peak, "peak_kind": peak_kind,
                      "unit": "GB/s", "frac": round(achieved / peak, 4),
-                     "algorithmic_bytes": "(k+1) * num_blocks per launch",
+                     "algorithmic_bytes": "(k+1) * num_blocks per launch (SURVEY.md 8(d))",
+                     "moved_bytes_per_step": round(moved_bytes / steps),
+                     "moved_GBps": round(moved_bytes / (merge_total_ms * 1e-3) / 1e9, 1),
+                     "moved_frac": round(moved_bytes / (merge_total_ms * 1e-3) / 1e9 / peak, 4),
                      "traffic": traffic_from_profiles(), "merge_ms_per_step":
                          round(merge_total_ms / steps, 5)},
         "e2e": {"value": round(voxels_rank * world * steps / (e2e_ms * 1e-3) / 1e9, 2),

@@ -84,6 +84,30 @@ int pdm_combine(const uint8_t *pdms, int64_t plane_pitch, int64_t map_bytes, int
 int pdm_combine_flags(const uint8_t *pdms, int64_t plane_pitch, int64_t map_bytes, int32_t n,
                       const uint8_t *flags, uint8_t *out, pdm_stream_t stream);
 
+/* ---- nibble-packed planes (B200 storage for the merge) --------------------
+ * Each map is a clamped Chebyshev distance field, so 16 consecutive blocks of
+ * a z row span <= 15 values: chunk c (blocks 16c..16c+15) is stored as
+ * base[c] = its min plus 8 bytes of 4-bit offsets (nib[c], block 16c+2j in
+ * the low nibble of byte j).  No reference counterpart: an internal encoding
+ * of acceleration.py:89-99 PdmSet.pdms; the merge over it is bit-identical to
+ * pdm_combine.  pdm_packed_chunks(map_bytes) = chunks per plane (even, padded
+ * with 255); nib_pitch >= 8 * chunks, base_pitch >= chunks.  *violations
+ * (device) receives the number of chunks spanning > 15 values; the packed
+ * planes are valid only when it is 0. */
+int pdm_packed_chunks(int64_t map_bytes);
+int pdm_pack_pdms(const uint8_t *pdms, int64_t plane_pitch, int64_t map_bytes, int32_t n,
+                  uint8_t *nib, int64_t nib_pitch, uint8_t *base, int64_t base_pitch,
+                  uint32_t *violations, pdm_stream_t stream);
+
+/* pdm_combine over packed planes (k <= 240), and pdm_combine_flags over them
+ * (n <= 4096, PDL behind pdm_select).  Output: plain uint8 D'. */
+int pdm_combine_packed(const uint8_t *nib, int64_t nib_pitch, const uint8_t *base,
+                       int64_t base_pitch, int64_t map_bytes, int32_t n, const int32_t *sel,
+                       int32_t k, uint8_t *out, pdm_stream_t stream);
+int pdm_combine_flags_packed(const uint8_t *nib, int64_t nib_pitch, const uint8_t *base,
+                             int64_t base_pitch, int64_t map_bytes, int32_t n,
+                             const uint8_t *flags, uint8_t *out, pdm_stream_t stream);
+
 /* ---- block reduction / occupancy (K1-K5) --------------------------------- */
 
 /* volume.py:289-300 block_min_max: per-block min/max over the block grown by a

@@ -30,6 +30,10 @@ _SIGNATURES = {
     "pdm_alpha_support": [_P, _I64, _I64, _P, _P, _P],
     "pdm_combine": [_P, _I64, _I64, _I32, _P, _I32, _P, _P],
     "pdm_combine_flags": [_P, _I64, _I64, _I32, _P, _P, _P],
+    "pdm_packed_chunks": [_I64],
+    "pdm_pack_pdms": [_P, _I64, _I64, _I32, _P, _I64, _P, _I64, _P, _P],
+    "pdm_combine_packed": [_P, _I64, _P, _I64, _I64, _I32, _P, _I32, _P, _P],
+    "pdm_combine_flags_packed": [_P, _I64, _P, _I64, _I64, _I32, _P, _P, _P],
     "pdm_block_min_max": [_P, _INT, _I64, _I64, _I64, _I32, _P, _P, _P],
     "pdm_partition_mask_voxel": [_P, _INT, _I64, _I64, _I64, _I32, _P, _I32, _P, _I32, _P],
     "pdm_partition_mask_range_apron": [_P, _INT, _I64, _I64, _I64, _I32, _P, _I32, _P, _I32, _P],

@@ -12,6 +12,8 @@
 #include <cstring>
 #include <string>
 
+#include <cuda_fp16.h>
+
 #include "pdm_common.cuh"
 
 namespace pdm {
@@ -53,11 +55,6 @@ int sm_count() {
 // partition: a whole CTA (256) for wide partitions, a warp for narrow ones.
 // With PDL the dependent merge launches while this runs and waits on
 // griddepcontrol before it reads the flags.
-__device__ __forceinline__ void pdl_launch_dependents() {
-    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-}
-__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
-
 template <int kTPP>
 __global__ void __launch_bounds__(256)
     select_kernel(const double *__restrict__ alpha, int64_t stride,
@@ -130,19 +127,27 @@ struct SelParam {
 // the accumulator keeps the even and the odd bytes of each word in separate
 // 16-bit lanes (PRMT splits an input word), so folding one 16-byte chunk costs
 // 8 PRMT + 8 VIMNMX instead of 28 ops.
+// The 16-bit lanes hold byte v as the fp16 number 1024 + v (PRMT fills the
+// high byte with 0x64): same order, and the min is HMNMX2 on the FMA pipe
+// instead of VIMNMX.U16x2, which issues to the narrower XU pipe.
 struct ByteMin16 {
     uint32_t lo[4], hi[4];  // lanes hold bytes {0,2} / {1,3} of each word
 
+    __device__ __forceinline__ static uint32_t hmin2_bits(uint32_t a, uint32_t b) {
+        __half2 r = __hmin2(*reinterpret_cast<const __half2 *>(&a),
+                            *reinterpret_cast<const __half2 *>(&b));
+        return *reinterpret_cast<uint32_t *>(&r);
+    }
     __device__ __forceinline__ void init_ff() {
 #pragma unroll
-        for (int w = 0; w < 4; ++w) lo[w] = hi[w] = 0x00FF00FFu;
+        for (int w = 0; w < 4; ++w) lo[w] = hi[w] = 0x64FF64FFu;
     }
     __device__ __forceinline__ void fold(uint4 v) {
         const uint32_t x[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
         for (int w = 0; w < 4; ++w) {
-            lo[w] = __vminu2(lo[w], __byte_perm(x[w], 0u, 0x4240));
-            hi[w] = __vminu2(hi[w], __byte_perm(x[w], 0u, 0x4341));
+            lo[w] = hmin2_bits(lo[w], __byte_perm(x[w], 0x64646464u, 0x4240));
+            hi[w] = hmin2_bits(hi[w], __byte_perm(x[w], 0x64646464u, 0x4341));
         }
     }
     __device__ __forceinline__ uint4 result() const {
@@ -422,23 +427,6 @@ __global__ void combine_bytes_kernel(const uint8_t *__restrict__ pdms, int64_t p
             acc = v < acc ? v : acc;
         }
         out[c] = (uint8_t)acc;
-    }
-}
-
-// Warp 0 compacts flags[0..n) into a shared index list (ballot + popc).
-__device__ __forceinline__ void compact_flags(const uint8_t *__restrict__ flags, int n,
-                                              int32_t *s_idx, int *s_k) {
-    if (threadIdx.x < 32) {
-        const unsigned lane = threadIdx.x;
-        int k = 0;
-        for (int base = 0; base < n; base += 32) {
-            const int p = base + (int)lane;
-            const bool on = p < n && flags[p] != 0;
-            const unsigned bal = __ballot_sync(0xFFFFFFFFu, on);
-            if (on) s_idx[k + __popc(bal & ((1u << lane) - 1u))] = p;
-            k += __popc(bal);
-        }
-        if (lane == 0) *s_k = k;
     }
 }
 

@@ -70,6 +70,29 @@ __device__ __forceinline__ uint4 vmin_u8x16(uint4 a, uint4 b) {
                       __vminu4(a.w, b.w));
 }
 
+// ---- programmatic dependent launch (select kernel -> merge kernel) ----------
+__device__ __forceinline__ void pdl_launch_dependents() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+// Warp 0 compacts flags[0..n) into a shared index list (ballot + popc).
+__device__ __forceinline__ void compact_flags(const uint8_t *__restrict__ flags, int n,
+                                              int32_t *s_idx, int *s_k) {
+    if (threadIdx.x < 32) {
+        const unsigned lane = threadIdx.x;
+        int k = 0;
+        for (int base = 0; base < n; base += 32) {
+            const int p = base + (int)lane;
+            const bool on = p < n && flags[p] != 0;
+            const unsigned bal = __ballot_sync(0xFFFFFFFFu, on);
+            if (on) s_idx[k + __popc(bal & ((1u << lane) - 1u))] = p;
+            k += __popc(bal);
+        }
+        if (lane == 0) *s_k = k;
+    }
+}
+
 // ---- TMA bulk copies + mbarriers (sm_90+ async proxy, used on sm_100a) ------
 namespace tma {
 

@@ -295,3 +295,68 @@ def test_device_born_volume_matches_oracle_synth():
     assert vol.intensity_range == (int(host.min()), int(host.max()))
     part = synth.synth_volume_device(dims, bits, seed=11, nbox=8, x_range=(8, 30))
     assert np.array_equal(part.voxels, host[8:30])
+
+
+# --- nibble-packed merge planes (csrc/packed.cu) ---------------------------------------
+
+@pytest.mark.parametrize("dims,b,bits,n,packs", [
+    ((64, 40, 64), 4, 16, 32, True),    # z rows of 16 blocks
+    ((40, 36, 48), 4, 8, 12, True),     # rows of 12: chunks straddle rows, still <= 11 apart
+    ((3, 5, 16), 1, 8, 4, True),        # 240 blocks: last 32-block item is partial
+    ((9, 7, 40), 1, 8, 6, None),        # rows of 40: straddling chunks may span > 15
+])
+def test_packed_merge_matches_oracle(dims, b, bits, n, packs):
+    rng = np.random.default_rng(sum(dims) * n)
+    vox = random_structured_volume(rng, dims, bits)
+    vol = pdm.Volume.from_array(vox)
+    grid = pdm.BlockGrid.for_dims(dims, b)
+    scheme = pdm.scheme_uniform(n, bits)
+    pset = pdm.build_pdm_set(vol, grid, scheme)
+    maps = oracle.build_pdm_set(vox, b, scheme.bounds(), "range_apron")
+    if packs is not None:
+        assert (pset.packed() is not None) == packs
+    for trial in range(24):
+        k = int(rng.integers(1, n + 1)) if trial else n
+        s = sorted(rng.choice(np.arange(1, n + 1), size=k, replace=False).tolist())
+        got = pdm.combine(pset, pdm.PartitionSelection(selected=frozenset(s), n=n))
+        assert np.array_equal(got.dist, oracle.combine(maps, s)), (k, s)
+        lut = np.zeros((1 << bits, 4))
+        for i in s:
+            part = scheme.partitions[i - 1]
+            lut[part.rho_lo: part.rho_hi + 1, 3] = 0.25
+        dev = pdm.update_from_tf(pset, pdm.TransferFunction(lut=lut))
+        assert np.array_equal(dev.device().cpu().numpy(), oracle.combine(maps, s)), (k, s)
+
+
+def test_packed_planes_decode_to_the_raw_planes():
+    """Unpack the device's packed planes on the host: base + nibbles == raw."""
+    rng = np.random.default_rng(12)
+    dims = (48, 32, 64)
+    vox = random_structured_volume(rng, dims, 16)
+    pset = pdm.build_pdm_set(pdm.Volume.from_array(vox), pdm.BlockGrid.for_dims(dims, 4),
+                             pdm.scheme_uniform(8, 16))
+    nib, nib_pitch, base, base_pitch = pset.packed()
+    nb = pset.grid.num_blocks
+    chunks = -(-nb // 32) * 2
+    nib = nib.cpu().numpy()[:, :chunks * 8].reshape(8, chunks, 8)
+    base = base.cpu().numpy()[:, :chunks]
+    vals = np.empty((8, chunks, 16), np.int64)
+    vals[:, :, 0::2] = nib & 15
+    vals[:, :, 1::2] = nib >> 4
+    vals += base[:, :, None]
+    raw = np.stack([d.dist.reshape(-1) for d in pset.pdms])
+    assert np.array_equal(vals.reshape(8, -1)[:, :nb], raw)
+    assert pset.device_bytes() == 8 * (pset.plane_pitch + nib_pitch + base_pitch)
+
+
+def test_packed_skipped_for_maps_that_are_not_distance_fields():
+    rng = np.random.default_rng(13)
+    bdims = (6, 5, 32)
+    maps = [rng.integers(0, 256, bdims).astype(np.uint8) for _ in range(5)]
+    grid = pdm.BlockGrid.for_dims(bdims, 1)
+    pset = pdm.PdmSet(grid=grid, scheme=pdm.scheme_uniform(5, 8),
+                      pdms=tuple(pdm.DistanceMap(1, bdims, m) for m in maps))
+    s = [1, 3, 4]
+    got = pdm.combine(pset, pdm.PartitionSelection(selected=frozenset(s), n=5)).dist
+    assert pset.packed() is None
+    assert np.array_equal(got, np.minimum.reduce([maps[i - 1] for i in s]))

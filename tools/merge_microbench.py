@@ -11,6 +11,7 @@ from __future__ import annotations
 import argparse
 import ctypes
 import json
+import os
 import sys
 from pathlib import Path
 
@@ -30,11 +31,21 @@ def main():
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--ks", type=int, nargs="+", default=[1, 2, 4, 8, 16, 24, 32])
     ap.add_argument("--no-host", action="store_true", help="skip the D' to host section")
+    ap.add_argument("--packed", action="store_true",
+                    help="also time pdm_combine_packed (planes are random walks along z, "
+                         "so they pack)")
     args = ap.parse_args()
     L = _lib.lib()
     nb, n = args.blocks, args.n
     pitch = device.plane_pitch(nb)
-    pdms = torch.randint(0, 256, (n, pitch), dtype=torch.uint8, device="cuda")
+    if args.packed:  # 1-Lipschitz rows of 256 blocks, like distance fields
+        steps = torch.randint(-1, 2, (n, pitch // 256, 256), dtype=torch.int16, device="cuda")
+        start = torch.randint(0, 256, (n, pitch // 256, 1), dtype=torch.int16, device="cuda")
+        walk = (start + steps.cumsum(2)).clamp_(0, 255)
+        pdms = walk.to(torch.uint8).reshape(n, pitch).contiguous()
+        del steps, start, walk
+    else:
+        pdms = torch.randint(0, 256, (n, pitch), dtype=torch.uint8, device="cuda")
     out = torch.empty(nb, dtype=torch.uint8, device="cuda")
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     drain = torch.zeros(32 << 20, dtype=torch.int64, device="cuda")
@@ -66,6 +77,38 @@ def main():
         res[k] = {"ms": round(ms, 5), "GB/s": round(gbs, 1)}
         want = pdms[:k, :nb].min(dim=0).values
         assert torch.equal(out, want)
+    packed = {}
+    if args.packed:
+        chunks = int(L.pdm_packed_chunks(nb))
+        nib_pitch, base_pitch = -(-chunks * 8 // 256) * 256, -(-chunks // 256) * 256
+        nib = torch.empty((n, nib_pitch), dtype=torch.uint8, device="cuda")
+        base = torch.empty((n, base_pitch), dtype=torch.uint8, device="cuda")
+        bad = torch.zeros(1, dtype=torch.int32, device="cuda")
+        _lib.check(L.pdm_pack_pdms(_lib.ptr(pdms), pitch, nb, n, _lib.ptr(nib), nib_pitch,
+                                   _lib.ptr(base), base_pitch, _lib.ptr(bad), st), "pack")
+        assert int(bad.item()) == 0
+        for k in args.ks:
+            if k > n:
+                break
+            sel = np.ascontiguousarray(np.arange(k), dtype=np.int32)
+            ts = []
+            for r in range(args.reps + 3):
+                _Flush.fill_(r & 0xFF)
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                _lib.check(L.pdm_combine_packed(_lib.ptr(nib), nib_pitch, _lib.ptr(base),
+                                                base_pitch, nb, n, sel.ctypes.data, k,
+                                                _lib.ptr(out), st), "pdm_combine_packed")
+                e1.record()
+                torch.cuda.synchronize()
+                if r >= 3:
+                    ts.append(e0.elapsed_time(e1))
+            ms = float(np.median(ts))
+            moved = k * nb * 9 / 16 + nb
+            packed[k] = {"ms": round(ms, 5), "moved GB/s": round(moved / (ms * 1e-3) / 1e9, 1),
+                         "effective GB/s": round((k + 1) * nb / (ms * 1e-3) / 1e9, 1)}
+            if not os.environ.get("PDM_MB_NOCHECK"):
+                assert torch.equal(out, pdms[:k, :nb].min(dim=0).values)
     # floor for the same bytes as k=1: a plain device copy of one map
     ts = []
     for r in range(args.reps + 3):
@@ -85,17 +128,24 @@ def main():
     host = torch.empty(nb, dtype=torch.uint8, pin_memory=True)
     for k in (() if args.no_host else (1, 16, 32)):
         sel = np.ascontiguousarray(np.arange(k), dtype=np.int32)
-        for mode in ("hbm+d2h", "zero-copy"):
+        modes = ("hbm+d2h", "zero-copy") + (("packed hbm+d2h", "packed zero-copy")
+                                             if args.packed else ())
+        for mode in modes:
             ts = []
             for r in range(8):
                 _Flush.fill_(r & 0xFF)
                 torch.cuda.synchronize()
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record()
-                dst = out if mode == "hbm+d2h" else host
-                _lib.check(L.pdm_combine(_lib.ptr(pdms), pitch, nb, n, sel.ctypes.data, k,
-                                         _lib.ptr(dst), st), "pdm_combine")
-                if mode == "hbm+d2h":
+                dst = out if mode.endswith("hbm+d2h") else host
+                if mode.startswith("packed"):
+                    _lib.check(L.pdm_combine_packed(_lib.ptr(nib), nib_pitch, _lib.ptr(base),
+                                                    base_pitch, nb, n, sel.ctypes.data, k,
+                                                    _lib.ptr(dst), st), "pdm_combine_packed")
+                else:
+                    _lib.check(L.pdm_combine(_lib.ptr(pdms), pitch, nb, n, sel.ctypes.data, k,
+                                             _lib.ptr(dst), st), "pdm_combine")
+                if mode.endswith("hbm+d2h"):
                     host.copy_(out, non_blocking=True)
                 e1.record()
                 torch.cuda.synchronize()
@@ -104,7 +154,7 @@ def main():
             ms = float(np.median(ts))
             to_host[f"{mode} k={k}"] = {"ms": round(ms, 4), "PCIe GB/s": round(nb / ms / 1e6, 1)}
             assert torch.equal(host.cuda(), pdms[:k, :nb].min(dim=0).values)
-    print(json.dumps({"blocks": nb, "n": n, "merge": res, "to_host": to_host}))
+    print(json.dumps({"blocks": nb, "n": n, "merge": res, "packed": packed, "to_host": to_host}))
 
 
 if __name__ == "__main__":
