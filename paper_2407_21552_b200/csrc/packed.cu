@@ -250,7 +250,8 @@ static int packed_grid(K kernel, int64_t map_bytes) {
 // SM (Little's law at ~3 us loaded HBM latency): 4 planes x 18 B x 1280
 // threads ~ 92 KB/SM gives ~3.9 TB/s of packed bytes; 6 and 8 need 63-64+
 // registers, drop to 3-4 CTAs and measured no faster (k=32: 82.9 / 95.8 us
-// vs 81.9 us).
+// vs 81.9 us).  One 16-block chunk per thread (8-register accumulator, 8-byte
+// loads, 8 or 12 planes per batch) measured slower too (k=32: 87 us).
 static int packed_batch() {
     static int b = 0;
     if (b == 0) {
