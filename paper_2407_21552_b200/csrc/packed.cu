@@ -251,7 +251,11 @@ static int packed_grid(K kernel, int64_t map_bytes) {
 // threads ~ 92 KB/SM gives ~3.9 TB/s of packed bytes; 6 and 8 need 63-64+
 // registers, drop to 3-4 CTAs and measured no faster (k=32: 82.9 / 95.8 us
 // vs 81.9 us).  One 16-block chunk per thread (8-register accumulator, 8-byte
-// loads, 8 or 12 planes per batch) measured slower too (k=32: 87 us).
+// loads, 8 or 12 planes per batch) measured slower too (k=32: 87 us).  A
+// dominance skip (read the selected planes' bases first, then only the
+// nibbles of planes whose base is within 15 of the chunk minimum) is exact but
+// measured slower at config c (63.4 vs 51.2 us per step): the dependent
+// second round of loads costs more latency than the skipped bytes save.
 static int packed_batch() {
     static int b = 0;
     if (b == 0) {
