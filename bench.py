@@ -307,7 +307,10 @@ def run_b200(args, rank, world, local_rank):
                          round(merge_total_ms / steps, 5)},
         "e2e": {"value": round(voxels_rank * world * steps / (e2e_ms * 1e-3) / 1e9, 2),
                 "unit": "Gvoxel/s", "ms_per_step": round(e2e_ms / steps, 4),
-                "h2d_bytes_per_step": span * 8, "d2h_bytes_per_step": n + B,
+                "h2d_bytes_per_step": span * 8,
+                "d2h_bytes_per_step": (-(-B // 32) * 2 * 9) if packed is not None else B,
+                "d2h_format": ("packed D' (base + 4-bit offsets per 16 blocks), expanded on "
+                               "the host" if packed is not None else "uint8 D'"),
                 "api": "select_partitions(tf, scheme) + combine(pdm_set, sel) + .dist",
                 "breakdown_ms": {"select_partitions": e2e_parts_ms[0], "combine_launch": e2e_parts_ms[1], "dist_merge_d2h": e2e_parts_ms[2]}},
         "gpu_launches": 2 * steps,

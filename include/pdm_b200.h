@@ -108,6 +108,23 @@ int pdm_combine_flags_packed(const uint8_t *nib, int64_t nib_pitch, const uint8_
                              int64_t base_pitch, int64_t map_bytes, int32_t n,
                              const uint8_t *flags, uint8_t *out, pdm_stream_t stream);
 
+/* The same two merges writing D' itself in the packed encoding (out_nib: 8 *
+ * chunks bytes, out_base: chunks bytes, 16/2-byte aligned) -- 9/16 of the
+ * bytes, for a D' headed to host memory over PCIe (combine(...).dist), where
+ * pdm_unpack_packed_host expands it into map_bytes plain bytes (host
+ * function, SSE2 + OpenMP; no device work). */
+int pdm_combine_packed_to_packed(const uint8_t *nib, int64_t nib_pitch, const uint8_t *base,
+                                 int64_t base_pitch, int64_t map_bytes, int32_t n,
+                                 const int32_t *sel, int32_t k, uint8_t *out_nib,
+                                 uint8_t *out_base, pdm_stream_t stream);
+int pdm_combine_flags_packed_to_packed(const uint8_t *nib, int64_t nib_pitch,
+                                       const uint8_t *base, int64_t base_pitch,
+                                       int64_t map_bytes, int32_t n, const uint8_t *flags,
+                                       uint8_t *out_nib, uint8_t *out_base,
+                                       pdm_stream_t stream);
+int pdm_unpack_packed_host(const uint8_t *nib, const uint8_t *base, int64_t map_bytes,
+                           uint8_t *out);
+
 /* ---- block reduction / occupancy (K1-K5) --------------------------------- */
 
 /* volume.py:289-300 block_min_max: per-block min/max over the block grown by a

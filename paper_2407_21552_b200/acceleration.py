@@ -75,6 +75,7 @@ class _BlockArray:
         self._host = None
         self._dev = None
         self._pending = None  # producer(out_tensor) for deferred results
+        self._pending_host = None  # producer(host ndarray), if the host view has its own path
         shape = tuple(data.shape)
         if shape != self.bdims:
             raise ValueError(f"{field} array shape does not match bdims")
@@ -84,21 +85,29 @@ class _BlockArray:
             self._dev = data
 
     @classmethod
-    def _deferred(cls, b, bdims, producer):
+    def _deferred(cls, b, bdims, producer, host_producer=None):
         """A result whose kernel is launched on first access: into HBM for
         .device(), or straight into pinned host memory for the host view (the
         kernel's stores then stream over PCIe while it runs, so the
-        download costs no separate copy)."""
+        download costs no separate copy).  ``host_producer(ndarray)``, when
+        given, fills the host view its own way (e.g. a packed D' over PCIe,
+        expanded on the host)."""
         self = cls.__new__(cls)
         self.b = int(b)
         self.bdims = tuple(int(v) for v in bdims)
         self._host = None
         self._dev = None
         self._pending = producer
+        self._pending_host = host_producer
         return self
 
     def _host_array(self):
         if self._host is None:
+            if self._dev is None and self._pending_host is not None:
+                host = np.empty(self.bdims, dtype=np.uint8)
+                self._pending_host(host)
+                self._host = host
+                return self._host
             if self._dev is None and self._pending is not None:
                 t = device.torch()
                 host_t = t.empty(self.bdims, dtype=t.uint8, pin_memory=True)
@@ -265,6 +274,18 @@ class PdmSet:
             self._finish_pack(self._start_pack())
         return self._packed or None
 
+    def _host_stage(self):
+        """Pinned host buffers receiving a packed D' (reused across merges;
+        each host merge synchronises before returning)."""
+        stage = getattr(self, "_stage", None)
+        if stage is None:
+            t = device.torch()
+            chunks = int(_lib.lib().pdm_packed_chunks(self.grid.num_blocks))
+            stage = (t.empty(chunks * 8, dtype=t.uint8, pin_memory=True),
+                     t.empty(chunks, dtype=t.uint8, pin_memory=True))
+            self._stage = stage
+        return stage
+
     def drop_packed(self) -> None:
         """Forget the packed copy (after writing into ``storage``)."""
         self._packed = None
@@ -430,8 +451,16 @@ def combine(pdm_set: PdmSet, selection: PartitionSelection,
     if (flags is not None and selection._selected is None and max_maps_per_pass is None
             and pdm_set.n <= _MAX_FLAGS):
         # selection still on the device (select_partitions): no host round trip
+        def host_produce(host):
+            packed = pdm_set.packed()
+            nib, nib_pitch, base, base_pitch = packed
+            _packed_to_host(pdm_set, host, lambda L, on, ob, st: L.pdm_combine_flags_packed_to_packed(
+                _lib.ptr(nib), nib_pitch, _lib.ptr(base), base_pitch, grid.num_blocks,
+                pdm_set.n, _lib.ptr(flags), on, ob, st), "pdm_combine_flags_packed_to_packed")
+
         return DistanceMap._deferred(grid.b, grid.bdims,
-                                     lambda out: combine_flags_into(pdm_set, flags, out))
+                                     lambda out: combine_flags_into(pdm_set, flags, out),
+                                     host_produce if pdm_set.packed() is not None else None)
     indices = selection.sorted
     if indices and max_maps_per_pass is not None and max_maps_per_pass < 1:
         raise ValueError(f"max_maps_per_pass must be >= 1, got {max_maps_per_pass}")
@@ -457,7 +486,28 @@ def combine(pdm_set: PdmSet, selection: PartitionSelection,
                                  sel.ctypes.data if sel.size else None, int(sel.size),
                                  _lib.ptr(out), _lib.stream_handle()), "pdm_combine")
 
-    return DistanceMap._deferred(grid.b, grid.bdims, produce)
+    def host_produce(host):
+        nib, nib_pitch, base, base_pitch = pdm_set.packed()
+        _packed_to_host(pdm_set, host, lambda L, on, ob, st: L.pdm_combine_packed_to_packed(
+            _lib.ptr(nib), nib_pitch, _lib.ptr(base), base_pitch, grid.num_blocks, pdm_set.n,
+            sel.ctypes.data, int(sel.size), on, ob, st), "pdm_combine_packed_to_packed")
+
+    use_host_packed = 0 < sel.size <= _MAX_PACKED_SEL and pdm_set.packed() is not None
+    return DistanceMap._deferred(grid.b, grid.bdims, produce,
+                                 host_produce if use_host_packed else None)
+
+
+def _packed_to_host(pdm_set: PdmSet, host: np.ndarray, launch, name: str) -> None:
+    """D' for the host: the merge writes it packed (9/16 of the bytes) into
+    pinned staging buffers over PCIe, then the host expands it in place."""
+    L = _lib.lib()
+    nib_h, base_h = pdm_set._host_stage()
+    st = _lib.stream_handle()
+    _lib.check(launch(L, _lib.ptr(nib_h), _lib.ptr(base_h), st), name)
+    device.torch().cuda.current_stream().synchronize()
+    _lib.check(L.pdm_unpack_packed_host(_lib.ptr(nib_h), _lib.ptr(base_h),
+                                        pdm_set.grid.num_blocks, host.ctypes.data),
+               "pdm_unpack_packed_host")
 
 
 def update_from_tf(pdm_set: PdmSet, tf, out=None, flags=None) -> DistanceMap:

@@ -23,6 +23,7 @@
 // and 4 PRMTs per 8 blocks restore byte order once at the end.
 
 #include <cuda_fp16.h>
+#include <emmintrin.h>
 
 #include <cstdlib>
 
@@ -129,6 +130,34 @@ struct PackedAcc {
             }
         }
     }
+    // Re-pack the merged 32 blocks (2 chunks) in the storage encoding: each
+    // chunk's min as its base, 4-bit offsets in the same nibble layout (the
+    // lanes of a[w][s] are exactly nibbles s and s+4 of word w).  D' is a
+    // distance field too, so every chunk spans <= 15 values.
+    __device__ __forceinline__ void encode(uint4 &nibs, uint32_t &bases) const {
+        uint32_t mn[2];
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+            uint32_t m = a[2 * c][0];
+#pragma unroll
+            for (int i = 2 * c; i < 2 * c + 2; ++i)
+#pragma unroll
+                for (int s = 0; s < 4; ++s) m = hmin2_bits(m, a[i][s]);
+            m = hmin2_bits(m, __byte_perm(m, 0u, 0x1032));  // fold the two lanes
+            mn[c] = m & 0xFFu;
+        }
+        uint32_t w[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const uint32_t bb = mn[i >> 1] * 0x00010001u + kHalfBias;
+            uint32_t v = 0;
+#pragma unroll
+            for (int s = 0; s < 4; ++s) v |= (a[i][s] - bb) << (4 * s);
+            w[i] = v;
+        }
+        nibs = make_uint4(w[0], w[1], w[2], w[3]);
+        bases = mn[0] | (mn[1] << 8);
+    }
     // 32 blocks in byte order.
     __device__ __forceinline__ void result(uint4 &lo, uint4 &hi) const {
         uint32_t o[8];
@@ -152,12 +181,16 @@ __device__ __forceinline__ uint32_t ld_stream_u16(const void *p) {
 
 // Thread item t covers blocks [32t, 32t + 32).  Items past the last full one
 // (map_bytes % 32) write byte by byte.
-template <int B>  // selected planes per load batch
+// kPackOut: write D' in the packed encoding (out = 16 nibble bytes per item,
+// out_base = 2 base bytes per item) -- 9/16 of the bytes, for D' headed to
+// the host over PCIe (unpacked there by pdm_unpack_packed_host).
+template <int B, bool kPackOut>  // B: selected planes per load batch
 __device__ __forceinline__ void merge_packed(const uint8_t *__restrict__ nib, int64_t nib_pitch,
                                              const uint8_t *__restrict__ base,
                                              int64_t base_pitch, int64_t map_bytes,
                                              const int32_t *idx, int k,
-                                             uint8_t *__restrict__ out) {
+                                             uint8_t *__restrict__ out,
+                                             uint8_t *__restrict__ out_base) {
     const int64_t items = ceil_div(map_bytes, 32);
     const int64_t T = (int64_t)gridDim.x * blockDim.x;
     for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < items; t += T) {
@@ -178,6 +211,14 @@ __device__ __forceinline__ void merge_packed(const uint8_t *__restrict__ nib, in
             for (int j = 0; j < B; ++j)
                 if (m + j < k) acc.fold(q[j], b[j]);
         }
+        if (kPackOut) {
+            uint4 nibs;
+            uint32_t bases;
+            acc.encode(nibs, bases);
+            st_stream_u4(out + t * 16, nibs);
+            *reinterpret_cast<uint16_t *>(out_base + t * 2) = (uint16_t)bases;
+            continue;
+        }
         uint4 lo, hi;
         acc.result(lo, hi);
         uint8_t *dst = out + t * 32;
@@ -191,28 +232,31 @@ __device__ __forceinline__ void merge_packed(const uint8_t *__restrict__ nib, in
     }
 }
 
-template <int B>
+template <int B, bool kPackOut>
 __global__ void __launch_bounds__(kPackedThreads, B >= 6 ? 4 : 5)
     combine_packed_kernel(const uint8_t *__restrict__ nib, int64_t nib_pitch,
                           const uint8_t *__restrict__ base, int64_t base_pitch, int64_t map_bytes,
-                          const __grid_constant__ PackedSel sel, uint8_t *__restrict__ out) {
-    merge_packed<B>(nib, nib_pitch, base, base_pitch, map_bytes, sel.idx, sel.k, out);
+                          const __grid_constant__ PackedSel sel, uint8_t *__restrict__ out,
+                          uint8_t *__restrict__ out_base) {
+    merge_packed<B, kPackOut>(nib, nib_pitch, base, base_pitch, map_bytes, sel.idx, sel.k, out,
+                              out_base);
 }
 
 // Selection resident on the device (written by the select kernel ahead of it
 // in the stream, PDL): every CTA compacts the flags, then merges.
-template <int B>
+template <int B, bool kPackOut>
 __global__ void __launch_bounds__(kPackedThreads, B >= 6 ? 4 : 5)
     combine_packed_flags_kernel(const uint8_t *__restrict__ nib, int64_t nib_pitch,
                                 const uint8_t *__restrict__ base, int64_t base_pitch,
                                 int64_t map_bytes, int n, const uint8_t *__restrict__ flags,
-                                uint8_t *__restrict__ out) {
+                                uint8_t *__restrict__ out, uint8_t *__restrict__ out_base) {
     __shared__ int32_t s_idx[kPackedMaxFlags];
     __shared__ int s_k;
     pdl_wait();
     compact_flags(flags, n, s_idx, &s_k);
     __syncthreads();
-    merge_packed<B>(nib, nib_pitch, base, base_pitch, map_bytes, s_idx, s_k, out);
+    merge_packed<B, kPackOut>(nib, nib_pitch, base, base_pitch, map_bytes, s_idx, s_k, out,
+                              out_base);
 }
 
 template <class K>
@@ -245,31 +289,83 @@ static int packed_grid(K kernel, int64_t map_bytes) {
     return grid < 1 ? 1 : (int)grid;
 }
 
-// PDM_PACKED_BATCH=4|6|8: planes per load batch (A/B measurements).  Default
-// 4: 48 registers, 5 CTAs per SM.  The merge is bound by bytes in flight per
-// SM (Little's law at ~3 us loaded HBM latency): 4 planes x 18 B x 1280
-// threads ~ 92 KB/SM gives ~3.9 TB/s of packed bytes; 6 and 8 need 63-64+
-// registers, drop to 3-4 CTAs and measured no faster (k=32: 82.9 / 95.8 us
-// vs 81.9 us).  One 16-block chunk per thread (8-register accumulator, 8-byte
-// loads, 8 or 12 planes per batch) measured slower too (k=32: 87 us).  A
-// dominance skip (read the selected planes' bases first, then only the
-// nibbles of planes whose base is within 15 of the chunk minimum) is exact but
-// measured slower at config c (63.4 vs 51.2 us per step): the dependent
-// second round of loads costs more latency than the skipped bytes save.
-static int packed_batch() {
-    static int b = 0;
-    if (b == 0) {
-        const char *e = getenv("PDM_PACKED_BATCH");
-        b = e ? atoi(e) : 4;
-        if (b != 6 && b != 8) b = 4;
-    }
-    return b;
-}
+// Planes per load batch: 4 (48 registers, 5 CTAs per SM).  The merge is
+// bound by bytes in flight per SM (Little's law at ~3 us loaded HBM latency):
+// 4 planes x 18 B x 1280 threads ~ 92 KB/SM moves ~3.9 TB/s of packed bytes.
+// Measured and rejected: batches of 6 and 8 (63-64+ registers, 3-4 CTAs;
+// k=32: 82.9 / 95.8 us vs 81.9 us); one 16-block chunk per thread (8-register
+// accumulator, 8-byte loads, 8 or 12 planes per batch: 87 us); a ring that
+// refills each slot right after folding it (90 us: loads issued at different
+// times share scoreboards); a dominance skip (read the selected planes' bases
+// first, then only the nibbles of planes whose base is within 15 of the chunk
+// minimum -- exact, but 63.4 vs 51.2 us per step: the dependent second round
+// of loads costs more latency than the skipped bytes save).
+constexpr int kPackedBatch = 4;
 
 static bool packed_layout_ok(const void *nib, int64_t nib_pitch, const void *base,
                              int64_t base_pitch, const void *out) {
     return nib_pitch % 16 == 0 && base_pitch % 2 == 0 && (uintptr_t)nib % 16 == 0 &&
            (uintptr_t)base % 2 == 0 && (uintptr_t)out % 16 == 0;
+}
+
+static int check_packed(const char *fn, const void *nib, int64_t nib_pitch, const void *base,
+                        int64_t base_pitch, int64_t map_bytes, int n, const void *out,
+                        const void *out_base, bool pack_out) {
+    PDM_REQUIRE(nib && base && out && (!pack_out || out_base), "%s: null pointer", fn);
+    PDM_REQUIRE(map_bytes >= 1 && n >= 1, "%s: bad sizes (map_bytes=%lld n=%d)", fn,
+                (long long)map_bytes, n);
+    PDM_REQUIRE(nib_pitch >= 16 * ceil_div(map_bytes, 32) &&
+                    base_pitch >= 2 * ceil_div(map_bytes, 32),
+                "%s: pitches below the packed plane size", fn);
+    PDM_REQUIRE(packed_layout_ok(nib, nib_pitch, base, base_pitch, out) &&
+                    (uintptr_t)out_base % 2 == 0,
+                "%s: needs 16-byte aligned nibble planes and output", fn);
+    return PDM_OK;
+}
+
+static int launch_packed(const uint8_t *nib, int64_t nib_pitch, const uint8_t *base,
+                         int64_t base_pitch, int64_t map_bytes, const PackedSel &p,
+                         uint8_t *out, uint8_t *out_base, cudaStream_t s) {
+    auto kern = out_base ? combine_packed_kernel<kPackedBatch, true>
+                         : combine_packed_kernel<kPackedBatch, false>;
+    kern<<<packed_grid(kern, map_bytes), kPackedThreads, 0, s>>>(nib, nib_pitch, base,
+                                                                  base_pitch, map_bytes, p, out,
+                                                                  out_base);
+    return cuda_status("combine_packed_kernel");
+}
+
+// Programmatic dependent launch behind the select kernel.
+static int launch_packed_flags(const uint8_t *nib, int64_t nib_pitch, const uint8_t *base,
+                               int64_t base_pitch, int64_t map_bytes, int n,
+                               const uint8_t *flags, uint8_t *out, uint8_t *out_base,
+                               cudaStream_t s) {
+    auto kern = out_base ? combine_packed_flags_kernel<kPackedBatch, true>
+                         : combine_packed_flags_kernel<kPackedBatch, false>;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)packed_grid(kern, map_bytes));
+    cfg.blockDim = dim3(kPackedThreads);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    PDM_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, nib, nib_pitch, base, base_pitch, map_bytes, n,
+                                    flags, out, out_base));
+    return cuda_status("combine_packed_flags_kernel");
+}
+
+static int packed_sel(const char *fn, const int32_t *sel, int k, int n, PackedSel &p) {
+    PDM_REQUIRE(k == 0 || sel, "%s: null selection", fn);
+    PDM_REQUIRE(k >= 0 && k <= n && k <= kPackedMaxSel, "%s: k=%d outside [0, min(n, %d)]", fn,
+                k, kPackedMaxSel);
+    p.k = k;
+    for (int i = 0; i < k; ++i) {
+        PDM_REQUIRE(sel[i] >= 0 && sel[i] < n, "%s: index %d outside [0, %d)", fn, sel[i], n);
+        p.idx[i] = sel[i];
+    }
+    return PDM_OK;
 }
 
 }  // namespace pdm
@@ -307,60 +403,78 @@ extern "C" int pdm_combine_packed(const uint8_t *nib, int64_t nib_pitch, const u
                                   int64_t base_pitch, int64_t map_bytes, int32_t n,
                                   const int32_t *sel, int32_t k, uint8_t *out,
                                   pdm_stream_t stream) {
-    PDM_REQUIRE(nib && base && out && (k == 0 || sel), "pdm_combine_packed: null pointer");
-    PDM_REQUIRE(map_bytes >= 1 && n >= 1 && k >= 0 && k <= n && k <= kPackedMaxSel,
-                "pdm_combine_packed: bad sizes (map_bytes=%lld n=%d k=%d, k <= %d)",
-                (long long)map_bytes, n, k, kPackedMaxSel);
-    PDM_REQUIRE(nib_pitch >= 16 * ceil_div(map_bytes, 32) && base_pitch >= 2 * ceil_div(map_bytes, 32),
-                "pdm_combine_packed: pitches below the packed plane size");
-    PDM_REQUIRE(packed_layout_ok(nib, nib_pitch, base, base_pitch, out),
-                "pdm_combine_packed: needs 16-byte aligned nibble planes and output");
+    const char *fn = "pdm_combine_packed";
+    int st = check_packed(fn, nib, nib_pitch, base, base_pitch, map_bytes, n, out, nullptr, false);
+    if (st) return st;
     PackedSel p;
-    p.k = k;
-    for (int i = 0; i < k; ++i) {
-        PDM_REQUIRE(sel[i] >= 0 && sel[i] < n, "pdm_combine_packed: index %d outside [0, %d)",
-                    sel[i], n);
-        p.idx[i] = sel[i];
-    }
-    cudaStream_t s = as_stream(stream);
-    if (packed_batch() == 4)
-        combine_packed_kernel<4><<<packed_grid(combine_packed_kernel<4>, map_bytes),
-                                   kPackedThreads, 0, s>>>(nib, nib_pitch, base, base_pitch,
-                                                           map_bytes, p, out);
-    else if (packed_batch() == 6)
-        combine_packed_kernel<6><<<packed_grid(combine_packed_kernel<6>, map_bytes),
-                                   kPackedThreads, 0, s>>>(nib, nib_pitch, base, base_pitch,
-                                                           map_bytes, p, out);
-    else
-        combine_packed_kernel<8><<<packed_grid(combine_packed_kernel<8>, map_bytes),
-                                   kPackedThreads, 0, s>>>(nib, nib_pitch, base, base_pitch,
-                                                           map_bytes, p, out);
-    return cuda_status("combine_packed_kernel");
+    if ((st = packed_sel(fn, sel, k, n, p))) return st;
+    return launch_packed(nib, nib_pitch, base, base_pitch, map_bytes, p, out, nullptr,
+                         as_stream(stream));
 }
 
 extern "C" int pdm_combine_flags_packed(const uint8_t *nib, int64_t nib_pitch,
                                         const uint8_t *base, int64_t base_pitch,
                                         int64_t map_bytes, int32_t n, const uint8_t *flags,
                                         uint8_t *out, pdm_stream_t stream) {
-    PDM_REQUIRE(nib && base && flags && out, "pdm_combine_flags_packed: null pointer");
-    PDM_REQUIRE(map_bytes >= 1 && n >= 1 && n <= kPackedMaxFlags,
-                "pdm_combine_flags_packed: bad sizes (n=%d, <= %d)", n, kPackedMaxFlags);
-    PDM_REQUIRE(nib_pitch >= 16 * ceil_div(map_bytes, 32) && base_pitch >= 2 * ceil_div(map_bytes, 32),
-                "pdm_combine_flags_packed: pitches below the packed plane size");
-    PDM_REQUIRE(packed_layout_ok(nib, nib_pitch, base, base_pitch, out),
-                "pdm_combine_flags_packed: needs 16-byte aligned nibble planes and output");
-    auto kern = packed_batch() == 4 ? combine_packed_flags_kernel<4> : combine_packed_flags_kernel<8>;
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)packed_grid(kern, map_bytes));
-    cfg.blockDim = dim3(kPackedThreads);
-    cfg.dynamicSmemBytes = 0;
-    cfg.stream = as_stream(stream);
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    PDM_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, nib, nib_pitch, base,
-                                    base_pitch, map_bytes, (int)n, flags, out));
-    return cuda_status("combine_packed_flags_kernel");
+    const char *fn = "pdm_combine_flags_packed";
+    int st = check_packed(fn, nib, nib_pitch, base, base_pitch, map_bytes, n, out, nullptr, false);
+    if (st) return st;
+    PDM_REQUIRE(flags && n <= kPackedMaxFlags, "%s: flags null or n=%d above %d", fn, n,
+                kPackedMaxFlags);
+    return launch_packed_flags(nib, nib_pitch, base, base_pitch, map_bytes, n, flags, out,
+                               nullptr, as_stream(stream));
+}
+
+extern "C" int pdm_combine_packed_to_packed(const uint8_t *nib, int64_t nib_pitch,
+                                            const uint8_t *base, int64_t base_pitch,
+                                            int64_t map_bytes, int32_t n, const int32_t *sel,
+                                            int32_t k, uint8_t *out_nib, uint8_t *out_base,
+                                            pdm_stream_t stream) {
+    const char *fn = "pdm_combine_packed_to_packed";
+    int st = check_packed(fn, nib, nib_pitch, base, base_pitch, map_bytes, n, out_nib, out_base,
+                          true);
+    if (st) return st;
+    PackedSel p;
+    if ((st = packed_sel(fn, sel, k, n, p))) return st;
+    return launch_packed(nib, nib_pitch, base, base_pitch, map_bytes, p, out_nib, out_base,
+                         as_stream(stream));
+}
+
+extern "C" int pdm_combine_flags_packed_to_packed(const uint8_t *nib, int64_t nib_pitch,
+                                                  const uint8_t *base, int64_t base_pitch,
+                                                  int64_t map_bytes, int32_t n,
+                                                  const uint8_t *flags, uint8_t *out_nib,
+                                                  uint8_t *out_base, pdm_stream_t stream) {
+    const char *fn = "pdm_combine_flags_packed_to_packed";
+    int st = check_packed(fn, nib, nib_pitch, base, base_pitch, map_bytes, n, out_nib, out_base,
+                          true);
+    if (st) return st;
+    PDM_REQUIRE(flags && n <= kPackedMaxFlags, "%s: flags null or n=%d above %d", fn, n,
+                kPackedMaxFlags);
+    return launch_packed_flags(nib, nib_pitch, base, base_pitch, map_bytes, n, flags, out_nib,
+                               out_base, as_stream(stream));
+}
+
+// Host side: expand a packed map (pdm_combine_*_to_packed output, in host
+// memory) into map_bytes plain bytes.  SSE2 per chunk (unpack low/high
+// nibbles, interleave, add the base), OpenMP across chunks.
+extern "C" int pdm_unpack_packed_host(const uint8_t *nib, const uint8_t *base, int64_t map_bytes,
+                                      uint8_t *out) {
+    PDM_REQUIRE(nib && base && out && map_bytes >= 1, "pdm_unpack_packed_host: bad arguments");
+    const int64_t full = map_bytes / 16;
+    const __m128i lo4 = _mm_set1_epi8(0x0F);
+#pragma omp parallel for schedule(static)
+    for (int64_t c = 0; c < full; ++c) {
+        const __m128i q = _mm_loadl_epi64(reinterpret_cast<const __m128i *>(nib + 8 * c));
+        const __m128i even = _mm_and_si128(q, lo4);
+        const __m128i odd = _mm_and_si128(_mm_srli_epi16(q, 4), lo4);
+        __m128i v = _mm_unpacklo_epi8(even, odd);
+        v = _mm_add_epi8(v, _mm_set1_epi8((char)base[c]));
+        _mm_storeu_si128(reinterpret_cast<__m128i *>(out + 16 * c), v);
+    }
+    for (int64_t i = full * 16; i < map_bytes; ++i) {
+        const int64_t c = i / 16, j = i % 16;
+        out[i] = (uint8_t)(base[c] + ((nib[8 * c + j / 2] >> (4 * (j & 1))) & 15));
+    }
+    return PDM_OK;
 }

@@ -360,3 +360,30 @@ def test_packed_skipped_for_maps_that_are_not_distance_fields():
     got = pdm.combine(pset, pdm.PartitionSelection(selected=frozenset(s), n=5)).dist
     assert pset.packed() is None
     assert np.array_equal(got, np.minimum.reduce([maps[i - 1] for i in s]))
+
+
+def test_packed_dprime_to_host():
+    """combine(...).dist over a packable set ships D' packed over PCIe and
+    expands it on the host: identical to the oracle for device-flag and
+    host-index selections, including a map whose size is not a multiple of 16
+    (rows of 13 blocks still pack: straddling chunks stay <= 12 apart)."""
+    rng = np.random.default_rng(31)
+    for dims, b in (((64, 40, 64), 4), ((3, 5, 13), 1)):
+        vox = random_structured_volume(rng, dims, 8)
+        scheme = pdm.scheme_uniform(8, 8)
+        pset = pdm.build_pdm_set(pdm.Volume.from_array(vox), pdm.BlockGrid.for_dims(dims, b),
+                                 scheme)
+        assert pset.packed() is not None
+        maps = oracle.build_pdm_set(vox, b, scheme.bounds(), "range_apron")
+        for s in ([3], [1, 2, 5, 8], list(range(1, 9))):
+            lut = np.zeros((256, 4))
+            for i in s:
+                part = scheme.partitions[i - 1]
+                lut[part.rho_lo: part.rho_hi + 1, 3] = 0.5
+            want = oracle.combine(maps, s)
+            flags_path = pdm.combine(pset, pdm.select_partitions(pdm.TransferFunction(lut=lut),
+                                                                 scheme))
+            assert np.array_equal(flags_path.dist, want), (dims, s)
+            idx_path = pdm.combine(pset, pdm.PartitionSelection(selected=frozenset(s), n=8))
+            assert np.array_equal(idx_path.dist, want), (dims, s)
+            assert np.array_equal(idx_path.device().cpu().numpy(), want), (dims, s)

@@ -46,6 +46,26 @@ def test_library_rejects_bad_arguments_without_gpu():
     assert b"bits" in L.pdm_last_error()
 
 
+def test_unpack_packed_host_matches_numpy_decode():
+    """pdm_unpack_packed_host (host code, no GPU) against a numpy decode of
+    the packed encoding: base per 16-block chunk + 4-bit offsets, block
+    16c+2j in the low nibble of byte j; map sizes with a partial last chunk."""
+    L = _lib.load_library()
+    rng = np.random.default_rng(21)
+    for nb in (1, 15, 16, 17, 240, 1000, 4096 + 7):
+        chunks = 2 * (-(-nb // 32))
+        nib = rng.integers(0, 256, chunks * 8, dtype=np.uint8)
+        base = rng.integers(0, 241, chunks, dtype=np.uint8)
+        vals = np.empty((chunks, 16), np.int64)
+        vals[:, 0::2] = nib.reshape(chunks, 8) & 15
+        vals[:, 1::2] = nib.reshape(chunks, 8) >> 4
+        want = (vals + base[:, None].astype(np.int64)).reshape(-1)[:nb].astype(np.uint8)
+        out = np.zeros(nb, np.uint8)
+        assert L.pdm_unpack_packed_host(nib.ctypes.data, base.ctypes.data, nb,
+                                        out.ctypes.data) == _lib.PDM_OK
+        assert np.array_equal(out, want), nb
+
+
 def test_library_is_sm100a_only():
     lib = ROOT / "paper_2407_21552_b200" / "lib" / "libpdm_b200.so"
     import subprocess
