@@ -299,7 +299,11 @@ static int packed_grid(K kernel, int64_t map_bytes) {
 // times share scoreboards); a dominance skip (read the selected planes' bases
 // first, then only the nibbles of planes whose base is within 15 of the chunk
 // minimum -- exact, but 63.4 vs 51.2 us per step: the dependent second round
-// of loads costs more latency than the skipped bytes save).
+// of loads costs more latency than the skipped bytes save); a TMA variant
+// (one producer thread per CTA, 2 CTAs per SM, 20-stage ring of 4 KB nibble +
+// 512 B base bulk copies, consumers folding from shared memory) took 129 us
+// at k=32 under ncu vs 83 us -- the bulk-copy path is slower than LDG here,
+// as it was for the raw merge.
 constexpr int kPackedBatch = 4;
 
 static bool packed_layout_ok(const void *nib, int64_t nib_pitch, const void *base,
