@@ -1,12 +1,14 @@
 // capi.cu -- library plumbing plus the TF-change update: selection (K8) and
 // the min-merge over the selected partition distance maps (K7).
 //
-// K7 is HBM-bound: it reads k uint8 maps and writes one, (k+1) * B bytes for
-// B blocks.  Each thread owns 16-byte chunks of the map; it keeps 8 128-bit
-// loads of the selected maps in flight and folds them with a byte-wise min
-// (16-bit-lane VIMNMX).  Loads bypass L1 (read once), the store is
-// evict-first.  Measured shapes and the TMA / cp.async alternatives are in
-// DESIGN.md (merge section).
+// K7 over the raw planes is HBM-bound: it reads k uint8 maps and writes one,
+// (k+1) * B bytes for B blocks.  Each thread owns 16-byte chunks of the map;
+// it keeps 8 128-bit loads of the selected maps in flight and folds them with
+// a byte-wise min (fp16-biased 16-bit lanes, HMNMX2).  Loads bypass L1 (read
+// once), the store is evict-first.  The device-side default merges the
+// nibble-packed copy instead (packed.cu); this one serves unpackable sets and
+// host destinations of them.  TMA-bulk and cp.async ring variants were
+// measured slower and removed (merge section).
 #include <cuda_runtime.h>
 
 #include <cstring>
@@ -231,139 +233,6 @@ __device__ __forceinline__ void merge_large_k(const uint8_t *__restrict__ pdms, 
     }
 }
 
-// ---- K7 through cp.async (LDGSTS): the register budget caps the LDG merge at
-// 8 loads in flight per thread; staging through shared memory lifts that.  A
-// thread owns chunks v0, v0+T, ... and walks the flattened (chunk, map) item
-// stream; every item is one 16-byte cp.async into the thread's private ring
-// slot followed by one commit group, and cp.async.wait_group<D-1> retires
-// exactly the oldest item (groups complete in order), so D items stay in
-// flight for every k.  Ring slots are [depth][thread] 16-byte words: a warp's
-// shared accesses are 512 contiguous bytes (conflict-free).
-constexpr int kAsyncDepth = 12;
-
-template <bool kAccumulate>
-__device__ __forceinline__ void merge_async(const uint8_t *__restrict__ pdms, int64_t pitch,
-                                            int64_t nvec, const int32_t *idx, int k,
-                                            uint8_t *__restrict__ out, uint4 *s_ring) {
-    const int64_t T = (int64_t)gridDim.x * blockDim.x;
-    const int64_t v0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (v0 >= nvec) return;
-    if (k == 0) {
-        const uint4 ones = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
-        for (int64_t v = v0; v < nvec; v += T) st_stream_u4(out + v * 16, ones);
-        return;
-    }
-    const int64_t items = ((nvec - 1 - v0) / T + 1) * k;
-    uint4 *slot0 = s_ring + threadIdx.x;
-    const int B = blockDim.x;
-    int64_t load_off = v0 * 16;
-    int load_m = 0;
-#pragma unroll
-    for (int d = 0; d < kAsyncDepth; ++d) {
-        if (d < items) {
-            cpa::copy16(slot0 + d * B, pdms + (int64_t)idx[load_m] * pitch + load_off);
-            if (++load_m == k) {
-                load_m = 0;
-                load_off += T * 16;
-            }
-        }
-        cpa::commit();
-    }
-    int64_t store_off = v0 * 16;
-    int fold_m = 0, d = 0;
-    ByteMin16 acc;
-    acc.init_ff();
-    if (kAccumulate) acc.fold(*reinterpret_cast<const uint4 *>(out + store_off));
-    for (int64_t i = 0; i < items; ++i) {
-        cpa::wait<kAsyncDepth - 1>();
-        acc.fold(slot0[d * B]);
-        if (i + kAsyncDepth < items) {
-            cpa::copy16(slot0 + d * B, pdms + (int64_t)idx[load_m] * pitch + load_off);
-            if (++load_m == k) {
-                load_m = 0;
-                load_off += T * 16;
-            }
-        }
-        cpa::commit();
-        if (++d == kAsyncDepth) d = 0;
-        if (++fold_m == k) {
-            st_stream_u4(out + store_off, acc.result());
-            fold_m = 0;
-            store_off += T * 16;
-            acc.init_ff();
-            if (kAccumulate && store_off < nvec * 16)
-                acc.fold(*reinterpret_cast<const uint4 *>(out + store_off));
-        }
-    }
-    cpa::wait<0>();
-}
-
-constexpr int kAsyncThreads = 256;
-constexpr size_t kAsyncRingBytes = (size_t)kAsyncDepth * kAsyncThreads * 16;  // 48 KB
-
-// Selection in kernel parameters (pdm_combine).
-__global__ void __launch_bounds__(kAsyncThreads)
-    combine_async_kernel(const uint8_t *__restrict__ pdms, int64_t pitch, int64_t map_bytes,
-                         const __grid_constant__ SelParam sel, uint8_t *__restrict__ out,
-                         int accumulate) {
-    extern __shared__ __align__(16) uint8_t dsmem[];
-    uint4 *ring = reinterpret_cast<uint4 *>(dsmem);
-    const int64_t nvec = map_bytes / 16;
-    if (accumulate)
-        merge_async<true>(pdms, pitch, nvec, sel.idx, sel.k, out, ring);
-    else
-        merge_async<false>(pdms, pitch, nvec, sel.idx, sel.k, out, ring);
-    if (blockIdx.x == 0) {  // bytes past the last 16-byte chunk
-        for (int64_t c = nvec * 16 + threadIdx.x; c < map_bytes; c += blockDim.x) {
-            uint32_t a = accumulate ? out[c] : 255u;
-            for (int m = 0; m < sel.k; ++m) {
-                const uint32_t v = pdms[(int64_t)sel.idx[m] * pitch + c];
-                a = v < a ? v : a;
-            }
-            out[c] = (uint8_t)a;
-        }
-    }
-}
-
-// Selection resident on the device (pdm_combine_flags): compacted into the
-// shared index list that follows the ring in dynamic shared memory.
-__global__ void __launch_bounds__(kAsyncThreads)
-    combine_async_flags_kernel(const uint8_t *__restrict__ pdms, int64_t pitch,
-                               int64_t map_bytes, int n, const uint8_t *__restrict__ flags,
-                               uint8_t *__restrict__ out) {
-    extern __shared__ __align__(16) uint8_t dsmem[];
-    uint4 *ring = reinterpret_cast<uint4 *>(dsmem);
-    int32_t *s_idx = reinterpret_cast<int32_t *>(dsmem + kAsyncRingBytes);
-    __shared__ int s_k;
-    pdl_wait();  // flags come from the preceding select kernel (PDL)
-    if (threadIdx.x < 32) {
-        const unsigned lane = threadIdx.x;
-        int k = 0;
-        for (int base = 0; base < n; base += 32) {
-            const int p = base + (int)lane;
-            const bool on = p < n && flags[p] != 0;
-            const unsigned bal = __ballot_sync(0xFFFFFFFFu, on);
-            if (on) s_idx[k + __popc(bal & ((1u << lane) - 1u))] = p;
-            k += __popc(bal);
-        }
-        if (lane == 0) s_k = k;
-    }
-    __syncthreads();
-    const int k = s_k;
-    const int64_t nvec = map_bytes / 16;
-    merge_async<false>(pdms, pitch, nvec, s_idx, k, out, ring);
-    if (blockIdx.x == 0) {
-        for (int64_t c = nvec * 16 + threadIdx.x; c < map_bytes; c += blockDim.x) {
-            uint32_t a = 255u;
-            for (int m = 0; m < k; ++m) {
-                const uint32_t v = pdms[(int64_t)s_idx[m] * pitch + c];
-                a = v < a ? v : a;
-            }
-            out[c] = (uint8_t)a;
-        }
-    }
-}
-
 // shape != 0 forces one loop shape (PDM_MERGE_SHAPE, measurements only):
 // 1 = <1,8> packed, 2 = <2,4>, 3 = <4,2>, 4 = <8,1>, 5 = split-lane large-k.
 template <bool kAccumulate>
@@ -446,134 +315,6 @@ __global__ void __launch_bounds__(kMergeThreads, 4)
     merge_tail(pdms, pitch, nvec * 16, map_bytes, s_idx, k, false, out);
 }
 
-// ---------------------------------------------------------------------------
-// K7 on the TMA engine: a persistent CTA per SM streams (tile, selected map)
-// segments of kTmaStageBytes through a kTmaStages-deep shared-memory ring with
-// cp.async.bulk (one elected producer thread, mbarrier full/empty pairs), so
-// ~192 KB per SM are in flight with no register cost.  Each of the 256
-// consumer threads owns 16 bytes of the tile: it waits on the stage's full
-// barrier, folds the stage into its register accumulator with __vminu4 and
-// releases the stage (one arrive per warp); after the tile's last map it
-// stores 16 bytes of D' (evict-first).  Tiles are dealt round-robin to CTAs.
-constexpr int kTmaConsumers = 256;
-constexpr int kTmaStageBytes = kTmaConsumers * 16;  // 4 KB
-constexpr int kTmaStages = 48;                      // 192 KB ring
-constexpr int kTmaGroup = 4;                        // stages consumed per barrier round
-constexpr int kTmaThreads = kTmaConsumers + 32;     // + producer warp
-constexpr size_t kTmaSmem = (size_t)kTmaStages * kTmaStageBytes + 2 * kTmaStages * 8;
-
-template <bool kFlags>
-__global__ void __launch_bounds__(kTmaThreads, 1)
-    combine_tma_kernel(const uint8_t *__restrict__ pdms, int64_t pitch, int64_t map_bytes,
-                       const __grid_constant__ SelParam sel, int n,
-                       const uint8_t *__restrict__ flags, uint8_t *__restrict__ out) {
-    extern __shared__ __align__(128) uint8_t smem[];
-    uint8_t *ring = smem;
-    uint64_t *full = reinterpret_cast<uint64_t *>(smem + (size_t)kTmaStages * kTmaStageBytes);
-    uint64_t *empty = full + kTmaStages;
-    __shared__ int32_t s_idx[kMaxFlagsSmem];
-    __shared__ int s_k;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    if (kFlags) {
-        pdl_wait();  // flags come from the preceding select kernel (PDL)
-        compact_flags(flags, n, s_idx, &s_k);
-    } else {
-        for (int i = threadIdx.x; i < sel.k; i += blockDim.x) s_idx[i] = sel.idx[i];
-        if (threadIdx.x == 0) s_k = sel.k;
-    }
-    if (threadIdx.x == 0) {
-        for (int s = 0; s < kTmaStages; ++s) {
-            tma::mbar_init(&full[s], 1);
-            tma::mbar_init(&empty[s], kTmaConsumers / 32);
-        }
-        tma::fence_mbar_init();
-    }
-    __syncthreads();
-    const int k = s_k;
-    const int64_t ntiles = map_bytes / kTmaStageBytes;
-    const int64_t my_tiles =
-        blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-
-    if (warp == kTmaConsumers / 32) {  // ---- producer warp: one elected thread
-        if (lane == 0 && k > 0) {
-            int s = 0;
-            uint32_t phase = 0;
-            int64_t issued = 0;
-            for (int64_t i = 0; i < my_tiles; ++i) {
-                const int64_t off = (blockIdx.x + i * gridDim.x) * kTmaStageBytes;
-                for (int m = 0; m < k; ++m) {
-                    if (issued >= kTmaStages) tma::mbar_wait(&empty[s], phase ^ 1);
-                    tma::mbar_expect_tx(&full[s], kTmaStageBytes);
-                    tma::bulk_g2s(ring + (size_t)s * kTmaStageBytes,
-                                  pdms + (int64_t)s_idx[m] * pitch + off, kTmaStageBytes,
-                                  &full[s]);
-                    ++issued;
-                    if (++s == kTmaStages) {
-                        s = 0;
-                        phase ^= 1;
-                    }
-                }
-            }
-        }
-    } else {  // ---- consumers
-        // Stages are consumed in groups of kTmaGroup: all waits, then all
-        // shared loads, then all releases, so the per-stage barrier latency is
-        // paid once per group instead of once per stage.
-        int s = 0;
-        uint32_t phase = 0;
-        for (int64_t i = 0; i < my_tiles; ++i) {
-            ByteMin16 acc;
-            acc.init_ff();
-            for (int m = 0; m < k; m += kTmaGroup) {
-                const int g = k - m < kTmaGroup ? k - m : kTmaGroup;
-                int ss[kTmaGroup];
-                uint32_t ph[kTmaGroup];
-#pragma unroll
-                for (int j = 0; j < kTmaGroup; ++j) {
-                    ss[j] = s;
-                    ph[j] = phase;
-                    if (j < g && ++s == kTmaStages) {
-                        s = 0;
-                        phase ^= 1;
-                    }
-                }
-#pragma unroll
-                for (int j = 0; j < kTmaGroup; ++j)
-                    if (j < g) tma::mbar_wait(&full[ss[j]], ph[j]);
-                uint4 v[kTmaGroup];
-#pragma unroll
-                for (int j = 0; j < kTmaGroup; ++j)
-                    if (j < g)
-                        v[j] = *reinterpret_cast<const uint4 *>(
-                            ring + (size_t)ss[j] * kTmaStageBytes + threadIdx.x * 16);
-#pragma unroll
-                for (int j = 0; j < kTmaGroup; ++j)
-                    if (j < g) acc.fold(v[j]);
-                __syncwarp();
-                if (lane == 0) {
-#pragma unroll
-                    for (int j = 0; j < kTmaGroup; ++j)
-                        if (j < g) tma::mbar_arrive(&empty[ss[j]]);
-                }
-            }
-            const int64_t off = (blockIdx.x + i * gridDim.x) * kTmaStageBytes;
-            st_stream_u4(out + off + threadIdx.x * 16, acc.result());
-        }
-        // bytes past the last whole tile, by the last CTA's consumers
-        if (blockIdx.x == gridDim.x - 1) {
-            for (int64_t c = ntiles * kTmaStageBytes + threadIdx.x; c < map_bytes;
-                 c += kTmaConsumers) {
-                uint32_t a = 255u;
-                for (int m = 0; m < k; ++m) {
-                    const uint32_t v = pdms[(int64_t)s_idx[m] * pitch + c];
-                    a = v < a ? v : a;
-                }
-                out[c] = (uint8_t)a;
-            }
-        }
-    }
-}
-
 // Volume.intensity_range for device-born volumes (volume.py:86-90): out[0] =
 // min, out[1] = max over all voxels.  Grid-stride, warp shuffle, one atomic
 // per warp into out (pre-set to [UINT_MAX, 0] by the wrapper).
@@ -654,24 +395,6 @@ static int merge_grid(int64_t work_items, int per_sm, int U) {
     return grid < 1 ? 1 : (int)grid;
 }
 
-// Merge implementations (PDM_MERGE_IMPL, for A/B measurements):
-//   ldg (default)   -- register-staged loads, 8 x 16 B in flight per thread;
-//   async           -- cp.async ring, 12 x 16 B in flight per thread (measured
-//                      4.9 TB/s at k=32 vs 5.6 for ldg);
-//   tma             -- cp.async.bulk ring, one producer thread per SM (a
-//                      single SM's bulk-copy path sustained only ~30 GB/s in
-//                      our measurements).
-enum MergeImpl { kImplAsync = 0, kImplLdg = 1, kImplTma = 2 };
-static int merge_impl() {
-    static int mode = -1;
-    if (mode < 0) {
-        const char *e = getenv("PDM_MERGE_IMPL");
-        mode = kImplLdg;
-        if (e && strcmp(e, "async") == 0) mode = kImplAsync;
-        if (e && strcmp(e, "tma") == 0) mode = kImplTma;
-    }
-    return mode;
-}
 static int merge_shape() {
     static int shape = -1;
     if (shape < 0) {
@@ -680,52 +403,6 @@ static int merge_shape() {
     }
     return shape;
 }
-static bool use_tma(int64_t map_bytes) {
-    return merge_impl() == kImplTma && map_bytes >= (int64_t)kTmaStageBytes * 16;
-}
-
-template <class K>
-static int async_grid(K kernel, size_t smem, int64_t nvec) {
-    static int per_sm_cache[2] = {0, 0};
-    int &per_sm = per_sm_cache[smem > kAsyncRingBytes ? 1 : 0];
-    if (per_sm == 0) {
-        if (cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smem) != cudaSuccess ||
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kAsyncThreads, smem) !=
-                cudaSuccess ||
-            per_sm < 1)
-            per_sm = 1;
-    }
-    return merge_grid(nvec > 0 ? nvec : 1, per_sm, 1);
-}
-
-template <bool kFlags>
-static int launch_tma(const uint8_t *pdms, int64_t pitch, int64_t map_bytes, const SelParam &p,
-                      int n, const uint8_t *flags, uint8_t *out, cudaStream_t s) {
-    auto kern = combine_tma_kernel<kFlags>;
-    static bool attr_set[2] = {false, false};
-    if (!attr_set[kFlags]) {
-        PDM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          (int)kTmaSmem));
-        attr_set[kFlags] = true;
-    }
-    const int64_t ntiles = map_bytes / kTmaStageBytes;
-    int64_t grid = sm_count();
-    if (grid > ntiles) grid = ntiles > 0 ? ntiles : 1;
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)grid);
-    cfg.blockDim = dim3(kTmaThreads);
-    cfg.dynamicSmemBytes = kTmaSmem;
-    cfg.stream = s;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = kFlags ? 1 : 0;  // PDL only behind the select kernel
-    PDM_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, pdms, pitch, map_bytes, p, n, flags, out));
-    return cuda_status("combine_tma_kernel");
-}
-
 }  // namespace pdm
 
 using namespace pdm;
@@ -815,23 +492,6 @@ extern "C" int pdm_combine(const uint8_t *pdms, int64_t plane_pitch, int64_t map
     const bool vec = (plane_pitch % 16 == 0) && ((uintptr_t)pdms % 16 == 0) &&
                      ((uintptr_t)out % 16 == 0);
     SelParam p;
-    if (vec && k <= kMaxSelParam && use_tma(map_bytes)) {
-        p.k = k;
-        memcpy(p.idx, sel, sizeof(int32_t) * k);
-        return launch_tma<false>(pdms, plane_pitch, map_bytes, p, n, nullptr, out, s);
-    }
-    if (vec && merge_impl() == kImplAsync) {
-        for (int base = 0; base == 0 || base < k; base += kMaxSelParam) {
-            p.k = k - base < kMaxSelParam ? k - base : kMaxSelParam;
-            memcpy(p.idx, sel + base, sizeof(int32_t) * p.k);
-            const int grid = async_grid(combine_async_kernel, kAsyncRingBytes, map_bytes / 16);
-            combine_async_kernel<<<grid, kAsyncThreads, kAsyncRingBytes, s>>>(
-                pdms, plane_pitch, map_bytes, p, out, base > 0);
-            int st = cuda_status("combine_async_kernel");
-            if (st) return st;
-        }
-        return PDM_OK;
-    }
     for (int base = 0; base == 0 || base < k; base += kMaxSelParam) {  // >240: passes
         p.k = k - base < kMaxSelParam ? k - base : kMaxSelParam;
         memcpy(p.idx, sel + base, sizeof(int32_t) * p.k);
@@ -861,30 +521,6 @@ extern "C" int pdm_combine_flags(const uint8_t *pdms, int64_t plane_pitch, int64
     PDM_REQUIRE(n <= kMaxFlagsSmem, "pdm_combine_flags: n=%d above %d", n, kMaxFlagsSmem);
     PDM_REQUIRE(plane_pitch % 16 == 0 && (uintptr_t)pdms % 16 == 0 && (uintptr_t)out % 16 == 0,
                 "pdm_combine_flags: needs 16-byte aligned planes");
-    if (use_tma(map_bytes)) {
-        SelParam none;
-        none.k = 0;
-        return launch_tma<true>(pdms, plane_pitch, map_bytes, none, n, flags, out,
-                                as_stream(stream));
-    }
-    if (merge_impl() == kImplAsync) {
-        const size_t smem = kAsyncRingBytes + (size_t)n * sizeof(int32_t);
-        cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = dim3((unsigned)async_grid(combine_async_flags_kernel,
-                                                kAsyncRingBytes + kMaxFlagsSmem * 4,
-                                                map_bytes / 16));
-        cfg.blockDim = dim3(kAsyncThreads);
-        cfg.dynamicSmemBytes = smem;
-        cfg.stream = as_stream(stream);
-        cudaLaunchAttribute attr[1];
-        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-        attr[0].val.programmaticStreamSerializationAllowed = 1;
-        cfg.attrs = attr;
-        cfg.numAttrs = 1;
-        PDM_CUDA_TRY(cudaLaunchKernelEx(&cfg, combine_async_flags_kernel, pdms, plane_pitch,
-                                        map_bytes, (int)n, flags, out));
-        return cuda_status("combine_async_flags_kernel");
-    }
     // Programmatic dependent launch: the merge CTAs are scheduled while the
     // preceding select kernel finishes; they wait on griddepcontrol.wait.
     const int per_sm = resident_ctas(combine_flags_kernel, kMergeThreads);

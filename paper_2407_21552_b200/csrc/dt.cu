@@ -16,16 +16,19 @@
 // distances, so g3 == min(255, chamfer_chebyshev) cell for cell (pinned
 // against the reference's golden vectors and the C oracle in tests/).
 //
-// The lower-envelope passes use Meijster et al.'s linear-time scan with the
-// L-infinity separator (one lane per line, stack in local memory):
+// Lower envelopes of lines <= 256 use a stack-free forward/backward sweep with
+// a per-line table indexed by value (sweep_forward / sweep_backward below);
+// longer lines use Meijster et al.'s linear-time scan with the L-infinity
+// separator (one lane per line, stack in local memory):
 //   f(x, i)  = max(|x - i|, g(i))
 //   Sep(i,u) = g(i) <= g(u) ? max(i + g(u), (i + u) / 2) : min(u - g(i), (i + u) / 2)
-// Every pass works on warp tiles of 32 lines staged in shared memory: the
-// warp loads the tile with coalesced 32-bit accesses, each lane runs its line
-// from shared memory (the per-element dependency chain sees shared-memory
-// latency, not DRAM latency), and the warp writes the tile back.  Lines along
-// x and y are strided in memory (a tile is 32 consecutive z of one line
-// family); lines along z are contiguous rows (a tile is 32 consecutive rows).
+// Every pass works on warp tiles of 32 lines staged in shared memory with
+// cp.async: each lane runs its line from shared memory (the per-element
+// dependency chain sees shared-memory latency, not DRAM latency), and the warp
+// writes the tile back.  Lines along x and y are strided in memory (a tile is
+// 32 consecutive z of one line family); lines along z are contiguous rows (a
+// tile is 32 consecutive rows, 16-byte chunks swizzled by row).  The x pass
+// (1-D distance) of lines <= 256 runs 4 lines per lane on 128-z tiles.
 #include <cuda_runtime.h>
 
 #include "pdm_common.cuh"
@@ -86,73 +89,6 @@ __device__ __forceinline__ void cone_line(int m, Ld ld, St st) {
         const int d = max(abs(u - ent_s(top)), ent_g(top));
         st(u, d < kDistClamp ? d : kDistClamp);
         if (u == ent_t(top) && q > 0) top = stk[--q];
-    }
-}
-
-// Same scan for lines of m <= 256 with a compact stack: entries are 16 bits
-// (s | g << 8) in a caller-provided shared-memory column, the top two entries
-// stay in registers, and thresholds are recomputed from adjacent entries
-// (t(entry q) = 1 + Sep(entry q-1, entry q), t(bottom) = 0) instead of stored.
-__device__ __forceinline__ int sep16(uint32_t i, uint32_t u) {
-    const int si = (int)(i & 0xFFu), gi = (int)(i >> 8);
-    const int su = (int)(u & 0xFFu), gu = (int)(u >> 8);
-    const int mid = (si + su) >> 1;
-    return gi <= gu ? max(si + gu, mid) : min(su - gi, mid);
-}
-
-template <class Ld, class St, class Stk>
-__device__ __forceinline__ void cone_line16(int m, Ld ld, St st, Stk stk) {
-    // q = entries on the stack; top = entry q-1, below = entry q-2, stk(i)
-    // holds entries 0..q-3.
-    int q = 1;
-    uint32_t top = (uint32_t)ld(0) << 8, below = 0;
-    int t_top = 0;
-    int gnext = m > 1 ? ld(1) : 0;
-    for (int u = 1; u < m; ++u) {
-        const int gu = gnext;
-        if (u + 1 < m) gnext = ld(u + 1);
-        for (;;) {  // pop while the top's cone is above u's at the top's threshold
-            const int fs = max(abs(t_top - (int)(top & 0xFFu)), (int)(top >> 8));
-            const int fu = max(abs(t_top - u), gu);
-            if (fs <= fu) break;
-            if (--q == 0) break;
-            top = below;
-            if (q >= 2) {
-                below = stk(q - 2);
-                t_top = 1 + sep16(below, top);
-            } else {
-                t_top = 0;
-            }
-        }
-        const uint32_t cand = (uint32_t)u | ((uint32_t)gu << 8);
-        if (q == 0) {
-            q = 1;
-            top = cand;
-            t_top = 0;
-        } else {
-            const int w = 1 + sep16(top, cand);
-            if (w < m) {
-                if (q >= 2) stk(q - 2) = (uint16_t)below;
-                below = top;
-                top = cand;
-                t_top = w;
-                ++q;
-            }
-        }
-    }
-    for (int u = m - 1; u >= 0; --u) {
-        const int d = max(abs(u - (int)(top & 0xFFu)), (int)(top >> 8));
-        st(u, d < kDistClamp ? d : kDistClamp);
-        if (u == t_top && q > 1) {
-            --q;
-            top = below;
-            if (q >= 2) {
-                below = stk(q - 2);
-                t_top = 1 + sep16(below, top);
-            } else {
-                t_top = 0;
-            }
-        }
     }
 }
 
@@ -441,14 +377,8 @@ __global__ void __launch_bounds__(128)
     const int64_t S = AXIS == kAxisX ? by * bz : bz;  // element stride of strided lines
     const size_t tile_bytes = kRows ? 32 * (size_t)sstride : 32 * (size_t)L;
     uint8_t *s = s_tiles + (size_t)warp * tile_bytes;
-    // Per-warp scratch after all tiles: the sweep's [256][32] position table,
-    // or 16-bit envelope stacks [depth][lane] for short lines.  (For 256-long
-    // lines a 16 KB/warp stack halves the resident warps and measured slower
-    // than the local-memory stack: 7.5 vs 4.8 ms at config c.)
-    constexpr bool kSmemStack = !kDist1D && !kSweep && LMAX <= 64;
+    // Per-warp scratch after all tiles: the sweep's [256][32] table.
     uint8_t *tab_warp = s_tiles + (size_t)wpc * tile_bytes + (size_t)warp * 8192;
-    uint16_t *stk16 = reinterpret_cast<uint16_t *>(s_tiles + (size_t)wpc * tile_bytes) +
-                      (size_t)warp * 32 * L + lane;
     const int64_t zblocks = ceil_div(bz, 32);
     const bool vec = (bz & 3) == 0;
     // Swizzled 16-byte row tiles (the host sets sstride == L only when
@@ -516,7 +446,7 @@ __global__ void __launch_bounds__(128)
         auto ld = [&](int u) -> int { return line[u * es]; };
         auto st = [&](int u, int v) { line[u * es] = (uint8_t)v; };
         if (kSweep) {
-            const uint32_t tab = tma::smem_u32(tab_warp + lane);
+            const uint32_t tab = smem_addr(tab_warp + lane);
             for (int dir = 0; dir < 2; ++dir) {
                 clear_table(tab_warp, lane);
                 __syncwarp();
@@ -537,8 +467,6 @@ __global__ void __launch_bounds__(128)
         } else if (lane < nlines) {
             if (kDist1D)
                 dist1d_line(L, ld, st);
-            else if (kSmemStack)
-                cone_line16(L, ld, st, [&](int i) -> uint16_t & { return stk16[i * 32]; });
             else
                 cone_line<LMAX>(L, ld, st);
         }
@@ -578,110 +506,6 @@ __global__ void __launch_bounds__(128)
             } else {
                 for (int u = 0; u < L; ++u)
                     if (lane < nlines) g[(int64_t)u * S + lane] = s[u * 32 + lane];
-            }
-        }
-        __syncwarp();
-    }
-}
-
-// Envelope along a strided axis (x or y) for lines <= 256: the warp's tile of
-// 32 lines stays intact in shared memory ([u][32]), each lane's stack holds
-// 8-bit positions only ([depth][32] bytes, g(s) is re-read from the tile and
-// thresholds are recomputed from adjacent entries), and outputs go straight
-// to global memory -- all lanes store element u together, a coalesced 32-byte
-// access.  16 KB of shared memory per warp, no local memory.
-__device__ __forceinline__ int sep_pos(int si, int gi, int su, int gu) {
-    const int mid = (si + su) >> 1;
-    return gi <= gu ? max(si + gu, mid) : min(su - gi, mid);
-}
-
-template <int AXIS>
-__global__ void __launch_bounds__(128)
-    dt_env_strided_kernel(int n, int64_t bx, int64_t by, int64_t bz, uint8_t *__restrict__ pdms,
-                          int64_t pitch, int64_t tiles) {
-    extern __shared__ __align__(16) uint8_t s_env[];
-    const int lane = threadIdx.x & 31;
-    const int warp = threadIdx.x >> 5;
-    const int wpc = blockDim.x >> 5;
-    const int L = (int)(AXIS == kAxisX ? bx : by);
-    const int64_t S = AXIS == kAxisX ? by * bz : bz;
-    uint8_t *tile = s_env + (size_t)warp * 32 * L;
-    uint8_t *stack = s_env + (size_t)wpc * 32 * L + (size_t)warp * 32 * L;
-    const int64_t zblocks = ceil_div(bz, 32);
-    const int64_t outer_n = AXIS == kAxisX ? by : bx;
-    for (int64_t t = (int64_t)blockIdx.x * wpc + warp; t < tiles; t += (int64_t)gridDim.x * wpc) {
-        const int64_t po = t / zblocks;
-        const int64_t z0 = (t % zblocks) * 32;
-        const int p = (int)(po / outer_n);
-        const int64_t o = po % outer_n;
-        const int nlines = (int)min((int64_t)32, bz - z0);
-        uint8_t *g = pdms + (int64_t)p * pitch + (AXIS == kAxisX ? o * bz : o * by * bz) + z0;
-        if (nlines == 32 && (bz & 3) == 0) {
-            for (int i = lane; i < L * 8; i += 32) {
-                const int u = i >> 3, w = i & 7;
-                *reinterpret_cast<uint32_t *>(tile + u * 32 + 4 * w) =
-                    *reinterpret_cast<const uint32_t *>(g + (int64_t)u * S + 4 * w);
-            }
-        } else {
-            for (int u = 0; u < L; ++u)
-                if (lane < nlines) tile[u * 32 + lane] = g[(int64_t)u * S + lane];
-        }
-        __syncwarp();
-        if (lane < nlines) {
-            const uint8_t *col = tile + lane;
-            uint8_t *stk = stack + lane;
-            uint8_t *outp = g + lane;
-            int q = 1, top = 0, below = 0, gtop = col[0], gbelow = 0, t_top = 0;
-            for (int u = 1; u < L; ++u) {
-                const int gu = col[u * 32];
-                for (;;) {
-                    const int fs = max(abs(t_top - top), gtop);
-                    const int fu = max(abs(t_top - u), gu);
-                    if (fs <= fu) break;
-                    if (--q == 0) break;
-                    top = below;
-                    gtop = gbelow;
-                    if (q >= 2) {
-                        below = stk[(q - 2) * 32];
-                        gbelow = col[below * 32];
-                        t_top = 1 + sep_pos(below, gbelow, top, gtop);
-                    } else {
-                        t_top = 0;
-                    }
-                }
-                if (q == 0) {
-                    q = 1;
-                    top = u;
-                    gtop = gu;
-                    t_top = 0;
-                } else {
-                    const int w = 1 + sep_pos(top, gtop, u, gu);
-                    if (w < L) {
-                        if (q >= 2) stk[(q - 2) * 32] = (uint8_t)below;
-                        below = top;
-                        gbelow = gtop;
-                        top = u;
-                        gtop = gu;
-                        t_top = w;
-                        ++q;
-                    }
-                }
-            }
-            for (int u = L - 1; u >= 0; --u) {
-                const int d = max(abs(u - top), gtop);
-                outp[(int64_t)u * S] = (uint8_t)(d < kDistClamp ? d : kDistClamp);
-                if (u == t_top && q > 1) {
-                    --q;
-                    top = below;
-                    gtop = gbelow;
-                    if (q >= 2) {
-                        below = stk[(q - 2) * 32];
-                        gbelow = col[below * 32];
-                        t_top = 1 + sep_pos(below, gbelow, top, gtop);
-                    } else {
-                        t_top = 0;
-                    }
-                }
             }
         }
         __syncwarp();
@@ -783,230 +607,6 @@ __global__ void __launch_bounds__(256)
     }
 }
 
-// ---- streaming sweep: 4 lines per lane, only the tables in shared memory ----------
-// The tile kernels hold a 256-byte tile row and a 256-byte table per line
-// (16 KB per warp, 12 resident warps): the envelope's load -> compare ->
-// select chain then leaves the SM half idle.  Here the lines stay in global
-// memory -- the forward sweep reads g and writes L in place, the backward
-// sweep reads L back (an L2 hit: a warp's 32 KB of lines is revisited within
-// microseconds) and writes the result -- so shared memory holds only the
-// tables, [256 values][32 lanes][4 lines] bytes = 32 KB per warp, and an SM
-// keeps 7 warps x 128 lines in flight.  Each lane owns one bank of every
-// table row, so table accesses never conflict, and its 4 lines are 4
-// independent chains to interleave.  Register rings keep the loads of the
-// next elements in flight ahead of the chain.
-//   AXIS 1 (y lines): a warp = 128 consecutive z of one (p, x) plane; lane l
-//     has z0 + 4l .. +3, one 32-bit load/store per y (coalesced 512 B).
-//   AXIS 2 (z rows): a warp = 128 consecutive rows; lane l has rows
-//     r0 + 32t + l (t < 4), 16-byte loads/stores along each row.
-constexpr int kStreamTableBytes = 256 * 128;
-
-__device__ __forceinline__ uint32_t step_lane4(uint32_t &M, int g, int j, uint32_t tabt) {
-    const uint32_t G = tabt + 128u * (uint32_t)g;
-    const uint32_t a0 = min(G, M), a1 = min(G, M + 128u);
-    const int e = lds_u8(M);
-    uint32_t nM;
-    asm("{\n\t.reg .pred p;\n\t"
-        "setp.lt.s32 p, %1, %2;\n\t"
-        "selp.b32 %0, %3, %4, p;\n\t}"
-        : "=r"(nM)
-        : "r"(e), "r"(j), "r"(a1), "r"(a0));
-    sts_u8(G, min(g + j, kDistClamp));
-    M = nM;
-    return M - tabt;  // 128 * m
-}
-
-__device__ __forceinline__ void clear_stream_table(uint8_t *tab, int lane) {
-    uint4 *t = reinterpret_cast<uint4 *>(tab);
-#pragma unroll 8
-    for (int i = 0; i < kStreamTableBytes / 512; ++i) t[i * 32 + lane] = make_uint4(0u, 0u, 0u, 0u);
-}
-
-// One y position of the 4 lines of a lane: bytes of w are lines t = 0..3.
-__device__ __forceinline__ uint32_t step_word4(uint32_t (&M)[4], uint32_t w, int j, uint32_t tab) {
-    const uint32_t d0 = step_lane4(M[0], (int)__byte_perm(w, 0u, 0x4440u), j, tab);
-    const uint32_t d1 = step_lane4(M[1], (int)__byte_perm(w, 0u, 0x4441u), j, tab + 1);
-    const uint32_t d2 = step_lane4(M[2], (int)__byte_perm(w, 0u, 0x4442u), j, tab + 2);
-    const uint32_t d3 = step_lane4(M[3], (int)__byte_perm(w, 0u, 0x4443u), j, tab + 3);
-    return (d0 >> 7) | (d1 << 1) | (d2 << 9) | (d3 << 17);
-}
-
-template <bool kBackward>
-__device__ __forceinline__ void stream_y_sweep(uint8_t *base, int64_t bz, int L, bool act,
-                                               uint32_t tab) {
-    constexpr int R = 16;  // loads in flight ahead of the chain
-    uint32_t M[4];
-#pragma unroll
-    for (int t = 0; t < 4; ++t) M[t] = tab + t + 128u * kDistClamp;
-    auto addr = [&](int j) { return base + (int64_t)(kBackward ? L - 1 - j : j) * bz; };
-    // Loads are unconditional (clamped position; an inactive lane's base is
-    // lane 0's column): a predicated load into a ring slot makes the compiler
-    // merge old and new values with a move that waits on the load.
-    auto ld = [&](int j) {
-        const int jj = j < L ? j : L - 1;
-        return *reinterpret_cast<const uint32_t *>(base + (int64_t)(kBackward ? L - 1 - jj : jj) * bz);
-    };
-    uint32_t ring[R];
-#pragma unroll
-    for (int i = 0; i < R; ++i) ring[i] = ld(i);
-    for (int j0 = 0; j0 < L; j0 += R) {
-#pragma unroll
-        for (int i = 0; i < R; ++i) {
-            const int j = j0 + i;
-            if (j < L) {
-                const uint32_t w = ring[i];
-                ring[i] = ld(j + R);
-                const uint32_t o = step_word4(M, w, j, tab);
-                if (act) *reinterpret_cast<uint32_t *>(addr(j)) = o;
-            }
-        }
-    }
-}
-
-// 16 elements of each of the lane's 4 rows (chunk c of every row).
-template <bool kBackward>
-__device__ __forceinline__ void stream_z_chunk(uint32_t (&M)[4], const uint4 (&in)[4],
-                                               uint4 (&out)[4], int j0, uint32_t tab) {
-    uint32_t iw[4][4], ow[4][4];
-#pragma unroll
-    for (int t = 0; t < 4; ++t) {
-        iw[t][0] = in[t].x, iw[t][1] = in[t].y, iw[t][2] = in[t].z, iw[t][3] = in[t].w;
-    }
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {  // word of the chunk, in sweep order
-        const int word = kBackward ? 3 - q : q;
-        uint32_t d[4][4];
-#pragma unroll
-        for (int b = 0; b < 4; ++b) {  // byte of the word, in sweep order
-            const int byte = kBackward ? 3 - b : b;
-            const int j = j0 + 4 * q + b;
-#pragma unroll
-            for (int t = 0; t < 4; ++t)
-                d[t][byte] = step_lane4(M[t], (int)__byte_perm(iw[t][word], 0u, 0x4440u + byte), j,
-                                        tab + t);
-        }
-#pragma unroll
-        for (int t = 0; t < 4; ++t)
-            ow[t][word] = (d[t][0] >> 7) | (d[t][1] << 1) | (d[t][2] << 9) | (d[t][3] << 17);
-    }
-#pragma unroll
-    for (int t = 0; t < 4; ++t) out[t] = make_uint4(ow[t][0], ow[t][1], ow[t][2], ow[t][3]);
-}
-
-template <bool kBackward>
-__device__ __forceinline__ void stream_z_sweep(uint8_t *const (&row)[4], const bool (&act)[4],
-                                               int L, uint32_t tab) {
-    const int nc = L >> 4;
-    uint32_t M[4];
-#pragma unroll
-    for (int t = 0; t < 4; ++t) M[t] = tab + t + 128u * kDistClamp;
-    auto chunk = [&](int t, int c) {
-        return reinterpret_cast<uint4 *>(row[t]) + (kBackward ? nc - 1 - c : c);
-    };
-    // Unconditional loads (clamped chunk; inactive rows alias row 0 of the
-    // tile, which always exists): see stream_y_sweep.
-    uint4 cur[4];
-#pragma unroll
-    for (int t = 0; t < 4; ++t) cur[t] = *chunk(t, 0);
-    for (int c = 0; c < nc; ++c) {
-        uint4 nxt[4], out[4];
-        const int cn = c + 1 < nc ? c + 1 : c;
-#pragma unroll
-        for (int t = 0; t < 4; ++t) nxt[t] = *chunk(t, cn);
-        stream_z_chunk<kBackward>(M, cur, out, 16 * c, tab);
-#pragma unroll
-        for (int t = 0; t < 4; ++t) {
-            if (act[t]) *chunk(t, c) = out[t];
-            cur[t] = nxt[t];
-        }
-    }
-}
-
-constexpr int kStreamWarps = 7;  // 7 x 32 KB of tables: one CTA per SM
-
-// Tile geometry: AXIS 1 -> (p, x, 128 z) with `base` at z of lane 0;
-// AXIS 2 -> (p, 128 rows) with `base` at row 0.
-template <int AXIS>
-struct StreamTile {
-    uint8_t *base;
-    int64_t count;  // z (AXIS 1) or rows (AXIS 2) in the tile, <= 128
-};
-
-template <int AXIS>
-__device__ __forceinline__ StreamTile<AXIS> stream_tile(int64_t t, int64_t bx, int64_t by,
-                                                         int64_t bz, uint8_t *pdms,
-                                                         int64_t pitch) {
-    if (AXIS == kAxisY) {
-        const int64_t zt = ceil_div(bz, 128);
-        const int64_t px = t / zt, z0 = (t % zt) * 128;
-        return {pdms + (px / bx) * pitch + (px % bx) * by * bz + z0, min((int64_t)128, bz - z0)};
-    }
-    const int64_t rows = bx * by, rt = ceil_div(rows, 128);
-    const int64_t p = t / rt, r0 = (t % rt) * 128;
-    return {pdms + p * pitch + r0 * bz, min((int64_t)128, rows - r0)};
-}
-
-// Pull a tile's bytes into L2 ahead of its sweeps (the register rings then
-// wait on L2, not DRAM): y tiles are L rows of 128 B at stride bz, one
-// prefetch per row; z tiles are one contiguous span.
-template <int AXIS>
-__device__ __forceinline__ void stream_prefetch(const StreamTile<AXIS> &tl, int64_t bz, int L,
-                                                int lane) {
-    if (AXIS == kAxisY) {
-        for (int u = lane; u < L; u += 32)
-            asm volatile("prefetch.global.L2 [%0];" ::"l"(tl.base + (int64_t)u * bz));
-    } else if (lane == 0) {
-        const uint32_t bytes = (uint32_t)(tl.count * bz);  // multiple of 16 (bz % 16 == 0)
-        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(tl.base), "r"(bytes)
-                     : "memory");
-    }
-}
-
-template <int AXIS>
-__global__ void __launch_bounds__(32 * kStreamWarps)
-    dt_stream_kernel(int n, int64_t bx, int64_t by, int64_t bz, uint8_t *__restrict__ pdms,
-                     int64_t pitch, int64_t tiles) {
-    extern __shared__ __align__(16) uint8_t s_tab[];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    uint8_t *wtab = s_tab + (size_t)warp * kStreamTableBytes;
-    const uint32_t tab = tma::smem_u32(wtab) + 4u * lane;
-    const int L = (int)(AXIS == kAxisY ? by : bz);
-    const int64_t stride = (int64_t)gridDim.x * kStreamWarps;
-    int64_t t = (int64_t)blockIdx.x * kStreamWarps + warp;
-    if (t < tiles) stream_prefetch<AXIS>(stream_tile<AXIS>(t, bx, by, bz, pdms, pitch), bz, L, lane);
-    for (; t < tiles; t += stride) {
-        const StreamTile<AXIS> tl = stream_tile<AXIS>(t, bx, by, bz, pdms, pitch);
-        if (t + stride < tiles)
-            stream_prefetch<AXIS>(stream_tile<AXIS>(t + stride, bx, by, bz, pdms, pitch), bz, L,
-                                  lane);
-        uint8_t *row[4];
-        bool ract[4];
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            ract[k] = 32 * k + lane < tl.count;
-            row[k] = tl.base + (ract[k] ? (int64_t)(32 * k + lane) * bz : 0);
-        }
-        const bool yact = 4 * lane < tl.count;
-        uint8_t *ybase = tl.base + (yact ? 4 * lane : 0);
-        for (int dir = 0; dir < 2; ++dir) {
-            clear_stream_table(wtab, lane);
-            __syncwarp();
-            if (AXIS == kAxisY) {
-                if (dir == 0)
-                    stream_y_sweep<false>(ybase, bz, L, yact, tab);
-                else
-                    stream_y_sweep<true>(ybase, bz, L, yact, tab);
-            } else {
-                if (dir == 0)
-                    stream_z_sweep<false>(row, ract, L, tab);
-                else
-                    stream_z_sweep<true>(row, ract, L, tab);
-            }
-            __syncwarp();
-        }
-    }
-}
-
 // ---- slab pieces --------------------------------------------------------------------
 __global__ void slab_edges_kernel(const uint8_t *__restrict__ pdms, int64_t pitch, int n,
                                   int64_t bx, int64_t plane, uint8_t *__restrict__ edges) {
@@ -1078,7 +678,7 @@ static int tile_pass(int n, int64_t bx, int64_t by, int64_t bz, uint8_t *pdms, i
     const bool swz = kSweep && AXIS == kAxisZ && L % 128 == 0 && bz % 16 == 0;
     const int sstride = swz ? (int)L : 4 * sw;
     const size_t per_warp = (AXIS == kAxisZ ? (size_t)32 * sstride : (size_t)32 * L) +
-                            (kSweep ? (size_t)8192 : (!kDist1D && LMAX <= 64 ? (size_t)64 * L : 0));
+                            (kSweep ? (size_t)8192 : 0);
     int wpc = (int)(65536 / per_warp);
     wpc = wpc < 1 ? 1 : (wpc > 4 ? 4 : wpc);
     const size_t smem = per_warp * wpc;
@@ -1098,32 +698,6 @@ static int tile_pass(int n, int64_t bx, int64_t by, int64_t bz, uint8_t *pdms, i
     if (grid > cap) grid = cap;
     kern<<<(unsigned)grid, 32 * wpc, smem, s>>>(n, bx, by, bz, pdms, pitch, sstride, tiles);
     return cuda_status("dt_tile_kernel");
-}
-
-// Streaming sweep for lines <= 256: y lines need 4-byte aligned z runs, z
-// rows 16-byte aligned rows.  One warp per CTA, 32 KB of tables each.
-template <int AXIS>
-static int stream_pass(int n, int64_t bx, int64_t by, int64_t bz, uint8_t *pdms, int64_t pitch,
-                       cudaStream_t s) {
-    auto kern = dt_stream_kernel<AXIS>;
-    const int smem = kStreamWarps * kStreamTableBytes;
-    PDM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    const int64_t tiles = AXIS == kAxisY ? (int64_t)n * bx * ceil_div(bz, 128)
-                                         : (int64_t)n * ceil_div(bx * by, 128);
-    int64_t grid = ceil_div(tiles, kStreamWarps);
-    if (grid > sm_count()) grid = sm_count();
-    kern<<<(unsigned)grid, 32 * kStreamWarps, smem, s>>>(n, bx, by, bz, pdms, pitch, tiles);
-    return cuda_status("dt_stream_kernel");
-}
-
-static bool wide_enabled() {
-    static int on = -1;
-    if (on < 0) {
-        // PDM_DT_WIDE=0 keeps the per-lane x pass (A/B only).
-        const char *e = getenv("PDM_DT_WIDE");
-        on = (e && e[0] == '0') ? 0 : 1;
-    }
-    return on == 1;
 }
 
 // x pass (1-D distance along x) with 128-z tiles, 4 lines per lane.
@@ -1149,89 +723,20 @@ static int wide_x_pass(int n, int64_t bx, int64_t by, int64_t bz, uint8_t *pdms,
     return cuda_status("dt_dist1d_wide_kernel");
 }
 
-static bool stream_enabled() {
-    static int on = -1;
-    if (on < 0) {
-        // PDM_DT_STREAM=1 selects the streaming sweep (A/B only).  Off by
-        // default: at config c passes y+z took 6.1 ms vs 1.53 ms for the tile
-        // kernels -- with only 7 warps per SM the register rings cannot cover
-        // the global load latency (long-scoreboard stalls ~5 per issue).
-        const char *e = getenv("PDM_DT_STREAM");
-        on = (e && e[0] == '1') ? 1 : 0;
-    }
-    return on == 1;
-}
-
-static bool sweep_enabled() {
-    static int on = -1;
-    if (on < 0) {
-        // PDM_DT_SWEEP=0 falls back to the Meijster stack scan (A/B only).
-        const char *e = getenv("PDM_DT_SWEEP");
-        on = (e && e[0] == '0') ? 0 : 1;
-    }
-    return on == 1;
-}
-
-static bool env_strided_enabled() {
-    static int on = -1;
-    if (on < 0) {
-        // PDM_DT_ENV=1 selects the shared-stack strided envelope kernel.  Off by
-        // default: at config c it measured 5.14 ms for passes y+z vs 4.90 ms for
-        // the warp-tile kernel with local-memory stacks (fewer resident warps).
-        const char *e = getenv("PDM_DT_ENV");
-        on = (e && e[0] == '1') ? 1 : 0;
-    }
-    return on == 1;
-}
-
-template <int AXIS>
-static int env_strided_pass(int n, int64_t bx, int64_t by, int64_t bz, uint8_t *pdms,
-                            int64_t pitch, cudaStream_t s) {
-    const int64_t L = AXIS == kAxisX ? bx : by;
-    const int wpc = 4;
-    const size_t smem = (size_t)wpc * 64 * L;
-    auto kern = dt_env_strided_kernel<AXIS>;
-    PDM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)smem));
-    const int64_t tiles = (int64_t)n * (AXIS == kAxisX ? by : bx) * ceil_div(bz, 32);
-    int per_sm = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * wpc, smem) !=
-            cudaSuccess ||
-        per_sm < 1)
-        per_sm = 1;
-    int64_t grid = ceil_div(tiles, wpc);
-    const int64_t cap = (int64_t)sm_count() * per_sm;
-    if (grid > cap) grid = cap;
-    kern<<<(unsigned)grid, 32 * wpc, smem, s>>>(n, bx, by, bz, pdms, pitch, tiles);
-    return cuda_status("dt_env_strided_kernel");
-}
-
 template <int AXIS, bool kDist1D>
 static int axis_pass(int n, int64_t bx, int64_t by, int64_t bz, uint8_t *pdms, int64_t pitch,
                      cudaStream_t s) {
     const int64_t L = AXIS == kAxisX ? bx : (AXIS == kAxisY ? by : bz);
     if (L <= 1) return PDM_OK;  // a 1-long line is already final
-    if constexpr (kDist1D && AXIS == kAxisX) {
-        if (L <= 256 && bz % 16 == 0 && wide_enabled()) return wide_x_pass(n, bx, by, bz, pdms, pitch, s);
-    }
-    if constexpr (!kDist1D && AXIS != kAxisX) {
-        if (L <= 256 && stream_enabled() &&
-            (AXIS == kAxisY ? bz % 4 == 0 : bz % 16 == 0))
-            return stream_pass<AXIS>(n, bx, by, bz, pdms, pitch, s);
-    }
-    if constexpr (!kDist1D) {
-        if (L <= 256 && sweep_enabled())
-            return tile_pass<256, AXIS, false, true>(n, bx, by, bz, pdms, pitch, s);
-    }
-    if (kDist1D || L <= 64) {
-        if (L <= 64) return tile_pass<64, AXIS, kDist1D>(n, bx, by, bz, pdms, pitch, s);
-        if (L <= 1024) return tile_pass<64, AXIS, kDist1D>(n, bx, by, bz, pdms, pitch, s);
-    } else if (AXIS != kAxisZ && L <= 256 && env_strided_enabled()) {
-        return env_strided_pass<AXIS == kAxisZ ? kAxisY : AXIS>(n, bx, by, bz, pdms, pitch, s);
+    if constexpr (kDist1D) {
+        if (AXIS == kAxisX && L <= 256 && bz % 16 == 0)
+            return wide_x_pass(n, bx, by, bz, pdms, pitch, s);
+        if (L <= 1024) return tile_pass<64, AXIS, true>(n, bx, by, bz, pdms, pitch, s);
     } else {
-        if (L <= 256) return tile_pass<256, AXIS, kDist1D>(n, bx, by, bz, pdms, pitch, s);
-        if (L <= 512) return tile_pass<512, AXIS, kDist1D>(n, bx, by, bz, pdms, pitch, s);
-        if (L <= 1024) return tile_pass<1024, AXIS, kDist1D>(n, bx, by, bz, pdms, pitch, s);
+        // lines <= 256: stack-free sweep envelope; longer: Meijster's scan
+        if (L <= 256) return tile_pass<256, AXIS, false, true>(n, bx, by, bz, pdms, pitch, s);
+        if (L <= 512) return tile_pass<512, AXIS, false>(n, bx, by, bz, pdms, pitch, s);
+        if (L <= 1024) return tile_pass<1024, AXIS, false>(n, bx, by, bz, pdms, pitch, s);
     }
     const int64_t lines = (int64_t)n * bx * by * bz / L;
     dt_line_kernel<AXIS, kDist1D><<<grid_for(lines, 128, 16), 128, 0, s>>>(n, bx, by, bz, pdms,

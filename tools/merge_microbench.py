@@ -37,7 +37,7 @@ def main():
     args = ap.parse_args()
     L = _lib.lib()
     nb, n = args.blocks, args.n
-    pitch = device.plane_pitch(nb)
+    pitch = device.plane_pitch(nb) + int(os.environ.get("PDM_MB_RAW_PAD", "0"))
     if args.packed:  # 1-Lipschitz rows of 256 blocks, like distance fields
         steps = torch.randint(-1, 2, (n, pitch // 256, 256), dtype=torch.int16, device="cuda")
         start = torch.randint(0, 256, (n, pitch // 256, 1), dtype=torch.int16, device="cuda")
@@ -81,6 +81,8 @@ def main():
     if args.packed:
         chunks = int(L.pdm_packed_chunks(nb))
         nib_pitch, base_pitch = -(-chunks * 8 // 256) * 256, -(-chunks // 256) * 256
+        nib_pitch += int(os.environ.get("PDM_MB_NIB_PAD", "0"))  # plane-stride experiments
+        base_pitch += int(os.environ.get("PDM_MB_BASE_PAD", "0"))
         nib = torch.empty((n, nib_pitch), dtype=torch.uint8, device="cuda")
         base = torch.empty((n, base_pitch), dtype=torch.uint8, device="cuda")
         bad = torch.zeros(1, dtype=torch.int32, device="cuda")
