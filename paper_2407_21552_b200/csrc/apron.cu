@@ -162,14 +162,27 @@ __global__ void __launch_bounds__(32 * kApronWarps)
                 vmx[e] = 0;
             }
             uint32_t lmn = kHi, lmx = 0, rmn = kHi, rmx = 0;  // strip-edge voxels
+            // 16-bit voxels: reduce the rows two voxels per instruction
+            // (u16x2 min/max on the packed words), unpack once per plane.
+            uint32_t wmn[4] = {kHi, kHi, kHi, kHi}, wmx[4] = {0u, 0u, 0u, 0u};
             for (int yy = 0; yy < nrows; ++yy) {
                 if (active) {
-                    uint32_t v[VPC];
-                    unpack16<BITS>(ring_main[(slot * kRows + yy) * 32 + lane], v);
+                    const uint4 q = ring_main[(slot * kRows + yy) * 32 + lane];
+                    if (BITS == 16) {
+                        const uint32_t w[4] = {q.x, q.y, q.z, q.w};
 #pragma unroll
-                    for (int e = 0; e < VPC; ++e) {
-                        vmn[e] = min(vmn[e], v[e]);
-                        vmx[e] = max(vmx[e], v[e]);
+                        for (int i = 0; i < 4; ++i) {
+                            wmn[i] = __vminu2(wmn[i], w[i]);
+                            wmx[i] = __vmaxu2(wmx[i], w[i]);
+                        }
+                    } else {
+                        uint32_t v[VPC];
+                        unpack16<BITS>(q, v);
+#pragma unroll
+                        for (int e = 0; e < VPC; ++e) {
+                            vmn[e] = min(vmn[e], v[e]);
+                            vmx[e] = max(vmx[e], v[e]);
+                        }
                     }
                 }
                 if (lane == 0 && has_left) {  // voxel zs-1: top of its aligned word
@@ -183,6 +196,15 @@ __global__ void __launch_bounds__(32 * kApronWarps)
                     const uint32_t e = BITS == 8 ? w & 0xFFu : w & 0xFFFFu;
                     rmn = min(rmn, e);
                     rmx = max(rmx, e);
+                }
+            }
+            if (BITS == 16) {
+#pragma unroll
+                for (int i = 0; i < VPC / 2; ++i) {
+                    vmn[2 * i] = wmn[i] & 0xFFFFu;
+                    vmn[2 * i + 1] = wmn[i] >> 16;
+                    vmx[2 * i] = wmx[i] & 0xFFFFu;
+                    vmx[2 * i + 1] = wmx[i] >> 16;
                 }
             }
             issue_plane(x + kRing, slot);  // refill the slot just consumed
