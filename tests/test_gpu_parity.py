@@ -387,3 +387,27 @@ def test_packed_dprime_to_host():
             idx_path = pdm.combine(pset, pdm.PartitionSelection(selected=frozenset(s), n=8))
             assert np.array_equal(idx_path.dist, want), (dims, s)
             assert np.array_equal(idx_path.device().cpu().numpy(), want), (dims, s)
+
+
+def test_packed_disabled_by_env_and_dropped(monkeypatch):
+    """PDM_PACKED=0 keeps sets raw; drop_packed() forgets a packed copy; both
+    merge paths agree."""
+    rng = np.random.default_rng(41)
+    dims = (32, 24, 64)
+    vox = random_structured_volume(rng, dims, 16)
+    vol, grid, scheme = pdm.Volume.from_array(vox), pdm.BlockGrid.for_dims(dims, 4), \
+        pdm.scheme_uniform(8, 16)
+    packed_set = pdm.build_pdm_set(vol, grid, scheme)
+    assert packed_set.packed() is not None
+    assert packed_set.device_bytes() > packed_set.n * packed_set.plane_pitch
+    monkeypatch.setenv("PDM_PACKED", "0")
+    raw_set = pdm.build_pdm_set(vol, grid, scheme)
+    assert raw_set.packed() is None
+    assert raw_set.device_bytes() == raw_set.n * raw_set.plane_pitch
+    sel = pdm.PartitionSelection(selected=frozenset({2, 3, 7}), n=8)
+    assert np.array_equal(pdm.combine(raw_set, sel).dist, pdm.combine(packed_set, sel).dist)
+    monkeypatch.delenv("PDM_PACKED")
+    packed_set.drop_packed()
+    assert packed_set._packed is None
+    assert np.array_equal(pdm.combine(packed_set, sel).dist, pdm.combine(raw_set, sel).dist)
+    assert packed_set.packed() is not None  # re-packed on demand

@@ -128,6 +128,10 @@ def test_sharded_build_nccl_world1():
             assert got.slab == (0, 8, 8)
             assert np.array_equal(np.stack([d.dist for d in got.pdms]),
                                   np.stack([d.dist for d in want.pdms])), mode
+            # the slab's set is packed at build time and merges like the full set
+            assert got.packed() is not None
+            sel = pdm.PartitionSelection(selected=frozenset({1, 4, 9, 12}), n=n)
+            assert np.array_equal(pdm.combine(got, sel).dist, pdm.combine(want, sel).dist)
     finally:
         dist.destroy_process_group()
 
