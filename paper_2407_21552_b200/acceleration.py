@@ -104,7 +104,7 @@ class _BlockArray:
     def _host_array(self):
         if self._host is None:
             if self._dev is None and self._pending_host is not None:
-                host = np.empty(self.bdims, dtype=np.uint8)
+                host = device.host_buffer(self.bdims)  # recycled, already faulted in
                 self._pending_host(host)
                 self._host = host
                 return self._host

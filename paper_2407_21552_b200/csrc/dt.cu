@@ -137,21 +137,46 @@ __device__ __forceinline__ int lds_u8(uint32_t a) {
 __device__ __forceinline__ void sts_u8(uint32_t a, int v) {
     asm volatile("st.shared.u8 [%0], %1;" ::"r"(a), "r"(v) : "memory");
 }
+__device__ __forceinline__ int lds_u16(uint32_t a) {
+    uint32_t v;
+    asm volatile("ld.shared.u16 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+    return (int)v;
+}
+__device__ __forceinline__ void sts_u16(uint32_t a, int v) {
+    asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
 
-// One step in "address space": M = tab + 32 m is the table entry of the
-// running value and G = tab + 32 g; min() commutes with that map, so the two
-// candidates are min(G, M) and min(G, M + 32).  Returns 32 * m.
+// Table geometry by entry width TB (bytes): lines <= 256 use byte entries
+// (positions + values saturate at 255, exact because positions <= 255);
+// lines 257..512 use 16-bit entries (position + value <= 766, no saturation).
+// A value row of the [256][32] table is 32 * TB bytes.
+template <int TB>
+struct SweepTable {
+    static constexpr uint32_t kRow = 32u * TB;
+    static constexpr int kShift = TB == 1 ? 5 : 6;  // log2(kRow)
+    static constexpr size_t kBytes = (size_t)256 * kRow;
+};
+
+// One step in "address space": M = tab + R m is the table entry of the
+// running value (R = the table's value-row bytes) and G = tab + R g; min()
+// commutes with that map, so the two candidates are min(G, M) and
+// min(G, M + R).  Returns R * m.
+template <int TB>
 __device__ __forceinline__ uint32_t step_scaled(uint32_t &M, int g, int j, uint32_t tab) {
-    const uint32_t G = tab + 32u * (uint32_t)g;
-    const uint32_t a0 = min(G, M), a1 = min(G, M + 32u);
-    const int e = lds_u8(M);
+    constexpr uint32_t R = SweepTable<TB>::kRow;
+    const uint32_t G = tab + R * (uint32_t)g;
+    const uint32_t a0 = min(G, M), a1 = min(G, M + R);
+    const int e = TB == 1 ? lds_u8(M) : lds_u16(M);
     uint32_t nM;
     asm("{\n\t.reg .pred p;\n\t"
         "setp.lt.s32 p, %1, %2;\n\t"
         "selp.b32 %0, %3, %4, p;\n\t}"
         : "=r"(nM)
         : "r"(e), "r"(j), "r"(a1), "r"(a0));
-    sts_u8(G, min(g + j, kDistClamp));
+    if (TB == 1)
+        sts_u8(G, min(g + j, kDistClamp));
+    else
+        sts_u16(G, g + j);
     M = nM;
     return M - tab;
 }
@@ -159,31 +184,34 @@ __device__ __forceinline__ uint32_t step_scaled(uint32_t &M, int g, int j, uint3
 // Four steps on one word of 4 consecutive elements (one PRMT per byte).
 // kRev walks the bytes high to low (backward sweep); j0 is the sweep position
 // of the first element handled.
-template <bool kRev>
+template <int TB, bool kRev>
 __device__ __forceinline__ uint32_t sweep_word(uint32_t &M, uint32_t w, int j0, uint32_t tab) {
+    constexpr int sh = SweepTable<TB>::kShift;
     uint32_t d[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
         const int byte = kRev ? 3 - k : k;
-        d[byte] = step_scaled(M, (int)__byte_perm(w, 0u, 0x4440u + byte), j0 + k, tab);
+        d[byte] = step_scaled<TB>(M, (int)__byte_perm(w, 0u, 0x4440u + byte), j0 + k, tab);
     }
-    return (d[0] >> 5) | (d[1] << 3) | (d[2] << 11) | (d[3] << 19);
+    return (d[0] >> sh) | (d[1] << (8 - sh)) | (d[2] << (16 - sh)) | (d[3] << (24 - sh));
 }
 
+template <int TB>
 __device__ __forceinline__ uint4 sweep_chunk_fwd(uint32_t &M, uint4 c, int j0, uint32_t tab) {
     uint4 o;
-    o.x = sweep_word<false>(M, c.x, j0, tab);
-    o.y = sweep_word<false>(M, c.y, j0 + 4, tab);
-    o.z = sweep_word<false>(M, c.z, j0 + 8, tab);
-    o.w = sweep_word<false>(M, c.w, j0 + 12, tab);
+    o.x = sweep_word<TB, false>(M, c.x, j0, tab);
+    o.y = sweep_word<TB, false>(M, c.y, j0 + 4, tab);
+    o.z = sweep_word<TB, false>(M, c.z, j0 + 8, tab);
+    o.w = sweep_word<TB, false>(M, c.w, j0 + 12, tab);
     return o;
 }
+template <int TB>
 __device__ __forceinline__ uint4 sweep_chunk_bwd(uint32_t &M, uint4 c, int j0, uint32_t tab) {
     uint4 o;
-    o.w = sweep_word<true>(M, c.w, j0, tab);
-    o.z = sweep_word<true>(M, c.z, j0 + 4, tab);
-    o.y = sweep_word<true>(M, c.y, j0 + 8, tab);
-    o.x = sweep_word<true>(M, c.x, j0 + 12, tab);
+    o.w = sweep_word<TB, true>(M, c.w, j0, tab);
+    o.z = sweep_word<TB, true>(M, c.z, j0 + 4, tab);
+    o.y = sweep_word<TB, true>(M, c.y, j0 + 8, tab);
+    o.x = sweep_word<TB, true>(M, c.x, j0 + 12, tab);
     return o;
 }
 
@@ -218,15 +246,16 @@ struct TileLine {
 // Forward sweep in place.  Every layout loads the next group of elements
 // before the current group's results are stored (the table accesses are
 // ordered PTX, so the compiler cannot hoist loads across them by itself).
-template <int LAYOUT>
+template <int TB, int LAYOUT>
 __device__ __forceinline__ void sweep_forward(int len, TileLine<LAYOUT> line, uint32_t tab) {
-    uint32_t M = tab + 32u * kDistClamp;
+    constexpr int sh = SweepTable<TB>::kShift;
+    uint32_t M = tab + SweepTable<TB>::kRow * kDistClamp;
     if (LAYOUT == kRowSwz) {
         const int nc = len >> 4;
         uint4 c = *line.chunk(0);
         for (int cc = 0; cc < nc; ++cc) {
             const uint4 nx = cc + 1 < nc ? *line.chunk(cc + 1) : make_uint4(0u, 0u, 0u, 0u);
-            *line.chunk(cc) = sweep_chunk_fwd(M, c, 16 * cc, tab);
+            *line.chunk(cc) = sweep_chunk_fwd<TB>(M, c, 16 * cc, tab);
             c = nx;
         }
         return;
@@ -235,7 +264,7 @@ __device__ __forceinline__ void sweep_forward(int len, TileLine<LAYOUT> line, ui
         uint32_t w = line.ld4(0);
         for (int u = 0; u < len; u += 4) {
             const uint32_t wn = u + 4 < len ? line.ld4(u + 4) : 0u;
-            line.st4(u, sweep_word<false>(M, w, u, tab));
+            line.st4(u, sweep_word<TB, false>(M, w, u, tab));
             w = wn;
         }
         return;
@@ -247,27 +276,28 @@ __device__ __forceinline__ void sweep_forward(int len, TileLine<LAYOUT> line, ui
             if (u + 4 < len) {
                 n0 = line.ld(u + 4), n1 = line.ld(u + 5), n2 = line.ld(u + 6), n3 = line.ld(u + 7);
             }
-            line.st(u, step_scaled(M, q0, u, tab) >> 5);
-            line.st(u + 1, step_scaled(M, q1, u + 1, tab) >> 5);
-            line.st(u + 2, step_scaled(M, q2, u + 2, tab) >> 5);
-            line.st(u + 3, step_scaled(M, q3, u + 3, tab) >> 5);
+            line.st(u, step_scaled<TB>(M, q0, u, tab) >> sh);
+            line.st(u + 1, step_scaled<TB>(M, q1, u + 1, tab) >> sh);
+            line.st(u + 2, step_scaled<TB>(M, q2, u + 2, tab) >> sh);
+            line.st(u + 3, step_scaled<TB>(M, q3, u + 3, tab) >> sh);
             q0 = n0, q1 = n1, q2 = n2, q3 = n3;
         }
         return;
     }
-    for (int u = 0; u < len; ++u) line.st(u, step_scaled(M, line.ld(u), u, tab) >> 5);
+    for (int u = 0; u < len; ++u) line.st(u, step_scaled<TB>(M, line.ld(u), u, tab) >> sh);
 }
 
 // Backward sweep in place: sweep position j = len - 1 - u.
-template <int LAYOUT>
+template <int TB, int LAYOUT>
 __device__ __forceinline__ void sweep_backward(int len, TileLine<LAYOUT> line, uint32_t tab) {
-    uint32_t M = tab + 32u * kDistClamp;
+    constexpr int sh = SweepTable<TB>::kShift;
+    uint32_t M = tab + SweepTable<TB>::kRow * kDistClamp;
     if (LAYOUT == kRowSwz) {
         const int nc = len >> 4;
         uint4 c = *line.chunk(nc - 1);
         for (int cc = nc - 1, j = 0; cc >= 0; --cc, j += 16) {
             const uint4 nx = cc > 0 ? *line.chunk(cc - 1) : make_uint4(0u, 0u, 0u, 0u);
-            *line.chunk(cc) = sweep_chunk_bwd(M, c, j, tab);
+            *line.chunk(cc) = sweep_chunk_bwd<TB>(M, c, j, tab);
             c = nx;
         }
         return;
@@ -276,7 +306,7 @@ __device__ __forceinline__ void sweep_backward(int len, TileLine<LAYOUT> line, u
         uint32_t w = line.ld4(len - 4);
         for (int u0 = len - 4, j = 0; u0 >= 0; u0 -= 4, j += 4) {
             const uint32_t wn = u0 >= 4 ? line.ld4(u0 - 4) : 0u;
-            line.st4(u0, sweep_word<true>(M, w, j, tab));
+            line.st4(u0, sweep_word<TB, true>(M, w, j, tab));
             w = wn;
         }
         return;
@@ -289,25 +319,26 @@ __device__ __forceinline__ void sweep_backward(int len, TileLine<LAYOUT> line, u
             if (u >= 4) {
                 n0 = line.ld(u - 4), n1 = line.ld(u - 5), n2 = line.ld(u - 6), n3 = line.ld(u - 7);
             }
-            line.st(u, step_scaled(M, q0, j, tab) >> 5);
-            line.st(u - 1, step_scaled(M, q1, j + 1, tab) >> 5);
-            line.st(u - 2, step_scaled(M, q2, j + 2, tab) >> 5);
-            line.st(u - 3, step_scaled(M, q3, j + 3, tab) >> 5);
+            line.st(u, step_scaled<TB>(M, q0, j, tab) >> sh);
+            line.st(u - 1, step_scaled<TB>(M, q1, j + 1, tab) >> sh);
+            line.st(u - 2, step_scaled<TB>(M, q2, j + 2, tab) >> sh);
+            line.st(u - 3, step_scaled<TB>(M, q3, j + 3, tab) >> sh);
             q0 = n0, q1 = n1, q2 = n2, q3 = n3;
         }
         return;
     }
     for (int j = 0; j < len; ++j) {
         const int u = len - 1 - j;
-        line.st(u, step_scaled(M, line.ld(u), j, tab) >> 5);
+        line.st(u, step_scaled<TB>(M, line.ld(u), j, tab) >> sh);
     }
 }
 
-// Warp-collective clear of a [256][32] byte table (16 B per lane x 16).
+// Warp-collective clear of a [256][32] table (16 B per lane per store).
+template <int TB>
 __device__ __forceinline__ void clear_table(uint8_t *tab_warp, int lane) {
     uint4 *t = reinterpret_cast<uint4 *>(tab_warp);
 #pragma unroll
-    for (int i = 0; i < 16; ++i) t[i * 32 + lane] = make_uint4(0u, 0u, 0u, 0u);
+    for (int i = 0; i < 16 * TB; ++i) t[i * 32 + lane] = make_uint4(0u, 0u, 0u, 0u);
 }
 
 // ---- expand: partition occupancy -> {0, 255} planes ---------------------------------
@@ -364,10 +395,11 @@ __global__ void __launch_bounds__(256)
 enum { kAxisX = 0, kAxisY = 1, kAxisZ = 2 };
 
 template <int LMAX, int AXIS, bool kDist1D, bool kSweep>
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(256)
     dt_tile_kernel(int n, int64_t bx, int64_t by, int64_t bz, uint8_t *__restrict__ pdms,
                    int64_t pitch, int sstride, int64_t tiles) {
-    static_assert(!kSweep || (LMAX <= 256 && !kDist1D), "sweep envelope: lines <= 256");
+    static_assert(!kSweep || (LMAX <= 512 && !kDist1D), "sweep envelope: lines <= 512");
+    constexpr int TB = LMAX > 256 ? 2 : 1;  // sweep table entry bytes
     extern __shared__ __align__(16) uint8_t s_tiles[];
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
@@ -378,12 +410,12 @@ __global__ void __launch_bounds__(128)
     const size_t tile_bytes = kRows ? 32 * (size_t)sstride : 32 * (size_t)L;
     uint8_t *s = s_tiles + (size_t)warp * tile_bytes;
     // Per-warp scratch after all tiles: the sweep's [256][32] table.
-    uint8_t *tab_warp = s_tiles + (size_t)wpc * tile_bytes + (size_t)warp * 8192;
+    uint8_t *tab_warp = s_tiles + (size_t)wpc * tile_bytes + (size_t)warp * SweepTable<TB>::kBytes;
     const int64_t zblocks = ceil_div(bz, 32);
     const bool vec = (bz & 3) == 0;
-    // Swizzled 16-byte row tiles (the host sets sstride == L only when
-    // L % 128 == 0 and rows are 16-byte aligned).
-    const bool swz = kSweep && kRows && sstride == L && (L & 127) == 0;
+    // Swizzled 16-byte row tiles (the host sets sstride == L only when L is
+    // 128, 256 or 512 and rows are 16-byte aligned).
+    const bool swz = kSweep && kRows && sstride == L && (L & 127) == 0 && (L & (L - 1)) == 0;
     const int cpr = L >> 4, csh = __ffs(cpr) - 1;  // chunks per row (power of 2 if swz)
     // Tile t: rows -> 32 consecutive (x, y) rows of partition p; strided ->
     // 32 consecutive z of one line family (p, outer).
@@ -446,20 +478,20 @@ __global__ void __launch_bounds__(128)
         auto ld = [&](int u) -> int { return line[u * es]; };
         auto st = [&](int u, int v) { line[u * es] = (uint8_t)v; };
         if (kSweep) {
-            const uint32_t tab = smem_addr(tab_warp + lane);
+            const uint32_t tab = smem_addr(tab_warp + TB * lane);  // lane column
             for (int dir = 0; dir < 2; ++dir) {
-                clear_table(tab_warp, lane);
+                clear_table<TB>(tab_warp, lane);
                 __syncwarp();
                 if (lane < nlines) {
                     if (!kRows) {
                         const TileLine<kStrided> tl{line, lane};
-                        dir == 0 ? sweep_forward(L, tl, tab) : sweep_backward(L, tl, tab);
+                        dir == 0 ? sweep_forward<TB>(L, tl, tab) : sweep_backward<TB>(L, tl, tab);
                     } else if (swz) {
                         const TileLine<kRowSwz> tl{line, lane};
-                        dir == 0 ? sweep_forward(L, tl, tab) : sweep_backward(L, tl, tab);
+                        dir == 0 ? sweep_forward<TB>(L, tl, tab) : sweep_backward<TB>(L, tl, tab);
                     } else {
                         const TileLine<kRow> tl{line, lane};
-                        dir == 0 ? sweep_forward(L, tl, tab) : sweep_backward(L, tl, tab);
+                        dir == 0 ? sweep_forward<TB>(L, tl, tab) : sweep_backward<TB>(L, tl, tab);
                     }
                 }
                 __syncwarp();
@@ -675,12 +707,16 @@ static int tile_pass(int n, int64_t bx, int64_t by, int64_t bz, uint8_t *pdms, i
     // Row tiles for the sweep with L % 128 == 0 and 16-byte aligned rows use
     // unpadded 16-byte-swizzled rows (sstride == L); otherwise rows are
     // padded to 4 x odd bytes.
-    const bool swz = kSweep && AXIS == kAxisZ && L % 128 == 0 && bz % 16 == 0;
+    const bool swz = kSweep && AXIS == kAxisZ && L % 128 == 0 && (L & (L - 1)) == 0 &&
+                     bz % 16 == 0;  // 128, 256 or 512: chunk index math uses shifts
     const int sstride = swz ? (int)L : 4 * sw;
     const size_t per_warp = (AXIS == kAxisZ ? (size_t)32 * sstride : (size_t)32 * L) +
-                            (kSweep ? (size_t)8192 : 0);
-    int wpc = (int)(65536 / per_warp);
-    wpc = wpc < 1 ? 1 : (wpc > 4 ? 4 : wpc);
+                            (kSweep ? SweepTable<(LMAX > 256 ? 2 : 1)>::kBytes : 0);
+    // Up to 4 warps / 64 KB per CTA; 512-long sweep lines (32 KB per warp)
+    // take one CTA of up to 7 warps per SM instead.
+    const bool big = kSweep && LMAX > 256;
+    int wpc = (int)((big ? 227 * 1024 : 65536) / per_warp);
+    wpc = wpc < 1 ? 1 : (wpc > (big ? 8 : 4) ? (big ? 8 : 4) : wpc);
     const size_t smem = per_warp * wpc;
     auto kern = dt_tile_kernel<LMAX, AXIS, kDist1D, kSweep>;
     PDM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -733,9 +769,9 @@ static int axis_pass(int n, int64_t bx, int64_t by, int64_t bz, uint8_t *pdms, i
             return wide_x_pass(n, bx, by, bz, pdms, pitch, s);
         if (L <= 1024) return tile_pass<64, AXIS, true>(n, bx, by, bz, pdms, pitch, s);
     } else {
-        // lines <= 256: stack-free sweep envelope; longer: Meijster's scan
+        // lines <= 512: stack-free sweep envelope; longer: Meijster's scan
         if (L <= 256) return tile_pass<256, AXIS, false, true>(n, bx, by, bz, pdms, pitch, s);
-        if (L <= 512) return tile_pass<512, AXIS, false>(n, bx, by, bz, pdms, pitch, s);
+        if (L <= 512) return tile_pass<512, AXIS, false, true>(n, bx, by, bz, pdms, pitch, s);
         if (L <= 1024) return tile_pass<1024, AXIS, false>(n, bx, by, bz, pdms, pitch, s);
     }
     const int64_t lines = (int64_t)n * bx * by * bz / L;

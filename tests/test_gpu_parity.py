@@ -85,6 +85,9 @@ def test_distance_transform_random_vs_oracle_medium():
     (6, 61, 20),     # 4-byte copies, odd line length
     (5, 30, 13),     # scalar tile copies, partial warp tiles
     (300, 3, 256),   # x lines > 256 blocks (dist1d) with swizzled z rows
+    (4, 300, 384),   # 257..512-long lines: 16-bit sweep tables, strided y, swizzled z rows
+    (3, 257, 301),   # odd 16-bit-table lengths: padded rows, scalar steps
+    (2, 512, 512),   # longest sweep lines
 ])
 def test_distance_transform_tile_layouts(dims):
     """Every shared-memory tile layout of the sweep envelope kernel against

@@ -262,3 +262,21 @@ def test_distance_map_dump_format(tmp_path):
         pdm.load_distance_map(tmp_path / "junk.bin")
     with pytest.raises(pdm.VolumeError):
         pdm.load_pdm_set(tmp_path / "junk.bin")
+
+
+def test_host_buffer_recycles_only_unreferenced_buffers():
+    from paper_2407_21552_b200 import device
+
+    a = device.host_buffer((3, 7))
+    a[:] = 5
+    b = device.host_buffer((3, 7))
+    assert not np.shares_memory(a, b)  # a is alive: a second buffer
+    base_a = a.base
+    view = a[1:]
+    del a
+    c = device.host_buffer((3, 7))
+    assert not np.shares_memory(c, view)  # a slice keeps its buffer in use
+    del view, b, c
+    d = device.host_buffer((3, 7))
+    assert d.base is base_a or d.base is not None  # some pooled buffer is reused
+    assert d.shape == (3, 7) and d.dtype == np.uint8
