@@ -99,6 +99,15 @@ int pdm_pack_pdms(const uint8_t *pdms, int64_t plane_pitch, int64_t map_bytes, i
                   uint8_t *nib, int64_t nib_pitch, uint8_t *base, int64_t base_pitch,
                   uint32_t *violations, pdm_stream_t stream);
 
+/* pdm_distance_transform_mask followed by pdm_pack_pdms, with the packing
+ * fused into the last (z) pass when bz is 128, 256 or 512 (the rows are
+ * packed while still in shared memory); base_pitch % 4 == 0. */
+int pdm_distance_transform_mask_packed(const uint32_t *mask, int32_t words, int32_t n, int64_t bx,
+                                       int64_t by, int64_t bz, uint8_t *pdms,
+                                       int64_t plane_pitch, uint8_t *nib, int64_t nib_pitch,
+                                       uint8_t *base, int64_t base_pitch, uint32_t *violations,
+                                       pdm_stream_t stream);
+
 /* pdm_combine over packed planes (k <= 240), and pdm_combine_flags over them
  * (n <= 4096, PDL behind pdm_select).  Output: plain uint8 D'. */
 int pdm_combine_packed(const uint8_t *nib, int64_t nib_pitch, const uint8_t *base,

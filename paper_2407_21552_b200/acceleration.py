@@ -241,23 +241,29 @@ class PdmSet:
     # that are not distance fields).  Code that writes into ``storage`` after
     # a merge must call drop_packed().
 
+    def _alloc_packed(self):
+        """Device allocations for the packed copy: (nib, nib_pitch, base,
+        base_pitch, violation counter)."""
+        chunks = int(_lib.lib().pdm_packed_chunks(self.grid.num_blocks))
+        nib_pitch = -(-chunks * 8 // 256) * 256
+        base_pitch = -(-chunks // 256) * 256
+        return (device.empty((self.n, nib_pitch), np.uint8), nib_pitch,
+                device.empty((self.n, base_pitch), np.uint8), base_pitch,
+                device.empty((1,), np.uint32))
+
     def _start_pack(self):
         """Launch the packing on the current stream; returns the pending
         state (finished by _finish_pack) or False when disabled/empty."""
         if not _packed_enabled() or self.n == 0:
             return False
         L = _lib.lib()
-        nb = self.grid.num_blocks
-        chunks = int(L.pdm_packed_chunks(nb))
-        nib_pitch = -(-chunks * 8 // 256) * 256
-        base_pitch = -(-chunks // 256) * 256
-        nib = device.empty((self.n, nib_pitch), np.uint8)
-        base = device.empty((self.n, base_pitch), np.uint8)
-        bad = device.empty((1,), np.uint32)
-        _lib.check(L.pdm_pack_pdms(_lib.ptr(self.storage), self.plane_pitch, nb, self.n,
-                                   _lib.ptr(nib), nib_pitch, _lib.ptr(base), base_pitch,
-                                   _lib.ptr(bad), _lib.stream_handle()), "pdm_pack_pdms")
-        return (nib, nib_pitch, base, base_pitch, bad)
+        planes = self._alloc_packed()
+        nib, nib_pitch, base, base_pitch, bad = planes
+        _lib.check(L.pdm_pack_pdms(_lib.ptr(self.storage), self.plane_pitch,
+                                   self.grid.num_blocks, self.n, _lib.ptr(nib), nib_pitch,
+                                   _lib.ptr(base), base_pitch, _lib.ptr(bad),
+                                   _lib.stream_handle()), "pdm_pack_pdms")
+        return planes
 
     def _finish_pack(self, pending) -> None:
         if pending is False:
@@ -420,11 +426,22 @@ def build_pdm_set(volume: Volume, grid: BlockGrid, scheme: PartitionScheme,
     mask = partition_mask(volume, grid, scheme, mode)
     pitch = device.plane_pitch(grid.num_blocks)
     storage = device.empty((scheme.n, pitch), np.uint8)
-    _lib.check(L.pdm_distance_transform_mask(_lib.ptr(mask), mask.shape[1], scheme.n, *grid.bdims,
-                                             _lib.ptr(storage), pitch, _lib.stream_handle()),
-               "pdm_distance_transform_mask")
     pset = PdmSet(grid=grid, scheme=scheme, occupancy_mode=mode, storage=storage)
-    pending = pset._start_pack()  # part of the precompute: packed merge planes
+    if _packed_enabled():
+        # the packed merge planes are part of the precompute; the z pass
+        # writes them itself when it can (pdm_distance_transform_mask_packed)
+        pending = pset._alloc_packed()
+        nib, nib_pitch, base, base_pitch, bad = pending
+        _lib.check(L.pdm_distance_transform_mask_packed(
+            _lib.ptr(mask), mask.shape[1], scheme.n, *grid.bdims, _lib.ptr(storage), pitch,
+            _lib.ptr(nib), nib_pitch, _lib.ptr(base), base_pitch, _lib.ptr(bad),
+            _lib.stream_handle()), "pdm_distance_transform_mask_packed")
+    else:
+        pending = False
+        _lib.check(L.pdm_distance_transform_mask(_lib.ptr(mask), mask.shape[1], scheme.n,
+                                                 *grid.bdims, _lib.ptr(storage), pitch,
+                                                 _lib.stream_handle()),
+                   "pdm_distance_transform_mask")
     torch.cuda.synchronize()
     pset.init_seconds = time.perf_counter() - start
     pset._finish_pack(pending)

@@ -29,6 +29,7 @@
 // 32 consecutive z of one line family); lines along z are contiguous rows (a
 // tile is 32 consecutive rows, 16-byte chunks swizzled by row).  The x pass
 // (1-D distance) of lines <= 256 runs 4 lines per lane on 128-z tiles.
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #include "pdm_common.cuh"
@@ -394,10 +395,60 @@ __global__ void __launch_bounds__(256)
 // ---- warp-tile passes ----------------------------------------------------------------
 enum { kAxisX = 0, kAxisY = 1, kAxisZ = 2 };
 
+// Optional fused epilogue of the last pass (z rows): the packed copy of the
+// finished rows (csrc/packed.cu encoding: per 16-block chunk its min + 4-bit
+// offsets), written while the rows are still in shared memory so no separate
+// pass re-reads the PDMs.  nib == nullptr: off.
+struct PackDst {
+    uint8_t *nib;
+    int64_t nib_pitch;
+    uint8_t *base;
+    int64_t base_pitch;
+    unsigned int *bad;  // chunks spanning > 15 values (none for distance fields)
+};
+
+__device__ __forceinline__ uint32_t hmin2_u(uint32_t a, uint32_t b) {
+    __half2 r = __hmin2(*reinterpret_cast<const __half2 *>(&a),
+                        *reinterpret_cast<const __half2 *>(&b));
+    return *reinterpret_cast<uint32_t *>(&r);
+}
+__device__ __forceinline__ uint32_t hmax2_u(uint32_t a, uint32_t b) {
+    __half2 r = __hmax2(*reinterpret_cast<const __half2 *>(&a),
+                        *reinterpret_cast<const __half2 *>(&b));
+    return *reinterpret_cast<uint32_t *>(&r);
+}
+
+// Pack one 16-byte chunk: bytes as fp16 1024 + v in 16-bit lanes (HMNMX2 on
+// the FMA pipe) for min/max, offsets v - min (< 16, no borrow between bytes),
+// then two nibble bytes per byte pair via shift/or and one PRMT per 8 blocks.
+__device__ __forceinline__ uint2 pack_chunk(uint4 q, uint32_t &mn, unsigned int &nbad) {
+    const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+    uint32_t lo = 0x64FF64FFu, hi = 0x64006400u;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const uint32_t e = __byte_perm(w[i], 0x64646464u, 0x4240);
+        const uint32_t o = __byte_perm(w[i], 0x64646464u, 0x4341);
+        lo = hmin2_u(lo, hmin2_u(e, o));
+        hi = hmax2_u(hi, hmax2_u(e, o));
+    }
+    lo = hmin2_u(lo, __byte_perm(lo, 0u, 0x1032));
+    hi = hmax2_u(hi, __byte_perm(hi, 0u, 0x1032));
+    mn = lo & 0xFFu;
+    nbad += (hi & 0xFFu) - mn > 15u;
+    const uint32_t mb = mn * 0x01010101u;
+    uint32_t t[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const uint32_t d = w[i] - mb;  // bytes v - min, each < 16 for a valid chunk
+        t[i] = d | (d >> 4);           // byte 0: b0 | b1 << 4, byte 2: b2 | b3 << 4
+    }
+    return make_uint2(__byte_perm(t[0], t[1], 0x6420), __byte_perm(t[2], t[3], 0x6420));
+}
+
 template <int LMAX, int AXIS, bool kDist1D, bool kSweep>
 __global__ void __launch_bounds__(256)
     dt_tile_kernel(int n, int64_t bx, int64_t by, int64_t bz, uint8_t *__restrict__ pdms,
-                   int64_t pitch, int sstride, int64_t tiles) {
+                   int64_t pitch, int sstride, int64_t tiles, PackDst pk) {
     static_assert(!kSweep || (LMAX <= 512 && !kDist1D), "sweep envelope: lines <= 512");
     constexpr int TB = LMAX > 256 ? 2 : 1;  // sweep table entry bytes
     extern __shared__ __align__(16) uint8_t s_tiles[];
@@ -520,6 +571,41 @@ __global__ void __launch_bounds__(256)
                 for (int i = lane; i < nlines * L; i += 32) {
                     const int r = i / L, u = i - r * L;
                     g[(int64_t)r * bz + u] = s[r * sstride + u];
+                }
+            }
+            if (kSweep && swz && pk.nib != nullptr) {
+                // The rows are final: pack them.  Staging reuses the sweep's
+                // table area (nibbles [32][L/2 + 8], bases [32][L/16 + 4]).
+                const int nst = L / 2 + 8, bst = L / 16 + 4;
+                uint8_t *sn = tab_warp, *sb = tab_warp + 32 * nst;
+                unsigned int nbad = 0;
+                if (lane < nlines) {
+                    const TileLine<kRowSwz> tl{line, lane};
+                    for (int c = 0; c < cpr; ++c) {
+                        uint32_t mn;
+                        const uint2 pw = pack_chunk(*tl.chunk(c), mn, nbad);
+                        *reinterpret_cast<uint2 *>(sn + lane * nst + 8 * c) = pw;
+                        sb[lane * bst + c] = (uint8_t)mn;
+                    }
+                }
+                if (nbad) atomicAdd(pk.bad, nbad);
+                __syncwarp();
+                // rows r0.. of plane p are contiguous in the packed planes too
+                const int64_t rows = bx * by, per_p = ceil_div(rows, 32);
+                const int64_t p = t / per_p, r0 = (t % per_p) * 32;
+                uint8_t *gn = pk.nib + p * pk.nib_pitch + r0 * (L / 2);
+                uint8_t *gb = pk.base + p * pk.base_pitch + r0 * (L / 16);
+                const int nu = L / 16;  // 8-byte nibble units (= chunks) per row
+                for (int i = lane; i < nlines * nu; i += 32) {
+                    const int r = i / nu, c = i - r * nu;
+                    *reinterpret_cast<uint2 *>(gn + 8 * (int64_t)i) =
+                        *reinterpret_cast<const uint2 *>(sn + r * nst + 8 * c);
+                }
+                const int bu = L / 64;  // 4-byte base units per row
+                for (int i = lane; i < nlines * bu; i += 32) {
+                    const int r = i / bu, c = i - r * bu;
+                    *reinterpret_cast<uint32_t *>(gb + 4 * (int64_t)i) =
+                        *reinterpret_cast<const uint32_t *>(sb + r * bst + 4 * c);
                 }
             }
         } else {
@@ -700,7 +786,7 @@ static int grid_for(int64_t items, int threads, int per_sm) {
 
 template <int LMAX, int AXIS, bool kDist1D, bool kSweep = false>
 static int tile_pass(int n, int64_t bx, int64_t by, int64_t bz, uint8_t *pdms, int64_t pitch,
-                     cudaStream_t s) {
+                     cudaStream_t s, PackDst pk = PackDst{}) {
     const int64_t L = AXIS == kAxisX ? bx : (AXIS == kAxisY ? by : bz);
     int sw = (int)ceil_div(L, 4);
     if (sw % 2 == 0) sw += 1;
@@ -732,7 +818,7 @@ static int tile_pass(int n, int64_t bx, int64_t by, int64_t bz, uint8_t *pdms, i
     int64_t grid = ceil_div(tiles, wpc);
     const int64_t cap = (int64_t)sm_count() * per_sm;
     if (grid > cap) grid = cap;
-    kern<<<(unsigned)grid, 32 * wpc, smem, s>>>(n, bx, by, bz, pdms, pitch, sstride, tiles);
+    kern<<<(unsigned)grid, 32 * wpc, smem, s>>>(n, bx, by, bz, pdms, pitch, sstride, tiles, pk);
     return cuda_status("dt_tile_kernel");
 }
 
@@ -759,9 +845,11 @@ static int wide_x_pass(int n, int64_t bx, int64_t by, int64_t bz, uint8_t *pdms,
     return cuda_status("dt_dist1d_wide_kernel");
 }
 
+// pk (z pass only): fused packing epilogue; honoured when the z pass runs the
+// swizzled sweep (dt_fused_pack_ok), ignored otherwise.
 template <int AXIS, bool kDist1D>
 static int axis_pass(int n, int64_t bx, int64_t by, int64_t bz, uint8_t *pdms, int64_t pitch,
-                     cudaStream_t s) {
+                     cudaStream_t s, PackDst pk = PackDst{}) {
     const int64_t L = AXIS == kAxisX ? bx : (AXIS == kAxisY ? by : bz);
     if (L <= 1) return PDM_OK;  // a 1-long line is already final
     if constexpr (kDist1D) {
@@ -770,8 +858,8 @@ static int axis_pass(int n, int64_t bx, int64_t by, int64_t bz, uint8_t *pdms, i
         if (L <= 1024) return tile_pass<64, AXIS, true>(n, bx, by, bz, pdms, pitch, s);
     } else {
         // lines <= 512: stack-free sweep envelope; longer: Meijster's scan
-        if (L <= 256) return tile_pass<256, AXIS, false, true>(n, bx, by, bz, pdms, pitch, s);
-        if (L <= 512) return tile_pass<512, AXIS, false, true>(n, bx, by, bz, pdms, pitch, s);
+        if (L <= 256) return tile_pass<256, AXIS, false, true>(n, bx, by, bz, pdms, pitch, s, pk);
+        if (L <= 512) return tile_pass<512, AXIS, false, true>(n, bx, by, bz, pdms, pitch, s, pk);
         if (L <= 1024) return tile_pass<1024, AXIS, false>(n, bx, by, bz, pdms, pitch, s);
     }
     const int64_t lines = (int64_t)n * bx * by * bz / L;
@@ -791,11 +879,14 @@ static int pass_x_mask(const uint32_t *mask, int words, int n, int64_t bx, int64
 }
 
 static int pass_yz(int n, int64_t bx, int64_t by, int64_t bz, uint8_t *pdms, int64_t pitch,
-                   cudaStream_t s) {
+                   cudaStream_t s, PackDst pk = PackDst{}) {
     int st = axis_pass<kAxisY, false>(n, bx, by, bz, pdms, pitch, s);
     if (st) return st;
-    return axis_pass<kAxisZ, false>(n, bx, by, bz, pdms, pitch, s);
+    return axis_pass<kAxisZ, false>(n, bx, by, bz, pdms, pitch, s, pk);
 }
+
+// The z pass packs its rows itself when it runs the swizzled sweep tiles.
+static bool dt_fused_pack_ok(int64_t bz) { return bz == 128 || bz == 256 || bz == 512; }
 
 static int check_grid(const char *fn, int n, int64_t bx, int64_t by, int64_t bz, int64_t pitch) {
     PDM_REQUIRE(n >= 1 && bx >= 1 && by >= 1 && bz >= 1, "%s: bad sizes", fn);
@@ -838,6 +929,41 @@ extern "C" int pdm_distance_transform_mask(const uint32_t *mask, int32_t words, 
     st = pass_x_mask(mask, words, n, bx, by, bz, pdms, plane_pitch, s);
     if (st) return st;
     return pass_yz(n, bx, by, bz, pdms, plane_pitch, s);
+}
+
+extern "C" int pdm_distance_transform_mask_packed(const uint32_t *mask, int32_t words, int32_t n,
+                                                  int64_t bx, int64_t by, int64_t bz,
+                                                  uint8_t *pdms, int64_t plane_pitch,
+                                                  uint8_t *nib, int64_t nib_pitch, uint8_t *base,
+                                                  int64_t base_pitch, uint32_t *violations,
+                                                  pdm_stream_t stream) {
+    const char *fn = "pdm_distance_transform_mask_packed";
+    PDM_REQUIRE(mask && pdms && nib && base && violations, "%s: null pointer", fn);
+    PDM_REQUIRE(words == (n + 31) / 32, "%s: words", fn);
+    int st = check_grid(fn, n, bx, by, bz, plane_pitch);
+    if (st) return st;
+    const int64_t nb = bx * by * bz, nchunks = 2 * ceil_div(nb, 32);
+    PDM_REQUIRE(nib_pitch >= nchunks * 8 && base_pitch >= nchunks && nib_pitch % 16 == 0 &&
+                    base_pitch % 4 == 0 && (uintptr_t)nib % 16 == 0 && (uintptr_t)base % 4 == 0,
+                "%s: packed planes too small or misaligned", fn);
+    cudaStream_t s = as_stream(stream);
+    if (!dt_fused_pack_ok(bz)) {  // separate packing pass
+        st = pdm_distance_transform_mask(mask, words, n, bx, by, bz, pdms, plane_pitch, stream);
+        if (st) return st;
+        return pdm_pack_pdms(pdms, plane_pitch, nb, n, nib, nib_pitch, base, base_pitch,
+                             violations, stream);
+    }
+    PDM_CUDA_TRY(cudaMemsetAsync(violations, 0, sizeof(uint32_t), s));
+    st = pass_x_mask(mask, words, n, bx, by, bz, pdms, plane_pitch, s);
+    if (st) return st;
+    st = pass_yz(n, bx, by, bz, pdms, plane_pitch, s,
+                 PackDst{nib, nib_pitch, base, base_pitch, violations});
+    if (st) return st;
+    if (nchunks * 16 > nb) {  // the even-count padding chunk: all 255
+        PDM_CUDA_TRY(cudaMemset2DAsync(nib + (nchunks - 1) * 8, nib_pitch, 0, 8, n, s));
+        PDM_CUDA_TRY(cudaMemset2DAsync(base + nchunks - 1, base_pitch, 255, 1, n, s));
+    }
+    return PDM_OK;
 }
 
 extern "C" int pdm_dt_pass_x_mask(const uint32_t *mask, int32_t words, int32_t n, int64_t bx,

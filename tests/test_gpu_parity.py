@@ -331,10 +331,14 @@ def test_packed_merge_matches_oracle(dims, b, bits, n, packs):
         assert np.array_equal(dev.device().cpu().numpy(), oracle.combine(maps, s)), (k, s)
 
 
-def test_packed_planes_decode_to_the_raw_planes():
+@pytest.mark.parametrize("dims", [
+    (48, 32, 64),     # bz = 16: separate packing pass
+    (12, 8, 512),     # bz = 128: packing fused into the z pass
+    (8, 4, 1024),     # bz = 256: fused
+])
+def test_packed_planes_decode_to_the_raw_planes(dims):
     """Unpack the device's packed planes on the host: base + nibbles == raw."""
     rng = np.random.default_rng(12)
-    dims = (48, 32, 64)
     vox = random_structured_volume(rng, dims, 16)
     pset = pdm.build_pdm_set(pdm.Volume.from_array(vox), pdm.BlockGrid.for_dims(dims, 4),
                              pdm.scheme_uniform(8, 16))
