@@ -134,6 +134,18 @@ int pdm_combine_flags_packed_to_packed(const uint8_t *nib, int64_t nib_pitch,
 int pdm_unpack_packed_host(const uint8_t *nib, const uint8_t *base, int64_t map_bytes,
                            uint8_t *out);
 
+/* combine(...).dist in one call: the packed-output merge in `pieces` launches
+ * (an event after each) storing straight into pinned host staging
+ * stage_nib / stage_base (sized like one packed plane), and the host
+ * expansion of piece i into the host array `out` (map_bytes) while later
+ * pieces cross PCIe.  Selection: device flags[n] when flags != NULL (PDL
+ * behind pdm_select), else host sel[0..k).  Returns once `out` is complete. */
+int pdm_merge_packed_to_host(const uint8_t *nib, int64_t nib_pitch, const uint8_t *base,
+                             int64_t base_pitch, int64_t map_bytes, int32_t n,
+                             const uint8_t *flags, const int32_t *sel, int32_t k,
+                             uint8_t *stage_nib, uint8_t *stage_base, uint8_t *out,
+                             int32_t pieces, pdm_stream_t stream);
+
 /* ---- block reduction / occupancy (K1-K5) --------------------------------- */
 
 /* volume.py:289-300 block_min_max: per-block min/max over the block grown by a

@@ -469,13 +469,7 @@ def combine(pdm_set: PdmSet, selection: PartitionSelection,
             and pdm_set.n <= _MAX_FLAGS):
         # selection still on the device (select_partitions): no host round trip
         def host_produce(host):
-            packed = pdm_set.packed()
-            nib, nib_pitch, base, base_pitch = packed
-            _packed_to_host(pdm_set, host, lambda L, t0, nbytes, on, ob, st:
-                            L.pdm_combine_flags_packed_to_packed(
-                                _lib.ptr(nib) + 16 * t0, nib_pitch, _lib.ptr(base) + 2 * t0,
-                                base_pitch, nbytes, pdm_set.n, _lib.ptr(flags), on, ob, st),
-                            "pdm_combine_flags_packed_to_packed")
+            _packed_to_host(pdm_set, host, _lib.ptr(flags), None, 0)
 
         return DistanceMap._deferred(grid.b, grid.bdims,
                                      lambda out: combine_flags_into(pdm_set, flags, out),
@@ -506,48 +500,29 @@ def combine(pdm_set: PdmSet, selection: PartitionSelection,
                                  _lib.ptr(out), _lib.stream_handle()), "pdm_combine")
 
     def host_produce(host):
-        nib, nib_pitch, base, base_pitch = pdm_set.packed()
-        _packed_to_host(pdm_set, host, lambda L, t0, nbytes, on, ob, st:
-                        L.pdm_combine_packed_to_packed(
-                            _lib.ptr(nib) + 16 * t0, nib_pitch, _lib.ptr(base) + 2 * t0,
-                            base_pitch, nbytes, pdm_set.n, sel.ctypes.data, int(sel.size), on,
-                            ob, st),
-                        "pdm_combine_packed_to_packed")
+        _packed_to_host(pdm_set, host, None, sel.ctypes.data, int(sel.size))
 
     use_host_packed = 0 < sel.size <= _MAX_PACKED_SEL and pdm_set.packed() is not None
     return DistanceMap._deferred(grid.b, grid.bdims, produce,
                                  host_produce if use_host_packed else None)
 
 
-_HOST_PIECE_ITEMS = 1 << 17  # 32-block items per pipelined piece (4 pieces at config c; 8 measured slower)
+_HOST_PIECE_ITEMS = 1 << 17  # 32-block items per pipelined piece (4 pieces at config c)
 
 
-def _packed_to_host(pdm_set: PdmSet, host: np.ndarray, launch, name: str) -> None:
-    """D' for the host: the merge writes it packed (9/16 of the bytes) into
-    pinned staging buffers over PCIe, and the host expands it.  The map goes
-    in pieces (one merge launch each, an event after each) so the host
-    expands piece i while piece i+1 is still crossing PCIe.
-    ``launch(L, t0, nbytes, out_nib, out_base, stream)`` merges the blocks
-    [32 t0, 32 t0 + nbytes) into the given staging pointers."""
+def _packed_to_host(pdm_set: PdmSet, host: np.ndarray, flags_ptr, sel_ptr, k: int) -> None:
+    """D' for the host (pdm_merge_packed_to_host): the merge writes it packed
+    (9/16 of the bytes) into pinned staging over PCIe in pieces, and the host
+    expands piece i while piece i+1 is still in flight."""
     L = _lib.lib()
-    torch = device.torch()
+    nib, nib_pitch, base, base_pitch = pdm_set.packed()
     nib_h, base_h = pdm_set._host_stage()
-    st = _lib.stream_handle()
     nb = pdm_set.grid.num_blocks
-    items = -(-nb // 32)
-    pieces = []
-    for t0 in range(0, items, _HOST_PIECE_ITEMS):
-        nbytes = min(nb, 32 * (t0 + _HOST_PIECE_ITEMS)) - 32 * t0
-        _lib.check(launch(L, t0, nbytes, _lib.ptr(nib_h) + 16 * t0, _lib.ptr(base_h) + 2 * t0,
-                          st), name)
-        ev = torch.cuda.Event()
-        ev.record()
-        pieces.append((t0, nbytes, ev))
-    out = host.ctypes.data
-    for t0, nbytes, ev in pieces:
-        ev.synchronize()
-        _lib.check(L.pdm_unpack_packed_host(_lib.ptr(nib_h) + 16 * t0, _lib.ptr(base_h) + 2 * t0,
-                                            nbytes, out + 32 * t0), "pdm_unpack_packed_host")
+    pieces = max(1, min(16, (-(-nb // 32)) // _HOST_PIECE_ITEMS))
+    _lib.check(L.pdm_merge_packed_to_host(
+        _lib.ptr(nib), nib_pitch, _lib.ptr(base), base_pitch, nb, pdm_set.n, flags_ptr, sel_ptr,
+        k, _lib.ptr(nib_h), _lib.ptr(base_h), host.ctypes.data, pieces, _lib.stream_handle()),
+        "pdm_merge_packed_to_host")
 
 
 def update_from_tf(pdm_set: PdmSet, tf, out=None, flags=None) -> DistanceMap:
