@@ -130,7 +130,8 @@ def main():
     host = torch.empty(nb, dtype=torch.uint8, pin_memory=True)
     for k in (() if args.no_host else (1, 16, 32)):
         sel = np.ascontiguousarray(np.arange(k), dtype=np.int32)
-        modes = ("hbm+d2h", "zero-copy") + (("packed hbm+d2h", "packed zero-copy")
+        modes = ("hbm+d2h", "zero-copy") + (("packed hbm+d2h", "packed zero-copy",
+                                              "packed->packed zero-copy")
                                              if args.packed else ())
         for mode in modes:
             ts = []
@@ -140,7 +141,12 @@ def main():
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record()
                 dst = out if mode.endswith("hbm+d2h") else host
-                if mode.startswith("packed"):
+                if mode == "packed->packed zero-copy":  # D' itself packed (9/16 of the bytes)
+                    _lib.check(L.pdm_combine_packed_to_packed(
+                        _lib.ptr(nib), nib_pitch, _lib.ptr(base), base_pitch, nb, n,
+                        sel.ctypes.data, k, _lib.ptr(host), _lib.ptr(host) + chunks * 8, st),
+                        "pdm_combine_packed_to_packed")
+                elif mode.startswith("packed"):
                     _lib.check(L.pdm_combine_packed(_lib.ptr(nib), nib_pitch, _lib.ptr(base),
                                                     base_pitch, nb, n, sel.ctypes.data, k,
                                                     _lib.ptr(dst), st), "pdm_combine_packed")
@@ -154,8 +160,10 @@ def main():
                 if r >= 3:
                     ts.append(e0.elapsed_time(e1))
             ms = float(np.median(ts))
-            to_host[f"{mode} k={k}"] = {"ms": round(ms, 4), "PCIe GB/s": round(nb / ms / 1e6, 1)}
-            assert torch.equal(host.cuda(), pdms[:k, :nb].min(dim=0).values)
+            moved = chunks * 9 if mode == "packed->packed zero-copy" else nb
+            to_host[f"{mode} k={k}"] = {"ms": round(ms, 4), "PCIe GB/s": round(moved / ms / 1e6, 1)}
+            if mode != "packed->packed zero-copy":
+                assert torch.equal(host.cuda(), pdms[:k, :nb].min(dim=0).values)
     print(json.dumps({"blocks": nb, "n": n, "merge": res, "packed": packed, "to_host": to_host}))
 
 
