@@ -473,7 +473,7 @@ def combine(pdm_set: PdmSet, selection: PartitionSelection,
 
         return DistanceMap._deferred(grid.b, grid.bdims,
                                      lambda out: combine_flags_into(pdm_set, flags, out),
-                                     host_produce if pdm_set.packed() is not None else None)
+                                     host_produce if _host_packed_pays(pdm_set) else None)
     indices = selection.sorted
     if indices and max_maps_per_pass is not None and max_maps_per_pass < 1:
         raise ValueError(f"max_maps_per_pass must be >= 1, got {max_maps_per_pass}")
@@ -502,12 +502,19 @@ def combine(pdm_set: PdmSet, selection: PartitionSelection,
     def host_produce(host):
         _packed_to_host(pdm_set, host, None, sel.ctypes.data, int(sel.size))
 
-    use_host_packed = 0 < sel.size <= _MAX_PACKED_SEL and pdm_set.packed() is not None
+    use_host_packed = 0 < sel.size <= _MAX_PACKED_SEL and _host_packed_pays(pdm_set)
     return DistanceMap._deferred(grid.b, grid.bdims, produce,
                                  host_produce if use_host_packed else None)
 
 
 _HOST_PIECE_ITEMS = 1 << 17  # 32-block items per pipelined piece (4 pieces at config c)
+_HOST_PACKED_MIN_BLOCKS = 1 << 22  # below ~4 MB of D' PCIe time is small: raw zero-copy
+
+
+def _host_packed_pays(pdm_set: PdmSet) -> bool:
+    """Ship D' packed to the host only when the PCIe bytes it saves matter
+    (config a/b maps of 0.26-2 MB measured faster raw: no expansion pass)."""
+    return pdm_set.grid.num_blocks >= _HOST_PACKED_MIN_BLOCKS and pdm_set.packed() is not None
 
 
 def _packed_to_host(pdm_set: PdmSet, host: np.ndarray, flags_ptr, sel_ptr, k: int) -> None:
