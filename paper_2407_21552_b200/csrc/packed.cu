@@ -26,6 +26,7 @@
 #include <emmintrin.h>
 
 #include <cstdlib>
+#include <mutex>
 
 #include "pdm_common.cuh"
 
@@ -261,9 +262,11 @@ __global__ void __launch_bounds__(kPackedThreads, B >= 6 ? 4 : 5)
 
 template <class K>
 static int packed_grid(K kernel, int64_t map_bytes) {
+    static std::mutex mu;  // ctypes callers may come from several host threads
     static const void *keys[8] = {nullptr};
     static int vals[8] = {0};
     int per_sm = 0;
+    std::lock_guard<std::mutex> lock(mu);
     for (int i = 0; i < 8; ++i) {
         if (keys[i] == (const void *)kernel) {
             per_sm = vals[i];
@@ -492,9 +495,10 @@ extern "C" int pdm_unpack_packed_host(const uint8_t *nib, const uint8_t *base, i
 // flags != nullptr: device selection (PDL behind the select kernel), else the
 // host index list sel[0..k).  Pieces are whole 32-block items.
 namespace pdm {
+// Per host thread and device: concurrent callers must not share events.
 static cudaEvent_t piece_event(int i) {
     constexpr int kMaxPieces = 64;
-    static cudaEvent_t ev[8][kMaxPieces] = {};
+    thread_local cudaEvent_t ev[8][kMaxPieces] = {};
     int dev = 0;
     cudaGetDevice(&dev);
     dev = dev < 0 ? 0 : (dev > 7 ? 7 : dev);
