@@ -111,7 +111,9 @@ __global__ void __launch_bounds__(32 * kApronWarps)
         auto issue_plane = [&](int64_t px, int slot) {
             if (px <= xe) {
                 const T *plane = vox + px * ny * nz + y0 * nz;
-                for (int yy = 0; yy < nrows; ++yy) {
+#pragma unroll
+                for (int yy = 0; yy < kRows; ++yy) {  // unrolled, rows past nrows skipped
+                    if (yy >= nrows) break;
                     const T *row = plane + (int64_t)yy * nz;
                     if (active) cpa::copy16(&ring_main[(slot * kRows + yy) * 32 + lane], row + zl);
                     if (lane == 0 && has_left)
@@ -165,7 +167,9 @@ __global__ void __launch_bounds__(32 * kApronWarps)
             // 16-bit voxels: reduce the rows two voxels per instruction
             // (u16x2 min/max on the packed words), unpack once per plane.
             uint32_t wmn[4] = {kHi, kHi, kHi, kHi}, wmx[4] = {0u, 0u, 0u, 0u};
-            for (int yy = 0; yy < nrows; ++yy) {
+#pragma unroll
+            for (int yy = 0; yy < kRows; ++yy) {
+                if (yy >= nrows) break;
                 if (active) {
                     const uint4 q = ring_main[(slot * kRows + yy) * 32 + lane];
                     if (BITS == 16) {
