@@ -422,3 +422,33 @@ def test_packed_disabled_by_env_and_dropped(monkeypatch):
     assert packed_set._packed is None
     assert np.array_equal(pdm.combine(packed_set, sel).dist, pdm.combine(raw_set, sel).dist)
     assert packed_set.packed() is not None  # re-packed on demand
+
+
+@pytest.mark.parametrize("packed", [True, False])
+def test_merge_writes_stay_inside_the_map(monkeypatch, packed):
+    """Guard bytes after D' (map sizes not a multiple of 16 or 32) survive every
+    merge path: device flags, host indices, HBM and host destinations."""
+    if not packed:
+        monkeypatch.setenv("PDM_PACKED", "0")
+    rng = np.random.default_rng(51)
+    dims = (5, 7, 13)  # 455 blocks
+    vox = random_structured_volume(rng, dims, 8)
+    scheme = pdm.scheme_uniform(6, 8)
+    pset = pdm.build_pdm_set(pdm.Volume.from_array(vox), pdm.BlockGrid.for_dims(dims, 1), scheme)
+    assert (pset.packed() is not None) == packed
+    maps = oracle.build_pdm_set(vox, 1, scheme.bounds(), "range_apron")
+    torch = pdm.device.torch()
+    nb = pset.grid.num_blocks
+    big = torch.full((nb + 64,), 0xAB, dtype=torch.uint8, device="cuda")
+    for s in ([2], [1, 3, 6], [1, 2, 3, 4, 5, 6]):
+        lut = np.zeros((256, 4))
+        for i in s:
+            part = scheme.partitions[i - 1]
+            lut[part.rho_lo: part.rho_hi + 1, 3] = 0.5
+        out = big[:nb].view(pset.grid.bdims)
+        pdm.update_from_tf(pset, pdm.TransferFunction(lut=lut), out=out)
+        assert np.array_equal(out.cpu().numpy(), oracle.combine(maps, s)), s
+        assert int((big[nb:] != 0xAB).sum()) == 0, s
+        sel = pdm.PartitionSelection(selected=frozenset(s), n=6)
+        host = pdm.combine(pset, sel).dist
+        assert np.array_equal(host, oracle.combine(maps, s)), s
