@@ -109,13 +109,17 @@ int pdm_distance_transform_mask_packed(const uint32_t *mask, int32_t words, int3
                                        pdm_stream_t stream);
 
 /* pdm_combine over packed planes (k <= 240), and pdm_combine_flags over them
- * (n <= 4096, PDL behind pdm_select).  Output: plain uint8 D'. */
+ * (n <= 4096, PDL behind pdm_select).  Output: plain uint8 D'.  zero_count
+ * (device uint64, may be NULL): set to the number of D' blocks equal to 0 --
+ * DistanceMap.occupied_fraction (acceleration.py:77-79) fused into the merge. */
 int pdm_combine_packed(const uint8_t *nib, int64_t nib_pitch, const uint8_t *base,
                        int64_t base_pitch, int64_t map_bytes, int32_t n, const int32_t *sel,
-                       int32_t k, uint8_t *out, pdm_stream_t stream);
+                       int32_t k, uint8_t *out, unsigned long long *zero_count,
+                       pdm_stream_t stream);
 int pdm_combine_flags_packed(const uint8_t *nib, int64_t nib_pitch, const uint8_t *base,
                              int64_t base_pitch, int64_t map_bytes, int32_t n,
-                             const uint8_t *flags, uint8_t *out, pdm_stream_t stream);
+                             const uint8_t *flags, uint8_t *out, unsigned long long *zero_count,
+                             pdm_stream_t stream);
 
 /* The same two merges writing D' itself in the packed encoding (out_nib: 8 *
  * chunks bytes, out_base: chunks bytes, 16/2-byte aligned) -- 9/16 of the

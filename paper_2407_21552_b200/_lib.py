@@ -34,8 +34,8 @@ _SIGNATURES = {
     "pdm_pack_pdms": [_P, _I64, _I64, _I32, _P, _I64, _P, _I64, _P, _P],
     "pdm_distance_transform_mask_packed": [_P, _I32, _I32, _I64, _I64, _I64, _P, _I64, _P, _I64,
                                            _P, _I64, _P, _P],
-    "pdm_combine_packed": [_P, _I64, _P, _I64, _I64, _I32, _P, _I32, _P, _P],
-    "pdm_combine_flags_packed": [_P, _I64, _P, _I64, _I64, _I32, _P, _P, _P],
+    "pdm_combine_packed": [_P, _I64, _P, _I64, _I64, _I32, _P, _I32, _P, _P, _P],
+    "pdm_combine_flags_packed": [_P, _I64, _P, _I64, _I64, _I32, _P, _P, _P, _P],
     "pdm_combine_packed_to_packed": [_P, _I64, _P, _I64, _I64, _I32, _P, _I32, _P, _P, _P],
     "pdm_combine_flags_packed_to_packed": [_P, _I64, _P, _I64, _I64, _I32, _P, _P, _P, _P],
     "pdm_unpack_packed_host": [_P, _P, _I64, _P],

@@ -172,6 +172,9 @@ class DistanceMap(_BlockArray):
         if self._host is not None:
             d = self._host
             return float(np.count_nonzero(d == 0)) / d.size
+        zeros = getattr(self, "_zero_count", None)  # counted by the merge itself
+        if zeros is not None:
+            return int(zeros.item()) / float(np.prod(self.bdims))
         return count_value(self.device(), 0) / float(np.prod(self.bdims))
 
 
@@ -490,7 +493,8 @@ def combine(pdm_set: PdmSet, selection: PartitionSelection,
             nib, nib_pitch, base, base_pitch = packed
             _lib.check(L.pdm_combine_packed(_lib.ptr(nib), nib_pitch, _lib.ptr(base), base_pitch,
                                             grid.num_blocks, pdm_set.n, sel.ctypes.data,
-                                            int(sel.size), _lib.ptr(out), _lib.stream_handle()),
+                                            int(sel.size), _lib.ptr(out), None,
+                                            _lib.stream_handle()),
                        "pdm_combine_packed")
             return
         storage = pdm_set.storage if sel.size else None
@@ -542,9 +546,11 @@ def update_from_tf(pdm_set: PdmSet, tf, out=None, flags=None) -> DistanceMap:
     return combine_flags_into(pdm_set, flags, out)
 
 
-def combine_flags_into(pdm_set: PdmSet, flags, out=None) -> DistanceMap:
+def combine_flags_into(pdm_set: PdmSet, flags, out=None, count_zeros: bool = False) -> DistanceMap:
     """K7 with a device-resident selection (uint8 flags[n], e.g. from
-    select_partitions_device) writing into ``out`` (allocated if None)."""
+    select_partitions_device) writing into ``out`` (allocated if None).
+    count_zeros: the packed merge also counts D''s zero blocks, so the result's
+    occupied_fraction needs no second pass (the live session's report)."""
     L = _lib.lib()
     grid = pdm_set.grid
     if out is None:
@@ -552,11 +558,16 @@ def combine_flags_into(pdm_set: PdmSet, flags, out=None) -> DistanceMap:
     packed = pdm_set.packed() if out.is_cuda else None  # host out: see combine()
     if packed is not None:
         nib, nib_pitch, base, base_pitch = packed
+        zeros = device.empty((1,), np.int64) if count_zeros else None
         _lib.check(L.pdm_combine_flags_packed(_lib.ptr(nib), nib_pitch, _lib.ptr(base), base_pitch,
                                               grid.num_blocks, pdm_set.n, _lib.ptr(flags),
-                                              _lib.ptr(out), _lib.stream_handle()),
+                                              _lib.ptr(out),
+                                              _lib.ptr(zeros) if zeros is not None else None,
+                                              _lib.stream_handle()),
                    "pdm_combine_flags_packed")
-        return DistanceMap(b=grid.b, bdims=grid.bdims, dist=out)
+        dm = DistanceMap(b=grid.b, bdims=grid.bdims, dist=out)
+        dm._zero_count = zeros
+        return dm
     _lib.check(L.pdm_combine_flags(_lib.ptr(pdm_set.storage), pdm_set.plane_pitch,
                                    grid.num_blocks, pdm_set.n, _lib.ptr(flags), _lib.ptr(out),
                                    _lib.stream_handle()), "pdm_combine_flags")

@@ -185,13 +185,23 @@ __device__ __forceinline__ uint32_t ld_stream_u16(const void *p) {
 // kPackOut: write D' in the packed encoding (out = 16 nibble bytes per item,
 // out_base = 2 base bytes per item) -- 9/16 of the bytes, for D' headed to
 // the host over PCIe (unpacked there by pdm_unpack_packed_host).
-template <int B, bool kPackOut>  // B: selected planes per load batch
+// zeros != nullptr (D' bytes only): also count D''s zero blocks -- the
+// occupied fraction the live session reports (service/app.py:129,
+// acceleration.py:77-79) -- without a second pass over D'.
+__device__ __forceinline__ uint32_t zero_bytes(uint32_t w) {
+    const uint32_t t = ~(((w & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | w | 0x7F7F7F7Fu);
+    return (uint32_t)__popc(t);  // bit 7 of each byte set iff the byte is 0
+}
+
+template <int B, bool kPackOut, bool kCount = false>  // B: selected planes per load batch
 __device__ __forceinline__ void merge_packed(const uint8_t *__restrict__ nib, int64_t nib_pitch,
                                              const uint8_t *__restrict__ base,
                                              int64_t base_pitch, int64_t map_bytes,
                                              const int32_t *idx, int k,
                                              uint8_t *__restrict__ out,
-                                             uint8_t *__restrict__ out_base) {
+                                             uint8_t *__restrict__ out_base,
+                                             unsigned long long *zeros = nullptr) {
+    uint32_t nzero = 0;
     const int64_t items = ceil_div(map_bytes, 32);
     const int64_t T = (int64_t)gridDim.x * blockDim.x;
     for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < items; t += T) {
@@ -226,38 +236,51 @@ __device__ __forceinline__ void merge_packed(const uint8_t *__restrict__ nib, in
         if (t * 32 + 32 <= map_bytes) {
             st_stream_u4(dst, lo);
             st_stream_u4(dst + 16, hi);
+            if (kCount)
+                nzero += zero_bytes(lo.x) + zero_bytes(lo.y) + zero_bytes(lo.z) +
+                         zero_bytes(lo.w) + zero_bytes(hi.x) + zero_bytes(hi.y) +
+                         zero_bytes(hi.z) + zero_bytes(hi.w);
         } else {
             const uint32_t o[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
-            for (int i = 0; t * 32 + i < map_bytes; ++i) dst[i] = (uint8_t)(o[i >> 2] >> (8 * (i & 3)));
+            for (int i = 0; t * 32 + i < map_bytes; ++i) {
+                const uint8_t v = (uint8_t)(o[i >> 2] >> (8 * (i & 3)));
+                dst[i] = v;
+                if (kCount) nzero += v == 0;
+            }
         }
+    }
+    if (kCount) {  // every thread of the grid reaches it
+        const uint32_t w = __reduce_add_sync(0xFFFFFFFFu, nzero);
+        if ((threadIdx.x & 31) == 0 && w) atomicAdd(zeros, (unsigned long long)w);
     }
 }
 
-template <int B, bool kPackOut>
+template <int B, bool kPackOut, bool kCount>
 __global__ void __launch_bounds__(kPackedThreads, B >= 6 ? 4 : 5)
     combine_packed_kernel(const uint8_t *__restrict__ nib, int64_t nib_pitch,
                           const uint8_t *__restrict__ base, int64_t base_pitch, int64_t map_bytes,
                           const __grid_constant__ PackedSel sel, uint8_t *__restrict__ out,
-                          uint8_t *__restrict__ out_base) {
-    merge_packed<B, kPackOut>(nib, nib_pitch, base, base_pitch, map_bytes, sel.idx, sel.k, out,
-                              out_base);
+                          uint8_t *__restrict__ out_base, unsigned long long *zeros) {
+    merge_packed<B, kPackOut, kCount>(nib, nib_pitch, base, base_pitch, map_bytes, sel.idx, sel.k, out,
+                              out_base, zeros);
 }
 
 // Selection resident on the device (written by the select kernel ahead of it
 // in the stream, PDL): every CTA compacts the flags, then merges.
-template <int B, bool kPackOut>
+template <int B, bool kPackOut, bool kCount>
 __global__ void __launch_bounds__(kPackedThreads, B >= 6 ? 4 : 5)
     combine_packed_flags_kernel(const uint8_t *__restrict__ nib, int64_t nib_pitch,
                                 const uint8_t *__restrict__ base, int64_t base_pitch,
                                 int64_t map_bytes, int n, const uint8_t *__restrict__ flags,
-                                uint8_t *__restrict__ out, uint8_t *__restrict__ out_base) {
+                                uint8_t *__restrict__ out, uint8_t *__restrict__ out_base,
+                                unsigned long long *zeros) {
     __shared__ int32_t s_idx[kPackedMaxFlags];
     __shared__ int s_k;
     pdl_wait();
     compact_flags(flags, n, s_idx, &s_k);
     __syncthreads();
-    merge_packed<B, kPackOut>(nib, nib_pitch, base, base_pitch, map_bytes, s_idx, s_k, out,
-                              out_base);
+    merge_packed<B, kPackOut, kCount>(nib, nib_pitch, base, base_pitch, map_bytes, s_idx, s_k, out,
+                              out_base, zeros);
 }
 
 template <class K>
@@ -332,12 +355,15 @@ static int check_packed(const char *fn, const void *nib, int64_t nib_pitch, cons
 
 static int launch_packed(const uint8_t *nib, int64_t nib_pitch, const uint8_t *base,
                          int64_t base_pitch, int64_t map_bytes, const PackedSel &p,
-                         uint8_t *out, uint8_t *out_base, cudaStream_t s) {
-    auto kern = out_base ? combine_packed_kernel<kPackedBatch, true>
-                         : combine_packed_kernel<kPackedBatch, false>;
+                         uint8_t *out, uint8_t *out_base, cudaStream_t s,
+                         unsigned long long *zeros = nullptr) {
+    if (zeros) PDM_CUDA_TRY(cudaMemsetAsync(zeros, 0, sizeof(unsigned long long), s));
+    auto kern = out_base ? combine_packed_kernel<kPackedBatch, true, false>
+                : zeros  ? combine_packed_kernel<kPackedBatch, false, true>
+                         : combine_packed_kernel<kPackedBatch, false, false>;
     kern<<<packed_grid(kern, map_bytes), kPackedThreads, 0, s>>>(nib, nib_pitch, base,
                                                                   base_pitch, map_bytes, p, out,
-                                                                  out_base);
+                                                                  out_base, zeros);
     return cuda_status("combine_packed_kernel");
 }
 
@@ -345,9 +371,10 @@ static int launch_packed(const uint8_t *nib, int64_t nib_pitch, const uint8_t *b
 static int launch_packed_flags(const uint8_t *nib, int64_t nib_pitch, const uint8_t *base,
                                int64_t base_pitch, int64_t map_bytes, int n,
                                const uint8_t *flags, uint8_t *out, uint8_t *out_base,
-                               cudaStream_t s) {
-    auto kern = out_base ? combine_packed_flags_kernel<kPackedBatch, true>
-                         : combine_packed_flags_kernel<kPackedBatch, false>;
+                               cudaStream_t s, unsigned long long *zeros = nullptr) {
+    auto kern = out_base ? combine_packed_flags_kernel<kPackedBatch, true, false>
+                : zeros  ? combine_packed_flags_kernel<kPackedBatch, false, true>
+                         : combine_packed_flags_kernel<kPackedBatch, false, false>;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)packed_grid(kern, map_bytes));
     cfg.blockDim = dim3(kPackedThreads);
@@ -359,7 +386,7 @@ static int launch_packed_flags(const uint8_t *nib, int64_t nib_pitch, const uint
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     PDM_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, nib, nib_pitch, base, base_pitch, map_bytes, n,
-                                    flags, out, out_base));
+                                    flags, out, out_base, zeros));
     return cuda_status("combine_packed_flags_kernel");
 }
 
@@ -409,27 +436,31 @@ extern "C" int pdm_pack_pdms(const uint8_t *pdms, int64_t plane_pitch, int64_t m
 extern "C" int pdm_combine_packed(const uint8_t *nib, int64_t nib_pitch, const uint8_t *base,
                                   int64_t base_pitch, int64_t map_bytes, int32_t n,
                                   const int32_t *sel, int32_t k, uint8_t *out,
-                                  pdm_stream_t stream) {
+                                  unsigned long long *zero_count, pdm_stream_t stream) {
     const char *fn = "pdm_combine_packed";
     int st = check_packed(fn, nib, nib_pitch, base, base_pitch, map_bytes, n, out, nullptr, false);
     if (st) return st;
     PackedSel p;
     if ((st = packed_sel(fn, sel, k, n, p))) return st;
     return launch_packed(nib, nib_pitch, base, base_pitch, map_bytes, p, out, nullptr,
-                         as_stream(stream));
+                         as_stream(stream), zero_count);
 }
 
 extern "C" int pdm_combine_flags_packed(const uint8_t *nib, int64_t nib_pitch,
                                         const uint8_t *base, int64_t base_pitch,
                                         int64_t map_bytes, int32_t n, const uint8_t *flags,
-                                        uint8_t *out, pdm_stream_t stream) {
+                                        uint8_t *out, unsigned long long *zero_count,
+                                        pdm_stream_t stream) {
     const char *fn = "pdm_combine_flags_packed";
     int st = check_packed(fn, nib, nib_pitch, base, base_pitch, map_bytes, n, out, nullptr, false);
     if (st) return st;
     PDM_REQUIRE(flags && n <= kPackedMaxFlags, "%s: flags null or n=%d above %d", fn, n,
                 kPackedMaxFlags);
+    if (zero_count)  // (sits between the select kernel and the merge: no PDL overlap then)
+        PDM_CUDA_TRY(cudaMemsetAsync(zero_count, 0, sizeof(unsigned long long),
+                                     as_stream(stream)));
     return launch_packed_flags(nib, nib_pitch, base, base_pitch, map_bytes, n, flags, out,
-                               nullptr, as_stream(stream));
+                               nullptr, as_stream(stream), zero_count);
 }
 
 extern "C" int pdm_combine_packed_to_packed(const uint8_t *nib, int64_t nib_pitch,

@@ -5,8 +5,10 @@ Mirrors /root/reference/pkg/src/pdmrender/service/session.py:60-127
 combined map resident in HBM: ``set_tf`` selects and merges on the GPU
 (select_partitions_device + combine_flags_into, no host round trip), times
 both with CUDA events, and reports the combined map's occupied fraction (the
-service's ``dprime_nonzero_fraction``, service/app.py:129) from a device
-count, so an edit moves 8 bytes back to the host instead of the 16.8 MB map.
+service's ``dprime_nonzero_fraction``, service/app.py:129) from a zero count
+the merge kernel keeps while it writes D' (packed sets; a separate count
+kernel otherwise), so an edit moves 8 bytes back to the host instead of the
+16.8 MB map.
 The (tf, selection, dprime) triple is swapped under a lock like the
 reference; readers holding an older snapshot keep a valid map because every
 update writes a fresh buffer.
@@ -101,9 +103,9 @@ class PdmSessionStore:
         ev[0].record()
         flags = select_partitions_device(alpha_to_device(tf), scheme)
         ev[1].record()
-        dprime = combine_flags_into(pdm_set, flags)
+        dprime = combine_flags_into(pdm_set, flags, count_zeros=True)
         ev[2].record()
-        occupied = dprime.occupied_fraction  # device count; synchronises the stream
+        occupied = dprime.occupied_fraction  # zero count from the merge; synchronises
         wall_ms = (time.perf_counter() - t_wall) * 1e3
         return Session(volume=volume, grid=grid, scheme=scheme, pdm_set=pdm_set,
                        occupancy_mode=mode, tf=tf,

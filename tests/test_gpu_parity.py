@@ -452,3 +452,24 @@ def test_merge_writes_stay_inside_the_map(monkeypatch, packed):
         sel = pdm.PartitionSelection(selected=frozenset(s), n=6)
         host = pdm.combine(pset, sel).dist
         assert np.array_equal(host, oracle.combine(maps, s)), s
+
+
+def test_merge_fused_zero_count():
+    """combine_flags_into(count_zeros=True): the packed merge counts D''s zero
+    blocks itself; occupied_fraction equals the host count (map size not a
+    multiple of 32, selections from empty-ish to full)."""
+    rng = np.random.default_rng(61)
+    dims = (9, 11, 48)  # 4752 blocks
+    vox = random_structured_volume(rng, dims, 8)
+    scheme = pdm.scheme_uniform(8, 8)
+    pset = pdm.build_pdm_set(pdm.Volume.from_array(vox), pdm.BlockGrid.for_dims(dims, 1), scheme)
+    assert pset.packed() is not None
+    torch = pdm.device.torch()
+    for s in ([1], [3, 4], [2, 5, 7], list(range(1, 9))):
+        flags = torch.zeros(8, dtype=torch.uint8, device="cuda")
+        flags[[i - 1 for i in s]] = 1
+        dm = pdm.acceleration.combine_flags_into(pset, flags, count_zeros=True)
+        assert dm._zero_count is not None
+        want = np.minimum.reduce([pset.pdms[i - 1].dist for i in s])
+        assert dm.occupied_fraction == np.count_nonzero(want == 0) / want.size, s
+        assert np.array_equal(dm.dist, want), s

@@ -100,7 +100,7 @@ def main():
                 e0.record()
                 _lib.check(L.pdm_combine_packed(_lib.ptr(nib), nib_pitch, _lib.ptr(base),
                                                 base_pitch, nb, n, sel.ctypes.data, k,
-                                                _lib.ptr(out), st), "pdm_combine_packed")
+                                                _lib.ptr(out), None, st), "pdm_combine_packed")
                 e1.record()
                 torch.cuda.synchronize()
                 if r >= 3:
@@ -149,7 +149,7 @@ def main():
                 elif mode.startswith("packed"):
                     _lib.check(L.pdm_combine_packed(_lib.ptr(nib), nib_pitch, _lib.ptr(base),
                                                     base_pitch, nb, n, sel.ctypes.data, k,
-                                                    _lib.ptr(dst), st), "pdm_combine_packed")
+                                                    _lib.ptr(dst), None, st), "pdm_combine_packed")
                 else:
                     _lib.check(L.pdm_combine(_lib.ptr(pdms), pitch, nb, n, sel.ctypes.data, k,
                                              _lib.ptr(dst), st), "pdm_combine")
