@@ -798,11 +798,15 @@ static int tile_pass(int n, int64_t bx, int64_t by, int64_t bz, uint8_t *pdms, i
     const int sstride = swz ? (int)L : 4 * sw;
     const size_t per_warp = (AXIS == kAxisZ ? (size_t)32 * sstride : (size_t)32 * L) +
                             (kSweep ? SweepTable<(LMAX > 256 ? 2 : 1)>::kBytes : 0);
-    // Up to 4 warps / 64 KB per CTA; 512-long sweep lines (32 KB per warp)
-    // take one CTA of up to 7 warps per SM instead.
+    // Sweep tiles: as many warps per SM as shared memory holds -- 2 CTAs of up
+    // to 7 warps (<= 113 KB each) for lines <= 256 (14 warps instead of 12),
+    // one CTA of up to 7 warps for 512-long lines (32 KB per warp).  Other
+    // passes: up to 4 warps / 64 KB per CTA.
     const bool big = kSweep && LMAX > 256;
-    int wpc = (int)((big ? 227 * 1024 : 65536) / per_warp);
-    wpc = wpc < 1 ? 1 : (wpc > (big ? 8 : 4) ? (big ? 8 : 4) : wpc);
+    const size_t budget = big ? 227 * 1024 : (kSweep ? 113 * 1024 : 65536);
+    const int wmax = kSweep ? 7 : 4;
+    int wpc = (int)(budget / per_warp);
+    wpc = wpc < 1 ? 1 : (wpc > wmax ? wmax : wpc);
     const size_t smem = per_warp * wpc;
     auto kern = dt_tile_kernel<LMAX, AXIS, kDist1D, kSweep>;
     PDM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
