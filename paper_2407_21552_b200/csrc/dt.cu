@@ -32,6 +32,8 @@
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "pdm_common.cuh"
 
 namespace pdm {
@@ -661,65 +663,69 @@ __global__ void __launch_bounds__(128)
     }
 }
 
-// ---- x pass, wide tiles: 1-D distance of 4 lines per lane in 16-bit lanes -------
+// ---- x pass, wide tiles: 1-D distance of 2 lines per lane in 16-bit lanes -------
 // The 1-D distance has no lookup in its chain (run = nonzero ? run + 1 : 0),
-// so it is instruction bound; here each lane runs 4 adjacent z lines at once
-// as two u16x2 registers (even and odd bytes of a 32-bit word).  Runs are not
-// clamped while sweeping (they stay <= 255 + L <= 511, inside the 9-bit lane
-// mask) and are clamped with one VIMNMX.U16x2 on output.  Tile: [u][128 z]
-// bytes per warp, lane l owns z0 + 4l .. z0 + 4l + 3; lines <= 256.
+// so it is instruction bound; each lane runs 2 adjacent z lines at once in
+// one u16x2 register.  Runs are not clamped while sweeping (they stay <= 255
+// + L <= 511, inside the 9-bit lane mask) and are clamped with one
+// VIMNMX.U16x2 on output.  Lines <= 256.  (4 lines per lane on 128-z tiles
+// measured 0.49 vs 0.46 ms for expand + pass x at config c: half the
+// resident warps.)
 __device__ __forceinline__ uint32_t nonzero16(uint32_t x) {  // u16x2 lanes <= 255
     return (((x + 0x00FF00FFu) >> 8) & 0x00010001u) * 0x1FFu;  // 0x1FF where x != 0
 }
 
+// Tile: [u][64 z] bytes per warp (16 KB for L = 256), lane l owns z0 + 2l,
+// z0 + 2l + 1.  The forward sweep relies on its input being the expand
+// kernels' {0, 255} planes (mask = byte * 0x101); the backward sweep tests its
+// general input.
 __global__ void __launch_bounds__(256)
     dt_dist1d_wide_kernel(int n, int64_t bx, int64_t by, int64_t bz, uint8_t *__restrict__ pdms,
-                          int64_t pitch, int64_t tiles) {
+                           int64_t pitch, int64_t tiles) {
     extern __shared__ __align__(16) uint8_t s_wide[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, wpc = blockDim.x >> 5;
     const int L = (int)bx;
     const int64_t S = by * bz;
-    uint8_t *s = s_wide + (size_t)warp * 128 * L;
-    uint32_t *col = reinterpret_cast<uint32_t *>(s) + lane;  // word u at col[32 u]
-    const int64_t zq = ceil_div(bz, 128);
+    uint8_t *s = s_wide + (size_t)warp * 64 * L;
+    uint16_t *col = reinterpret_cast<uint16_t *>(s) + lane;  // element pair u at col[32 u]
+    const int64_t zq = ceil_div(bz, 64);
     for (int64_t t = (int64_t)blockIdx.x * wpc + warp; t < tiles; t += (int64_t)gridDim.x * wpc) {
-        const int64_t py = t / zq, z0 = (t % zq) * 128;
-        const int nz = (int)min((int64_t)128, bz - z0);  // multiple of 16 (bz % 16 == 0)
+        const int64_t py = t / zq, z0 = (t % zq) * 64;
+        const int nz = (int)min((int64_t)64, bz - z0);  // multiple of 16 (bz % 16 == 0)
         uint8_t *g = pdms + (py / by) * pitch + (py % by) * bz + z0;
-        for (int i = lane; i < L * 8; i += 32) {
-            const int u = i >> 3, c = i & 7;
-            if (16 * c < nz) cpa::copy16(s + u * 128 + 16 * c, g + (int64_t)u * S + 16 * c);
+        for (int i = lane; i < L * 4; i += 32) {
+            const int u = i >> 2, c = i & 3;
+            if (16 * c < nz) cpa::copy16(s + u * 64 + 16 * c, g + (int64_t)u * S + 16 * c);
         }
         cpa::commit();
         cpa::wait<0>();
         __syncwarp();
-        if (4 * lane < nz) {
-            uint32_t re = 0x00FF00FFu, ro = 0x00FF00FFu;  // "no occupied block yet" = 255
+        if (2 * lane < nz) {
+            uint32_t r = 0x00FF00FFu;  // "no occupied block yet" = 255
             uint32_t w = col[0];
             for (int u = 0; u < L; ++u) {
                 const uint32_t wn = u + 1 < L ? col[32 * (u + 1)] : 0u;
-                re = (re + 0x00010001u) & nonzero16(w & 0x00FF00FFu);
-                ro = (ro + 0x00010001u) & nonzero16((w >> 8) & 0x00FF00FFu);
-                col[32 * u] = __vminu2(re, 0x00FF00FFu) | (__vminu2(ro, 0x00FF00FFu) << 8);
+                const uint32_t x = __byte_perm(w, 0u, 0x4140);  // bytes -> u16x2 lanes
+                r = (r + 0x00010001u) & (x * 0x101u);          // {0, 255} -> {0, 0xFFFF}
+                col[32 * u] = (uint16_t)__byte_perm(__vminu2(r, 0x00FF00FFu), 0u, 0x0020);
                 w = wn;
             }
-            re = ro = 0x00FF00FFu;
+            r = 0x00FF00FFu;
             w = col[32 * (L - 1)];
             for (int u = L - 1; u >= 0; --u) {
                 const uint32_t wn = u > 0 ? col[32 * (u - 1)] : 0u;
-                const uint32_t fe = w & 0x00FF00FFu, fo = (w >> 8) & 0x00FF00FFu;
-                re = (re + 0x00010001u) & nonzero16(fe);
-                ro = (ro + 0x00010001u) & nonzero16(fo);
-                col[32 * u] = __vminu2(re, fe) | (__vminu2(ro, fo) << 8);
+                const uint32_t f = __byte_perm(w, 0u, 0x4140);
+                r = (r + 0x00010001u) & nonzero16(f);
+                col[32 * u] = (uint16_t)__byte_perm(__vminu2(r, f), 0u, 0x0020);
                 w = wn;
             }
         }
         __syncwarp();
-        for (int i = lane; i < L * 8; i += 32) {
-            const int u = i >> 3, c = i & 7;
+        for (int i = lane; i < L * 4; i += 32) {
+            const int u = i >> 2, c = i & 3;
             if (16 * c < nz)
                 *reinterpret_cast<uint4 *>(g + (int64_t)u * S + 16 * c) =
-                    *reinterpret_cast<const uint4 *>(s + u * 128 + 16 * c);
+                    *reinterpret_cast<const uint4 *>(s + u * 64 + 16 * c);
         }
         __syncwarp();
     }
@@ -826,26 +832,27 @@ static int tile_pass(int n, int64_t bx, int64_t by, int64_t bz, uint8_t *pdms, i
     return cuda_status("dt_tile_kernel");
 }
 
-// x pass (1-D distance along x) with 128-z tiles, 4 lines per lane.
+// x pass (1-D distance along x) on 64-z tiles, 2 lines per lane.
 static int wide_x_pass(int n, int64_t bx, int64_t by, int64_t bz, uint8_t *pdms, int64_t pitch,
                        cudaStream_t s) {
-    const size_t per_warp = (size_t)128 * bx;
-    int wpc = (int)((227 * 1024) / per_warp);
+    constexpr int zw = 64;
+    auto kern = dt_dist1d_wide_kernel;
+    const size_t per_warp = (size_t)zw * bx;
+    const size_t budget = 113 * 1024;  // 2 CTAs per SM
+    int wpc = (int)(budget / per_warp);
     wpc = wpc < 1 ? 1 : (wpc > 8 ? 8 : wpc);
     const size_t smem = per_warp * wpc;
-    PDM_CUDA_TRY(cudaFuncSetAttribute(dt_dist1d_wide_kernel,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    const int64_t tiles = (int64_t)n * by * ceil_div(bz, 128);
+    PDM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const int64_t tiles = (int64_t)n * by * ceil_div(bz, zw);
     int per_sm = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dt_dist1d_wide_kernel, 32 * wpc,
-                                                      smem) != cudaSuccess ||
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * wpc, smem) !=
+            cudaSuccess ||
         per_sm < 1)
         per_sm = 1;
     int64_t grid = ceil_div(tiles, wpc);
     const int64_t cap = (int64_t)sm_count() * per_sm;
     if (grid > cap) grid = cap;
-    dt_dist1d_wide_kernel<<<(unsigned)grid, 32 * wpc, smem, s>>>(n, bx, by, bz, pdms, pitch,
-                                                                  tiles);
+    kern<<<(unsigned)grid, 32 * wpc, smem, s>>>(n, bx, by, bz, pdms, pitch, tiles);
     return cuda_status("dt_dist1d_wide_kernel");
 }
 
