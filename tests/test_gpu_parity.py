@@ -308,7 +308,8 @@ def test_device_born_volume_matches_oracle_synth():
     ((3, 5, 16), 1, 8, 4, True),        # 240 blocks: last 32-block item is partial
     ((9, 7, 40), 1, 8, 6, None),        # rows of 40: straddling chunks may span > 15
 ])
-def test_packed_merge_matches_oracle(dims, b, bits, n, packs):
+def test_packed_merge_matches_oracle(monkeypatch, dims, b, bits, n, packs):
+    monkeypatch.setenv("PDM_PACKED", "1")
     rng = np.random.default_rng(sum(dims) * n)
     vox = random_structured_volume(rng, dims, bits)
     vol = pdm.Volume.from_array(vox)
@@ -336,7 +337,8 @@ def test_packed_merge_matches_oracle(dims, b, bits, n, packs):
     (12, 8, 512),     # bz = 128: packing fused into the z pass
     (8, 4, 1024),     # bz = 256: fused
 ])
-def test_packed_planes_decode_to_the_raw_planes(dims):
+def test_packed_planes_decode_to_the_raw_planes(monkeypatch, dims):
+    monkeypatch.setenv("PDM_PACKED", "1")
     """Unpack the device's packed planes on the host: base + nibbles == raw."""
     rng = np.random.default_rng(12)
     vox = random_structured_volume(rng, dims, 16)
@@ -378,6 +380,7 @@ def test_packed_dprime_to_host(monkeypatch, min_blocks):
     not a multiple of 16 (rows of 13 blocks still pack: straddling chunks
     stay <= 12 apart)."""
     monkeypatch.setattr(pdm.acceleration, "_HOST_PACKED_MIN_BLOCKS", min_blocks)
+    monkeypatch.setenv("PDM_PACKED", "1")
     rng = np.random.default_rng(31)
     for dims, b in (((64, 40, 64), 4), ((3, 5, 13), 1)):
         vox = random_structured_volume(rng, dims, 8)
@@ -403,6 +406,7 @@ def test_packed_dprime_to_host(monkeypatch, min_blocks):
 def test_packed_disabled_by_env_and_dropped(monkeypatch):
     """PDM_PACKED=0 keeps sets raw; drop_packed() forgets a packed copy; both
     merge paths agree."""
+    monkeypatch.setenv("PDM_PACKED", "1")
     rng = np.random.default_rng(41)
     dims = (32, 24, 64)
     vox = random_structured_volume(rng, dims, 16)
@@ -428,8 +432,7 @@ def test_packed_disabled_by_env_and_dropped(monkeypatch):
 def test_merge_writes_stay_inside_the_map(monkeypatch, packed):
     """Guard bytes after D' (map sizes not a multiple of 16 or 32) survive every
     merge path: device flags, host indices, HBM and host destinations."""
-    if not packed:
-        monkeypatch.setenv("PDM_PACKED", "0")
+    monkeypatch.setenv("PDM_PACKED", "1" if packed else "0")
     rng = np.random.default_rng(51)
     dims = (5, 7, 13)  # 455 blocks
     vox = random_structured_volume(rng, dims, 8)
@@ -454,10 +457,11 @@ def test_merge_writes_stay_inside_the_map(monkeypatch, packed):
         assert np.array_equal(host, oracle.combine(maps, s)), s
 
 
-def test_merge_fused_zero_count():
+def test_merge_fused_zero_count(monkeypatch):
     """combine_flags_into(count_zeros=True): the packed merge counts D''s zero
     blocks itself; occupied_fraction equals the host count (map size not a
     multiple of 32, selections from empty-ish to full)."""
+    monkeypatch.setenv("PDM_PACKED", "1")
     rng = np.random.default_rng(61)
     dims = (9, 11, 48)  # 4752 blocks
     vox = random_structured_volume(rng, dims, 8)

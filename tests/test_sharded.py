@@ -109,9 +109,10 @@ def test_fold_restatement_matches_full_transform():
 
 
 @pytest.mark.gpu
-def test_sharded_build_nccl_world1():
+def test_sharded_build_nccl_world1(monkeypatch):
     """The NCCL plumbing of build_pdm_set_sharded (slab table and edge
     all_gathers on CUDA tensors) on a one-rank process group."""
+    monkeypatch.setenv("PDM_PACKED", "1")
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(_free_port())
     torch.cuda.set_device(0)
