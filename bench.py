@@ -225,6 +225,9 @@ def run_b200(args, rank, world, local_rank):
     total_ms = sum(step_ms)
     merge_bytes = sum((k + 1) * B for k in ks)  # SURVEY.md §8(d) algorithmic bytes
     packed = pset.packed()
+    # D' form the e2e step ships to the host (acceleration._packed_to_host)
+    host_packed = pdm.acceleration._host_packed_pays(pset)
+    delta = host_packed and pset._delta_ok and pdm.acceleration._host_delta_enabled()
     if packed is not None:  # bytes the packed merge actually moves: nibbles + bases + D'
         per_plane = -(-B // 32) * 2 * 9
         moved_bytes = sum(k * per_plane + B for k in ks)
@@ -308,9 +311,10 @@ def run_b200(args, rank, world, local_rank):
         "e2e": {"value": round(voxels_rank * world * steps / (e2e_ms * 1e-3) / 1e9, 2),
                 "unit": "Gvoxel/s", "ms_per_step": round(e2e_ms / steps, 4),
                 "h2d_bytes_per_step": span * 8,
-                "d2h_bytes_per_step": (-(-B // 32) * 2 * 9) if packed is not None else B,
-                "d2h_format": ("packed D' (base + 4-bit offsets per 16 blocks), expanded on "
-                               "the host" if packed is not None else "uint8 D'"),
+                "d2h_bytes_per_step": (-(-B // 32) * (10 if delta else 18)) if host_packed else B,
+                "d2h_format": (("packed D' (base + 2-bit z-deltas per 16 blocks)" if delta else
+                                "packed D' (base + 4-bit offsets per 16 blocks)") +
+                               ", expanded on the host" if host_packed else "uint8 D'"),
                 "api": "select_partitions(tf, scheme) + combine(pdm_set, sel) + .dist",
                 "breakdown_ms": {"select_partitions": e2e_parts_ms[0], "combine_launch": e2e_parts_ms[1], "dist_merge_d2h": e2e_parts_ms[2]}},
         "gpu_launches": 2 * steps,

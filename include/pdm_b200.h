@@ -138,17 +138,28 @@ int pdm_combine_flags_packed_to_packed(const uint8_t *nib, int64_t nib_pitch,
 int pdm_unpack_packed_host(const uint8_t *nib, const uint8_t *base, int64_t map_bytes,
                            uint8_t *out);
 
-/* combine(...).dist in one call: the packed-output merge in `pieces` launches
- * (an event after each) storing straight into pinned host staging
- * stage_nib / stage_base (sized like one packed plane), and the host
- * expansion of piece i into the host array `out` (map_bytes) while later
- * pieces cross PCIe.  Selection: device flags[n] when flags != NULL (PDL
- * behind pdm_select), else host sel[0..k).  Returns once `out` is complete. */
+/* Host expansion of D' in the delta form: per 16-block chunk c, base[c] is
+ * block 16c and code word c (little-endian u32 at codes + 4c) holds, for
+ * blocks 1..15, (step from the previous block + 1) in 2 bits each.  Valid
+ * for maps that change by at most 1 per block inside each chunk.  Host
+ * function (AVX-512 VBMI when present, else SSE2; OpenMP). */
+int pdm_unpack_delta_host(const uint8_t *codes, const uint8_t *base, int64_t map_bytes,
+                          uint8_t *out);
+
+/* combine(...).dist in one call: the merge writes D' in a compact form in
+ * `pieces` launches (an event after each) straight into pinned host staging
+ * (stage_nib: 8 (format 1, nibbles) or 4 (format 2, deltas) bytes per chunk;
+ * stage_base: 1 byte per chunk), and the host expands piece i into `out`
+ * (map_bytes) while later pieces cross PCIe.  Format 2 requires every
+ * selected map to be 1-Lipschitz along z within chunks (true for sets built
+ * by the distance transform with bz % 16 == 0).  Selection: device flags[n]
+ * when flags != NULL (PDL behind pdm_select), else host sel[0..k).  Returns
+ * once `out` is complete. */
 int pdm_merge_packed_to_host(const uint8_t *nib, int64_t nib_pitch, const uint8_t *base,
                              int64_t base_pitch, int64_t map_bytes, int32_t n,
                              const uint8_t *flags, const int32_t *sel, int32_t k,
                              uint8_t *stage_nib, uint8_t *stage_base, uint8_t *out,
-                             int32_t pieces, pdm_stream_t stream);
+                             int32_t pieces, int32_t format, pdm_stream_t stream);
 
 /* ---- block reduction / occupancy (K1-K5) --------------------------------- */
 

@@ -205,6 +205,10 @@ class PdmSet:
         self.plane_pitch = device.plane_pitch(grid.num_blocks)
         self._storage = storage
         self._packed = None  # None: not packed yet; False: does not pack; else planes
+        # every map is a distance field whose z rows hold whole 16-block chunks
+        # (built here by the distance transform with bz % 16 == 0): D' can then
+        # go to the host in the 5/16-size delta form
+        self._delta_ok = False
         if storage is not None:
             nb = grid.num_blocks
             self.pdms = tuple(
@@ -430,6 +434,7 @@ def build_pdm_set(volume: Volume, grid: BlockGrid, scheme: PartitionScheme,
     pitch = device.plane_pitch(grid.num_blocks)
     storage = device.empty((scheme.n, pitch), np.uint8)
     pset = PdmSet(grid=grid, scheme=scheme, occupancy_mode=mode, storage=storage)
+    pset._delta_ok = grid.bdims[2] % 16 == 0
     if _packed_enabled():
         # the packed merge planes are part of the precompute; the z pass
         # writes them itself when it can (pdm_distance_transform_mask_packed)
@@ -530,10 +535,16 @@ def _packed_to_host(pdm_set: PdmSet, host: np.ndarray, flags_ptr, sel_ptr, k: in
     nib_h, base_h = pdm_set._host_stage()
     nb = pdm_set.grid.num_blocks
     pieces = max(1, min(16, (-(-nb // 32)) // _HOST_PIECE_ITEMS))
+    fmt = 2 if pdm_set._delta_ok and _host_delta_enabled() else 1
     _lib.check(L.pdm_merge_packed_to_host(
         _lib.ptr(nib), nib_pitch, _lib.ptr(base), base_pitch, nb, pdm_set.n, flags_ptr, sel_ptr,
-        k, _lib.ptr(nib_h), _lib.ptr(base_h), host.ctypes.data, pieces, _lib.stream_handle()),
-        "pdm_merge_packed_to_host")
+        k, _lib.ptr(nib_h), _lib.ptr(base_h), host.ctypes.data, pieces, fmt,
+        _lib.stream_handle()), "pdm_merge_packed_to_host")
+
+
+def _host_delta_enabled() -> bool:
+    # PDM_HOST_DELTA=0: nibble form for D' to the host (A/B measurements)
+    return os.environ.get("PDM_HOST_DELTA", "1") != "0"
 
 
 def update_from_tf(pdm_set: PdmSet, tf, out=None, flags=None) -> DistanceMap:

@@ -23,7 +23,6 @@
 // and 4 PRMTs per 8 blocks restore byte order once at the end.
 
 #include <cuda_fp16.h>
-#include <emmintrin.h>
 
 #include <cstdlib>
 #include <mutex>
@@ -159,6 +158,37 @@ struct PackedAcc {
         nibs = make_uint4(w[0], w[1], w[2], w[3]);
         bases = mn[0] | (mn[1] << 8);
     }
+    // Delta form of the merged 32 blocks (2 chunks), for D' headed to the
+    // host: per chunk its first value as the base and, for blocks 1..15, the
+    // step from the previous block + 1 (in {0, 1, 2}, 2 bits each; a z row of
+    // a distance field changes by at most 1 per block) -- 5 bytes per 16
+    // blocks.  Only valid for maps that are 1-Lipschitz along z within every
+    // chunk (the caller checks); steps are masked so nothing else is touched.
+    __device__ __forceinline__ void encode_delta(uint2 &codes, uint32_t &bases) const {
+        uint4 lo, hi;
+        result(lo, hi);
+        const uint32_t wl[4] = {lo.x, lo.y, lo.z, lo.w}, wh[4] = {hi.x, hi.y, hi.z, hi.w};
+        uint32_t cw[2];
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+            const uint32_t *w = c == 0 ? wl : wh;
+            uint32_t code = 0;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const uint32_t prev = __funnelshift_l(j == 0 ? 0u : w[j - 1], w[j], 8);
+                const uint32_t de = __byte_perm(w[j], 0u, 0x4240) + 0x00010001u -
+                                    __byte_perm(prev, 0u, 0x4240);
+                const uint32_t dd = __byte_perm(w[j], 0u, 0x4341) + 0x00010001u -
+                                    __byte_perm(prev, 0u, 0x4341);
+                const uint32_t g = (de & 3u) | ((dd & 3u) << 2) | (((de >> 16) & 3u) << 4) |
+                                   (((dd >> 16) & 3u) << 6);
+                code |= g << (8 * j);
+            }
+            cw[c] = code >> 2;  // block 0 of the chunk is the base, no step
+        }
+        codes = make_uint2(cw[0], cw[1]);
+        bases = (wl[0] & 0xFFu) | ((wh[0] & 0xFFu) << 8);
+    }
     // 32 blocks in byte order.
     __device__ __forceinline__ void result(uint4 &lo, uint4 &hi) const {
         uint32_t o[8];
@@ -182,9 +212,11 @@ __device__ __forceinline__ uint32_t ld_stream_u16(const void *p) {
 
 // Thread item t covers blocks [32t, 32t + 32).  Items past the last full one
 // (map_bytes % 32) write byte by byte.
-// kPackOut: write D' in the packed encoding (out = 16 nibble bytes per item,
-// out_base = 2 base bytes per item) -- 9/16 of the bytes, for D' headed to
-// the host over PCIe (unpacked there by pdm_unpack_packed_host).
+// kOut: 0 = D' bytes; 1 = D' in the packed encoding (out = 16 nibble bytes
+// per item, out_base = 2 base bytes per item, 9/16 of the bytes); 2 = D' in
+// the delta form (out = 8 code bytes per item, out_base = 2 bases, 5/16 of
+// the bytes).  1 and 2 are for D' headed to the host over PCIe, expanded
+// there by pdm_unpack_packed_host / pdm_unpack_delta_host.
 // zeros != nullptr (D' bytes only): also count D''s zero blocks -- the
 // occupied fraction the live session reports (service/app.py:129,
 // acceleration.py:77-79) -- without a second pass over D'.
@@ -193,7 +225,7 @@ __device__ __forceinline__ uint32_t zero_bytes(uint32_t w) {
     return (uint32_t)__popc(t);  // bit 7 of each byte set iff the byte is 0
 }
 
-template <int B, bool kPackOut, bool kCount = false>  // B: selected planes per load batch
+template <int B, int kOut, bool kCount = false>  // B: selected planes per load batch
 __device__ __forceinline__ void merge_packed(const uint8_t *__restrict__ nib, int64_t nib_pitch,
                                              const uint8_t *__restrict__ base,
                                              int64_t base_pitch, int64_t map_bytes,
@@ -222,11 +254,21 @@ __device__ __forceinline__ void merge_packed(const uint8_t *__restrict__ nib, in
             for (int j = 0; j < B; ++j)
                 if (m + j < k) acc.fold(q[j], b[j]);
         }
-        if (kPackOut) {
+        if (kOut == 1) {
             uint4 nibs;
             uint32_t bases;
             acc.encode(nibs, bases);
             st_stream_u4(out + t * 16, nibs);
+            *reinterpret_cast<uint16_t *>(out_base + t * 2) = (uint16_t)bases;
+            continue;
+        }
+        if (kOut == 2) {
+            uint2 codes;
+            uint32_t bases;
+            acc.encode_delta(codes, bases);
+            asm volatile("st.global.cs.v2.u32 [%0], {%1,%2};" ::"l"(out + t * 8), "r"(codes.x),
+                         "r"(codes.y)
+                         : "memory");
             *reinterpret_cast<uint16_t *>(out_base + t * 2) = (uint16_t)bases;
             continue;
         }
@@ -255,19 +297,19 @@ __device__ __forceinline__ void merge_packed(const uint8_t *__restrict__ nib, in
     }
 }
 
-template <int B, bool kPackOut, bool kCount>
+template <int B, int kOut, bool kCount>
 __global__ void __launch_bounds__(kPackedThreads, B >= 6 ? 4 : 5)
     combine_packed_kernel(const uint8_t *__restrict__ nib, int64_t nib_pitch,
                           const uint8_t *__restrict__ base, int64_t base_pitch, int64_t map_bytes,
                           const __grid_constant__ PackedSel sel, uint8_t *__restrict__ out,
                           uint8_t *__restrict__ out_base, unsigned long long *zeros) {
-    merge_packed<B, kPackOut, kCount>(nib, nib_pitch, base, base_pitch, map_bytes, sel.idx, sel.k, out,
+    merge_packed<B, kOut, kCount>(nib, nib_pitch, base, base_pitch, map_bytes, sel.idx, sel.k, out,
                               out_base, zeros);
 }
 
 // Selection resident on the device (written by the select kernel ahead of it
 // in the stream, PDL): every CTA compacts the flags, then merges.
-template <int B, bool kPackOut, bool kCount>
+template <int B, int kOut, bool kCount>
 __global__ void __launch_bounds__(kPackedThreads, B >= 6 ? 4 : 5)
     combine_packed_flags_kernel(const uint8_t *__restrict__ nib, int64_t nib_pitch,
                                 const uint8_t *__restrict__ base, int64_t base_pitch,
@@ -279,7 +321,7 @@ __global__ void __launch_bounds__(kPackedThreads, B >= 6 ? 4 : 5)
     pdl_wait();
     compact_flags(flags, n, s_idx, &s_k);
     __syncthreads();
-    merge_packed<B, kPackOut, kCount>(nib, nib_pitch, base, base_pitch, map_bytes, s_idx, s_k, out,
+    merge_packed<B, kOut, kCount>(nib, nib_pitch, base, base_pitch, map_bytes, s_idx, s_k, out,
                               out_base, zeros);
 }
 
@@ -357,11 +399,13 @@ static int check_packed(const char *fn, const void *nib, int64_t nib_pitch, cons
 static int launch_packed(const uint8_t *nib, int64_t nib_pitch, const uint8_t *base,
                          int64_t base_pitch, int64_t map_bytes, const PackedSel &p,
                          uint8_t *out, uint8_t *out_base, cudaStream_t s,
-                         unsigned long long *zeros = nullptr) {
+                         unsigned long long *zeros = nullptr, int out_mode = -1) {
     if (zeros) PDM_CUDA_TRY(cudaMemsetAsync(zeros, 0, sizeof(unsigned long long), s));
-    auto kern = out_base ? combine_packed_kernel<kPackedBatch, true, false>
-                : zeros  ? combine_packed_kernel<kPackedBatch, false, true>
-                         : combine_packed_kernel<kPackedBatch, false, false>;
+    if (out_mode < 0) out_mode = out_base ? 1 : 0;
+    auto kern = out_mode == 2 ? combine_packed_kernel<kPackedBatch, 2, false>
+                : out_mode == 1 ? combine_packed_kernel<kPackedBatch, 1, false>
+                : zeros   ? combine_packed_kernel<kPackedBatch, 0, true>
+                          : combine_packed_kernel<kPackedBatch, 0, false>;
     kern<<<packed_grid(kern, map_bytes), kPackedThreads, 0, s>>>(nib, nib_pitch, base,
                                                                   base_pitch, map_bytes, p, out,
                                                                   out_base, zeros);
@@ -372,10 +416,13 @@ static int launch_packed(const uint8_t *nib, int64_t nib_pitch, const uint8_t *b
 static int launch_packed_flags(const uint8_t *nib, int64_t nib_pitch, const uint8_t *base,
                                int64_t base_pitch, int64_t map_bytes, int n,
                                const uint8_t *flags, uint8_t *out, uint8_t *out_base,
-                               cudaStream_t s, unsigned long long *zeros = nullptr) {
-    auto kern = out_base ? combine_packed_flags_kernel<kPackedBatch, true, false>
-                : zeros  ? combine_packed_flags_kernel<kPackedBatch, false, true>
-                         : combine_packed_flags_kernel<kPackedBatch, false, false>;
+                               cudaStream_t s, unsigned long long *zeros = nullptr,
+                               int out_mode = -1) {
+    if (out_mode < 0) out_mode = out_base ? 1 : 0;
+    auto kern = out_mode == 2 ? combine_packed_flags_kernel<kPackedBatch, 2, false>
+                : out_mode == 1 ? combine_packed_flags_kernel<kPackedBatch, 1, false>
+                : zeros   ? combine_packed_flags_kernel<kPackedBatch, 0, true>
+                          : combine_packed_flags_kernel<kPackedBatch, 0, false>;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)packed_grid(kern, map_bytes));
     cfg.blockDim = dim3(kPackedThreads);
@@ -494,30 +541,6 @@ extern "C" int pdm_combine_flags_packed_to_packed(const uint8_t *nib, int64_t ni
                                out_base, as_stream(stream));
 }
 
-// Host side: expand a packed map (pdm_combine_*_to_packed output, in host
-// memory) into map_bytes plain bytes.  SSE2 per chunk (unpack low/high
-// nibbles, interleave, add the base), OpenMP across chunks: 0.12 ms for a
-// 16.8 MB map on 16 cores (non-temporal stores measured slower: 0.14 ms).
-extern "C" int pdm_unpack_packed_host(const uint8_t *nib, const uint8_t *base, int64_t map_bytes,
-                                      uint8_t *out) {
-    PDM_REQUIRE(nib && base && out && map_bytes >= 1, "pdm_unpack_packed_host: bad arguments");
-    const int64_t full = map_bytes / 16;
-    const __m128i lo4 = _mm_set1_epi8(0x0F);
-#pragma omp parallel for schedule(static)
-    for (int64_t c = 0; c < full; ++c) {
-        const __m128i q = _mm_loadl_epi64(reinterpret_cast<const __m128i *>(nib + 8 * c));
-        const __m128i even = _mm_and_si128(q, lo4);
-        const __m128i odd = _mm_and_si128(_mm_srli_epi16(q, 4), lo4);
-        __m128i v = _mm_unpacklo_epi8(even, odd);
-        v = _mm_add_epi8(v, _mm_set1_epi8((char)base[c]));
-        _mm_storeu_si128(reinterpret_cast<__m128i *>(out + 16 * c), v);
-    }
-    for (int64_t i = full * 16; i < map_bytes; ++i) {
-        const int64_t c = i / 16, j = i % 16;
-        out[i] = (uint8_t)(base[c] + ((nib[8 * c + j / 2] >> (4 * (j & 1))) & 15));
-    }
-    return PDM_OK;
-}
 
 // ---- D' straight to a host array: pieces, events, host expansion ------------
 // One call does what combine(...).dist needs: the merge writes D' packed into
@@ -544,8 +567,10 @@ extern "C" int pdm_merge_packed_to_host(const uint8_t *nib, int64_t nib_pitch, c
                                         int64_t base_pitch, int64_t map_bytes, int32_t n,
                                         const uint8_t *flags, const int32_t *sel, int32_t k,
                                         uint8_t *stage_nib, uint8_t *stage_base, uint8_t *out,
-                                        int32_t pieces, pdm_stream_t stream) {
+                                        int32_t pieces, int32_t format, pdm_stream_t stream) {
     const char *fn = "pdm_merge_packed_to_host";
+    PDM_REQUIRE(format == 1 || format == 2, "%s: format must be 1 (nibble) or 2 (delta)", fn);
+    const int64_t per_item = format == 1 ? 16 : 8;  // staged code bytes per 32 blocks
     int st = check_packed(fn, nib, nib_pitch, base, base_pitch, map_bytes, n, stage_nib,
                           stage_base, true);
     if (st) return st;
@@ -563,10 +588,11 @@ extern "C" int pdm_merge_packed_to_host(const uint8_t *nib, int64_t nib_pitch, c
     for (int64_t t0 = 0; t0 < items; t0 += per, ++used) {
         const int64_t nbytes = min(map_bytes, 32 * (t0 + per)) - 32 * t0;
         st = flags ? launch_packed_flags(nib + 16 * t0, nib_pitch, base + 2 * t0, base_pitch,
-                                         nbytes, n, flags, stage_nib + 16 * t0,
-                                         stage_base + 2 * t0, s)
+                                         nbytes, n, flags, stage_nib + per_item * t0,
+                                         stage_base + 2 * t0, s, nullptr, format)
                    : launch_packed(nib + 16 * t0, nib_pitch, base + 2 * t0, base_pitch, nbytes, p,
-                                   stage_nib + 16 * t0, stage_base + 2 * t0, s);
+                                   stage_nib + per_item * t0, stage_base + 2 * t0, s, nullptr,
+                                   format);
         if (st) return st;
         PDM_CUDA_TRY(cudaEventRecord(piece_event(used), s));
     }
@@ -574,8 +600,10 @@ extern "C" int pdm_merge_packed_to_host(const uint8_t *nib, int64_t nib_pitch, c
         const int64_t t0 = i * per;
         const int64_t nbytes = min(map_bytes, 32 * (t0 + per)) - 32 * t0;
         PDM_CUDA_TRY(cudaEventSynchronize(piece_event(i)));
-        st = pdm_unpack_packed_host(stage_nib + 16 * t0, stage_base + 2 * t0, nbytes,
-                                    out + 32 * t0);
+        st = format == 1 ? pdm_unpack_packed_host(stage_nib + 16 * t0, stage_base + 2 * t0,
+                                                  nbytes, out + 32 * t0)
+                         : pdm_unpack_delta_host(stage_nib + 8 * t0, stage_base + 2 * t0, nbytes,
+                                                 out + 32 * t0);
         if (st) return st;
     }
     return PDM_OK;

@@ -192,6 +192,7 @@ def build_pdm_set_sharded(volume: Volume, b: int, scheme: PartitionScheme,
     slab_phase_fold(storage, pitch, n, bdims, edges_all, world, rank, starts, ops)
     pset = PdmSet(grid=grid, scheme=scheme, occupancy_mode=mode, storage=storage)
     pset.slab = (int(starts[rank]), int(starts[rank + 1]), int(starts[-1]))
+    pset._delta_ok = bdims[2] % 16 == 0  # distance-transform output (see build_pdm_set)
     if storage.is_cuda:
         pset.packed()  # pack the final planes now, not in the first merge
     return pset

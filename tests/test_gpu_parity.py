@@ -371,8 +371,9 @@ def test_packed_skipped_for_maps_that_are_not_distance_fields():
     assert np.array_equal(got, np.minimum.reduce([maps[i - 1] for i in s]))
 
 
+@pytest.mark.parametrize("delta", ["1", "0"])
 @pytest.mark.parametrize("min_blocks", [0, 1 << 30])
-def test_packed_dprime_to_host(monkeypatch, min_blocks):
+def test_packed_dprime_to_host(monkeypatch, min_blocks, delta):
     """combine(...).dist over a packable set ships D' packed over PCIe and
     expands it on the host (min_blocks=0 forces that path for these small
     maps; 1 << 30 forces the raw zero-copy path): identical to the oracle
@@ -381,6 +382,7 @@ def test_packed_dprime_to_host(monkeypatch, min_blocks):
     stay <= 12 apart)."""
     monkeypatch.setattr(pdm.acceleration, "_HOST_PACKED_MIN_BLOCKS", min_blocks)
     monkeypatch.setenv("PDM_PACKED", "1")
+    monkeypatch.setenv("PDM_HOST_DELTA", delta)  # delta form where bz % 16 == 0
     rng = np.random.default_rng(31)
     for dims, b in (((64, 40, 64), 4), ((3, 5, 13), 1)):
         vox = random_structured_volume(rng, dims, 8)

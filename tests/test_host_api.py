@@ -280,3 +280,27 @@ def test_host_buffer_recycles_only_unreferenced_buffers():
     d = device.host_buffer((3, 7))
     assert d.base is base_a or d.base is not None  # some pooled buffer is reused
     assert d.shape == (3, 7) and d.dtype == np.uint8
+
+
+@pytest.mark.parametrize("avx512", [True, False])
+def test_unpack_delta_host_matches_numpy_decode(monkeypatch, avx512):
+    """pdm_unpack_delta_host (host code, no GPU): base = block 16c, blocks
+    1..15 of a chunk from 2-bit (step + 1) codes; 1-Lipschitz random walks
+    that touch 0 and 255, map sizes with partial chunk groups; the AVX-512
+    path (when the CPU has it) and the SSE2 path."""
+    if not avx512:
+        monkeypatch.setenv("PDM_NO_AVX512", "1")
+    L = _lib.load_library()
+    rng = np.random.default_rng(22)
+    for nb in (1, 15, 16, 17, 64, 65, 240, 1000, 4096 + 7, 1 << 16):
+        chunks = 2 * (-(-nb // 32))
+        steps = rng.integers(-1, 2, (chunks, 16))
+        start = rng.choice([0, 1, 128, 254, 255], chunks)
+        vals = np.clip(start[:, None] + np.cumsum(steps, 1) - steps[:, :1], 0, 255)
+        d = np.diff(vals, axis=1) + 1                       # blocks 1..15: 0, 1, 2
+        codes = (d << (2 * np.arange(15))).sum(1).astype(np.uint32)
+        base = vals[:, 0].astype(np.uint8)
+        out = np.zeros(nb, np.uint8)
+        assert L.pdm_unpack_delta_host(codes.ctypes.data, base.ctypes.data, nb,
+                                       out.ctypes.data) == _lib.PDM_OK
+        assert np.array_equal(out, vals.reshape(-1)[:nb].astype(np.uint8)), nb
