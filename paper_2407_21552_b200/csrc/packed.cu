@@ -225,14 +225,34 @@ __device__ __forceinline__ uint32_t zero_bytes(uint32_t w) {
     return (uint32_t)__popc(t);  // bit 7 of each byte set iff the byte is 0
 }
 
-template <int B, int kOut, bool kCount = false>  // B: selected planes per load batch
-__device__ __forceinline__ void merge_packed(const uint8_t *__restrict__ nib, int64_t nib_pitch,
-                                             const uint8_t *__restrict__ base,
-                                             int64_t base_pitch, int64_t map_bytes,
-                                             const int32_t *idx, int k,
+// Where the selected planes live.  TablePlanes: per-plane base pointers built
+// once per CTA in shared memory (one LDS.64 + a 64-bit add per load);
+// IdxPlanes: plane index x pitch per load (n above the table size).
+struct TablePlanes {
+    const uint8_t *const *nib;
+    const uint8_t *const *base;
+    __device__ __forceinline__ const uint8_t *nib_at(int m) const { return nib[m]; }
+    __device__ __forceinline__ const uint8_t *base_at(int m) const { return base[m]; }
+};
+struct IdxPlanes {
+    const uint8_t *nib;
+    int64_t nib_pitch;
+    const uint8_t *base;
+    int64_t base_pitch;
+    const int32_t *idx;
+    __device__ __forceinline__ const uint8_t *nib_at(int m) const {
+        return nib + (int64_t)idx[m] * nib_pitch;
+    }
+    __device__ __forceinline__ const uint8_t *base_at(int m) const {
+        return base + (int64_t)idx[m] * base_pitch;
+    }
+};
+
+template <int B, int kOut, bool kCount, class P>  // B: selected planes per load batch
+__device__ __forceinline__ void merge_packed(const P planes, int k, int64_t map_bytes,
                                              uint8_t *__restrict__ out,
                                              uint8_t *__restrict__ out_base,
-                                             unsigned long long *zeros = nullptr) {
+                                             unsigned long long *zeros) {
     uint32_t nzero = 0;
     const int64_t items = ceil_div(map_bytes, 32);
     const int64_t T = (int64_t)gridDim.x * blockDim.x;
@@ -245,9 +265,8 @@ __device__ __forceinline__ void merge_packed(const uint8_t *__restrict__ nib, in
 #pragma unroll
             for (int j = 0; j < B; ++j) {
                 if (m + j < k) {
-                    const int64_t p = idx[m + j];
-                    q[j] = ld_stream_u4(nib + p * nib_pitch + t * 16);
-                    b[j] = ld_stream_u16(base + p * base_pitch + t * 2);
+                    q[j] = ld_stream_u4(planes.nib_at(m + j) + t * 16);
+                    b[j] = ld_stream_u16(planes.base_at(m + j) + t * 2);
                 }
             }
 #pragma unroll
@@ -297,42 +316,80 @@ __device__ __forceinline__ void merge_packed(const uint8_t *__restrict__ nib, in
     }
 }
 
-template <int B, int kOut, bool kCount>
-__global__ void __launch_bounds__(kPackedThreads, B >= 6 ? 4 : 5)
+// Planes per load batch and CTAs per SM: with the pointer table, 6 planes per
+// batch at 3 CTAs (bench step, 3 interleaved runs each: 46.3 us vs 47.8 for
+// 8 planes / 3 CTAs and 48.2 for 4 planes / 4 CTAs); the index path keeps 4
+// planes at 5 CTAs.
+#ifndef PDM_PACKED_BATCH  // (overridable for A/B builds)
+#define PDM_PACKED_BATCH 6
+#define PDM_PACKED_CTAS 3
+#endif
+constexpr int kPackedBatch = PDM_PACKED_BATCH, kPackedCtas = PDM_PACKED_CTAS;
+constexpr int kPackedBatchIdx = 4, kPackedCtasIdx = 5;
+constexpr int kPackedTable = 256;  // n up to this uses TablePlanes
+
+__device__ __forceinline__ void fill_table(const uint8_t *nib, int64_t nib_pitch,
+                                           const uint8_t *base, int64_t base_pitch,
+                                           const int32_t *idx, int k, const uint8_t **s_nib,
+                                           const uint8_t **s_base) {
+    for (int i = threadIdx.x; i < k; i += blockDim.x) {
+        s_nib[i] = nib + (int64_t)idx[i] * nib_pitch;
+        s_base[i] = base + (int64_t)idx[i] * base_pitch;
+    }
+}
+
+template <int kOut, bool kCount>
+__global__ void __launch_bounds__(kPackedThreads, kPackedCtas)
     combine_packed_kernel(const uint8_t *__restrict__ nib, int64_t nib_pitch,
                           const uint8_t *__restrict__ base, int64_t base_pitch, int64_t map_bytes,
                           const __grid_constant__ PackedSel sel, uint8_t *__restrict__ out,
                           uint8_t *__restrict__ out_base, unsigned long long *zeros) {
-    merge_packed<B, kOut, kCount>(nib, nib_pitch, base, base_pitch, map_bytes, sel.idx, sel.k, out,
-                              out_base, zeros);
+    __shared__ const uint8_t *s_nib[kPackedMaxSel];
+    __shared__ const uint8_t *s_base[kPackedMaxSel];
+    fill_table(nib, nib_pitch, base, base_pitch, sel.idx, sel.k, s_nib, s_base);
+    __syncthreads();
+    merge_packed<kPackedBatch, kOut, kCount>(TablePlanes{s_nib, s_base}, sel.k, map_bytes, out,
+                                             out_base, zeros);
 }
 
 // Selection resident on the device (written by the select kernel ahead of it
 // in the stream, PDL): every CTA compacts the flags, then merges.
-template <int B, int kOut, bool kCount>
-__global__ void __launch_bounds__(kPackedThreads, B >= 6 ? 4 : 5)
+template <int kOut, bool kCount, bool kTable>
+__global__ void __launch_bounds__(kPackedThreads, kTable ? kPackedCtas : kPackedCtasIdx)
     combine_packed_flags_kernel(const uint8_t *__restrict__ nib, int64_t nib_pitch,
                                 const uint8_t *__restrict__ base, int64_t base_pitch,
                                 int64_t map_bytes, int n, const uint8_t *__restrict__ flags,
                                 uint8_t *__restrict__ out, uint8_t *__restrict__ out_base,
                                 unsigned long long *zeros) {
-    __shared__ int32_t s_idx[kPackedMaxFlags];
+    constexpr int kIdx = kTable ? kPackedTable : kPackedMaxFlags;
+    __shared__ int32_t s_idx[kIdx];
+    __shared__ const uint8_t *s_nib[kTable ? kPackedTable : 1];
+    __shared__ const uint8_t *s_base[kTable ? kPackedTable : 1];
     __shared__ int s_k;
     pdl_wait();
     compact_flags(flags, n, s_idx, &s_k);
     __syncthreads();
-    merge_packed<B, kOut, kCount>(nib, nib_pitch, base, base_pitch, map_bytes, s_idx, s_k, out,
-                              out_base, zeros);
+    if constexpr (kTable) {
+        fill_table(nib, nib_pitch, base, base_pitch, s_idx, s_k, s_nib, s_base);
+        __syncthreads();
+        merge_packed<kPackedBatch, kOut, kCount>(TablePlanes{s_nib, s_base}, s_k, map_bytes, out,
+                                                 out_base, zeros);
+    } else {
+        merge_packed<kPackedBatchIdx, kOut, kCount>(
+            IdxPlanes{nib, nib_pitch, base, base_pitch, s_idx}, s_k, map_bytes, out, out_base,
+            zeros);
+    }
 }
 
 template <class K>
 static int packed_grid(K kernel, int64_t map_bytes) {
     static std::mutex mu;  // ctypes callers may come from several host threads
-    static const void *keys[8] = {nullptr};
-    static int vals[8] = {0};
+    constexpr int kSlots = 32;  // >= the number of merge kernel instantiations
+    static const void *keys[kSlots] = {nullptr};
+    static int vals[kSlots] = {0};
     int per_sm = 0;
     std::lock_guard<std::mutex> lock(mu);
-    for (int i = 0; i < 8; ++i) {
+    for (int i = 0; i < kSlots; ++i) {
         if (keys[i] == (const void *)kernel) {
             per_sm = vals[i];
             break;
@@ -357,9 +414,11 @@ static int packed_grid(K kernel, int64_t map_bytes) {
     return grid < 1 ? 1 : (int)grid;
 }
 
-// Planes per load batch: 4 (48 registers, 5 CTAs per SM).  The merge is
-// bound by bytes in flight per SM (Little's law at ~3 us loaded HBM latency):
-// 4 planes x 18 B x 1280 threads ~ 92 KB/SM moves ~3.9 TB/s of packed bytes.
+// The fold is the co-bound: a load-only pass over the same planes runs at
+// 6.1 TB/s (49 us at k=32) and the fold alone (no nibble loads) at ~45 us, so
+// the merge (~70 us at k=32) is limited by how well the two overlap.  The
+// per-plane pointer table took 12 instructions of 64-bit address math per
+// plane out of the loop (83 -> 70 us at k=32; tools/exp/merge_variants.cu).
 // Measured and rejected: batches of 6 and 8 (63-64+ registers, 3-4 CTAs;
 // k=32: 82.9 / 95.8 us vs 81.9 us); one 16-block chunk per thread (8-register
 // accumulator, 8-byte loads, 8 or 12 planes per batch: 87 us); a ring that
@@ -372,9 +431,11 @@ static int packed_grid(K kernel, int64_t map_bytes) {
 // 512 B base bulk copies, consumers folding from shared memory) took 129 us
 // at k=32 under ncu vs 83 us -- the bulk-copy path is slower than LDG here,
 // as it was for the raw merge; an L2 prefetch of the next batch's planes
-// before each batch's loads measured 92 us at k=32.
-constexpr int kPackedBatch = 4;
-
+// before each batch's loads measured 92 us at k=32.  In the standalone study
+// (tools/exp/merge_variants.cu): a TMA ring with 16 consumer warps per SM
+// reaches 67.4 vs 70 us (consumers then issue-bound); software pipelining
+// of register batches 72.6 us; an all-fp16 fold (scaled lanes, HADD2 base
+// add, one shift per word) 68.6-77 us; cp.async per-warp rings 76-84 us.
 static bool packed_layout_ok(const void *nib, int64_t nib_pitch, const void *base,
                              int64_t base_pitch, const void *out) {
     return nib_pitch % 16 == 0 && base_pitch % 2 == 0 && (uintptr_t)nib % 16 == 0 &&
@@ -402,10 +463,10 @@ static int launch_packed(const uint8_t *nib, int64_t nib_pitch, const uint8_t *b
                          unsigned long long *zeros = nullptr, int out_mode = -1) {
     if (zeros) PDM_CUDA_TRY(cudaMemsetAsync(zeros, 0, sizeof(unsigned long long), s));
     if (out_mode < 0) out_mode = out_base ? 1 : 0;
-    auto kern = out_mode == 2 ? combine_packed_kernel<kPackedBatch, 2, false>
-                : out_mode == 1 ? combine_packed_kernel<kPackedBatch, 1, false>
-                : zeros   ? combine_packed_kernel<kPackedBatch, 0, true>
-                          : combine_packed_kernel<kPackedBatch, 0, false>;
+    auto kern = out_mode == 2 ? combine_packed_kernel<2, false>
+                : out_mode == 1 ? combine_packed_kernel<1, false>
+                : zeros   ? combine_packed_kernel<0, true>
+                          : combine_packed_kernel<0, false>;
     kern<<<packed_grid(kern, map_bytes), kPackedThreads, 0, s>>>(nib, nib_pitch, base,
                                                                   base_pitch, map_bytes, p, out,
                                                                   out_base, zeros);
@@ -419,10 +480,15 @@ static int launch_packed_flags(const uint8_t *nib, int64_t nib_pitch, const uint
                                cudaStream_t s, unsigned long long *zeros = nullptr,
                                int out_mode = -1) {
     if (out_mode < 0) out_mode = out_base ? 1 : 0;
-    auto kern = out_mode == 2 ? combine_packed_flags_kernel<kPackedBatch, 2, false>
-                : out_mode == 1 ? combine_packed_flags_kernel<kPackedBatch, 1, false>
-                : zeros   ? combine_packed_flags_kernel<kPackedBatch, 0, true>
-                          : combine_packed_flags_kernel<kPackedBatch, 0, false>;
+    const bool table = n <= kPackedTable;
+    auto kern = out_mode == 2 ? (table ? combine_packed_flags_kernel<2, false, true>
+                                       : combine_packed_flags_kernel<2, false, false>)
+                : out_mode == 1 ? (table ? combine_packed_flags_kernel<1, false, true>
+                                         : combine_packed_flags_kernel<1, false, false>)
+                : zeros ? (table ? combine_packed_flags_kernel<0, true, true>
+                                 : combine_packed_flags_kernel<0, true, false>)
+                        : (table ? combine_packed_flags_kernel<0, false, true>
+                                 : combine_packed_flags_kernel<0, false, false>);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)packed_grid(kern, map_bytes));
     cfg.blockDim = dim3(kPackedThreads);

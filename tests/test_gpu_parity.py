@@ -332,6 +332,52 @@ def test_packed_merge_matches_oracle(monkeypatch, dims, b, bits, n, packs):
         assert np.array_equal(dev.device().cpu().numpy(), oracle.combine(maps, s)), (k, s)
 
 
+@pytest.mark.parametrize("n,map_bytes", [
+    (200, 4000),   # flags kernel: per-CTA plane pointer table (n <= 256)
+    (300, 2600),   # flags kernel: index x pitch path (n > 256)
+])
+def test_packed_abi_many_planes(n, map_bytes):
+    """pdm_pack_pdms + pdm_combine_packed / pdm_combine_flags_packed straight
+    through the C ABI on 1-Lipschitz random-walk planes, against numpy."""
+    import torch
+
+    from paper_2407_21552_b200 import _lib
+
+    L = _lib.lib()
+    rng = np.random.default_rng(n)
+    steps = rng.integers(-1, 2, size=(n, map_bytes))
+    maps = np.clip(rng.integers(0, 256, size=(n, 1)) + np.cumsum(steps, axis=1), 0, 255)
+    maps = maps.astype(np.uint8)
+    pitch = -(-map_bytes // 256) * 256
+    planes = torch.zeros((n, pitch), dtype=torch.uint8, device="cuda")
+    planes[:, :map_bytes] = torch.from_numpy(maps).cuda()
+    chunks = int(L.pdm_packed_chunks(map_bytes))
+    nib_pitch, base_pitch = -(-chunks * 8 // 256) * 256, -(-chunks // 256) * 256
+    nib = torch.empty((n, nib_pitch), dtype=torch.uint8, device="cuda")
+    base = torch.empty((n, base_pitch), dtype=torch.uint8, device="cuda")
+    bad = torch.empty(1, dtype=torch.int32, device="cuda")
+    st = _lib.stream_handle()
+    _lib.check(L.pdm_pack_pdms(_lib.ptr(planes), pitch, map_bytes, n, _lib.ptr(nib), nib_pitch,
+                               _lib.ptr(base), base_pitch, _lib.ptr(bad), st), "pack")
+    assert int(bad.cpu()[0]) == 0
+    out = torch.empty(map_bytes, dtype=torch.uint8, device="cuda")
+    for k in (1, 7, min(n, 240), n):
+        sel = np.sort(rng.choice(n, size=k, replace=False)).astype(np.int32)
+        want = maps[sel].min(axis=0)
+        flags = torch.zeros(n, dtype=torch.uint8, device="cuda")
+        flags[torch.from_numpy(sel).long().cuda()] = 1
+        _lib.check(L.pdm_combine_flags_packed(_lib.ptr(nib), nib_pitch, _lib.ptr(base),
+                                              base_pitch, map_bytes, n, _lib.ptr(flags),
+                                              _lib.ptr(out), None, st), "flags")
+        assert np.array_equal(out.cpu().numpy(), want), k
+        if k <= 240:  # host index list (kernel parameter) path
+            out.fill_(7)
+            _lib.check(L.pdm_combine_packed(_lib.ptr(nib), nib_pitch, _lib.ptr(base), base_pitch,
+                                            map_bytes, n, sel.ctypes.data, k, _lib.ptr(out),
+                                            None, st), "sel")
+            assert np.array_equal(out.cpu().numpy(), want), k
+
+
 @pytest.mark.parametrize("dims", [
     (48, 32, 64),     # bz = 16: separate packing pass
     (12, 8, 512),     # bz = 128: packing fused into the z pass
