@@ -50,6 +50,45 @@ def peaks():
     return 6650.0, "fallback"
 
 
+HOST_FORMATS = {
+    0: "uint8 D'",
+    1: "packed D' (base + 4-bit offsets per 16 blocks), expanded on the host",
+    2: "packed D' (base + 2-bit z-deltas per 16 blocks), expanded on the host",
+    3: "sparse packed D' (per 16 blocks: nothing if all zero, the base if flat, else base "
+       "+ 2-bit z-deltas; 16 B of chunk bitmaps per 64 chunks), expanded on the host",
+}
+
+
+def d2h_bytes_per_step(pset, fmt: int, alphas, out) -> int:
+    """Mean bytes the e2e step's D' moves over PCIe (untimed recount): fixed
+    for formats 0-2; for the sparse form, 16 bitmap bytes per 64 chunks plus
+    a base per non-zero chunk and a 4-byte code per non-flat chunk, counted
+    from each step's D' (recomputed on the device)."""
+    import torch
+
+    import paper_2407_21552_b200 as pdm
+
+    B = pset.grid.num_blocks
+    items = -(-B // 32)
+    if fmt == 0:
+        return B
+    if fmt in (1, 2):
+        return items * (18 if fmt == 1 else 10)
+    total = 0
+    for a in alphas:
+        pdm.update_from_tf(pset, torch.as_tensor(a, device=out.device), out=out)
+        flat = out.reshape(-1)
+        pad = (-flat.numel()) % 16
+        if pad:
+            flat = torch.cat([flat, flat[-1:].expand(pad)])
+        ch = flat.view(-1, 16)
+        mn, mx = ch.amin(1), ch.amax(1)
+        is_flat = mn == mx
+        nonzero = ~(is_flat & (mn == 0))
+        total += 16 * -(-items // 32) + int(nonzero.sum()) + 4 * int((~is_flat).sum())
+    return round(total / len(alphas))
+
+
 def tf_sequence(n: int, span: int, steps: int, seed: int):
     """Aligned TFs (support = union of k whole partitions), k = 1..n cycled."""
     from paper_2407_21552_b200 import scheme_uniform
@@ -227,7 +266,7 @@ def run_b200(args, rank, world, local_rank):
     packed = pset.packed()
     # D' form the e2e step ships to the host (acceleration._packed_to_host)
     host_packed = pdm.acceleration._host_packed_pays(pset)
-    delta = host_packed and pset._delta_ok and pdm.acceleration._host_delta_enabled()
+    host_fmt = pdm.acceleration._host_format(pset) if host_packed else 0
     if packed is not None:  # bytes the packed merge actually moves: nibbles + bases + D'
         per_plane = -(-B // 32) * 2 * 9
         moved_bytes = sum(k * per_plane + B for k in ks)
@@ -265,6 +304,7 @@ def run_b200(args, rank, world, local_rank):
     assert host.shape == grid.bdims
     e2e_parts_ms = (parts / steps * 1e3).round(4).tolist()
     barrier()
+    d2h_bytes = d2h_bytes_per_step(pset, host_fmt, [a for _, a in seq[warm:warm + steps]], out)
 
     # ---- max over ranks ----------------------------------------------------------------
     vals = torch.tensor([total_ms, e2e_s * 1e3, sum(merge_ms)], dtype=torch.float64, device=dev)
@@ -311,10 +351,8 @@ def run_b200(args, rank, world, local_rank):
         "e2e": {"value": round(voxels_rank * world * steps / (e2e_ms * 1e-3) / 1e9, 2),
                 "unit": "Gvoxel/s", "ms_per_step": round(e2e_ms / steps, 4),
                 "h2d_bytes_per_step": span * 8,
-                "d2h_bytes_per_step": (-(-B // 32) * (10 if delta else 18)) if host_packed else B,
-                "d2h_format": (("packed D' (base + 2-bit z-deltas per 16 blocks)" if delta else
-                                "packed D' (base + 4-bit offsets per 16 blocks)") +
-                               ", expanded on the host" if host_packed else "uint8 D'"),
+                "d2h_bytes_per_step": d2h_bytes,
+                "d2h_format": HOST_FORMATS[host_fmt],
                 "api": "select_partitions(tf, scheme) + combine(pdm_set, sel) + .dist",
                 "breakdown_ms": {"select_partitions": e2e_parts_ms[0], "combine_launch": e2e_parts_ms[1], "dist_merge_d2h": e2e_parts_ms[2]}},
         "gpu_launches": 2 * steps,

@@ -146,13 +146,23 @@ int pdm_unpack_packed_host(const uint8_t *nib, const uint8_t *base, int64_t map_
 int pdm_unpack_delta_host(const uint8_t *codes, const uint8_t *base, int64_t map_bytes,
                           uint8_t *out);
 
+/* Host expansion of D' in the sparse delta form (format 3): per 32 items (64
+ * chunks) one 336-byte region -- u32 nz[2], u32 dd[2] (bit l of [p]: chunk
+ * 2l+p is not all-zero / is not flat), the bases of the non-zero chunks, then
+ * from the next 4-byte boundary the delta code words (as in
+ * pdm_unpack_delta_host) of the non-flat chunks, both compacted in chunk
+ * order.  Host function. */
+int pdm_unpack_sparse_host(const uint8_t *regions, int64_t map_bytes, uint8_t *out);
+
 /* combine(...).dist in one call: the merge writes D' in a compact form in
  * `pieces` launches (an event after each) straight into pinned host staging
  * (stage_nib: 8 (format 1, nibbles) or 4 (format 2, deltas) bytes per chunk;
- * stage_base: 1 byte per chunk), and the host expands piece i into `out`
- * (map_bytes) while later pieces cross PCIe.  Format 2 requires every
- * selected map to be 1-Lipschitz along z within chunks (true for sets built
- * by the distance transform with bz % 16 == 0).  Selection: device flags[n]
+ * stage_base: 1 byte per chunk; format 3, sparse deltas: stage_nib holds
+ * ceil(items / 32) regions of 336 bytes, stage_base is unused), and the host
+ * expands piece i into `out` (map_bytes) while later pieces cross PCIe.
+ * Formats 2 and 3 require every selected map to be 1-Lipschitz along z
+ * within chunks (true for sets built by the distance transform with
+ * bz % 16 == 0).  Selection: device flags[n]
  * when flags != NULL (PDL behind pdm_select), else host sel[0..k).  Returns
  * once `out` is complete. */
 int pdm_merge_packed_to_host(const uint8_t *nib, int64_t nib_pitch, const uint8_t *base,

@@ -42,6 +42,7 @@ _SIGNATURES = {
     "pdm_merge_packed_to_host": [_P, _I64, _P, _I64, _I64, _I32, _P, _P, _I32, _P, _P, _P, _I32,
                                  _I32, _P],
     "pdm_unpack_delta_host": [_P, _P, _I64, _P],
+    "pdm_unpack_sparse_host": [_P, _I64, _P],
     "pdm_block_min_max": [_P, _INT, _I64, _I64, _I64, _I32, _P, _P, _P],
     "pdm_partition_mask_voxel": [_P, _INT, _I64, _I64, _I64, _I32, _P, _I32, _P, _I32, _P],
     "pdm_partition_mask_range_apron": [_P, _INT, _I64, _I64, _I64, _I32, _P, _I32, _P, _I32, _P],

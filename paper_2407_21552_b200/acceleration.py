@@ -294,7 +294,8 @@ class PdmSet:
         if stage is None:
             t = device.torch()
             chunks = int(_lib.lib().pdm_packed_chunks(self.grid.num_blocks))
-            stage = (t.empty(chunks * 8, dtype=t.uint8, pin_memory=True),
+            regions = -(-chunks // 64) * 336  # format 3: one 336-byte region per 64 chunks
+            stage = (t.empty(max(chunks * 8, regions), dtype=t.uint8, pin_memory=True),
                      t.empty(chunks, dtype=t.uint8, pin_memory=True))
             self._stage = stage
         return stage
@@ -535,16 +536,22 @@ def _packed_to_host(pdm_set: PdmSet, host: np.ndarray, flags_ptr, sel_ptr, k: in
     nib_h, base_h = pdm_set._host_stage()
     nb = pdm_set.grid.num_blocks
     pieces = max(1, min(16, (-(-nb // 32)) // _HOST_PIECE_ITEMS))
-    fmt = 2 if pdm_set._delta_ok and _host_delta_enabled() else 1
+    fmt = _host_format(pdm_set)
     _lib.check(L.pdm_merge_packed_to_host(
         _lib.ptr(nib), nib_pitch, _lib.ptr(base), base_pitch, nb, pdm_set.n, flags_ptr, sel_ptr,
         k, _lib.ptr(nib_h), _lib.ptr(base_h), host.ctypes.data, pieces, fmt,
         _lib.stream_handle()), "pdm_merge_packed_to_host")
 
 
-def _host_delta_enabled() -> bool:
-    # PDM_HOST_DELTA=0: nibble form for D' to the host (A/B measurements)
-    return os.environ.get("PDM_HOST_DELTA", "1") != "0"
+def _host_format(pdm_set: PdmSet) -> int:
+    """Form of D' on the PCIe link (pdm_merge_packed_to_host `format`): 3 =
+    sparse deltas (default), 2 = deltas, 1 = nibbles.  The delta forms need
+    chunks that never straddle a z row (bz % 16 == 0).  PDM_HOST_FORMAT
+    picks a lower one for A/B measurements."""
+    want = int(os.environ.get("PDM_HOST_FORMAT", "3"))
+    if want not in (1, 2, 3):
+        raise ValueError(f"PDM_HOST_FORMAT must be 1, 2 or 3, got {want}")
+    return want if pdm_set._delta_ok else 1
 
 
 def update_from_tf(pdm_set: PdmSet, tf, out=None, flags=None) -> DistanceMap:

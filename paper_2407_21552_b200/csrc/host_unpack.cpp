@@ -135,3 +135,128 @@ extern "C" int pdm_unpack_delta_host(const uint8_t *codes, const uint8_t *base, 
     return PDM_OK;
 }
 
+
+// Host side: expand the sparse delta form (format 3, packed.cu store_sparse).
+// Region w (kRegion bytes) covers chunks 64w .. 64w+63.  AVX-512 VBMI2 path:
+// VPEXPANDB spreads the compacted bases over the 64 chunks (0 for all-zero
+// chunks), VPEXPANDD the code words (the flat code elsewhere), then the
+// 4-chunks-per-vector delta expansion writes the region's 1 KB contiguously;
+// no per-chunk branches.  Scalar-per-chunk SSE path otherwise.
+namespace {
+constexpr int64_t kRegion = 336;
+constexpr uint32_t kFlatCode = 0x15555555u;
+
+struct RegionHead {
+    uint64_t nz, dd;
+    const uint8_t *bases, *codes;
+    explicit RegionHead(const uint8_t *r) {
+        memcpy(&nz, r, 8);
+        memcpy(&dd, r + 8, 8);
+        bases = r + 16;
+        codes = r + 16 + ((__builtin_popcountll(nz) + 3) & ~3);
+    }
+};
+
+static void sparse_region_sse(const uint8_t *r, int64_t chunks, uint8_t *out, int64_t tail) {
+    const RegionHead h(r);
+    int bi = 0, ci = 0;
+    for (int64_t c = 0; c < chunks; ++c) {
+        __m128i v = _mm_setzero_si128();
+        if ((h.nz >> c) & 1u) {
+            const uint8_t b = h.bases[bi++];
+            if ((h.dd >> c) & 1u) {
+                uint32_t code;
+                memcpy(&code, h.codes + 4 * ci++, 4);
+                v = delta_chunk_sse(code, b);
+            } else {
+                v = _mm_set1_epi8((char)b);
+            }
+        }
+        if (c + 1 < chunks || tail == 16) {
+            _mm_storeu_si128(reinterpret_cast<__m128i *>(out + 16 * c), v);
+        } else {
+            alignas(16) uint8_t tmp[16];
+            _mm_store_si128(reinterpret_cast<__m128i *>(tmp), v);
+            memcpy(out + 16 * c, tmp, (size_t)tail);
+        }
+    }
+}
+
+__attribute__((target("avx2,avx512f,avx512bw,avx512vl,avx512vbmi,avx512vbmi2"))) static void
+sparse_region_vbmi2(const uint8_t *r, uint8_t *out) {
+    const RegionHead h(r);
+    if (h.nz == 0) {  // all-zero region (occupied space)
+        const __m512i z = _mm512_setzero_si512();
+        for (int i = 0; i < 16; ++i) _mm512_storeu_si512(reinterpret_cast<void *>(out + 64 * i), z);
+        return;
+    }
+    alignas(64) uint8_t ctl[64];
+    for (int l = 0; l < 4; ++l)
+        for (int i = 0; i < 16; ++i) ctl[16 * l + i] = (uint8_t)(2 * (i & 7));
+    const __m512i vctl = _mm512_load_si512(ctl);
+    const __m256i dup = _mm256_setr_epi32(0, 0, 1, 1, 2, 2, 3, 3);
+    const __m512i three = _mm512_set1_epi8(3), one = _mm512_set1_epi8(1);
+    const __mmask64 first = 0x0001000100010001ull;
+    // byte 16j of lane j <- base of chunk 4q + j
+    const __m512i bsel = _mm512_set_epi8(3, 3, 3, 3, 3, 3, 3, 3, 3, 3, 3, 3, 3, 3, 3, 3,
+                                         2, 2, 2, 2, 2, 2, 2, 2, 2, 2, 2, 2, 2, 2, 2, 2,
+                                         1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1,
+                                         0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0);
+    const __m512i bases = _mm512_maskz_expandloadu_epi8(h.nz, h.bases);
+    const uint8_t *cp = h.codes;
+    for (int g = 0; g < 4; ++g) {  // 16 chunks
+        const __mmask16 m = (__mmask16)(h.dd >> (16 * g));
+        const __m512i codes =
+            _mm512_mask_expandloadu_epi32(_mm512_set1_epi32((int)kFlatCode), m, cp);
+        cp += 4 * __builtin_popcount(m);
+        for (int q = 0; q < 4; ++q) {  // 4 chunks per vector
+            __m128i c4q;
+            switch (q) {
+                case 0: c4q = _mm512_extracti32x4_epi32(codes, 0); break;
+                case 1: c4q = _mm512_extracti32x4_epi32(codes, 1); break;
+                case 2: c4q = _mm512_extracti32x4_epi32(codes, 2); break;
+                default: c4q = _mm512_extracti32x4_epi32(codes, 3); break;
+            }
+            __m512i src = _mm512_cvtepu32_epi64(
+                _mm256_permutexvar_epi32(dup, _mm256_castsi128_si256(c4q)));
+            src = _mm512_slli_epi64(src, 2);
+            src = _mm512_mask_srli_epi64(src, 0xAA, src, 16);
+            __m512i x = _mm512_multishift_epi64_epi8(vctl, src);
+            x = _mm512_sub_epi8(_mm512_and_si512(x, three), one);
+            const int c0 = 16 * g + 4 * q;  // first chunk of this vector
+            const __m512i bv = _mm512_permutexvar_epi8(
+                _mm512_add_epi8(bsel, _mm512_set1_epi8((char)c0)), bases);
+            x = _mm512_mask_blend_epi8(first, x, bv);
+            x = _mm512_add_epi8(x, _mm512_bslli_epi128(x, 1));
+            x = _mm512_add_epi8(x, _mm512_bslli_epi128(x, 2));
+            x = _mm512_add_epi8(x, _mm512_bslli_epi128(x, 4));
+            x = _mm512_add_epi8(x, _mm512_bslli_epi128(x, 8));
+            _mm512_storeu_si512(reinterpret_cast<void *>(out + 16 * c0), x);
+        }
+    }
+}
+
+static bool have_avx512vbmi2() {
+    static const bool ok = have_avx512vbmi() && __builtin_cpu_supports("avx512vbmi2");
+    return ok;
+}
+}  // namespace
+
+extern "C" int pdm_unpack_sparse_host(const uint8_t *regions, int64_t map_bytes, uint8_t *out) {
+    REQUIRE(regions && out && map_bytes >= 1, "pdm_unpack_sparse_host: bad arguments");
+    const int64_t chunks = (map_bytes + 15) / 16;
+    const int64_t nreg = (chunks + 63) / 64;
+    const int64_t tail = map_bytes - 16 * (chunks - 1);  // bytes of the last chunk
+    const bool vec = have_avx512vbmi2() && getenv("PDM_NO_AVX512") == nullptr;
+    // dynamic: coded regions cluster in space (surfaces), zero ones in bulk
+#pragma omp parallel for schedule(dynamic, 64)
+    for (int64_t w = 0; w < nreg; ++w) {
+        const bool full = 1024 * (w + 1) <= map_bytes;
+        if (vec && full)
+            sparse_region_vbmi2(regions + kRegion * w, out + 1024 * w);
+        else
+            sparse_region_sse(regions + kRegion * w, w + 1 < nreg ? 64 : chunks - 64 * w,
+                              out + 1024 * w, w + 1 < nreg ? 16 : tail);
+    }
+    return PDM_OK;
+}

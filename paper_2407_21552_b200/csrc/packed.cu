@@ -215,8 +215,22 @@ __device__ __forceinline__ uint32_t ld_stream_u16(const void *p) {
 // kOut: 0 = D' bytes; 1 = D' in the packed encoding (out = 16 nibble bytes
 // per item, out_base = 2 base bytes per item, 9/16 of the bytes); 2 = D' in
 // the delta form (out = 8 code bytes per item, out_base = 2 bases, 5/16 of
-// the bytes).  1 and 2 are for D' headed to the host over PCIe, expanded
-// there by pdm_unpack_packed_host / pdm_unpack_delta_host.
+// the bytes); 3 = D' in the sparse delta form (below).  1-3 are for D'
+// headed to the host over PCIe, expanded there by pdm_unpack_packed_host /
+// pdm_unpack_delta_host / pdm_unpack_sparse_host.
+//
+// Sparse delta form (kOut 3): a warp's 32 items (64 chunks of 16 blocks) own
+// a fixed kSparseRegion-byte region of `out` but write only what they need:
+//   u64 nz     bit c: chunk c is not all-zero
+//   u64 dd     bit c: chunk c is not flat (carries a code word)
+//   bases of the non-zero chunks, then (from the next 4-byte boundary) the
+//   code words of the non-flat chunks, both compacted in chunk order.
+// The warp assembles its region in shared memory and writes the used part
+// with whole 16-byte stores (byte and word stores straight to host memory
+// made small PCIe writes: 2x slower than the 5-byte form despite fewer bytes).
+// A flat chunk (16 equal values) is just its base, an all-zero chunk nothing:
+// in D' most chunks are one or the other (occupied regions, far field), so a
+// TF change sends 1.3-2.9 bytes per 16 blocks instead of 5.
 // zeros != nullptr (D' bytes only): also count D''s zero blocks -- the
 // occupied fraction the live session reports (service/app.py:129,
 // acceleration.py:77-79) -- without a second pass over D'.
@@ -248,18 +262,68 @@ struct IdxPlanes {
     }
 };
 
+constexpr int kSparseRegion = 336;       // 16 + 64 + 256 bytes per 32 items
+constexpr uint32_t kFlatCode = 0x15555555u;  // 15 steps of 0 (coded as 1)
+
+// kOut 3 epilogue: classify the thread's two chunks, then compact the warp's
+// bases and code words into its region (see above).  All 32 lanes take part;
+// lanes past the map pass an all-zero pair.
+// bit i of x -> bit 2i
+__device__ __forceinline__ uint64_t spread_bits(uint32_t x) {
+    uint64_t v = x;
+    v = (v | (v << 16)) & 0x0000FFFF0000FFFFull;
+    v = (v | (v << 8)) & 0x00FF00FF00FF00FFull;
+    v = (v | (v << 4)) & 0x0F0F0F0F0F0F0F0Full;
+    v = (v | (v << 2)) & 0x3333333333333333ull;
+    return (v | (v << 1)) & 0x5555555555555555ull;
+}
+
+__device__ __forceinline__ void store_sparse(uint8_t *region, uint4 *stage, uint2 codes,
+                                             uint32_t bases) {
+    const int lane = threadIdx.x & 31;
+    uint8_t *sm = reinterpret_cast<uint8_t *>(stage);
+    const uint32_t b0 = bases & 0xFFu, b1 = (bases >> 8) & 0xFFu;
+    const bool f0 = codes.x == kFlatCode, f1 = codes.y == kFlatCode;
+    const bool nz0 = !f0 || b0 != 0, nz1 = !f1 || b1 != 0;
+    const uint32_t NZ0 = __ballot_sync(0xFFFFFFFFu, nz0), NZ1 = __ballot_sync(0xFFFFFFFFu, nz1);
+    const uint32_t D0 = __ballot_sync(0xFFFFFFFFu, !f0), D1 = __ballot_sync(0xFFFFFFFFu, !f1);
+    const uint32_t lt = (1u << lane) - 1u;
+    if (lane == 0) {  // chunk order: lane l's chunks are 2l and 2l+1
+        const uint64_t nz = spread_bits(NZ0) | (spread_bits(NZ1) << 1);
+        const uint64_t dd = spread_bits(D0) | (spread_bits(D1) << 1);
+        stage[0] = make_uint4((uint32_t)nz, (uint32_t)(nz >> 32), (uint32_t)dd,
+                              (uint32_t)(dd >> 32));
+    }
+    int bi = __popc(NZ0 & lt) + __popc(NZ1 & lt);
+    if (nz0) sm[16 + bi++] = (uint8_t)b0;
+    if (nz1) sm[16 + bi] = (uint8_t)b1;
+    const int cofs = 16 + ((__popc(NZ0) + __popc(NZ1) + 3) & ~3);
+    int ci = __popc(D0 & lt) + __popc(D1 & lt);
+    uint32_t *cw = reinterpret_cast<uint32_t *>(sm + cofs);
+    if (!f0) cw[ci++] = codes.x;
+    if (!f1) cw[ci] = codes.y;
+    __syncwarp();
+    const int n16 = (cofs + 4 * (__popc(D0) + __popc(D1)) + 15) >> 4;  // <= 21
+    if (lane < n16) st_stream_u4(region + 16 * lane, stage[lane]);
+    __syncwarp();  // the stage is reused by the warp's next item
+}
+
 template <int B, int kOut, bool kCount, class P>  // B: selected planes per load batch
 __device__ __forceinline__ void merge_packed(const P planes, int k, int64_t map_bytes,
                                              uint8_t *__restrict__ out,
                                              uint8_t *__restrict__ out_base,
-                                             unsigned long long *zeros) {
+                                             unsigned long long *zeros, uint4 *stage = nullptr) {
     uint32_t nzero = 0;
     const int64_t items = ceil_div(map_bytes, 32);
     const int64_t T = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < items; t += T) {
+    // kOut 3 keeps whole warps in the loop (warp-wide compaction)
+    const int64_t lane_off = kOut == 3 ? (threadIdx.x & 31) : 0;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t - lane_off < items;
+         t += T) {
+        const bool live = kOut != 3 || t < items;
         PackedAcc acc;
         acc.init();
-        for (int m = 0; m < k; m += B) {
+        for (int m = 0; live && m < k; m += B) {
             uint4 q[B];
             uint32_t b[B];
 #pragma unroll
@@ -279,6 +343,14 @@ __device__ __forceinline__ void merge_packed(const P planes, int k, int64_t map_
             acc.encode(nibs, bases);
             st_stream_u4(out + t * 16, nibs);
             *reinterpret_cast<uint16_t *>(out_base + t * 2) = (uint16_t)bases;
+            continue;
+        }
+        if (kOut == 3) {  // (one call site: the whole warp reaches the ballots)
+            uint2 codes = make_uint2(kFlatCode, kFlatCode);
+            uint32_t bases = 0;
+            if (live) acc.encode_delta(codes, bases);
+            store_sparse(out + (t >> 5) * kSparseRegion,
+                         stage + (threadIdx.x >> 5) * (kSparseRegion / 16), codes, bases);
             continue;
         }
         if (kOut == 2) {
@@ -346,10 +418,11 @@ __global__ void __launch_bounds__(kPackedThreads, kPackedCtas)
                           uint8_t *__restrict__ out_base, unsigned long long *zeros) {
     __shared__ const uint8_t *s_nib[kPackedMaxSel];
     __shared__ const uint8_t *s_base[kPackedMaxSel];
+    __shared__ uint4 s_stage[kOut == 3 ? kPackedThreads / 32 * kSparseRegion / 16 : 1];
     fill_table(nib, nib_pitch, base, base_pitch, sel.idx, sel.k, s_nib, s_base);
     __syncthreads();
     merge_packed<kPackedBatch, kOut, kCount>(TablePlanes{s_nib, s_base}, sel.k, map_bytes, out,
-                                             out_base, zeros);
+                                             out_base, zeros, s_stage);
 }
 
 // Selection resident on the device (written by the select kernel ahead of it
@@ -365,6 +438,7 @@ __global__ void __launch_bounds__(kPackedThreads, kTable ? kPackedCtas : kPacked
     __shared__ int32_t s_idx[kIdx];
     __shared__ const uint8_t *s_nib[kTable ? kPackedTable : 1];
     __shared__ const uint8_t *s_base[kTable ? kPackedTable : 1];
+    __shared__ uint4 s_stage[kOut == 3 ? kPackedThreads / 32 * kSparseRegion / 16 : 1];
     __shared__ int s_k;
     pdl_wait();
     compact_flags(flags, n, s_idx, &s_k);
@@ -373,11 +447,11 @@ __global__ void __launch_bounds__(kPackedThreads, kTable ? kPackedCtas : kPacked
         fill_table(nib, nib_pitch, base, base_pitch, s_idx, s_k, s_nib, s_base);
         __syncthreads();
         merge_packed<kPackedBatch, kOut, kCount>(TablePlanes{s_nib, s_base}, s_k, map_bytes, out,
-                                                 out_base, zeros);
+                                                 out_base, zeros, s_stage);
     } else {
         merge_packed<kPackedBatchIdx, kOut, kCount>(
             IdxPlanes{nib, nib_pitch, base, base_pitch, s_idx}, s_k, map_bytes, out, out_base,
-            zeros);
+            zeros, s_stage);
     }
 }
 
@@ -463,7 +537,8 @@ static int launch_packed(const uint8_t *nib, int64_t nib_pitch, const uint8_t *b
                          unsigned long long *zeros = nullptr, int out_mode = -1) {
     if (zeros) PDM_CUDA_TRY(cudaMemsetAsync(zeros, 0, sizeof(unsigned long long), s));
     if (out_mode < 0) out_mode = out_base ? 1 : 0;
-    auto kern = out_mode == 2 ? combine_packed_kernel<2, false>
+    auto kern = out_mode == 3 ? combine_packed_kernel<3, false>
+                : out_mode == 2 ? combine_packed_kernel<2, false>
                 : out_mode == 1 ? combine_packed_kernel<1, false>
                 : zeros   ? combine_packed_kernel<0, true>
                           : combine_packed_kernel<0, false>;
@@ -481,7 +556,9 @@ static int launch_packed_flags(const uint8_t *nib, int64_t nib_pitch, const uint
                                int out_mode = -1) {
     if (out_mode < 0) out_mode = out_base ? 1 : 0;
     const bool table = n <= kPackedTable;
-    auto kern = out_mode == 2 ? (table ? combine_packed_flags_kernel<2, false, true>
+    auto kern = out_mode == 3 ? (table ? combine_packed_flags_kernel<3, false, true>
+                                       : combine_packed_flags_kernel<3, false, false>)
+                : out_mode == 2 ? (table ? combine_packed_flags_kernel<2, false, true>
                                        : combine_packed_flags_kernel<2, false, false>)
                 : out_mode == 1 ? (table ? combine_packed_flags_kernel<1, false, true>
                                          : combine_packed_flags_kernel<1, false, false>)
@@ -635,10 +712,11 @@ extern "C" int pdm_merge_packed_to_host(const uint8_t *nib, int64_t nib_pitch, c
                                         uint8_t *stage_nib, uint8_t *stage_base, uint8_t *out,
                                         int32_t pieces, int32_t format, pdm_stream_t stream) {
     const char *fn = "pdm_merge_packed_to_host";
-    PDM_REQUIRE(format == 1 || format == 2, "%s: format must be 1 (nibble) or 2 (delta)", fn);
+    PDM_REQUIRE(format >= 1 && format <= 3,
+                "%s: format must be 1 (nibble), 2 (delta) or 3 (sparse delta)", fn);
     const int64_t per_item = format == 1 ? 16 : 8;  // staged code bytes per 32 blocks
     int st = check_packed(fn, nib, nib_pitch, base, base_pitch, map_bytes, n, stage_nib,
-                          stage_base, true);
+                          stage_base, format != 3);  // format 3 uses stage_nib only
     if (st) return st;
     PDM_REQUIRE(out && pieces >= 1 && pieces <= 64, "%s: out null or pieces outside [1, 64]", fn);
     PackedSel p;
@@ -649,16 +727,20 @@ extern "C" int pdm_merge_packed_to_host(const uint8_t *nib, int64_t nib_pitch, c
     }
     cudaStream_t s = as_stream(stream);
     const int64_t items = ceil_div(map_bytes, 32);
-    const int64_t per = ceil_div(items, pieces);
+    int64_t per = ceil_div(items, pieces);
+    if (format == 3) per = 32 * ceil_div(per, 32);  // pieces of whole warp regions
+    // format 3: stage_nib holds ceil(items / 32) regions of kSparseRegion bytes
+    auto stage_at = [&](int64_t t0) {
+        return format == 3 ? stage_nib + (t0 / 32) * kSparseRegion : stage_nib + per_item * t0;
+    };
     int used = 0;
     for (int64_t t0 = 0; t0 < items; t0 += per, ++used) {
         const int64_t nbytes = min(map_bytes, 32 * (t0 + per)) - 32 * t0;
         st = flags ? launch_packed_flags(nib + 16 * t0, nib_pitch, base + 2 * t0, base_pitch,
-                                         nbytes, n, flags, stage_nib + per_item * t0,
-                                         stage_base + 2 * t0, s, nullptr, format)
+                                         nbytes, n, flags, stage_at(t0), stage_base + 2 * t0, s,
+                                         nullptr, format)
                    : launch_packed(nib + 16 * t0, nib_pitch, base + 2 * t0, base_pitch, nbytes, p,
-                                   stage_nib + per_item * t0, stage_base + 2 * t0, s, nullptr,
-                                   format);
+                                   stage_at(t0), stage_base + 2 * t0, s, nullptr, format);
         if (st) return st;
         PDM_CUDA_TRY(cudaEventRecord(piece_event(used), s));
     }
@@ -666,10 +748,11 @@ extern "C" int pdm_merge_packed_to_host(const uint8_t *nib, int64_t nib_pitch, c
         const int64_t t0 = i * per;
         const int64_t nbytes = min(map_bytes, 32 * (t0 + per)) - 32 * t0;
         PDM_CUDA_TRY(cudaEventSynchronize(piece_event(i)));
-        st = format == 1 ? pdm_unpack_packed_host(stage_nib + 16 * t0, stage_base + 2 * t0,
-                                                  nbytes, out + 32 * t0)
-                         : pdm_unpack_delta_host(stage_nib + 8 * t0, stage_base + 2 * t0, nbytes,
-                                                 out + 32 * t0);
+        st = format == 1   ? pdm_unpack_packed_host(stage_nib + 16 * t0, stage_base + 2 * t0,
+                                                    nbytes, out + 32 * t0)
+             : format == 2 ? pdm_unpack_delta_host(stage_nib + 8 * t0, stage_base + 2 * t0,
+                                                   nbytes, out + 32 * t0)
+                           : pdm_unpack_sparse_host(stage_at(t0), nbytes, out + 32 * t0);
         if (st) return st;
     }
     return PDM_OK;

@@ -378,6 +378,63 @@ def test_packed_abi_many_planes(n, map_bytes):
             assert np.array_equal(out.cpu().numpy(), want), k
 
 
+@pytest.mark.parametrize("fmt", [1, 2, 3])
+def test_merge_packed_to_host_formats_and_pieces(fmt):
+    """pdm_merge_packed_to_host through the C ABI: nibble, delta and sparse
+    delta forms, 1-7 pieces (piece edges inside and between warp regions),
+    device-flag and host-index selections, on 1-Lipschitz planes mixing zero
+    plateaus, flat runs and slopes; map sizes with a partial last chunk."""
+    import torch
+
+    from paper_2407_21552_b200 import _lib
+
+    L = _lib.lib()
+    n = 12
+    rng = np.random.default_rng(fmt)
+    for map_bytes in (70000, 4096 * 3 + 5):
+        steps = rng.choice([-1, 0, 0, 0, 1], size=(n, map_bytes))
+        steps[:, rng.integers(0, map_bytes, 40)] = 0
+        maps = np.clip(rng.integers(0, 40, size=(n, 1)) + np.cumsum(steps, axis=1), 0, 255)
+        maps[:, : map_bytes // 5] = 0  # a zero plateau (all-zero chunks)
+        maps = np.clip(maps, 0, 255)
+        ok = np.abs(np.diff(maps.astype(np.int16), axis=1)).max() <= 1
+        if not ok:  # the plateau edge may jump: make the walk climb out of 0
+            maps[:, map_bytes // 5:] = np.minimum(
+                maps[:, map_bytes // 5:], np.arange(1, map_bytes - map_bytes // 5 + 1))
+        maps = maps.astype(np.uint8)
+        pitch = -(-map_bytes // 256) * 256
+        planes = torch.zeros((n, pitch), dtype=torch.uint8, device="cuda")
+        planes[:, :map_bytes] = torch.from_numpy(maps).cuda()
+        chunks = int(L.pdm_packed_chunks(map_bytes))
+        nib_pitch, base_pitch = -(-chunks * 8 // 256) * 256, -(-chunks // 256) * 256
+        nib = torch.empty((n, nib_pitch), dtype=torch.uint8, device="cuda")
+        base = torch.empty((n, base_pitch), dtype=torch.uint8, device="cuda")
+        bad = torch.empty(1, dtype=torch.int32, device="cuda")
+        st = _lib.stream_handle()
+        _lib.check(L.pdm_pack_pdms(_lib.ptr(planes), pitch, map_bytes, n, _lib.ptr(nib),
+                                   nib_pitch, _lib.ptr(base), base_pitch, _lib.ptr(bad), st),
+                   "pack")
+        assert int(bad.cpu()[0]) == 0
+        stage_n = torch.empty(max(chunks * 8, -(-chunks // 64) * 336), dtype=torch.uint8,
+                              pin_memory=True)
+        stage_b = torch.empty(chunks, dtype=torch.uint8, pin_memory=True)
+        for pieces in (1, 3, 7):
+            for k in (1, 5, n):
+                sel = np.sort(rng.choice(n, size=k, replace=False)).astype(np.int32)
+                want = maps[sel].min(axis=0)
+                flags = torch.zeros(n, dtype=torch.uint8, device="cuda")
+                flags[torch.from_numpy(sel).long().cuda()] = 1
+                for use_flags in (True, False):
+                    out = np.full(map_bytes + 32, 0xCD, np.uint8)
+                    _lib.check(L.pdm_merge_packed_to_host(
+                        _lib.ptr(nib), nib_pitch, _lib.ptr(base), base_pitch, map_bytes, n,
+                        _lib.ptr(flags) if use_flags else None,
+                        None if use_flags else sel.ctypes.data, k, stage_n.data_ptr(),
+                        stage_b.data_ptr(), out.ctypes.data, pieces, fmt, st), "to_host")
+                    assert np.array_equal(out[:map_bytes], want), (map_bytes, pieces, k)
+                    assert (out[map_bytes:] == 0xCD).all()
+
+
 @pytest.mark.parametrize("dims", [
     (48, 32, 64),     # bz = 16: separate packing pass
     (12, 8, 512),     # bz = 128: packing fused into the z pass
@@ -417,9 +474,9 @@ def test_packed_skipped_for_maps_that_are_not_distance_fields():
     assert np.array_equal(got, np.minimum.reduce([maps[i - 1] for i in s]))
 
 
-@pytest.mark.parametrize("delta", ["1", "0"])
+@pytest.mark.parametrize("fmt", ["3", "2", "1"])
 @pytest.mark.parametrize("min_blocks", [0, 1 << 30])
-def test_packed_dprime_to_host(monkeypatch, min_blocks, delta):
+def test_packed_dprime_to_host(monkeypatch, min_blocks, fmt):
     """combine(...).dist over a packable set ships D' packed over PCIe and
     expands it on the host (min_blocks=0 forces that path for these small
     maps; 1 << 30 forces the raw zero-copy path): identical to the oracle
@@ -428,7 +485,7 @@ def test_packed_dprime_to_host(monkeypatch, min_blocks, delta):
     stay <= 12 apart)."""
     monkeypatch.setattr(pdm.acceleration, "_HOST_PACKED_MIN_BLOCKS", min_blocks)
     monkeypatch.setenv("PDM_PACKED", "1")
-    monkeypatch.setenv("PDM_HOST_DELTA", delta)  # delta form where bz % 16 == 0
+    monkeypatch.setenv("PDM_HOST_FORMAT", fmt)  # delta forms where bz % 16 == 0
     rng = np.random.default_rng(31)
     for dims, b in (((64, 40, 64), 4), ((3, 5, 13), 1)):
         vox = random_structured_volume(rng, dims, 8)

@@ -304,3 +304,51 @@ def test_unpack_delta_host_matches_numpy_decode(monkeypatch, avx512):
         assert L.pdm_unpack_delta_host(codes.ctypes.data, base.ctypes.data, nb,
                                        out.ctypes.data) == _lib.PDM_OK
         assert np.array_equal(out, vals.reshape(-1)[:nb].astype(np.uint8)), nb
+
+
+def _sparse_regions(vals: np.ndarray) -> np.ndarray:
+    """numpy restatement of the sparse delta encoder (packed.cu store_sparse):
+    vals is (chunks, 16) with chunks a multiple of 64; one 336-byte region per
+    64 chunks."""
+    chunks = vals.shape[0]
+    d = np.diff(vals, axis=1) + 1
+    codes = (d << (2 * np.arange(15))).sum(1).astype(np.uint32)
+    base = vals[:, 0].astype(np.uint8)
+    flat = (d == 1).all(axis=1)
+    nz = ~(flat & (base == 0))
+    regions = np.zeros((chunks // 64, 336), np.uint8)
+    for w in range(chunks // 64):
+        sl = slice(64 * w, 64 * w + 64)
+        words = [int((m.astype(np.uint64) << np.arange(64, dtype=np.uint64)).sum())
+                 for m in (nz[sl], ~flat[sl])]  # bit c: chunk c
+        regions[w, :16] = np.array(words, dtype=np.uint64).view(np.uint8)
+        b = base[sl][nz[sl]]
+        regions[w, 16:16 + b.size] = b
+        c = codes[sl][~flat[sl]]
+        cofs = 16 + (-(-b.size // 4)) * 4
+        regions[w, cofs:cofs + 4 * c.size] = c.view(np.uint8)
+    return regions
+
+
+@pytest.mark.parametrize("avx512", [True, False])
+def test_unpack_sparse_host_matches_numpy_encoder(monkeypatch, avx512):
+    """pdm_unpack_sparse_host (host code, no GPU) against a numpy encoder of
+    the sparse delta form: maps mixing all-zero, flat and coded chunks, sizes
+    with partial regions and a partial last chunk."""
+    if not avx512:
+        monkeypatch.setenv("PDM_NO_AVX512", "1")
+    L = _lib.load_library()
+    rng = np.random.default_rng(23)
+    for nb in (1, 16, 17, 1000, 1024, 1025, 4096 + 7, 1 << 16):
+        chunks = 64 * (-(-nb // 1024))
+        kind = rng.choice(3, chunks, p=[0.4, 0.3, 0.3])          # zero / flat / coded
+        steps = rng.integers(-1, 2, (chunks, 16))
+        steps[kind != 2] = 0
+        start = rng.choice([0, 1, 37, 254, 255], chunks)
+        start[kind == 0] = 0
+        vals = np.clip(start[:, None] + np.cumsum(steps, 1) - steps[:, :1], 0, 255)
+        regions = _sparse_regions(vals)
+        out = np.full(nb + 16, 0xAB, np.uint8)
+        assert L.pdm_unpack_sparse_host(regions.ctypes.data, nb, out.ctypes.data) == _lib.PDM_OK
+        assert np.array_equal(out[:nb], vals.reshape(-1)[:nb].astype(np.uint8)), nb
+        assert (out[nb:] == 0xAB).all(), nb  # nothing written past map_bytes
