@@ -98,6 +98,12 @@ __device__ __forceinline__ uint32_t umulhi_pow2(uint32_t x, int e) {
 // saturated (the fold was XU bound at ~3.9 TB/s of packed bytes).
 constexpr uint32_t kHalfBias = 0x64006400u;
 
+__device__ __forceinline__ uint32_t hmax2_bits(uint32_t a, uint32_t b) {
+    __half2 r = __hmax2(*reinterpret_cast<const __half2 *>(&a),
+                        *reinterpret_cast<const __half2 *>(&b));
+    return *reinterpret_cast<uint32_t *>(&r);
+}
+
 __device__ __forceinline__ uint32_t hmin2_bits(uint32_t a, uint32_t b) {
     __half2 r = __hmin2(*reinterpret_cast<const __half2 *>(&a),
                         *reinterpret_cast<const __half2 *>(&b));
@@ -129,6 +135,23 @@ struct PackedAcc {
                 a[i][s] = hmin2_bits(a[i][s], (sh & 0x000F000Fu) + bb);
             }
         }
+    }
+    // Per chunk, the largest merged value so far as its biased fp16 pattern
+    // (0x6400 + v): a plane whose chunk base is >= it cannot lower anything.
+    __device__ __forceinline__ void chunk_max(uint32_t &m0, uint32_t &m1) const {
+        uint32_t mc[2];
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+            uint32_t m = a[2 * c][0];
+#pragma unroll
+            for (int i = 2 * c; i < 2 * c + 2; ++i)
+#pragma unroll
+                for (int s = 0; s < 4; ++s) m = hmax2_bits(m, a[i][s]);
+            m = hmax2_bits(m, __byte_perm(m, 0u, 0x1032));
+            mc[c] = m & 0xFFFFu;
+        }
+        m0 = mc[0];
+        m1 = mc[1];
     }
     // Re-pack the merged 32 blocks (2 chunks) in the storage encoding: each
     // chunk's min as its base, 4-bit offsets in the same nibble layout (the
@@ -332,6 +355,26 @@ __device__ __forceinline__ void merge_packed(const P planes, int k, int64_t map_
                     q[j] = ld_stream_u4(planes.nib_at(m + j) + t * 16);
                     b[j] = ld_stream_u16(planes.base_at(m + j) + t * 2);
                 }
+            }
+            if (m > 0) {
+                // Warp-uniform dominance skip (exact): a plane whose two chunk
+                // bases are >= the chunks' current maxima cannot lower any of
+                // the warp's blocks, so its fold is skipped.  The maxima only
+                // fall, so testing against the batch-start maxima is safe.
+                // Bench step 46.1 -> 43.9 us (k=29: 68 -> 58 us).  Also skipping
+                // the nibble loads (bases fetched one batch ahead) measured
+                // slower: 49.8 us -- the vote now sits between two loads.
+                uint32_t m0, m1;
+                acc.chunk_max(m0, m1);
+#pragma unroll
+                for (int j = 0; j < B; ++j) {
+                    if (m + j < k) {
+                        const bool dom = (0x6400u | (b[j] & 0xFFu)) >= m0 &&
+                                         (0x6400u | ((b[j] >> 8) & 0xFFu)) >= m1;
+                        if (!__all_sync(__activemask(), dom)) acc.fold(q[j], b[j]);
+                    }
+                }
+                continue;
             }
 #pragma unroll
             for (int j = 0; j < B; ++j)
