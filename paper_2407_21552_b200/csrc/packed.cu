@@ -331,6 +331,88 @@ __device__ __forceinline__ void store_sparse(uint8_t *region, uint4 *stage, uint
     __syncwarp();  // the stage is reused by the warp's next item
 }
 
+// Fold one batch of planes m..m+B-1 (those < k).  After the first batch a
+// warp-uniform dominance skip applies (exact): a plane whose two chunk bases
+// are >= the chunks' current maxima cannot lower any of the warp's blocks, so
+// its fold is skipped; the maxima only fall, so testing against the
+// batch-start maxima is safe.  `vote` lanes outside the map vote "skip".
+// Bench step 46.1 -> 43.9 us (k=29: 68 -> 58 us).  Also skipping the nibble
+// loads (bases fetched one batch ahead) measured slower: 49.8 us -- the vote
+// then sits between two dependent loads.
+template <int B>
+__device__ __forceinline__ void fold_batch(PackedAcc &acc, const uint4 (&q)[B],
+                                           const uint32_t (&b)[B], int m, int k, bool vote) {
+    if (m > 0) {
+        uint32_t m0, m1;
+        acc.chunk_max(m0, m1);
+#pragma unroll
+        for (int j = 0; j < B; ++j) {
+            if (m + j < k) {
+                const bool dom = (0x6400u | (b[j] & 0xFFu)) >= m0 &&
+                                 (0x6400u | ((b[j] >> 8) & 0xFFu)) >= m1;
+                if (!__all_sync(__activemask(), dom || !vote)) acc.fold(q[j], b[j]);
+            }
+        }
+        return;
+    }
+#pragma unroll
+    for (int j = 0; j < B; ++j)
+        if (m + j < k) acc.fold(q[j], b[j]);
+}
+
+// Write item t's merged 32 blocks in output form kOut (see above).  kOut 3
+// must be reached by the whole warp (live = t inside the map).
+template <int kOut, bool kCount>
+__device__ __forceinline__ void emit_item(const PackedAcc &acc, int64_t t, bool live,
+                                          int64_t map_bytes, uint8_t *__restrict__ out,
+                                          uint8_t *__restrict__ out_base, uint4 *warp_stage,
+                                          uint32_t &nzero) {
+    if (kOut == 1) {
+        uint4 nibs;
+        uint32_t bases;
+        acc.encode(nibs, bases);
+        st_stream_u4(out + t * 16, nibs);
+        *reinterpret_cast<uint16_t *>(out_base + t * 2) = (uint16_t)bases;
+    } else if (kOut == 3) {
+        uint2 codes = make_uint2(kFlatCode, kFlatCode);
+        uint32_t bases = 0;
+        if (live) acc.encode_delta(codes, bases);
+        store_sparse(out + (t >> 5) * kSparseRegion, warp_stage, codes, bases);
+    } else if (kOut == 2) {
+        uint2 codes;
+        uint32_t bases;
+        acc.encode_delta(codes, bases);
+        asm volatile("st.global.cs.v2.u32 [%0], {%1,%2};" ::"l"(out + t * 8), "r"(codes.x),
+                     "r"(codes.y)
+                     : "memory");
+        *reinterpret_cast<uint16_t *>(out_base + t * 2) = (uint16_t)bases;
+    } else {
+        uint4 lo, hi;
+        acc.result(lo, hi);
+        uint8_t *dst = out + t * 32;
+        if (t * 32 + 32 <= map_bytes) {
+            st_stream_u4(dst, lo);
+            st_stream_u4(dst + 16, hi);
+            if (kCount)
+                nzero += zero_bytes(lo.x) + zero_bytes(lo.y) + zero_bytes(lo.z) +
+                         zero_bytes(lo.w) + zero_bytes(hi.x) + zero_bytes(hi.y) +
+                         zero_bytes(hi.z) + zero_bytes(hi.w);
+        } else {
+            const uint32_t o[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
+            for (int i = 0; t * 32 + i < map_bytes; ++i) {
+                const uint8_t v = (uint8_t)(o[i >> 2] >> (8 * (i & 3)));
+                dst[i] = v;
+                if (kCount) nzero += v == 0;
+            }
+        }
+    }
+}
+
+__device__ __forceinline__ void add_zero_count(uint32_t nzero, unsigned long long *zeros) {
+    const uint32_t w = __reduce_add_sync(__activemask(), nzero);
+    if ((threadIdx.x & 31) == 0 && w) atomicAdd(zeros, (unsigned long long)w);
+}
+
 template <int B, int kOut, bool kCount, class P>  // B: selected planes per load batch
 __device__ __forceinline__ void merge_packed(const P planes, int k, int64_t map_bytes,
                                              uint8_t *__restrict__ out,
@@ -356,79 +438,12 @@ __device__ __forceinline__ void merge_packed(const P planes, int k, int64_t map_
                     b[j] = ld_stream_u16(planes.base_at(m + j) + t * 2);
                 }
             }
-            if (m > 0) {
-                // Warp-uniform dominance skip (exact): a plane whose two chunk
-                // bases are >= the chunks' current maxima cannot lower any of
-                // the warp's blocks, so its fold is skipped.  The maxima only
-                // fall, so testing against the batch-start maxima is safe.
-                // Bench step 46.1 -> 43.9 us (k=29: 68 -> 58 us).  Also skipping
-                // the nibble loads (bases fetched one batch ahead) measured
-                // slower: 49.8 us -- the vote now sits between two loads.
-                uint32_t m0, m1;
-                acc.chunk_max(m0, m1);
-#pragma unroll
-                for (int j = 0; j < B; ++j) {
-                    if (m + j < k) {
-                        const bool dom = (0x6400u | (b[j] & 0xFFu)) >= m0 &&
-                                         (0x6400u | ((b[j] >> 8) & 0xFFu)) >= m1;
-                        if (!__all_sync(__activemask(), dom)) acc.fold(q[j], b[j]);
-                    }
-                }
-                continue;
-            }
-#pragma unroll
-            for (int j = 0; j < B; ++j)
-                if (m + j < k) acc.fold(q[j], b[j]);
+            fold_batch<B>(acc, q, b, m, k, true);
         }
-        if (kOut == 1) {
-            uint4 nibs;
-            uint32_t bases;
-            acc.encode(nibs, bases);
-            st_stream_u4(out + t * 16, nibs);
-            *reinterpret_cast<uint16_t *>(out_base + t * 2) = (uint16_t)bases;
-            continue;
-        }
-        if (kOut == 3) {  // (one call site: the whole warp reaches the ballots)
-            uint2 codes = make_uint2(kFlatCode, kFlatCode);
-            uint32_t bases = 0;
-            if (live) acc.encode_delta(codes, bases);
-            store_sparse(out + (t >> 5) * kSparseRegion,
-                         stage + (threadIdx.x >> 5) * (kSparseRegion / 16), codes, bases);
-            continue;
-        }
-        if (kOut == 2) {
-            uint2 codes;
-            uint32_t bases;
-            acc.encode_delta(codes, bases);
-            asm volatile("st.global.cs.v2.u32 [%0], {%1,%2};" ::"l"(out + t * 8), "r"(codes.x),
-                         "r"(codes.y)
-                         : "memory");
-            *reinterpret_cast<uint16_t *>(out_base + t * 2) = (uint16_t)bases;
-            continue;
-        }
-        uint4 lo, hi;
-        acc.result(lo, hi);
-        uint8_t *dst = out + t * 32;
-        if (t * 32 + 32 <= map_bytes) {
-            st_stream_u4(dst, lo);
-            st_stream_u4(dst + 16, hi);
-            if (kCount)
-                nzero += zero_bytes(lo.x) + zero_bytes(lo.y) + zero_bytes(lo.z) +
-                         zero_bytes(lo.w) + zero_bytes(hi.x) + zero_bytes(hi.y) +
-                         zero_bytes(hi.z) + zero_bytes(hi.w);
-        } else {
-            const uint32_t o[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
-            for (int i = 0; t * 32 + i < map_bytes; ++i) {
-                const uint8_t v = (uint8_t)(o[i >> 2] >> (8 * (i & 3)));
-                dst[i] = v;
-                if (kCount) nzero += v == 0;
-            }
-        }
+        emit_item<kOut, kCount>(acc, t, live, map_bytes, out, out_base,
+                                stage + (threadIdx.x >> 5) * (kSparseRegion / 16), nzero);
     }
-    if (kCount) {  // every thread of the grid reaches it
-        const uint32_t w = __reduce_add_sync(0xFFFFFFFFu, nzero);
-        if ((threadIdx.x & 31) == 0 && w) atomicAdd(zeros, (unsigned long long)w);
-    }
+    if (kCount) add_zero_count(nzero, zeros);  // every thread of the grid reaches it
 }
 
 // Planes per load batch and CTAs per SM: with the pointer table, 6 planes per
@@ -550,7 +565,10 @@ static int packed_grid(K kernel, int64_t map_bytes) {
 // as it was for the raw merge; an L2 prefetch of the next batch's planes
 // before each batch's loads measured 92 us at k=32.  In the standalone study
 // (tools/exp/merge_variants.cu): a TMA ring with 16 consumer warps per SM
-// reaches 67.4 vs 70 us (consumers then issue-bound); software pipelining
+// reaches 67.4 vs 70 us (consumers then issue-bound); with the dominance skip
+// a product TMA merge (16 consumer warps + 1 producer per SM, 3 x 36 KB ring)
+// measured the same as this kernel (bench step 43.4 vs 43.5 us) and was
+// dropped; software pipelining
 // of register batches 72.6 us; an all-fp16 fold (scaled lanes, HADD2 base
 // add, one shift per word) 68.6-77 us; cp.async per-warp rings 76-84 us.
 static bool packed_layout_ok(const void *nib, int64_t nib_pitch, const void *base,

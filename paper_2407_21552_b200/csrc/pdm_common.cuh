@@ -120,6 +120,7 @@ __device__ __forceinline__ void wait() {
 
 }  // namespace cpa
 
+
 template <int BITS>
 struct VoxT;
 template <>
