@@ -268,6 +268,30 @@ int pdm_synth_volume(int bits, int64_t nx, int64_t ny, int64_t nz, int64_t xs0, 
                      const int64_t *boxes, int32_t nbox, uint64_t seed, void *out,
                      pdm_stream_t stream);
 
+/* ---- GPU consumer of D': ray casting --------------- */
+
+/* raycast.py:163-200 camera_rays, per-pixel part: dirs[width*height][3]
+ * (device, float64, row-major pixels) from the camera frame
+ * frame = {forward, right, up} (host, 9 doubles, voxel-space unit vectors),
+ * tan(fov/2), aspect = width/height and spacing (host, 3 doubles). */
+int pdm_camera_rays(const double *frame, double tan_half, double aspect, const double *spacing,
+                    int32_t width, int32_t height, double *dirs, pdm_stream_t stream);
+
+/* _kernels.py:206-365 march_rays (raycast.py:232-283 render): front-to-back
+ * float64 compositing of n_rays rays from origin (host, 3 doubles) along
+ * dirs (device) over the fixed sample grid t_entry + k*step, skipping with
+ * the per-block distance field dist[ceil(n/b)^3] (device; all zeros = no
+ * skipping).  vox: device [nx][ny][nz] uint8/uint16; lut: device float64
+ * [lut_len][4].  Outputs (device, each optional): rgba[n][4] float64,
+ * counters[n][4] int64 (total, evaluated, skip events, ert), pixels[n][4]
+ * uint8 (clip, *255, round half to even), totals[4] (column sums).
+ * Bit-identical to the reference marcher (no FMA contraction). */
+int pdm_march_rays(const void *vox, int32_t bits, int64_t nx, int64_t ny, int64_t nz,
+                   const double *lut, int64_t lut_len, const uint8_t *dist, int32_t b,
+                   double step, int32_t ert_enabled, double ert_threshold, const double *origin,
+                   const double *dirs, int64_t n_rays, double *rgba, int64_t *counters,
+                   uint8_t *pixels, unsigned long long *totals, pdm_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -34,8 +34,9 @@ _P = ctypes.c_void_p
 
 def build(force: bool = False) -> Path:
     """Compile pdm_oracle.c with the committed Makefile (gcc, OpenMP)."""
-    src = _HERE / "pdm_oracle.c"
-    if force or not _LIB_PATH.exists() or _LIB_PATH.stat().st_mtime < src.stat().st_mtime:
+    newest = max((_HERE / f).stat().st_mtime for f in ("pdm_oracle.c", "march_oracle.c",
+                                                        "Makefile"))
+    if force or not _LIB_PATH.exists() or _LIB_PATH.stat().st_mtime < newest:
         subprocess.run(["make", "-C", str(_HERE), "-B" if force else "-s"], check=True)
     return _LIB_PATH
 
@@ -61,6 +62,9 @@ def lib() -> ctypes.CDLL:
             "oracle_range_apron_tf": (ctypes.c_int, [_P, _P, ctypes.c_int, _I64, _P, _I64, _I64, _P]),
             "oracle_select": (None, [_P, _I64, _I64, _P, _I64, _P]),
             "oracle_combine": (None, [_P, _I64, _P, _I64, _P]),
+            "oracle_march_rays": (None, [_P, ctypes.c_int, _I64, _I64, _I64, _P, _I64, _P, _I64,
+                                         ctypes.c_double, ctypes.c_int, ctypes.c_double, _P, _P,
+                                         _I64, _P, _P]),
             "oracle_synth_volume": (
                 None, [ctypes.c_int, _I64, _I64, _I64, _I64, _I64, _P, _I64, ctypes.c_uint64, _P]),
         }
@@ -248,3 +252,19 @@ def synth_volume(bits: int, dims, boxes: np.ndarray, seed: int, x_range=None) ->
     lib().oracle_synth_volume(bits, nx, ny, nz, xs0, xs1, _ptr(boxes), boxes.shape[0],
                               ctypes.c_uint64(seed), _ptr(out))
     return out
+
+
+def march_rays(vox, lut, dist, b, step, ert_on, ert_thr, origin, dirs):
+    """_kernels.py:206-365 -- (rgba float64 [n, 4], counters int64 [n, 4])."""
+    vox = np.ascontiguousarray(vox)
+    lut = np.ascontiguousarray(lut, dtype=np.float64)
+    dist = np.ascontiguousarray(dist, dtype=np.uint8)
+    origin = np.ascontiguousarray(origin, dtype=np.float64)
+    dirs = np.ascontiguousarray(dirs, dtype=np.float64)
+    n = dirs.shape[0]
+    rgba = np.empty((n, 4), np.float64)
+    counters = np.empty((n, 4), np.int64)
+    lib().oracle_march_rays(_ptr(vox), _bits(vox), *vox.shape, _ptr(lut), lut.shape[0],
+                            _ptr(dist), int(b), float(step), int(bool(ert_on)), float(ert_thr),
+                            _ptr(origin), _ptr(dirs), n, _ptr(rgba), _ptr(counters))
+    return rgba, counters

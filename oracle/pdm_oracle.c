@@ -32,6 +32,7 @@
 static int g_threads = 1;
 
 void oracle_set_threads(int n) { g_threads = n < 1 ? 1 : n; }
+int oracle_threads(void) { return g_threads; }
 
 int oracle_max_threads(void) {
 #ifdef _OPENMP

@@ -20,6 +20,7 @@ _P = ctypes.c_void_p
 _I32 = ctypes.c_int32
 _I64 = ctypes.c_int64
 _INT = ctypes.c_int
+_F64 = ctypes.c_double
 
 # name -> argtypes (all return int status unless listed in _RESTYPES)
 _SIGNATURES = {
@@ -60,6 +61,9 @@ _SIGNATURES = {
     "pdm_count_value": [_P, _I64, ctypes.c_uint32, _P, _P],
     "pdm_minmax_fold": [_P, _P, _P, _P, _INT, _I64, _P],
     "pdm_synth_volume": [_INT, _I64, _I64, _I64, _I64, _I64, _P, _I32, ctypes.c_uint64, _P, _P],
+    "pdm_camera_rays": [_P, _F64, _F64, _P, _I32, _I32, _P, _P],
+    "pdm_march_rays": [_P, _I32, _I64, _I64, _I64, _P, _I64, _P, _I32, _F64, _I32, _F64, _P, _P,
+                       _I64, _P, _P, _P, _P, _P],
 }
 _RESTYPES = {"pdm_last_error": ctypes.c_char_p}
 
