@@ -27,6 +27,8 @@ assert session.combine is b2.combine and session.build_pdm_set is b2.build_pdm_s
 assert cli.select_partitions is b2.select_partitions
 assert pdmrender.Volume is b2.Volume and pdmrender.BlockGrid is b2.BlockGrid
 assert raycast.DistanceMap is b2.DistanceMap
+assert raycast.render is b2.render and pdmrender.render is b2.render  # the GPU marcher
+assert pdmrender.camera_rays is b2.camera_rays and callable(raycast.encode_png)
 assert pdmrender._kernels.__file__.startswith(sys.argv[1])  # non-hot modules stay the reference's
 v = pdmrender.synth_volume("two_spheres", 16, seed=1)
 assert type(v) is b2.Volume and v.bits == 8
