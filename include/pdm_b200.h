@@ -147,8 +147,8 @@ int pdm_unpack_delta_host(const uint8_t *codes, const uint8_t *base, int64_t map
                           uint8_t *out);
 
 /* Host expansion of D' in the sparse delta form (format 3): per 32 items (64
- * chunks) one 336-byte region -- u32 nz[2], u32 dd[2] (bit l of [p]: chunk
- * 2l+p is not all-zero / is not flat), the bases of the non-zero chunks, then
+ * chunks) one 336-byte region -- u64 nz, u64 dd (bit c: chunk c is not
+ * all-zero / is not flat), the bases of the non-zero chunks, then
  * from the next 4-byte boundary the delta code words (as in
  * pdm_unpack_delta_host) of the non-flat chunks, both compacted in chunk
  * order.  Host function. */

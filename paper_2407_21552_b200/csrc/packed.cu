@@ -568,7 +568,14 @@ static int packed_grid(K kernel, int64_t map_bytes) {
 // reaches 67.4 vs 70 us (consumers then issue-bound); with the dominance skip
 // a product TMA merge (16 consumer warps + 1 producer per SM, 3 x 36 KB ring)
 // measured the same as this kernel (bench step 43.4 vs 43.5 us) and was
-// dropped; software pipelining
+// dropped; a tile-level skip (per plane and 8192-block tile its minimum,
+// made at pack time; each CTA folds its planes nearest-first and, after each
+// batch, drops every plane whose tile minimum is >= the tile's merged
+// maximum, loads included) was exact but slower: 51.9 vs 43.8 us per step --
+// the per-tile barriers, sort and tile-minimum fetch cost more than the
+// skipped planes save once the warp-level skip is in (far planes were
+// already not folded, and near-tie planes keep the tile maximum high);
+// software pipelining
 // of register batches 72.6 us; an all-fp16 fold (scaled lanes, HADD2 base
 // add, one shift per word) 68.6-77 us; cp.async per-warp rings 76-84 us.
 static bool packed_layout_ok(const void *nib, int64_t nib_pitch, const void *base,
