@@ -80,8 +80,10 @@ struct MarchArgs {
     int ert_on;
 };
 
-// _kernels.py:206-365, one thread per ray.
-template <class V>
+// _kernels.py:206-365, one thread per ray.  I: index type (int32 when the
+// volume has < 2^31 voxels -- cheaper conversions and address math; the
+// values are the same).
+template <class V, class I>
 __global__ void __launch_bounds__(128)
     march_rays_kernel(const V *__restrict__ vox, const double *__restrict__ lut,
                       const uint8_t *__restrict__ dist, const double *__restrict__ dirs,
@@ -93,9 +95,9 @@ __global__ void __launch_bounds__(128)
     double acc_r = 0.0, acc_g = 0.0, acc_b = 0.0, acc_a = 0.0;
     if (r < a.n_rays) {
         const double hx = a.nx - 1.0, hy = a.ny - 1.0, hz = a.nz - 1.0;
-        const int64_t x_hi = a.nx >= 2 ? a.nx - 2 : 0;
-        const int64_t y_hi = a.ny >= 2 ? a.ny - 2 : 0;
-        const int64_t z_hi = a.nz >= 2 ? a.nz - 2 : 0;
+        const I x_hi = a.nx >= 2 ? (I)(a.nx - 2) : 0;
+        const I y_hi = a.ny >= 2 ? (I)(a.ny - 2) : 0;
+        const I z_hi = a.nz >= 2 ? (I)(a.nz - 2) : 0;
         const double dx = dirs[3 * r], dy = dirs[3 * r + 1], dz = dirs[3 * r + 2];
         // slab intersection with the voxel-centre hull [0, n-1]^3
         double tmin = -kBig, tmax = kBig;
@@ -121,32 +123,37 @@ __global__ void __launch_bounds__(128)
         if (hit && !(tmax < tmin) && !(tmax < 0.0)) {
             const double t_entry = tmin > 0.0 ? tmin : 0.0;
             total = (int64_t)((tmax - t_entry) / a.step) + 1;
-            const int64_t plane = a.ny * a.nz;
+            const I plane = (I)(a.ny * a.nz), nzi = (I)a.nz;
+            const I bb = (I)a.b, byi = (I)a.by, bzi = (I)a.bz;
+            const int bshift = (a.b & (a.b - 1)) == 0 ? __ffs(a.b) - 1 : -1;
             int64_t k = 0;
             while (k < total) {
                 const double t = t_entry + k * a.step;
                 const double px = clampd(a.ox + t * dx, hx);
                 const double py = clampd(a.oy + t * dy, hy);
                 const double pz = clampd(a.oz + t * dz, hz);
-                const int64_t vx = (int64_t)px, vy = (int64_t)py, vz = (int64_t)pz;
-                const int64_t bi = vx / a.b, bj = vy / a.b, bk = vz / a.b;
-                const int dval = dist[(bi * a.by + bj) * a.bz + bk];
+                const I vx = (I)px, vy = (I)py, vz = (I)pz;
+                // block coordinates: a shift for power-of-two edges (b = 4, 8, ...)
+                const I bi = bshift >= 0 ? vx >> bshift : vx / bb;
+                const I bj = bshift >= 0 ? vy >> bshift : vy / bb;
+                const I bk = bshift >= 0 ? vz >> bshift : vz / bb;
+                const int dval = dist[(bi * byi + bj) * bzi + bk];
                 if (dval == 0) {
-                    const int64_t x0 = vx < x_hi ? vx : x_hi;
-                    const int64_t y0 = vy < y_hi ? vy : y_hi;
-                    const int64_t z0 = vz < z_hi ? vz : z_hi;
+                    const I x0 = vx < x_hi ? vx : x_hi;
+                    const I y0 = vy < y_hi ? vy : y_hi;
+                    const I z0 = vz < z_hi ? vz : z_hi;
                     const double fx = px - x0, fy = py - y0, fz = pz - z0;
-                    const int64_t x1 = a.nx >= 2 ? x0 + 1 : x0;
-                    const int64_t y1 = a.ny >= 2 ? y0 + 1 : y0;
-                    const int64_t z1 = a.nz >= 2 ? z0 + 1 : z0;
-                    const double c000 = vox[x0 * plane + y0 * a.nz + z0];
-                    const double c100 = vox[x1 * plane + y0 * a.nz + z0];
-                    const double c010 = vox[x0 * plane + y1 * a.nz + z0];
-                    const double c110 = vox[x1 * plane + y1 * a.nz + z0];
-                    const double c001 = vox[x0 * plane + y0 * a.nz + z1];
-                    const double c101 = vox[x1 * plane + y0 * a.nz + z1];
-                    const double c011 = vox[x0 * plane + y1 * a.nz + z1];
-                    const double c111 = vox[x1 * plane + y1 * a.nz + z1];
+                    const I x1 = a.nx >= 2 ? x0 + 1 : x0;
+                    const I y1 = a.ny >= 2 ? y0 + 1 : y0;
+                    const I z1 = a.nz >= 2 ? z0 + 1 : z0;
+                    const double c000 = vox[x0 * plane + y0 * nzi + z0];
+                    const double c100 = vox[x1 * plane + y0 * nzi + z0];
+                    const double c010 = vox[x0 * plane + y1 * nzi + z0];
+                    const double c110 = vox[x1 * plane + y1 * nzi + z0];
+                    const double c001 = vox[x0 * plane + y0 * nzi + z1];
+                    const double c101 = vox[x1 * plane + y0 * nzi + z1];
+                    const double c011 = vox[x0 * plane + y1 * nzi + z1];
+                    const double c111 = vox[x1 * plane + y1 * nzi + z1];
                     const double gx = 1.0 - fx, gy = 1.0 - fy, gz = 1.0 - fz;
                     const double value =
                         gz * (gy * (gx * c000 + fx * c100) + fy * (gx * c010 + fx * c110)) +
@@ -256,13 +263,20 @@ extern "C" int pdm_march_rays(const void *vox, int32_t bits, int64_t nx, int64_t
     cudaStream_t s = as_stream(stream);
     if (totals) PDM_CUDA_TRY(cudaMemsetAsync(totals, 0, 4 * sizeof(unsigned long long), s));
     const unsigned grid = (unsigned)ceil_div(n_rays, 128);
-    if (bits == 8)
-        march_rays_kernel<uint8_t><<<grid, 128, 0, s>>>(static_cast<const uint8_t *>(vox), lut,
-                                                         dist, dirs, a, rgba, counters, pixels,
-                                                         totals);
+    const bool small = nx * ny * nz < ((int64_t)1 << 31);
+    if (bits == 8 && small)
+        march_rays_kernel<uint8_t, int32_t><<<grid, 128, 0, s>>>(
+            static_cast<const uint8_t *>(vox), lut, dist, dirs, a, rgba, counters, pixels, totals);
+    else if (bits == 8)
+        march_rays_kernel<uint8_t, int64_t><<<grid, 128, 0, s>>>(
+            static_cast<const uint8_t *>(vox), lut, dist, dirs, a, rgba, counters, pixels, totals);
+    else if (small)
+        march_rays_kernel<uint16_t, int32_t><<<grid, 128, 0, s>>>(
+            static_cast<const uint16_t *>(vox), lut, dist, dirs, a, rgba, counters, pixels,
+            totals);
     else
-        march_rays_kernel<uint16_t><<<grid, 128, 0, s>>>(static_cast<const uint16_t *>(vox), lut,
-                                                          dist, dirs, a, rgba, counters, pixels,
-                                                          totals);
+        march_rays_kernel<uint16_t, int64_t><<<grid, 128, 0, s>>>(
+            static_cast<const uint16_t *>(vox), lut, dist, dirs, a, rgba, counters, pixels,
+            totals);
     return cuda_status("march_rays_kernel");
 }

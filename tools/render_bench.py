@@ -75,9 +75,12 @@ def main():
     for mode, accel in (("none", None), ("pdm", dprime)):
         st = pdm.RenderSettings(args.size, args.size, step=0.5, ess_mode=mode)
         ms = timed(lambda: raycast._march(vol, tf, cam, st, accel))
-        t0 = time.perf_counter()
-        fb, stats = pdm.render(vol, tf, cam, st, accel)
-        api_ms = (time.perf_counter() - t0) * 1e3
+        api = []
+        for _ in range(5):
+            t0 = time.perf_counter()
+            fb, stats = pdm.render(vol, tf, cam, st, accel)
+            api.append((time.perf_counter() - t0) * 1e3)
+        api_ms = float(np.median(api))
         total = stats.samples_evaluated + stats.samples_skipped
         out[mode] = {"frame_ms": round(ms, 3), "render_api_ms": round(api_ms, 3),
                      "samples_total": total, "samples_evaluated": stats.samples_evaluated,
