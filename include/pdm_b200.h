@@ -68,7 +68,8 @@ int pdm_select(const double *alpha, int64_t span, int64_t alpha_stride, const in
 
 /* transfer.py:250-259 on the LUT alone: nz[v] = alpha[v] > 0.0 and, when
  * prefix != NULL, prefix[v+1] = #{u <= v : alpha[u] > 0} with prefix[0] = 0
- * (the np.cumsum of acceleration.py:171).  prefix needs span+1 int32. */
+ * (the np.cumsum of acceleration.py:171).  prefix needs span+1 int32 and
+ * then nz must be 16-byte aligned. */
 int pdm_alpha_support(const double *alpha, int64_t span, int64_t alpha_stride, uint8_t *nz,
                       int32_t *prefix, pdm_stream_t stream);
 
@@ -232,6 +233,23 @@ int pdm_occupancy_minmax_prefix(const void *mins, const void *maxs, int bits, in
 /* One map from a uint8 occupancy [bx][by][bz] (nonzero = occupied). */
 int pdm_distance_transform(const uint8_t *occ, int64_t bx, int64_t by, int64_t bz, uint8_t *out,
                            pdm_stream_t stream);
+
+/* Full recompute for one TF, fused (acceleration.py:184-196
+ * standard_distance_map = occupancy_for_tf :145-174 + distance_transform
+ * :177-181): the block occupancy is written straight into out as the
+ * transform's seed (0 occupied, 255 empty) and the passes run in place, so no
+ * bool map is materialised.  out = uint8 [bx][by][bz], identical to
+ * pdm_block_any_lut / pdm_occupancy_minmax_prefix followed by
+ * pdm_distance_transform.
+ * voxel: lut = the TF's nz LUT (pdm_alpha_support), voxel-exact occupancy.
+ * minmax: range_apron occupancy from apron mins/maxs (pdm_block_min_max) and
+ *   the TF's prefix count (pdm_alpha_support). */
+int pdm_standard_distance_map_voxel(const void *vox, int bits, int64_t nx, int64_t ny, int64_t nz,
+                                    int32_t b, const uint8_t *lut, uint8_t *out,
+                                    pdm_stream_t stream);
+int pdm_standard_distance_map_minmax(const void *mins, const void *maxs, int bits, int64_t bx,
+                                     int64_t by, int64_t bz, const int32_t *prefix, uint8_t *out,
+                                     pdm_stream_t stream);
 
 /* All n partition maps of a mask (acceleration.py:230-233, the batched
  * transforms of build_pdm_set) into pdms [n][plane_pitch]. */

@@ -52,6 +52,8 @@ _SIGNATURES = {
     "pdm_occupancy_minmax_range": [_P, _P, _INT, _I64, ctypes.c_uint32, ctypes.c_uint32, _P, _P],
     "pdm_occupancy_minmax_prefix": [_P, _P, _INT, _I64, _P, _P, _P],
     "pdm_distance_transform": [_P, _I64, _I64, _I64, _P, _P],
+    "pdm_standard_distance_map_voxel": [_P, _INT, _I64, _I64, _I64, _I32, _P, _P, _P],
+    "pdm_standard_distance_map_minmax": [_P, _P, _INT, _I64, _I64, _I64, _P, _P, _P],
     "pdm_distance_transform_mask": [_P, _I32, _I32, _I64, _I64, _I64, _P, _I64, _P],
     "pdm_dt_pass_x_mask": [_P, _I32, _I32, _I64, _I64, _I64, _P, _I64, _P],
     "pdm_dt_slab_edges": [_P, _I64, _I32, _I64, _I64, _I64, _P, _P],

@@ -349,7 +349,31 @@ def _minmax_device(volume, grid, minmax):
     if isinstance(mins, np.ndarray):
         mins = device.to_device(np.ascontiguousarray(mins, dtype=volume.dtype))
         maxs = device.to_device(np.ascontiguousarray(maxs, dtype=volume.dtype))
+    if tuple(mins.shape) != tuple(grid.bdims) or tuple(maxs.shape) != tuple(grid.bdims):
+        # the reference's OccupancyMap rejects the mis-shaped result
+        # (acceleration.py:51-52); here it is caught before any kernel reads
+        raise ValueError("occupancy array shape does not match bdims")
     return mins.contiguous(), maxs.contiguous()
+
+
+def _tf_support(volume: Volume, grid: BlockGrid, tf: TransferFunction, mode: str):
+    """Validation shared by occupancy_for_tf / standard_distance_map
+    (acceleration.py:158-163), then the TF's nz LUT and, for range_apron, its
+    prefix count (pdm_alpha_support) on the device."""
+    _require_mode(mode)
+    check_pair(volume, grid)
+    if tf.lut.shape[0] != (1 << volume.bits):
+        raise VolumeError(
+            f"tf covers {tf.lut.shape[0]} intensities, volume needs {1 << volume.bits}")
+    L = _lib.lib()
+    span = 1 << volume.bits
+    alpha = alpha_to_device(tf)
+    nz = device.empty((span,), np.uint8)
+    prefix = device.empty((span + 1,), np.int32) if mode == "range_apron" else None
+    _lib.check(L.pdm_alpha_support(_lib.ptr(alpha), span, 1, _lib.ptr(nz),
+                                   _lib.ptr(prefix) if prefix is not None else None,
+                                   _lib.stream_handle()), "pdm_alpha_support")
+    return nz, prefix
 
 
 def occupancy_for_tf(volume: Volume, grid: BlockGrid, tf: TransferFunction, mode: str = "voxel",
@@ -357,20 +381,9 @@ def occupancy_for_tf(volume: Volume, grid: BlockGrid, tf: TransferFunction, mode
     """Blocks that can contribute opacity under a TF (acceleration.py:145-174):
     voxel = any voxel with alpha > 0; range_apron = alpha > 0 somewhere inside
     the block's apron [min, max] (prefix count)."""
-    _require_mode(mode)
-    check_pair(volume, grid)
-    if tf.lut.shape[0] != (1 << volume.bits):
-        raise VolumeError(
-            f"tf covers {tf.lut.shape[0]} intensities, volume needs {1 << volume.bits}")
+    nz, prefix = _tf_support(volume, grid, tf, mode)
     L = _lib.lib()
     st = _lib.stream_handle()
-    span = 1 << volume.bits
-    alpha = alpha_to_device(tf)
-    nz = device.empty((span,), np.uint8)
-    prefix = device.empty((span + 1,), np.int32) if mode == "range_apron" else None
-    _lib.check(L.pdm_alpha_support(_lib.ptr(alpha), span, 1, _lib.ptr(nz),
-                                   _lib.ptr(prefix) if prefix is not None else None, st),
-               "pdm_alpha_support")
     out = device.empty(grid.bdims, np.uint8)
     if mode == "voxel":
         vox = volume.device_voxels()
@@ -399,8 +412,25 @@ def distance_transform(occ: OccupancyMap) -> DistanceMap:
 def standard_distance_map(volume: Volume, grid: BlockGrid, tf: TransferFunction,
                           mode: str = "voxel", minmax=None) -> DistanceMap:
     """Full recompute for one TF: occupancy scan + distance transform
-    (acceleration.py:184-196, the Deakin & Knackstedt baseline)."""
-    return distance_transform(occupancy_for_tf(volume, grid, tf, mode, minmax))
+    (acceleration.py:184-196, the Deakin & Knackstedt baseline), fused: the
+    occupancy kernel writes the transform's {0, 255} seed into D directly
+    (pdm_standard_distance_map_voxel / _minmax), the passes run in place."""
+    nz, prefix = _tf_support(volume, grid, tf, mode)
+    L = _lib.lib()
+    st = _lib.stream_handle()
+    out = device.empty(grid.bdims, np.uint8)
+    if mode == "voxel":
+        vox = volume.device_voxels()
+        _lib.check(L.pdm_standard_distance_map_voxel(_lib.ptr(vox), volume.bits, *volume.dims,
+                                                     grid.b, _lib.ptr(nz), _lib.ptr(out), st),
+                   "pdm_standard_distance_map_voxel")
+    else:
+        mins, maxs = _minmax_device(volume, grid, minmax)
+        _lib.check(L.pdm_standard_distance_map_minmax(_lib.ptr(mins), _lib.ptr(maxs),
+                                                      volume.bits, *grid.bdims,
+                                                      _lib.ptr(prefix), _lib.ptr(out), st),
+                   "pdm_standard_distance_map_minmax")
+    return DistanceMap(b=grid.b, bdims=grid.bdims, dist=out)
 
 
 def partition_mask(volume: Volume, grid: BlockGrid, scheme: PartitionScheme,

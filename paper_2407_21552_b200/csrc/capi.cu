@@ -79,37 +79,74 @@ __global__ void __launch_bounds__(256)
 }
 
 // acceleration.py:166,171 -- nz = alpha > 0 and its exclusive prefix count.
-// One CTA: each thread counts a contiguous chunk, a block scan turns counts
-// into chunk offsets, then each thread writes its chunk of the prefix.
-__global__ void __launch_bounds__(1024)
-    alpha_support_kernel(const double *__restrict__ alpha, int64_t span, int64_t stride,
-                         uint8_t *__restrict__ nz, int32_t *__restrict__ prefix) {
-    __shared__ int32_t s_sum[1024];
-    const int t = threadIdx.x;
-    const int64_t per = (span + blockDim.x - 1) / blockDim.x;
-    const int64_t lo = t * per, hi = lo + per < span ? lo + per : span;
+// Two launches over tiles of 1024 intensities (CTA i = tile i, coalesced):
+// alpha_nz_kernel writes nz; alpha_prefix_kernel gives CTA i its carry by
+// summing the 0/1 bytes of nz[0, 1024 i) (at most 64 KB, L2-resident), then
+// ranks its own tile with warp ballots and a shuffle scan of the 32 warp
+// counts.  No workspace, no serial walk over the span.
+constexpr int kAlphaTile = 1024;
+
+__global__ void __launch_bounds__(256)
+    alpha_nz_kernel(const double *__restrict__ alpha, int64_t span, int64_t stride,
+                    uint8_t *__restrict__ nz) {
+    const int64_t base = (int64_t)blockIdx.x * kAlphaTile + threadIdx.x;
+    bool on[kAlphaTile / 256];
+#pragma unroll
+    for (int j = 0; j < kAlphaTile / 256; ++j) {
+        const int64_t v = base + j * 256;
+        on[j] = v < span && alpha[v * stride] > 0.0;  // NaN compares false
+    }
+#pragma unroll
+    for (int j = 0; j < kAlphaTile / 256; ++j) {
+        const int64_t v = base + j * 256;
+        if (v < span) nz[v] = on[j];
+    }
+}
+
+__global__ void __launch_bounds__(kAlphaTile)
+    alpha_prefix_kernel(const uint8_t *__restrict__ nz, int64_t span,
+                        int32_t *__restrict__ prefix) {
+    __shared__ int32_t s_warp[32];
+    __shared__ int32_t s_carry;
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const int64_t tile0 = (int64_t)blockIdx.x * kAlphaTile;
+    // carry: bytes of nz before this tile (tile0 is a multiple of 16)
     int32_t cnt = 0;
-    for (int64_t v = lo; v < hi; ++v) {
-        uint8_t on = alpha[v * stride] > 0.0;
-        nz[v] = on;
-        cnt += on;
+    for (int64_t q = t; q < tile0 / 16; q += kAlphaTile) {
+        const uint4 w = __ldg(reinterpret_cast<const uint4 *>(nz) + q);
+        cnt += (int32_t)(((w.x * 0x01010101u) >> 24) + ((w.y * 0x01010101u) >> 24) +
+                         ((w.z * 0x01010101u) >> 24) + ((w.w * 0x01010101u) >> 24));
     }
-    s_sum[t] = cnt;
+#pragma unroll
+    for (int off = 16; off; off >>= 1) cnt += __shfl_xor_sync(0xFFFFFFFFu, cnt, off);
+    if (lane == 0) s_warp[warp] = cnt;
     __syncthreads();
-    for (int off = 1; off < (int)blockDim.x; off <<= 1) {  // Hillis-Steele inclusive scan
-        int32_t add = t >= off ? s_sum[t - off] : 0;
-        __syncthreads();
-        s_sum[t] += add;
-        __syncthreads();
+    if (warp == 0) {
+        int32_t c = s_warp[lane];
+#pragma unroll
+        for (int off = 16; off; off >>= 1) c += __shfl_xor_sync(0xFFFFFFFFu, c, off);
+        if (lane == 0) s_carry = c;
     }
-    if (prefix) {
-        int32_t run = s_sum[t] - cnt;  // exclusive
-        if (t == 0) prefix[0] = 0;
-        for (int64_t v = lo; v < hi; ++v) {
-            run += nz[v];
-            prefix[v + 1] = run;
+    __syncthreads();  // s_warp is reused below
+    const int64_t v = tile0 + t;
+    const bool on = v < span && nz[v];
+    const uint32_t bal = __ballot_sync(0xFFFFFFFFu, on);
+    if (lane == 0) s_warp[warp] = __popc(bal);
+    __syncthreads();
+    if (warp == 0) {  // exclusive scan of the 32 warp counts
+        const int32_t c = s_warp[lane];
+        int32_t inc = c;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const int32_t y = __shfl_up_sync(0xFFFFFFFFu, inc, off);
+            if (lane >= off) inc += y;
         }
+        s_warp[lane] = inc - c;
     }
+    __syncthreads();
+    if (v < span)
+        prefix[v + 1] = s_carry + s_warp[warp] + __popc(bal & ((1u << lane) - 1u)) + on;
+    if (v == 0) prefix[0] = 0;
 }
 
 // ---------------------------------------------------------------------------
@@ -471,9 +508,15 @@ extern "C" int pdm_alpha_support(const double *alpha, int64_t span, int64_t alph
     PDM_REQUIRE(alpha && nz, "pdm_alpha_support: null pointer");
     PDM_REQUIRE(span >= 1 && span <= (1 << 16) && alpha_stride >= 1,
                 "pdm_alpha_support: span must be in [1, 65536]");
-    alpha_support_kernel<<<1, 1024, 0, as_stream(stream)>>>(alpha, span, alpha_stride, nz,
-                                                             prefix);
-    return cuda_status("alpha_support_kernel");
+    PDM_REQUIRE(!prefix || (uintptr_t)nz % 16 == 0,
+                "pdm_alpha_support: nz must be 16-byte aligned when prefix is requested");
+    cudaStream_t s = as_stream(stream);
+    const int tiles = (int)ceil_div(span, kAlphaTile);
+    alpha_nz_kernel<<<tiles, 256, 0, s>>>(alpha, span, alpha_stride, nz);
+    int st = cuda_status("alpha_nz_kernel");
+    if (st || !prefix) return st;
+    alpha_prefix_kernel<<<tiles, kAlphaTile, 0, s>>>(nz, span, prefix);
+    return cuda_status("alpha_prefix_kernel");
 }
 
 extern "C" int pdm_combine(const uint8_t *pdms, int64_t plane_pitch, int64_t map_bytes,

@@ -914,6 +914,16 @@ static int check_grid(const char *fn, int n, int64_t bx, int64_t by, int64_t bz,
 
 using namespace pdm;
 
+int pdm::dt_from_seed(const char *fn, int64_t bx, int64_t by, int64_t bz, uint8_t *map,
+                      cudaStream_t s) {
+    const int64_t nb = bx * by * bz;
+    int st = check_grid(fn, 1, bx, by, bz, nb);
+    if (st) return st;
+    st = axis_pass<kAxisX, true>(1, bx, by, bz, map, nb, s);
+    if (st) return st;
+    return pass_yz(1, bx, by, bz, map, nb, s);
+}
+
 extern "C" int pdm_distance_transform(const uint8_t *occ, int64_t bx, int64_t by, int64_t bz,
                                       uint8_t *out, pdm_stream_t stream) {
     PDM_REQUIRE(occ && out, "pdm_distance_transform: null pointer");
@@ -924,9 +934,7 @@ extern "C" int pdm_distance_transform(const uint8_t *occ, int64_t bx, int64_t by
     dt_expand_occ_kernel<<<grid_for(nb, 256, 8), 256, 0, s>>>(occ, nb, out);
     st = cuda_status("dt_expand_occ_kernel");
     if (st) return st;
-    st = axis_pass<kAxisX, true>(1, bx, by, bz, out, nb, s);
-    if (st) return st;
-    return pass_yz(1, bx, by, bz, out, nb, s);
+    return dt_from_seed("pdm_distance_transform", bx, by, bz, out, s);
 }
 
 extern "C" int pdm_distance_transform_mask(const uint32_t *mask, int32_t words, int32_t n,

@@ -39,6 +39,11 @@ inline cudaStream_t as_stream(pdm_stream_t s) { return reinterpret_cast<cudaStre
 
 int sm_count();  // cached SM count of the current device
 
+// dt.cu: the three Chebyshev passes in place over one {0, 255}-seeded map
+// (the tail of pdm_distance_transform, shared with the fused recompute).
+int dt_from_seed(const char *fn, int64_t bx, int64_t by, int64_t bz, uint8_t *map,
+                 cudaStream_t s);
+
 // apron.cu: streaming apron min/max (+ mask) when b divides a 16-byte voxel
 // chunk; returns PDM_EUNSUPPORTED without launching otherwise.  outs: bit 0 =
 // write mins/maxs, bit 1 = write the partition mask.

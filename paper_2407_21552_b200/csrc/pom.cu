@@ -21,15 +21,17 @@ namespace pdm {
 // ---- generic path -------------------------------------------------------------
 
 // _kernels.py:137-149 partition_presence / _kernels.py:84-134 block_any_*:
-// thread per block.  kBool: out[c] = OR of lut[v] (0/1);  otherwise mask bits
-// 1 << pid[v]; words > 2 uses global atomics into a pre-zeroed mask.
-template <int BITS, bool kBool>
+// thread per block.  kKind 1: out[c] = OR of lut[v] (0/1); kKind 2: the same
+// written as the distance transform's seed (0 occupied, 255 empty); kKind 0:
+// mask bits 1 << pid[v], words > 2 via global atomics into a pre-zeroed mask.
+template <int BITS, int kKind>
 __global__ void block_lut_generic_kernel(const typename VoxT<BITS>::type *__restrict__ vox,
                                          int64_t nx, int64_t ny, int64_t nz, int b,
                                          int64_t bx, int64_t by, int64_t bz,
                                          const int32_t *__restrict__ pid,
                                          const uint8_t *__restrict__ lut, uint32_t *mask,
                                          int words, uint8_t *out) {
+    constexpr bool kBool = kKind != 0;
     const int64_t nb = bx * by * bz;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < nb; c += stride) {
@@ -54,7 +56,7 @@ __global__ void block_lut_generic_kernel(const typename VoxT<BITS>::type *__rest
                 }
             }
         if (kBool) {
-            out[c] = m != 0;
+            out[c] = kKind == 2 ? (m != 0 ? 0 : kDistClamp) : (m != 0);
         } else if (words <= 2) {
             mask[c * words] = (uint32_t)m;
             if (words == 2) mask[c * words + 1] = (uint32_t)(m >> 32);
@@ -119,7 +121,8 @@ __global__ void apron_generic_kernel(const typename VoxT<BITS>::type *__restrict
 
 // Thread = (block row (i, j), 16-byte chunk q along z).  VPC voxels per chunk,
 // B the block edge (B divides VPC), ZB = VPC / B z-blocks per chunk.
-// kMode 0: mask words (1 or 2) from a u8 pid LUT; kMode 1: bool from a 0/1 LUT.
+// kMode 0: mask words (1 or 2) from a u8 pid LUT; kMode 1: bool from a 0/1 LUT;
+// kMode 2: that bool written as the distance transform's seed (0 / 255).
 template <int BITS, int B, int kMode, int WORDS>
 __global__ void __launch_bounds__(512)
     block_lut_fast_kernel(const typename VoxT<BITS>::type *__restrict__ vox, int64_t nx,
@@ -129,9 +132,28 @@ __global__ void __launch_bounds__(512)
     constexpr int SPAN = 1 << BITS;
     constexpr int VPC = 16 / (BITS / 8);
     constexpr int ZB = VPC / B;
-    extern __shared__ uint8_t s_lut[];  // SPAN bytes
-    for (int v = threadIdx.x; v < SPAN; v += blockDim.x)
-        s_lut[v] = kMode == 0 ? (uint8_t)pid[v] : lut01[v];
+    extern __shared__ __align__(16) uint8_t s_lut[];  // SPAN bytes
+    // LUT fill with vector loads (64 KB per CTA at 16 bits: a byte loop here
+    // was 128 dependent-latency loads per thread before the first voxel)
+    if (kMode == 0) {  // int32 pid -> bytes, 4 per int4 load
+        if (((uintptr_t)pid & 15) == 0) {
+#pragma unroll 8
+            for (int q = threadIdx.x; q < SPAN / 4; q += blockDim.x) {
+                const int4 p4 = __ldg(reinterpret_cast<const int4 *>(pid) + q);
+                reinterpret_cast<uint32_t *>(s_lut)[q] =
+                    (uint32_t)(p4.x & 0xFF) | (uint32_t)(p4.y & 0xFF) << 8 |
+                    (uint32_t)(p4.z & 0xFF) << 16 | (uint32_t)(p4.w & 0xFF) << 24;
+            }
+        } else {
+            for (int v = threadIdx.x; v < SPAN; v += blockDim.x) s_lut[v] = (uint8_t)pid[v];
+        }
+    } else if (((uintptr_t)lut01 & 15) == 0 && SPAN >= 16) {
+#pragma unroll 8
+        for (int q = threadIdx.x; q < SPAN / 16; q += blockDim.x)
+            reinterpret_cast<uint4 *>(s_lut)[q] = __ldg(reinterpret_cast<const uint4 *>(lut01) + q);
+    } else {
+        for (int v = threadIdx.x; v < SPAN; v += blockDim.x) s_lut[v] = lut01[v];
+    }
     __syncthreads();
 
     const int64_t nzc = nz / VPC;
@@ -178,8 +200,10 @@ __global__ void __launch_bounds__(512)
             if (kMode == 0) {
                 mask[(c0 + t) * WORDS] = (uint32_t)acc[t];
                 if (WORDS == 2) mask[(c0 + t) * WORDS + 1] = (uint32_t)(acc[t] >> 32);
-            } else {
+            } else if (kMode == 1) {
                 out[c0 + t] = acc[t] != 0;
+            } else {
+                out[c0 + t] = acc[t] != 0 ? 0 : kDistClamp;
             }
         }
     }
@@ -244,12 +268,69 @@ __global__ void minmax_range_kernel(const T *__restrict__ mins, const T *__restr
         out[c] = (uint32_t)mins[c] <= hi && (uint32_t)maxs[c] >= lo;
 }
 
+// kSeed: written as the distance transform's seed (0 occupied, 255 empty).
+// A thread takes 8 consecutive blocks: one vector load of their mins and one
+// of their maxs (8 * sizeof(T) bytes each), 16 prefix lookups (the intensity
+// range is spatially coherent, so they mostly hit L1), one 8-byte store; the
+// caller guarantees 8-block alignment of the three pointers for the vector
+// part, a scalar tail covers nb % 8.
 template <typename T>
+struct Vec8;
+template <>
+struct Vec8<uint8_t> {
+    using type = uint2;
+};
+template <>
+struct Vec8<uint16_t> {
+    using type = uint4;
+};
+
+template <typename T, bool kSeed = false>
 __global__ void minmax_prefix_kernel(const T *__restrict__ mins, const T *__restrict__ maxs,
-                                     int64_t nb, const int32_t *__restrict__ prefix, uint8_t *out) {
+                                     int64_t nb, const int32_t *__restrict__ prefix, uint8_t *out,
+                                     bool vec) {
+    using V = typename Vec8<T>::type;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < nb; c += stride)
-        out[c] = prefix[(uint32_t)maxs[c] + 1] - prefix[(uint32_t)mins[c]] > 0;
+    const int64_t nv = vec ? nb / 8 : 0;
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < nv; q += stride) {
+        V lo = __ldcs(reinterpret_cast<const V *>(mins) + q);
+        V hi = __ldcs(reinterpret_cast<const V *>(maxs) + q);
+        const T *l = reinterpret_cast<const T *>(&lo), *h = reinterpret_cast<const T *>(&hi);
+        uint32_t w[2];
+#pragma unroll
+        for (int half = 0; half < 2; ++half) {
+            uint32_t word = 0;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int i = half * 4 + e;
+                const bool occ = __ldg(prefix + (uint32_t)h[i] + 1) - __ldg(prefix + (uint32_t)l[i]) > 0;
+                const uint32_t byte = kSeed ? (occ ? 0u : (uint32_t)kDistClamp) : (uint32_t)occ;
+                word |= byte << (8 * e);
+            }
+            w[half] = word;
+        }
+        __stcs(reinterpret_cast<uint2 *>(out) + q, make_uint2(w[0], w[1]));
+    }
+    for (int64_t c = nv * 8 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < nb; c += stride) {
+        const bool occ = prefix[(uint32_t)maxs[c] + 1] - prefix[(uint32_t)mins[c]] > 0;
+        out[c] = kSeed ? (occ ? 0 : kDistClamp) : occ;
+    }
+}
+
+template <bool kSeed>
+static int launch_minmax_prefix(const void *mins, const void *maxs, int bits, int64_t nb,
+                                const int32_t *prefix, uint8_t *out, cudaStream_t s) {
+    const uintptr_t vb = bits == 8 ? 8 : 16;
+    const bool vec = (uintptr_t)mins % vb == 0 && (uintptr_t)maxs % vb == 0 &&
+                     (uintptr_t)out % 8 == 0;
+    const int grid = grid_for(vec ? ceil_div(nb, 8) : nb, 256, 8);
+    if (bits == 8)
+        minmax_prefix_kernel<uint8_t, kSeed><<<grid, 256, 0, s>>>(
+            (const uint8_t *)mins, (const uint8_t *)maxs, nb, prefix, out, vec);
+    else
+        minmax_prefix_kernel<uint16_t, kSeed><<<grid, 256, 0, s>>>(
+            (const uint16_t *)mins, (const uint16_t *)maxs, nb, prefix, out, vec);
+    return cuda_status("minmax_prefix_kernel");
 }
 
 template <typename T>
@@ -319,11 +400,11 @@ extern "C" int pdm_partition_mask_voxel(const void *vox, int bits, int64_t nx, i
     const int threads = 256;
     const int grid = grid_for(nb, threads, 8);
     if (bits == 8)
-        block_lut_generic_kernel<8, false><<<grid, threads, 0, s>>>(
+        block_lut_generic_kernel<8, 0><<<grid, threads, 0, s>>>(
             (const uint8_t *)vox, nx, ny, nz, b, d.bx, d.by, d.bz, pid, nullptr, mask, words,
             nullptr);
     else
-        block_lut_generic_kernel<16, false><<<grid, threads, 0, s>>>(
+        block_lut_generic_kernel<16, 0><<<grid, threads, 0, s>>>(
             (const uint16_t *)vox, nx, ny, nz, b, d.bx, d.by, d.bz, pid, nullptr, mask, words,
             nullptr);
     return cuda_status("block_lut_generic_kernel");
@@ -346,10 +427,10 @@ extern "C" int pdm_block_any_lut(const void *vox, int bits, int64_t nx, int64_t 
     const int threads = 256;
     const int grid = grid_for(nb, threads, 8);
     if (bits == 8)
-        block_lut_generic_kernel<8, true><<<grid, threads, 0, s>>>(
+        block_lut_generic_kernel<8, 1><<<grid, threads, 0, s>>>(
             (const uint8_t *)vox, nx, ny, nz, b, d.bx, d.by, d.bz, nullptr, lut, nullptr, 0, out);
     else
-        block_lut_generic_kernel<16, true><<<grid, threads, 0, s>>>(
+        block_lut_generic_kernel<16, 1><<<grid, threads, 0, s>>>(
             (const uint16_t *)vox, nx, ny, nz, b, d.bx, d.by, d.bz, nullptr, lut, nullptr, 0, out);
     return cuda_status("block_lut_generic_kernel");
 }
@@ -443,17 +524,8 @@ extern "C" int pdm_occupancy_minmax_prefix(const void *mins, const void *maxs, i
     PDM_REQUIRE(mins && maxs && prefix && out, "pdm_occupancy_minmax_prefix: null pointer");
     PDM_REQUIRE(bits == 8 || bits == 16, "pdm_occupancy_minmax_prefix: bits");
     PDM_REQUIRE(nblocks >= 1, "pdm_occupancy_minmax_prefix: nblocks");
-    cudaStream_t s = as_stream(stream);
-    const int grid = grid_for(nblocks, 256, 8);
-    if (bits == 8)
-        minmax_prefix_kernel<uint8_t><<<grid, 256, 0, s>>>((const uint8_t *)mins,
-                                                           (const uint8_t *)maxs, nblocks, prefix,
-                                                           out);
-    else
-        minmax_prefix_kernel<uint16_t><<<grid, 256, 0, s>>>((const uint16_t *)mins,
-                                                            (const uint16_t *)maxs, nblocks,
-                                                            prefix, out);
-    return cuda_status("minmax_prefix_kernel");
+    return launch_minmax_prefix<false>(mins, maxs, bits, nblocks, prefix, out,
+                                       as_stream(stream));
 }
 
 extern "C" int pdm_minmax_fold(void *mins, void *maxs, const void *plane_mins,
@@ -472,4 +544,48 @@ extern "C" int pdm_minmax_fold(void *mins, void *maxs, const void *plane_mins,
                                                           (const uint16_t *)plane_mins,
                                                           (const uint16_t *)plane_maxs, count);
     return cuda_status("minmax_fold_kernel");
+}
+
+// acceleration.py:184-196 standard_distance_map, fused: the TF's occupancy is
+// written directly as the distance transform's {0, 255} seed (no bool map, no
+// expand pass), then the three passes run in place (dt.cu dt_from_seed).
+extern "C" int pdm_standard_distance_map_voxel(const void *vox, int bits, int64_t nx, int64_t ny,
+                                               int64_t nz, int32_t b, const uint8_t *lut,
+                                               uint8_t *out, pdm_stream_t stream) {
+    Dims d;
+    int st = check_volume("pdm_standard_distance_map_voxel", vox, bits, nx, ny, nz, b, &d);
+    if (st) return st;
+    PDM_REQUIRE(lut && out, "pdm_standard_distance_map_voxel: null pointer");
+    cudaStream_t s = as_stream(stream);
+    if (fast_ok(bits, nz, b, vox)) {
+        st = bits == 8 ? dispatch_lut_fast<8, 2, 1>(b, vox, nx, ny, nz, d.bx, d.by, d.bz, nullptr, lut, nullptr, out, s)
+                       : dispatch_lut_fast<16, 2, 1>(b, vox, nx, ny, nz, d.bx, d.by, d.bz, nullptr, lut, nullptr, out, s);
+    } else {
+        const int grid = grid_for(d.bx * d.by * d.bz, 256, 8);
+        if (bits == 8)
+            block_lut_generic_kernel<8, 2><<<grid, 256, 0, s>>>(
+                (const uint8_t *)vox, nx, ny, nz, b, d.bx, d.by, d.bz, nullptr, lut, nullptr, 0,
+                out);
+        else
+            block_lut_generic_kernel<16, 2><<<grid, 256, 0, s>>>(
+                (const uint16_t *)vox, nx, ny, nz, b, d.bx, d.by, d.bz, nullptr, lut, nullptr, 0,
+                out);
+        st = cuda_status("block_lut_generic_kernel");
+    }
+    if (st) return st;
+    return dt_from_seed("pdm_standard_distance_map_voxel", d.bx, d.by, d.bz, out, s);
+}
+
+extern "C" int pdm_standard_distance_map_minmax(const void *mins, const void *maxs, int bits,
+                                                int64_t bx, int64_t by, int64_t bz,
+                                                const int32_t *prefix, uint8_t *out,
+                                                pdm_stream_t stream) {
+    const char *fn = "pdm_standard_distance_map_minmax";
+    PDM_REQUIRE(mins && maxs && prefix && out, "%s: null pointer", fn);
+    PDM_REQUIRE(bits == 8 || bits == 16, "%s: bits", fn);
+    PDM_REQUIRE(bx >= 1 && by >= 1 && bz >= 1, "%s: bad sizes", fn);
+    cudaStream_t s = as_stream(stream);
+    int st = launch_minmax_prefix<true>(mins, maxs, bits, bx * by * bz, prefix, out, s);
+    if (st) return st;
+    return dt_from_seed(fn, bx, by, bz, out, s);
 }

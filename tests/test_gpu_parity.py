@@ -153,6 +153,67 @@ def test_select_combine_and_recompute(case, mode):
         assert np.array_equal(std.dist, c[f"tf_{t}_std_{mode}"]), (t, mode)
 
 
+def test_fused_recompute_matches_composition(case):
+    """standard_distance_map runs fused (occupancy written as the DT seed);
+    it must equal distance_transform(occupancy_for_tf(...)) and the golden,
+    with minmax omitted, given on the device, or given as host arrays."""
+    c, vol, grid, _ = case
+    mm_dev = pdm.block_min_max_device(vol, grid)
+    mm_host = pdm.block_min_max(vol, grid)
+    for t in tf_names(c):
+        tf = _tf(c[f"tf_{t}_alpha"])
+        for mode in ("voxel", "range_apron"):
+            want = c[f"tf_{t}_std_{mode}"]
+            comp = pdm.distance_transform(pdm.occupancy_for_tf(vol, grid, tf, mode))
+            assert np.array_equal(comp.dist, want), (t, mode)
+            for mm in (None, mm_dev, mm_host):
+                got = pdm.standard_distance_map(vol, grid, tf, mode, minmax=mm)
+                assert np.array_equal(got.dist, want), (t, mode, type(mm))
+
+
+def test_recompute_minmax_shape_mismatch():
+    vol = pdm.Volume.from_array(np.zeros((8, 8, 8), np.uint8))
+    grid = pdm.BlockGrid.for_dims(vol.dims, 4)
+    bad = (np.zeros((2, 2, 1), np.uint8), np.zeros((2, 2, 1), np.uint8))
+    tf = pdm.tf_archetype("tf1", 8)
+    with pytest.raises(ValueError):
+        pdm.standard_distance_map(vol, grid, tf, "range_apron", minmax=bad)
+    with pytest.raises(ValueError):
+        pdm.occupancy_for_tf(vol, grid, tf, "range_apron", minmax=bad)
+
+
+@pytest.mark.parametrize("span", [1, 7, 1024, 1025, 8191, 8192, 8193, 40000, 65536])
+def test_alpha_support_kernel(span):
+    """pdm_alpha_support against numpy: nz = alpha > 0 (NaN transparent,
+    denormals visible) and prefix = [0] + cumsum(nz) (acceleration.py:166,171),
+    for spans that end inside a tile, on a tile and on a batch boundary, and
+    for a strided alpha (the LUT's column 3)."""
+    import torch
+
+    from paper_2407_21552_b200 import _lib
+
+    rng = np.random.default_rng(span)
+    lut = np.zeros((span, 4))
+    a = np.where(rng.random(span) < 0.3, rng.random(span), 0.0)
+    a[rng.random(span) < 0.01] = np.nan
+    a[rng.random(span) < 0.01] = 5e-324
+    lut[:, 3] = a
+    L = _lib.lib()
+    dev = torch.from_numpy(lut).cuda()
+    alpha = dev[:, 3]
+    nz = torch.empty(span, dtype=torch.uint8, device="cuda")
+    prefix = torch.full((span + 1,), -1, dtype=torch.int32, device="cuda")
+    _lib.check(L.pdm_alpha_support(_lib.ptr(alpha), span, alpha.stride(0), _lib.ptr(nz),
+                                   _lib.ptr(prefix), _lib.stream_handle()), "alpha_support")
+    want = (a > 0.0).astype(np.uint8)
+    assert np.array_equal(nz.cpu().numpy(), want)
+    assert np.array_equal(prefix.cpu().numpy(), np.concatenate(([0], np.cumsum(want))))
+    nz2 = torch.empty(span, dtype=torch.uint8, device="cuda")
+    _lib.check(L.pdm_alpha_support(_lib.ptr(alpha), span, alpha.stride(0), _lib.ptr(nz2), None,
+                                   _lib.stream_handle()), "alpha_support")
+    assert np.array_equal(nz2.cpu().numpy(), want)
+
+
 def test_worked_example():
     with np.load(GOLDEN / "worked_example.npz") as z:
         scheme = _scheme([tuple(map(int, r)) for r in z["bounds"]])
