@@ -547,7 +547,7 @@ def combine(pdm_set: PdmSet, selection: PartitionSelection,
                                  host_produce if use_host_packed else None)
 
 
-_HOST_PIECE_ITEMS = 1 << 17  # 32-block items per pipelined piece (4 pieces at config c)
+_HOST_PIECE_ITEMS = 1 << 18  # 32-block items per pipelined piece (2 pieces at config c)
 _HOST_PACKED_MIN_BLOCKS = 1 << 22  # below ~4 MB of D' PCIe time is small: raw zero-copy
 
 

@@ -182,12 +182,24 @@ static void sparse_region_sse(const uint8_t *r, int64_t chunks, uint8_t *out, in
     }
 }
 
+// kNT: non-temporal 64-byte stores (out 64-byte aligned): no read-for-
+// ownership of the 16.8 MB destination, which the plain stores pay.
+template <bool kNT>
+__attribute__((target("avx2,avx512f,avx512bw,avx512vl,avx512vbmi,avx512vbmi2"))) static inline void
+store64(uint8_t *p, __m512i v) {
+    if (kNT)
+        _mm512_stream_si512(reinterpret_cast<__m512i *>(p), v);
+    else
+        _mm512_storeu_si512(reinterpret_cast<void *>(p), v);
+}
+
+template <bool kNT>
 __attribute__((target("avx2,avx512f,avx512bw,avx512vl,avx512vbmi,avx512vbmi2"))) static void
 sparse_region_vbmi2(const uint8_t *r, uint8_t *out) {
     const RegionHead h(r);
     if (h.nz == 0) {  // all-zero region (occupied space)
         const __m512i z = _mm512_setzero_si512();
-        for (int i = 0; i < 16; ++i) _mm512_storeu_si512(reinterpret_cast<void *>(out + 64 * i), z);
+        for (int i = 0; i < 16; ++i) store64<kNT>(out + 64 * i, z);
         return;
     }
     alignas(64) uint8_t ctl[64];
@@ -210,6 +222,13 @@ sparse_region_vbmi2(const uint8_t *r, uint8_t *out) {
             _mm512_mask_expandloadu_epi32(_mm512_set1_epi32((int)kFlatCode), m, cp);
         cp += 4 * __builtin_popcount(m);
         for (int q = 0; q < 4; ++q) {  // 4 chunks per vector
+            const int c0 = 16 * g + 4 * q;  // first chunk of this vector
+            const __m512i bv = _mm512_permutexvar_epi8(
+                _mm512_add_epi8(bsel, _mm512_set1_epi8((char)c0)), bases);
+            if (((m >> (4 * q)) & 0xFu) == 0) {  // 4 flat / zero chunks: their bases
+                store64<kNT>(out + 16 * c0, bv);
+                continue;
+            }
             __m128i c4q;
             switch (q) {
                 case 0: c4q = _mm512_extracti32x4_epi32(codes, 0); break;
@@ -223,15 +242,12 @@ sparse_region_vbmi2(const uint8_t *r, uint8_t *out) {
             src = _mm512_mask_srli_epi64(src, 0xAA, src, 16);
             __m512i x = _mm512_multishift_epi64_epi8(vctl, src);
             x = _mm512_sub_epi8(_mm512_and_si512(x, three), one);
-            const int c0 = 16 * g + 4 * q;  // first chunk of this vector
-            const __m512i bv = _mm512_permutexvar_epi8(
-                _mm512_add_epi8(bsel, _mm512_set1_epi8((char)c0)), bases);
             x = _mm512_mask_blend_epi8(first, x, bv);
             x = _mm512_add_epi8(x, _mm512_bslli_epi128(x, 1));
             x = _mm512_add_epi8(x, _mm512_bslli_epi128(x, 2));
             x = _mm512_add_epi8(x, _mm512_bslli_epi128(x, 4));
             x = _mm512_add_epi8(x, _mm512_bslli_epi128(x, 8));
-            _mm512_storeu_si512(reinterpret_cast<void *>(out + 16 * c0), x);
+            store64<kNT>(out + 16 * c0, x);
         }
     }
 }
@@ -242,21 +258,49 @@ static bool have_avx512vbmi2() {
 }
 }  // namespace
 
-extern "C" int pdm_unpack_sparse_host(const uint8_t *regions, int64_t map_bytes, uint8_t *out) {
-    REQUIRE(regions && out && map_bytes >= 1, "pdm_unpack_sparse_host: bad arguments");
-    const int64_t chunks = (map_bytes + 15) / 16;
-    const int64_t nreg = (chunks + 63) / 64;
-    const int64_t tail = map_bytes - 16 * (chunks - 1);  // bytes of the last chunk
-    const bool vec = have_avx512vbmi2() && getenv("PDM_NO_AVX512") == nullptr;
-    // dynamic: coded regions cluster in space (surfaces), zero ones in bulk
-#pragma omp parallel for schedule(dynamic, 64)
-    for (int64_t w = 0; w < nreg; ++w) {
+namespace {
+// One region of the sparse form into out + 1024 w (the last region may be
+// partial: SSE path with the tail length).
+struct SparseExpand {
+    const uint8_t *regions;
+    uint8_t *out;
+    int64_t map_bytes, chunks, nreg, tail;
+    bool vec, nt;
+    SparseExpand(const uint8_t *r, int64_t bytes, uint8_t *o) : regions(r), out(o), map_bytes(bytes) {
+        chunks = (map_bytes + 15) / 16;
+        nreg = (chunks + 63) / 64;
+        tail = map_bytes - 16 * (chunks - 1);  // bytes of the last chunk
+        vec = have_avx512vbmi2() && getenv("PDM_NO_AVX512") == nullptr;
+        static const bool nt_env = [] {
+            const char *e = getenv("PDM_UNPACK_NT");
+            return e == nullptr || e[0] != '0';
+        }();
+        nt = vec && nt_env && ((uintptr_t)out & 63) == 0;
+    }
+    void operator()(int64_t w) const {
         const bool full = 1024 * (w + 1) <= map_bytes;
-        if (vec && full)
-            sparse_region_vbmi2(regions + kRegion * w, out + 1024 * w);
-        else
+        if (vec && full) {
+            if (nt)
+                sparse_region_vbmi2<true>(regions + kRegion * w, out + 1024 * w);
+            else
+                sparse_region_vbmi2<false>(regions + kRegion * w, out + 1024 * w);
+        } else {
             sparse_region_sse(regions + kRegion * w, w + 1 < nreg ? 64 : chunks - 64 * w,
                               out + 1024 * w, w + 1 < nreg ? 16 : tail);
+        }
+    }
+};
+}  // namespace
+
+extern "C" int pdm_unpack_sparse_host(const uint8_t *regions, int64_t map_bytes, uint8_t *out) {
+    REQUIRE(regions && out && map_bytes >= 1, "pdm_unpack_sparse_host: bad arguments");
+    const SparseExpand ex(regions, map_bytes, out);
+    // dynamic: coded regions cluster in space (surfaces), zero ones in bulk
+#pragma omp parallel
+    {
+#pragma omp for schedule(dynamic, 64) nowait
+        for (int64_t w = 0; w < ex.nreg; ++w) ex(w);
+        if (ex.nt) _mm_sfence();  // streaming stores visible before the caller reads out
     }
     return PDM_OK;
 }

@@ -107,9 +107,16 @@ def host_buffer(shape) -> np.ndarray:
     pool = _HOST_POOL.setdefault(nbytes, [])
     for buf in pool:
         # references: the pool list, the loop variable, getrefcount's argument
+        # (every view handed out has buf itself as its .base)
         if sys.getrefcount(buf) == 3:
-            return buf.reshape(shape)
-    buf = np.empty(nbytes, dtype=np.uint8)
+            return _aligned_view(buf, nbytes, shape)
+    buf = np.empty(nbytes + 64, dtype=np.uint8)
     if len(pool) < _HOST_POOL_CAP:
         pool.append(buf)
-    return buf.reshape(shape)
+    return _aligned_view(buf, nbytes, shape)
+
+
+def _aligned_view(buf: np.ndarray, nbytes: int, shape) -> np.ndarray:
+    """64-byte aligned start (the host expansion streams whole cache lines)."""
+    off = (-buf.ctypes.data) % 64
+    return buf[off:off + nbytes].reshape(shape)

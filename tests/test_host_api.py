@@ -339,16 +339,24 @@ def test_unpack_sparse_host_matches_numpy_encoder(monkeypatch, avx512):
         monkeypatch.setenv("PDM_NO_AVX512", "1")
     L = _lib.load_library()
     rng = np.random.default_rng(23)
+    from paper_2407_21552_b200 import device
+
     for nb in (1, 16, 17, 1000, 1024, 1025, 4096 + 7, 1 << 16):
         chunks = 64 * (-(-nb // 1024))
-        kind = rng.choice(3, chunks, p=[0.4, 0.3, 0.3])          # zero / flat / coded
-        steps = rng.integers(-1, 2, (chunks, 16))
-        steps[kind != 2] = 0
-        start = rng.choice([0, 1, 37, 254, 255], chunks)
-        start[kind == 0] = 0
-        vals = np.clip(start[:, None] + np.cumsum(steps, 1) - steps[:, :1], 0, 255)
-        regions = _sparse_regions(vals)
-        out = np.full(nb + 16, 0xAB, np.uint8)
-        assert L.pdm_unpack_sparse_host(regions.ctypes.data, nb, out.ctypes.data) == _lib.PDM_OK
-        assert np.array_equal(out[:nb], vals.reshape(-1)[:nb].astype(np.uint8)), nb
-        assert (out[nb:] == 0xAB).all(), nb  # nothing written past map_bytes
+        for runs in (1, 8):  # runs of 8: whole 4-chunk vectors flat / zero (fast path)
+            kind = np.repeat(rng.choice(3, chunks // runs, p=[0.4, 0.3, 0.3]), runs)
+            steps = rng.integers(-1, 2, (chunks, 16))             # zero / flat / coded
+            steps[kind != 2] = 0
+            start = rng.choice([0, 1, 37, 254, 255], chunks)
+            start[kind == 0] = 0
+            vals = np.clip(start[:, None] + np.cumsum(steps, 1) - steps[:, :1], 0, 255)
+            regions = _sparse_regions(vals)
+            # unaligned destination (plain stores) and a 64-byte aligned one
+            # (non-temporal stores on AVX-512 hosts)
+            buf = device.host_buffer((nb + 64 + 16,))
+            for out in (buf[1:nb + 17], buf[(-buf.ctypes.data) % 64:][:nb + 16]):
+                out[:] = 0xAB
+                assert L.pdm_unpack_sparse_host(regions.ctypes.data, nb,
+                                                out.ctypes.data) == _lib.PDM_OK
+                assert np.array_equal(out[:nb], vals.reshape(-1)[:nb].astype(np.uint8)), nb
+                assert (out[nb:] == 0xAB).all(), nb  # nothing written past map_bytes

@@ -21,7 +21,8 @@ def main():
     nb = grid.num_blocks
     chunks = int(L.pdm_packed_chunks(nb))
     sel = np.ascontiguousarray(np.arange(0, 32, 2), dtype=np.int32)  # k = 16
-    out = np.empty(nb, np.uint8)
+    from paper_2407_21552_b200 import device
+    out = device.host_buffer((nb,))  # 64-byte aligned, as .dist gets
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     st = _lib.stream_handle()
 
@@ -45,6 +46,13 @@ def main():
         _lib.ptr(nib_h), _lib.ptr(base_h), nb, out.ctypes.data))
     res["unpack_delta_only"] = timed(lambda: L.pdm_unpack_delta_host(
         _lib.ptr(nib_h), _lib.ptr(base_h), nb, out.ctypes.data))
+    for pieces in (1, 2, 4, 8, 16):  # 3 = sparse delta D' (the default)
+        res[f"pipeline_f3_{pieces}"] = timed(lambda: L.pdm_merge_packed_to_host(
+            _lib.ptr(nib), nib_pitch, _lib.ptr(base), base_pitch, nb, 32, None,
+            sel.ctypes.data, 16, _lib.ptr(nib_h), _lib.ptr(base_h), out.ctypes.data,
+            pieces, 3, st))
+    res["unpack_sparse_only"] = timed(lambda: L.pdm_unpack_sparse_host(
+        _lib.ptr(nib_h), nb, out.ctypes.data))
     for fmt in (1, 2):  # 1 = nibble D', 2 = 2-bit delta D'
         for pieces in (1, 2, 4, 8):
             res[f"pipeline_f{fmt}_{pieces}"] = timed(lambda: L.pdm_merge_packed_to_host(
