@@ -14,6 +14,14 @@ python bench.py --impl reference > "$o/bench_reference.jsonl" 2> "$o/bench_refer
 python tools/precompute_bench.py > "$o/precompute.json" 2>&1; echo "pre rc=$?" >> "$o/status.txt"
 python tools/merge_microbench.py --packed > "$o/merge_microbench.json" 2>&1; echo "mb rc=$?" >> "$o/status.txt"
 python tools/configs_bench.py --cpu > "$o/configs.jsonl" 2>&1; echo "cfg rc=$?" >> "$o/status.txt"
+python tools/recompute_probe.py > "$o/recompute_probe.json" 2>&1; echo "recompute rc=$?" >> "$o/status.txt"
+python tools/host_path_probe.py > "$o/host_path_probe.json" 2>&1; echo "host path rc=$?" >> "$o/status.txt"
+python tools/render_bench.py --reps 5 > "$o/render_bench.json" 2>&1; echo "render rc=$?" >> "$o/status.txt"
+# launch list of the fused recompute (standard_distance_map, both modes)
+python tools/exp/recompute_once.py && \
+  ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
+      --log-file "$o/recompute_launches.csv" python tools/exp/recompute_once.py \
+      > "$o/ncu_recompute.log" 2>&1; echo "ncu recompute rc=$?" >> "$o/status.txt"
 # launch list of a short bench run (cold-cache, serialised)
 python bench.py --steps 32 --warmup 3 --no-cpu-baseline > "$o/bench_short.jsonl" 2>&1 && \
   ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv \
