@@ -12,6 +12,7 @@
 #include <cuda_runtime.h>
 
 #include <cstring>
+#include <mutex>
 #include <string>
 
 #include <cuda_fp16.h>
@@ -48,6 +49,32 @@ int sm_count() {
         n = 148;
     if (dev >= 0 && dev < 64) cached[dev] = n;
     return n;
+}
+
+int resident_ctas(const void *kernel, int threads, size_t smem) {
+    struct Slot {
+        const void *k;
+        int threads;
+        size_t smem;
+        int dev, per_sm;
+    };
+    static std::mutex mu;  // ctypes callers may come from several host threads
+    static Slot slots[64];
+    static int used = 0;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lock(mu);
+    for (int i = 0; i < used; ++i)
+        if (slots[i].k == kernel && slots[i].threads == threads && slots[i].smem == smem &&
+            slots[i].dev == dev)
+            return slots[i].per_sm;
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem) !=
+            cudaSuccess ||
+        per_sm < 1)
+        per_sm = 1;
+    if (used < 64) slots[used++] = Slot{kernel, threads, smem, dev, per_sm};
+    return per_sm;
 }
 
 // ---------------------------------------------------------------------------

@@ -38,6 +38,9 @@ int cuda_status(const char *where);  // checks cudaGetLastError after a launch
 inline cudaStream_t as_stream(pdm_stream_t s) { return reinterpret_cast<cudaStream_t>(s); }
 
 int sm_count();  // cached SM count of the current device
+// Resident CTAs per SM of a kernel at (threads, dynamic smem), cached per
+// (kernel, threads, smem); at least 1.
+int resident_ctas(const void *kernel, int threads, size_t smem);
 
 // dt.cu: the three Chebyshev passes in place over one {0, 255}-seeded map
 // (the tail of pdm_distance_transform, shared with the fused recompute).
