@@ -37,4 +37,8 @@ python tools/precompute_bench.py --reps 1 > /dev/null 2>&1 && \
       -k "regex:dt_tile_kernel|dt_dist1d_wide|apron_fast|pack_kernel|dt_expand" -c 8 \
       -o "$o/precompute_full" python tools/precompute_bench.py --reps 1 \
       > "$o/ncu_pre.log" 2>&1; echo "ncu pre rc=$?" >> "$o/status.txt"
+# full capture of the voxel block scan (fused recompute's volume pass)
+ncu --set full --clock-control none --import-source on -k regex:block_lut_fast -c 1 \
+    -o "$o/blocklut_full" python tools/exp/recompute_once.py \
+    > "$o/ncu_blocklut.log" 2>&1; echo "ncu blocklut rc=$?" >> "$o/status.txt"
 cat "$o/status.txt"
