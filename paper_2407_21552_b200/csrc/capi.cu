@@ -387,7 +387,38 @@ __global__ void volume_range_kernel(const T *__restrict__ vox, int64_t count,
                                     uint32_t *__restrict__ out) {
     uint32_t mn = 0xFFFFFFFFu, mx = 0;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += stride) {
+    const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    // 16-byte loads, 4 in flight per thread (a scalar loop ran at 3.9 TB/s);
+    // the vector part needs a 16-byte aligned base, the tail is scalar
+    constexpr int kPer = 16 / sizeof(T);
+    const int64_t nvec = ((uintptr_t)vox % 16 == 0) ? count / kPer : 0;
+    const uint4 *v4 = reinterpret_cast<const uint4 *>(vox);
+    // packed lane-wise accumulators (4 u8 or 2 u16 lanes per word)
+    uint32_t pmn = 0xFFFFFFFFu, pmx = 0;
+    auto fold = [&](uint4 q) {
+        const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            pmn = sizeof(T) == 1 ? __vminu4(pmn, w[k]) : __vminu2(pmn, w[k]);
+            pmx = sizeof(T) == 1 ? __vmaxu4(pmx, w[k]) : __vmaxu2(pmx, w[k]);
+        }
+    };
+    int64_t q = t0;
+    for (; q + 3 * stride < nvec; q += 4 * stride) {
+        const uint4 a = __ldcs(v4 + q), b = __ldcs(v4 + q + stride), c = __ldcs(v4 + q + 2 * stride),
+                    d = __ldcs(v4 + q + 3 * stride);
+        fold(a), fold(b), fold(c), fold(d);
+    }
+    for (; q < nvec; q += stride) fold(__ldcs(v4 + q));
+    if (sizeof(T) == 1) {
+        pmn = __vminu4(pmn, pmn >> 16), pmx = __vmaxu4(pmx, pmx >> 16);
+        mn = min(pmn & 0xFFu, (pmn >> 8) & 0xFFu);
+        mx = max(pmx & 0xFFu, (pmx >> 8) & 0xFFu);
+    } else {
+        mn = min(pmn & 0xFFFFu, pmn >> 16);
+        mx = max(pmx & 0xFFFFu, pmx >> 16);
+    }
+    for (int64_t i = nvec * kPer + t0; i < count; i += stride) {
         const uint32_t v = vox[i];
         mn = v < mn ? v : mn;
         mx = v > mx ? v : mx;
@@ -428,23 +459,6 @@ __global__ void count_value_kernel(const uint8_t *__restrict__ data, int64_t byt
 __global__ void range_init_kernel(uint32_t *out) {
     out[0] = 0xFFFFFFFFu;
     out[1] = 0;
-}
-
-// Resident CTAs per SM of a kernel (cached per kernel), so a grid-stride merge
-// launches exactly one wave.
-template <class K>
-static int resident_ctas(K kernel, int threads) {
-    static int cached[64] = {0};
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (dev >= 0 && dev < 64 && cached[dev]) return cached[dev];
-    int per_sm = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, 0) !=
-            cudaSuccess ||
-        per_sm < 1)
-        per_sm = 1;
-    if (dev >= 0 && dev < 64) cached[dev] = per_sm;
-    return per_sm;
 }
 
 // One wave of resident CTAs; when the work does not fill it, just enough
@@ -567,7 +581,7 @@ extern "C" int pdm_combine(const uint8_t *pdms, int64_t plane_pitch, int64_t map
         memcpy(p.idx, sel + base, sizeof(int32_t) * p.k);
         const int acc = base > 0;
         if (vec) {
-            const int per_sm = resident_ctas(combine_kernel, kMergeThreads);
+            const int per_sm = resident_ctas((const void *)combine_kernel, kMergeThreads, 0);
             combine_kernel<<<merge_grid(map_bytes / 16 > 0 ? map_bytes / 16 : 1, per_sm,
                                         1),
                              kMergeThreads, 0, s>>>(pdms, plane_pitch, map_bytes, p, out, acc,
@@ -593,7 +607,7 @@ extern "C" int pdm_combine_flags(const uint8_t *pdms, int64_t plane_pitch, int64
                 "pdm_combine_flags: needs 16-byte aligned planes");
     // Programmatic dependent launch: the merge CTAs are scheduled while the
     // preceding select kernel finishes; they wait on griddepcontrol.wait.
-    const int per_sm = resident_ctas(combine_flags_kernel, kMergeThreads);
+    const int per_sm = resident_ctas((const void *)combine_flags_kernel, kMergeThreads, 0);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)merge_grid(map_bytes / 16 > 0 ? map_bytes / 16 : 1, per_sm, 1));
     cfg.blockDim = dim3(kMergeThreads);

@@ -643,3 +643,33 @@ def test_merge_fused_zero_count(monkeypatch):
         want = np.minimum.reduce([pset.pdms[i - 1].dist for i in s])
         assert dm.occupied_fraction == np.count_nonzero(want == 0) / want.size, s
         assert np.array_equal(dm.dist, want), s
+
+
+@pytest.mark.parametrize("bits", [8, 16])
+def test_volume_range_kernel(bits):
+    """pdm_volume_range (Volume.intensity_range of a device volume,
+    volume.py:86-90): 16-byte vector body, scalar tail, unaligned start; the
+    extremes placed in the tail, in the body and at the first voxel."""
+    import torch
+
+    from paper_2407_21552_b200 import _lib
+
+    L = _lib.lib()
+    dt = np.uint8 if bits == 8 else np.uint16
+    top = (1 << bits) - 1
+    rng = np.random.default_rng(bits)
+    for count in (1, 7, 8, 17, 1000, 4096 + 3, 1 << 20):
+        for where in ("body", "tail", "first"):
+            h = rng.integers(10, top - 10, count).astype(dt)
+            lo_i, hi_i = {"body": (count // 3, count // 2), "tail": (count - 1, count - 2),
+                          "first": (0, count // 2)}[where]
+            h[hi_i] = top - 3
+            h[lo_i] = 2
+            for off in (0, 1):  # off 1: the base is not 16-byte aligned
+                buf = torch.from_numpy(np.concatenate([np.full(off, 5, dt), h])).cuda()
+                src = buf[off:]
+                out = torch.empty(2, dtype=torch.int32, device="cuda")
+                _lib.check(L.pdm_volume_range(_lib.ptr(src), bits, count, _lib.ptr(out),
+                                              _lib.stream_handle()), "range")
+                got = tuple(int(v) for v in out.cpu().numpy().view(np.uint32))
+                assert got == (int(h.min()), int(h.max())), (count, where, off)
