@@ -504,8 +504,13 @@ extern "C" int pdm_volume_range(const void *vox, int bits, int64_t count, uint32
     PDM_REQUIRE((bits == 8 || bits == 16) && count >= 1, "pdm_volume_range: bad args");
     cudaStream_t s = as_stream(stream);
     range_init_kernel<<<1, 1, 0, s>>>(out);
-    int64_t grid = ceil_div(count, 256);
-    const int64_t cap = (int64_t)sm_count() * 8;
+    // one wave of resident CTAs, vector items (16 bytes) per thread
+    int64_t grid = ceil_div(ceil_div(count * (bits / 8), 16), 256);
+    const int64_t cap =
+        (int64_t)sm_count() *
+        resident_ctas(bits == 8 ? (const void *)volume_range_kernel<uint8_t>
+                                : (const void *)volume_range_kernel<uint16_t>,
+                      256, 0);
     if (grid > cap) grid = cap;
     if (bits == 8)
         volume_range_kernel<uint8_t><<<(unsigned)grid, 256, 0, s>>>((const uint8_t *)vox, count, out);

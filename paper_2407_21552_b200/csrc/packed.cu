@@ -685,7 +685,8 @@ extern "C" int pdm_pack_pdms(const uint8_t *pdms, int64_t plane_pitch, int64_t m
     cudaStream_t s = as_stream(stream);
     PDM_CUDA_TRY(cudaMemsetAsync(violations, 0, sizeof(uint32_t), s));
     int64_t grid = ceil_div((int64_t)n * nchunks, 256);
-    const int64_t cap = (int64_t)sm_count() * 8;
+    // one wave of resident CTAs (47 registers: 5 per SM, not 8)
+    const int64_t cap = (int64_t)sm_count() * resident_ctas((const void *)pack_kernel, 256, 0);
     if (grid > cap) grid = cap;
     pack_kernel<<<(unsigned)grid, 256, 0, s>>>(pdms, plane_pitch, map_bytes, n, nchunks, nib,
                                                nib_pitch, base, base_pitch, violations);
