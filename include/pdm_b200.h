@@ -172,6 +172,22 @@ int pdm_merge_packed_to_host(const uint8_t *nib, int64_t nib_pitch, const uint8_
                              uint8_t *stage_nib, uint8_t *stage_base, uint8_t *out,
                              int32_t pieces, int32_t format, pdm_stream_t stream);
 
+/* DistanceMap.dist for a finished D' in HBM (acceleration.py:71-79 host view;
+ * combine() itself completes D' on the device, acceleration.py:244-276): D'
+ * (map_bytes plain bytes, 16-byte aligned) is re-encoded in `pieces` launches
+ * in compact form `format` (1 nibbles, 2 deltas, 3 sparse deltas; staging as
+ * in pdm_merge_packed_to_host) straight into pinned host staging, and the
+ * host expands piece i into `out` while later pieces cross PCIe.  Formats 2
+ * and 3 require D' to be 1-Lipschitz along z within 16-block chunks (a min of
+ * distance fields with bz % 16 == 0).  Returns once `out` is complete. */
+int pdm_dprime_to_host(const uint8_t *d, int64_t map_bytes, uint8_t *stage, uint8_t *stage_base,
+                       uint8_t *out, int32_t pieces, int32_t format, pdm_stream_t stream);
+
+/* Host function: dst[i] = src[i * stride] for i < n (OpenMP) -- stages a
+ * TF's alpha column lut[:, 3] (transfer.py:44-70) into pinned memory for the
+ * select upload (transfer.py:250-259 reads tf.lut on every call). */
+int pdm_gather_f64_host(const double *src, int64_t n, int64_t stride, double *dst);
+
 /* ---- block reduction / occupancy (K1-K5) --------------------------------- */
 
 /* volume.py:289-300 block_min_max: per-block min/max over the block grown by a

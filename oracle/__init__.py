@@ -254,6 +254,39 @@ def synth_volume(bits: int, dims, boxes: np.ndarray, seed: int, x_range=None) ->
     return out
 
 
+def build_pdm_set_synth(bits: int, dims, boxes: np.ndarray, seed: int, b: int, bounds,
+                        mode: str = "range_apron", slab_voxels: int = 256) -> np.ndarray:
+    """acceleration.py:199-241 on the shared hash-box volume, generated and
+    reduced one x-slab at a time so a 2048^3 volume (17 GB) is never held
+    whole: each slab's block occupancy is computed on the slab grown by one
+    block per side (range_apron: the 1-voxel apron of the slab's edge blocks
+    lies in the neighbour slab; block_min_max clips only at the real volume
+    ends, volume.py:289-300), stitched into [n, bx, by, bz], then the
+    per-partition distance transforms run on the whole grid.  Identical to
+    build_pdm_set(synth_volume(...)) -- tested at small sizes."""
+    nx = int(dims[0])
+    n = len(bounds)
+    bd = _bdims(dims, b)
+    occs = np.zeros((n,) + bd, dtype=np.uint8)
+    step = max(b, (int(slab_voxels) // b) * b)
+    pid = pid_lut(bounds)
+    for x0 in range(0, nx, step):
+        x1 = min(nx, x0 + step)
+        bx0, bx1 = x0 // b, -(-x1 // b)
+        if mode == "voxel":
+            vox = synth_volume(bits, dims, boxes, seed, x_range=(x0, x1))
+            occs[:, bx0:bx1] = partition_presence(vox, b, pid, n)
+        else:
+            lo, hi = max(0, x0 - b), min(nx, x1 + b)
+            vox = synth_volume(bits, dims, boxes, seed, x_range=(lo, hi))
+            mins, maxs = block_min_max(vox, b)
+            off = (x0 - lo) // b
+            occs[:, bx0:bx1] = range_apron_presence(mins[off:off + bx1 - bx0],
+                                                    maxs[off:off + bx1 - bx0], bounds)
+        del vox
+    return distance_transform_batch(occs)
+
+
 def march_rays(vox, lut, dist, b, step, ert_on, ert_thr, origin, dirs):
     """_kernels.py:206-365 -- (rgba float64 [n, 4], counters int64 [n, 4])."""
     vox = np.ascontiguousarray(vox)

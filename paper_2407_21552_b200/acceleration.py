@@ -74,8 +74,7 @@ class _BlockArray:
         self.bdims = tuple(int(v) for v in bdims)
         self._host = None
         self._dev = None
-        self._pending = None  # producer(out_tensor) for deferred results
-        self._pending_host = None  # producer(host ndarray), if the host view has its own path
+        self._host_fill = None  # fills the host view its own way (compact D' over PCIe)
         shape = tuple(data.shape)
         if shape != self.bdims:
             raise ValueError(f"{field} array shape does not match bdims")
@@ -84,51 +83,20 @@ class _BlockArray:
         else:
             self._dev = data
 
-    @classmethod
-    def _deferred(cls, b, bdims, producer, host_producer=None):
-        """A result whose kernel is launched on first access: into HBM for
-        .device(), or straight into pinned host memory for the host view (the
-        kernel's stores then stream over PCIe while it runs, so the
-        download costs no separate copy).  ``host_producer(ndarray)``, when
-        given, fills the host view its own way (e.g. a packed D' over PCIe,
-        expanded on the host)."""
-        self = cls.__new__(cls)
-        self.b = int(b)
-        self.bdims = tuple(int(v) for v in bdims)
-        self._host = None
-        self._dev = None
-        self._pending = producer
-        self._pending_host = host_producer
-        return self
-
     def _host_array(self):
         if self._host is None:
-            if self._dev is None and self._pending_host is not None:
+            if self._host_fill is not None:
                 host = device.host_buffer(self.bdims)  # recycled, already faulted in
-                self._pending_host(host)
+                self._host_fill(host)
                 self._host = host
-                return self._host
-            if self._dev is None and self._pending is not None:
-                t = device.torch()
-                host_t = t.empty(self.bdims, dtype=t.uint8, pin_memory=True)
-                if host_t.data_ptr() % 16 == 0:
-                    self._pending(host_t)
-                    t.cuda.current_stream().synchronize()
-                    self._host_t = host_t  # owns the pinned buffer behind the view
-                    host = host_t.numpy()
-                    self._host = host.astype(bool) if self._np_dtype == np.bool_ else host
-                    return self._host
-            self._host = device.to_host(self.device(), self._np_dtype)
+            else:
+                self._host = device.to_host(self.device(), self._np_dtype)
         return self._host
 
     def device(self):
         """uint8 CUDA tensor of shape bdims (uploaded on first use, then cached)."""
         if self._dev is None:
-            if self._pending is not None:
-                self._dev = device.empty(self.bdims, np.uint8)
-                self._pending(self._dev)
-            else:
-                self._dev = device.to_device(np.ascontiguousarray(self._host, dtype=np.uint8))
+            self._dev = device.to_device(np.ascontiguousarray(self._host, dtype=np.uint8))
         return self._dev
 
 
@@ -339,6 +307,7 @@ def occupancy_for_partition(volume: Volume, grid: BlockGrid, partition: Partitio
             _lib.ptr(mins), _lib.ptr(maxs), volume.bits, grid.num_blocks,
             min(partition.rho_lo, 0xFFFFFFFF), min(partition.rho_hi, 0xFFFFFFFF),
             _lib.ptr(out), st), "pdm_occupancy_minmax_range")
+    device.complete()
     return OccupancyMap(b=grid.b, bdims=grid.bdims, occupied=out)
 
 
@@ -395,6 +364,7 @@ def occupancy_for_tf(volume: Volume, grid: BlockGrid, tf: TransferFunction, mode
                                                  grid.num_blocks, _lib.ptr(prefix),
                                                  _lib.ptr(out), st),
                    "pdm_occupancy_minmax_prefix")
+    device.complete()
     return OccupancyMap(b=grid.b, bdims=grid.bdims, occupied=out)
 
 
@@ -406,6 +376,7 @@ def distance_transform(occ: OccupancyMap) -> DistanceMap:
     out = device.empty(occ.bdims, np.uint8)
     _lib.check(L.pdm_distance_transform(_lib.ptr(src), *occ.bdims, _lib.ptr(out),
                                         _lib.stream_handle()), "pdm_distance_transform")
+    device.complete()
     return DistanceMap(b=occ.b, bdims=occ.bdims, dist=out)
 
 
@@ -430,6 +401,7 @@ def standard_distance_map(volume: Volume, grid: BlockGrid, tf: TransferFunction,
                                                       volume.bits, *grid.bdims,
                                                       _lib.ptr(prefix), _lib.ptr(out), st),
                    "pdm_standard_distance_map_minmax")
+    device.complete()
     return DistanceMap(b=grid.b, bdims=grid.bdims, dist=out)
 
 
@@ -494,11 +466,12 @@ def combine(pdm_set: PdmSet, selection: PartitionSelection,
     map once; max_maps_per_pass is validated like the reference and does not
     change the result (the reference guarantees chunked == direct).
 
-    The merge is launched when the result is first used: ``.device()`` runs it
-    into HBM, ``.dist`` runs it straight into pinned host memory (zero-copy
-    stores over PCIe overlap the merge), so the reference's host-array
-    contract costs one PCIe transfer and no extra pass.  Use update_from_tf /
-    combine_flags_into for an eager device-resident result."""
+    Like the reference, the call returns a finished map: the merge runs into a
+    fresh HBM buffer (never aliasing a PDM) and the call waits for it.  The
+    host view ``.dist`` is made on first access: for large maps D' crosses
+    PCIe re-encoded in a compact form and is expanded on the host
+    (pdm_dprime_to_host).  update_from_tf / combine_flags_into are the
+    asynchronous, caller-buffer variants."""
     if selection.n != pdm_set.n:
         raise SelectionError(
             f"selection is over {selection.n} partitions, set holds {pdm_set.n}")
@@ -507,44 +480,39 @@ def combine(pdm_set: PdmSet, selection: PartitionSelection,
     if (flags is not None and selection._selected is None and max_maps_per_pass is None
             and pdm_set.n <= _MAX_FLAGS):
         # selection still on the device (select_partitions): no host round trip
-        def host_produce(host):
-            _packed_to_host(pdm_set, host, _lib.ptr(flags), None, 0)
+        out = device.empty(grid.bdims, np.uint8)
+        combine_flags_into(pdm_set, flags, out)
+    else:
+        indices = selection.sorted
+        if indices and max_maps_per_pass is not None and max_maps_per_pass < 1:
+            raise ValueError(f"max_maps_per_pass must be >= 1, got {max_maps_per_pass}")
+        sel = np.ascontiguousarray([i - 1 for i in indices], dtype=np.int32)
+        out = device.empty(grid.bdims, np.uint8)
+        _combine_indices(pdm_set, sel, out)
+    device.complete()
+    dm = DistanceMap(b=grid.b, bdims=grid.bdims, dist=out)
+    if _host_packed_pays(pdm_set):
+        dm._host_fill = lambda host: _dprime_to_host(pdm_set, out, host)
+    return dm
 
-        return DistanceMap._deferred(grid.b, grid.bdims,
-                                     lambda out: combine_flags_into(pdm_set, flags, out),
-                                     host_produce if _host_packed_pays(pdm_set) else None)
-    indices = selection.sorted
-    if indices and max_maps_per_pass is not None and max_maps_per_pass < 1:
-        raise ValueError(f"max_maps_per_pass must be >= 1, got {max_maps_per_pass}")
-    sel = np.ascontiguousarray([i - 1 for i in indices], dtype=np.int32)
 
-    def produce(out):
-        L = _lib.lib()
-        # The packed merge is for HBM destinations; into pinned host memory
-        # (zero-copy over PCIe) the raw merge's contiguous 512-byte warp stores
-        # measured faster (0.34 vs 0.42-1.1 ms per D' at config c).
-        packed = (pdm_set.packed() if 0 < sel.size <= _MAX_PACKED_SEL and out.is_cuda
-                  else None)
-        if packed is not None:
-            nib, nib_pitch, base, base_pitch = packed
-            _lib.check(L.pdm_combine_packed(_lib.ptr(nib), nib_pitch, _lib.ptr(base), base_pitch,
-                                            grid.num_blocks, pdm_set.n, sel.ctypes.data,
-                                            int(sel.size), _lib.ptr(out), None,
-                                            _lib.stream_handle()),
-                       "pdm_combine_packed")
-            return
-        storage = pdm_set.storage if sel.size else None
-        _lib.check(L.pdm_combine(_lib.ptr(storage) if storage is not None else None,
-                                 pdm_set.plane_pitch, grid.num_blocks, max(pdm_set.n, 1),
-                                 sel.ctypes.data if sel.size else None, int(sel.size),
-                                 _lib.ptr(out), _lib.stream_handle()), "pdm_combine")
-
-    def host_produce(host):
-        _packed_to_host(pdm_set, host, None, sel.ctypes.data, int(sel.size))
-
-    use_host_packed = 0 < sel.size <= _MAX_PACKED_SEL and _host_packed_pays(pdm_set)
-    return DistanceMap._deferred(grid.b, grid.bdims, produce,
-                                 host_produce if use_host_packed else None)
+def _combine_indices(pdm_set: PdmSet, sel: np.ndarray, out) -> None:
+    """K7 over a host index list (0-based), into ``out`` (enqueued only)."""
+    L = _lib.lib()
+    grid = pdm_set.grid
+    packed = pdm_set.packed() if 0 < sel.size <= _MAX_PACKED_SEL else None
+    if packed is not None:
+        nib, nib_pitch, base, base_pitch = packed
+        _lib.check(L.pdm_combine_packed(_lib.ptr(nib), nib_pitch, _lib.ptr(base), base_pitch,
+                                        grid.num_blocks, pdm_set.n, sel.ctypes.data,
+                                        int(sel.size), _lib.ptr(out), None,
+                                        _lib.stream_handle()), "pdm_combine_packed")
+        return
+    storage = pdm_set.storage if sel.size else None
+    _lib.check(L.pdm_combine(_lib.ptr(storage) if storage is not None else None,
+                             pdm_set.plane_pitch, grid.num_blocks, max(pdm_set.n, 1),
+                             sel.ctypes.data if sel.size else None, int(sel.size),
+                             _lib.ptr(out), _lib.stream_handle()), "pdm_combine")
 
 
 _HOST_PIECE_ITEMS = 1 << 18  # 32-block items per pipelined piece (2 pieces at config c)
@@ -552,25 +520,24 @@ _HOST_PACKED_MIN_BLOCKS = 1 << 22  # below ~4 MB of D' PCIe time is small: raw z
 
 
 def _host_packed_pays(pdm_set: PdmSet) -> bool:
-    """Ship D' packed to the host only when the PCIe bytes it saves matter
-    (config a/b maps of 0.26-2 MB measured faster raw: no expansion pass)."""
+    """Ship D' compact to the host only when the PCIe bytes it saves matter
+    (config a/b maps of 0.26-2 MB measured faster raw: no expansion pass).
+    The compact forms rely on D' being a min of distance fields (packable set)."""
     return pdm_set.grid.num_blocks >= _HOST_PACKED_MIN_BLOCKS and pdm_set.packed() is not None
 
 
-def _packed_to_host(pdm_set: PdmSet, host: np.ndarray, flags_ptr, sel_ptr, k: int) -> None:
-    """D' for the host (pdm_merge_packed_to_host): the merge writes it packed
-    (9/16 of the bytes) into pinned staging over PCIe in pieces, and the host
-    expands piece i while piece i+1 is still in flight."""
+def _dprime_to_host(pdm_set: PdmSet, d_dev, host: np.ndarray) -> None:
+    """The host view of a finished D' (pdm_dprime_to_host): D' re-encoded in a
+    compact form (sparse deltas: ~1.8 MB instead of 16.8 MB at config c) is
+    stored into pinned staging over PCIe in pieces, and the host expands
+    piece i while piece i+1 is still in flight."""
     L = _lib.lib()
-    nib, nib_pitch, base, base_pitch = pdm_set.packed()
-    nib_h, base_h = pdm_set._host_stage()
+    stage, stage_base = pdm_set._host_stage()
     nb = pdm_set.grid.num_blocks
     pieces = max(1, min(16, (-(-nb // 32)) // _HOST_PIECE_ITEMS))
-    fmt = _host_format(pdm_set)
-    _lib.check(L.pdm_merge_packed_to_host(
-        _lib.ptr(nib), nib_pitch, _lib.ptr(base), base_pitch, nb, pdm_set.n, flags_ptr, sel_ptr,
-        k, _lib.ptr(nib_h), _lib.ptr(base_h), host.ctypes.data, pieces, fmt,
-        _lib.stream_handle()), "pdm_merge_packed_to_host")
+    _lib.check(L.pdm_dprime_to_host(_lib.ptr(d_dev), nb, _lib.ptr(stage), _lib.ptr(stage_base),
+                                    host.ctypes.data, pieces, _host_format(pdm_set),
+                                    _lib.stream_handle()), "pdm_dprime_to_host")
 
 
 def _host_format(pdm_set: PdmSet) -> int:

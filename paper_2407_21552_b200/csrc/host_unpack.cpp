@@ -304,3 +304,20 @@ extern "C" int pdm_unpack_sparse_host(const uint8_t *regions, int64_t map_bytes,
     }
     return PDM_OK;
 }
+
+// Host side: gather a strided f64 column into a contiguous (pinned) buffer --
+// the alpha channel lut[:, 3] of a TransferFunction (transfer.py:44-70,
+// 250-259) staged for its upload on every select_partitions call (the
+// reference re-reads tf.lut each call, so no copy is cached).  OpenMP across
+// the column: a 65,536-entry LUT is 2 MB of strided reads, ~100 us for one
+// core, a few us for the pool.
+extern "C" int pdm_gather_f64_host(const double *src, int64_t n, int64_t stride, double *dst) {
+    REQUIRE(src && dst && n >= 0 && stride >= 1, "pdm_gather_f64_host: bad arguments");
+    if (n < (1 << 14)) {
+        for (int64_t i = 0; i < n; ++i) dst[i] = src[i * stride];
+        return PDM_OK;
+    }
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < n; ++i) dst[i] = src[i * stride];
+    return PDM_OK;
+}

@@ -335,7 +335,8 @@ __device__ __forceinline__ void store_sparse(uint8_t *region, uint4 *stage, uint
 // warp-uniform dominance skip applies (exact): a plane whose two chunk bases
 // are >= the chunks' current maxima cannot lower any of the warp's blocks, so
 // its fold is skipped; the maxima only fall, so testing against the
-// batch-start maxima is safe.  `vote` lanes outside the map vote "skip".
+// batch-start maxima is safe.  `vote` lanes outside the map vote "skip"; the
+// whole warp calls this (merge_packed keeps warps converged).
 // Bench step 46.1 -> 43.9 us (k=29: 68 -> 58 us).  Also skipping the nibble
 // loads (bases fetched one batch ahead) measured slower: 49.8 us -- the vote
 // then sits between two dependent loads.
@@ -350,7 +351,7 @@ __device__ __forceinline__ void fold_batch(PackedAcc &acc, const uint4 (&q)[B],
             if (m + j < k) {
                 const bool dom = (0x6400u | (b[j] & 0xFFu)) >= m0 &&
                                  (0x6400u | ((b[j] >> 8) & 0xFFu)) >= m1;
-                if (!__all_sync(__activemask(), dom || !vote)) acc.fold(q[j], b[j]);
+                if (!__all_sync(0xFFFFFFFFu, dom || !vote)) acc.fold(q[j], b[j]);
             }
         }
         return;
@@ -409,7 +410,8 @@ __device__ __forceinline__ void emit_item(const PackedAcc &acc, int64_t t, bool 
 }
 
 __device__ __forceinline__ void add_zero_count(uint32_t nzero, unsigned long long *zeros) {
-    const uint32_t w = __reduce_add_sync(__activemask(), nzero);
+    __syncwarp();  // every lane of every warp arrives here (no early exits)
+    const uint32_t w = __reduce_add_sync(0xFFFFFFFFu, nzero);
     if ((threadIdx.x & 31) == 0 && w) atomicAdd(zeros, (unsigned long long)w);
 }
 
@@ -421,27 +423,31 @@ __device__ __forceinline__ void merge_packed(const P planes, int k, int64_t map_
     uint32_t nzero = 0;
     const int64_t items = ceil_div(map_bytes, 32);
     const int64_t T = (int64_t)gridDim.x * blockDim.x;
-    // kOut 3 keeps whole warps in the loop (warp-wide compaction)
-    const int64_t lane_off = kOut == 3 ? (threadIdx.x & 31) : 0;
+    // Whole warps stay in the loop together (t - lane = the warp's first item):
+    // the dominance vote and the kOut 3 compaction are full-warp operations.
+    const int64_t lane_off = threadIdx.x & 31;
     for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t - lane_off < items;
          t += T) {
-        const bool live = kOut != 3 || t < items;
+        const bool live = t < items;
         PackedAcc acc;
         acc.init();
-        for (int m = 0; live && m < k; m += B) {
+        for (int m = 0; m < k; m += B) {
             uint4 q[B];
             uint32_t b[B];
 #pragma unroll
             for (int j = 0; j < B; ++j) {
-                if (m + j < k) {
+                q[j] = make_uint4(0u, 0u, 0u, 0u);
+                b[j] = 0u;
+                if (live && m + j < k) {
                     q[j] = ld_stream_u4(planes.nib_at(m + j) + t * 16);
                     b[j] = ld_stream_u16(planes.base_at(m + j) + t * 2);
                 }
             }
-            fold_batch<B>(acc, q, b, m, k, true);
+            fold_batch<B>(acc, q, b, m, k, live);
         }
-        emit_item<kOut, kCount>(acc, t, live, map_bytes, out, out_base,
-                                stage + (threadIdx.x >> 5) * (kSparseRegion / 16), nzero);
+        if (kOut == 3 || live)
+            emit_item<kOut, kCount>(acc, t, live, map_bytes, out, out_base,
+                                    stage + (threadIdx.x >> 5) * (kSparseRegion / 16), nzero);
     }
     if (kCount) add_zero_count(nzero, zeros);  // every thread of the grid reaches it
 }
@@ -822,6 +828,129 @@ extern "C" int pdm_merge_packed_to_host(const uint8_t *nib, int64_t nib_pitch, c
              : format == 2 ? pdm_unpack_delta_host(stage_nib + 8 * t0, stage_base + 2 * t0,
                                                    nbytes, out + 32 * t0)
                            : pdm_unpack_sparse_host(stage_at(t0), nbytes, out + 32 * t0);
+        if (st) return st;
+    }
+    return PDM_OK;
+}
+
+// ---- a finished D' (plain bytes in HBM) to a host array ---------------------
+// combine() completes D' in HBM; its host view (.dist) is made on first
+// access.  encode_dprime_kernel re-encodes D' in one of the compact forms
+// above (thread = one 32-block item: two 16-byte loads) and stores it
+// straight into pinned host staging over PCIe; the host expands piece i while
+// piece i+1 is in flight -- the same pipeline as pdm_merge_packed_to_host,
+// fed by the merged map instead of the k packed planes, so the device
+// consumer of D' never pays for a host copy it does not read.
+namespace pdm {
+
+// The accumulator layout from 32 plain bytes (the inverse of result()):
+// lanes of a[i][s] = blocks (8i+s, 8i+s+4) = byte s of words 2i and 2i+1.
+__device__ __forceinline__ void acc_from_bytes(PackedAcc &acc, uint4 lo, uint4 hi) {
+    const uint32_t o[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int s = 0; s < 4; ++s)
+            acc.a[i][s] = (__byte_perm(o[2 * i], o[2 * i + 1], s | ((4 + s) << 8)) & 0x00FF00FFu) |
+                          kHalfBias;
+}
+
+template <int kOut>
+__global__ void __launch_bounds__(kPackedThreads)
+    encode_dprime_kernel(const uint8_t *__restrict__ d, int64_t map_bytes,
+                         uint8_t *__restrict__ out, uint8_t *__restrict__ out_base) {
+    __shared__ uint4 s_stage[kOut == 3 ? kPackedThreads / 32 * kSparseRegion / 16 : 1];
+    const int64_t items = ceil_div(map_bytes, 32);
+    const int64_t T = (int64_t)gridDim.x * blockDim.x;
+    const int64_t lane_off = kOut == 3 ? (threadIdx.x & 31) : 0;
+    uint32_t nzero = 0;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t - lane_off < items;
+         t += T) {
+        const bool live = t < items;
+        PackedAcc acc;
+        acc.init();
+        if (live) {
+            uint4 lo, hi;
+            if (t * 32 + 32 <= map_bytes) {
+                lo = ld_stream_u4(d + t * 32);
+                hi = ld_stream_u4(d + t * 32 + 16);
+            } else {  // tail item: repeat the last byte (steps of 0 past the map)
+                uint32_t w[8];
+                const uint8_t last = d[map_bytes - 1];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    uint32_t v = 0;
+#pragma unroll
+                    for (int b = 0; b < 4; ++b) {
+                        const int64_t at = t * 32 + 4 * j + b;
+                        v |= (uint32_t)(at < map_bytes ? d[at] : last) << (8 * b);
+                    }
+                    w[j] = v;
+                }
+                lo = make_uint4(w[0], w[1], w[2], w[3]);
+                hi = make_uint4(w[4], w[5], w[6], w[7]);
+            }
+            acc_from_bytes(acc, lo, hi);
+        }
+        emit_item<kOut, false>(acc, t, live, map_bytes, out, out_base,
+                               s_stage + (threadIdx.x >> 5) * (kSparseRegion / 16), nzero);
+    }
+}
+
+static int launch_encode(const uint8_t *d, int64_t map_bytes, uint8_t *out, uint8_t *out_base,
+                         int format, cudaStream_t s) {
+    auto kern = format == 3   ? encode_dprime_kernel<3>
+                : format == 2 ? encode_dprime_kernel<2>
+                              : encode_dprime_kernel<1>;
+    const int64_t items = ceil_div(map_bytes, 32);
+    const int64_t cap =
+        (int64_t)sm_count() * resident_ctas((const void *)kern, kPackedThreads, 0);
+    const int64_t laps = ceil_div(items, cap * kPackedThreads);
+    int64_t grid = ceil_div(items, laps * kPackedThreads);
+    grid = grid < 1 ? 1 : (grid > cap ? cap : grid);
+    kern<<<(unsigned)grid, kPackedThreads, 0, s>>>(d, map_bytes, out, out_base);
+    return cuda_status("encode_dprime_kernel");
+}
+
+}  // namespace pdm
+
+extern "C" int pdm_dprime_to_host(const uint8_t *d, int64_t map_bytes, uint8_t *stage,
+                                  uint8_t *stage_base, uint8_t *out, int32_t pieces,
+                                  int32_t format, pdm_stream_t stream) {
+    const char *fn = "pdm_dprime_to_host";
+    PDM_REQUIRE(format >= 1 && format <= 3,
+                "%s: format must be 1 (nibble), 2 (delta) or 3 (sparse delta)", fn);
+    PDM_REQUIRE(d && stage && out && (format == 3 || stage_base), "%s: null pointer", fn);
+    PDM_REQUIRE(map_bytes >= 1, "%s: map_bytes must be >= 1", fn);
+    PDM_REQUIRE((uintptr_t)d % 16 == 0 && (uintptr_t)stage % 16 == 0 &&
+                    (uintptr_t)stage_base % 2 == 0,
+                "%s: needs a 16-byte aligned D' and staging", fn);
+    PDM_REQUIRE(pieces >= 1 && pieces <= 64, "%s: pieces outside [1, 64]", fn);
+    const int64_t per_item = format == 1 ? 16 : 8;
+    cudaStream_t s = as_stream(stream);
+    const int64_t items = ceil_div(map_bytes, 32);
+    int64_t per = ceil_div(items, pieces);
+    if (format == 3) per = 32 * ceil_div(per, 32);
+    auto stage_at = [&](int64_t t0) {
+        return format == 3 ? stage + (t0 / 32) * kSparseRegion : stage + per_item * t0;
+    };
+    int used = 0;
+    for (int64_t t0 = 0; t0 < items; t0 += per, ++used) {
+        const int64_t nbytes = min(map_bytes, 32 * (t0 + per)) - 32 * t0;
+        int st = launch_encode(d + 32 * t0, nbytes, stage_at(t0),
+                               format == 3 ? nullptr : stage_base + 2 * t0, format, s);
+        if (st) return st;
+        PDM_CUDA_TRY(cudaEventRecord(piece_event(used), s));
+    }
+    for (int i = 0; i < used; ++i) {
+        const int64_t t0 = i * per;
+        const int64_t nbytes = min(map_bytes, 32 * (t0 + per)) - 32 * t0;
+        PDM_CUDA_TRY(cudaEventSynchronize(piece_event(i)));
+        int st = format == 1   ? pdm_unpack_packed_host(stage + 16 * t0, stage_base + 2 * t0,
+                                                        nbytes, out + 32 * t0)
+                 : format == 2 ? pdm_unpack_delta_host(stage + 8 * t0, stage_base + 2 * t0,
+                                                       nbytes, out + 32 * t0)
+                               : pdm_unpack_sparse_host(stage_at(t0), nbytes, out + 32 * t0);
         if (st) return st;
     }
     return PDM_OK;

@@ -8,7 +8,7 @@ full PCIe/C2C rate and are stream-ordered.
 
 from __future__ import annotations
 
-import sys
+import weakref
 
 import numpy as np
 
@@ -81,6 +81,13 @@ def to_host(t_dev, np_dtype) -> np.ndarray:
     return host.astype(np_dtype)
 
 
+def complete() -> None:
+    """Wait for the current stream: the public API returns completed results,
+    as the reference's synchronous numpy/numba functions do, so a caller's own
+    timer (bench.measure_ms, SessionStore.set_tf) measures the device work."""
+    torch().cuda.current_stream().synchronize()
+
+
 def empty(shape, np_dtype):
     return torch().empty(tuple(int(s) for s in shape), dtype=_torch_dtype(np_dtype),
                          device=device())
@@ -94,29 +101,40 @@ def plane_pitch(num_blocks: int) -> int:
 # Host views of device results (e.g. D' expanded on the host) land in pageable
 # buffers recycled per size: a fresh large numpy array pays its page faults
 # (and the kernel's page zeroing) on first touch -- ~6 ms for a 134 MB map --
-# while a recycled one is already mapped.  A buffer is reused only when
-# nothing but the pool references it (every view of it holds a reference to
-# its base), so results handed out are never overwritten.
+# while a recycled one is already mapped.  Ownership is explicit: each array
+# handed out is a view of a _PoolBlock (numpy keeps the block as the .base of
+# every view and slice made from it), and the block's finalizer returns the
+# raw buffer to the pool only when the last of those arrays is gone.
 _HOST_POOL: dict = {}
-_HOST_POOL_CAP = 4  # buffers kept per size
+_HOST_POOL_CAP = 4  # idle buffers kept per size
+
+
+class _PoolBlock:
+    """Buffer exporter owning one pooled raw buffer (PEP 688 __buffer__)."""
+
+    __slots__ = ("raw", "__weakref__")
+
+    def __init__(self, raw: np.ndarray):
+        self.raw = raw
+
+    def __buffer__(self, flags):
+        return memoryview(self.raw)
+
+
+def _recycle(nbytes: int, raw: np.ndarray) -> None:
+    pool = _HOST_POOL.setdefault(nbytes, [])
+    if len(pool) < _HOST_POOL_CAP:
+        pool.append(raw)
 
 
 def host_buffer(shape) -> np.ndarray:
-    """A writable uint8 array of `shape` backed by a recycled buffer."""
+    """A writable, 64-byte aligned uint8 array of `shape` backed by a recycled
+    buffer (returned to the pool once no array references it)."""
     nbytes = int(np.prod(shape))
     pool = _HOST_POOL.setdefault(nbytes, [])
-    for buf in pool:
-        # references: the pool list, the loop variable, getrefcount's argument
-        # (every view handed out has buf itself as its .base)
-        if sys.getrefcount(buf) == 3:
-            return _aligned_view(buf, nbytes, shape)
-    buf = np.empty(nbytes + 64, dtype=np.uint8)
-    if len(pool) < _HOST_POOL_CAP:
-        pool.append(buf)
-    return _aligned_view(buf, nbytes, shape)
-
-
-def _aligned_view(buf: np.ndarray, nbytes: int, shape) -> np.ndarray:
-    """64-byte aligned start (the host expansion streams whole cache lines)."""
-    off = (-buf.ctypes.data) % 64
-    return buf[off:off + nbytes].reshape(shape)
+    raw = pool.pop() if pool else np.empty(nbytes + 64, dtype=np.uint8)
+    blk = _PoolBlock(raw)
+    weakref.finalize(blk, _recycle, nbytes, raw)
+    flat = np.frombuffer(blk, dtype=np.uint8)
+    off = (-flat.ctypes.data) % 64  # the host expansion streams whole cache lines
+    return flat[off:off + nbytes].reshape(shape)

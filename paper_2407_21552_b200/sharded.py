@@ -18,7 +18,8 @@ slab, its slab of every partition map and (after an update) its slab of D'.
   and z are local.  Bit-exact against the single-GPU transform (min over
   slabs of clamped distances composes exactly).
 
-Collectives go through torch.distributed (NCCL on GPUs, gloo in CPU tests).
+Collectives go through torch.distributed (NCCL on GPUs; gloo in the CPU
+tests and the 2-process single-GPU test, with CUDA tensors staged via host).
 The per-slab compute is an ``ops`` object: ``GpuOps`` (libpdm_b200 kernels)
 in the product; tests substitute a host implementation to exercise the
 collective logic on CPU with gloo.
@@ -121,24 +122,65 @@ def slab_bounds(nx: int, b: int, world: int) -> list[int]:
     return starts + [nx]
 
 
-def _exchange_planes(vol_t, ops, rank, world, group):
+class _Comm:
+    """torch.distributed collectives for the sharded build.  NCCL moves CUDA
+    tensors directly (NVLink); other backends (gloo: CPU tests, and the
+    2-process single-GPU test) stage CUDA tensors through host memory."""
+
+    def __init__(self, group):
+        import torch.distributed as dist
+
+        self.dist = dist
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.nccl = dist.get_backend(group) == "nccl"
+
+    def _out(self, t):
+        return t if self.nccl or not t.is_cuda else t.cpu()
+
+    def all_gather(self, t):
+        """[world, *t.shape] of every rank's t, on t's device."""
+        import torch
+
+        src = self._out(t).contiguous()
+        parts = [torch.empty_like(src) for _ in range(self.world)]
+        self.dist.all_gather(parts, src, group=self.group)
+        return torch.stack(parts).to(t.device)
+
+    def exchange(self, sends, recvs):
+        """Point-to-point: sends = [(tensor, peer)], recvs = [(like_tensor,
+        peer)]; returns the received tensors (on the like tensors' devices)."""
+        P2P = self.dist.P2POp
+        ops, bufs = [], []
+        for t, peer in sends:
+            ops.append(P2P(self.dist.isend, self._out(t).contiguous(), peer, self.group))
+        for like, peer in recvs:
+            buf = self._out(like)
+            bufs.append((buf, like))
+            ops.append(P2P(self.dist.irecv, buf, peer, self.group))
+        if ops:
+            for req in self.dist.batch_isend_irecv(ops):
+                req.wait()
+        return [buf.to(like.device) if buf is not like else buf for buf, like in bufs]
+
+
+def _exchange_planes(vol_t, ops, comm: _Comm):
     """Swap boundary voxel planes with the x-neighbours.  Returns (below, above):
     the neighbour's plane at x0-1 and x1 (None at the volume ends)."""
-    import torch.distributed as dist
-
-    ops_list, below, above = [], None, None
+    rank, world = comm.rank, comm.world
     nxl = vol_t.shape[0]
+    shape = (1,) + tuple(vol_t.shape[1:])
+    sends, recvs = [], []
     if rank > 0:
-        below = ops.empty((1,) + tuple(vol_t.shape[1:]), _np_dtype(vol_t))
-        ops_list.append(dist.P2POp(dist.isend, ops.plane(vol_t, 0), rank - 1, group))
-        ops_list.append(dist.P2POp(dist.irecv, below, rank - 1, group))
+        sends.append((ops.plane(vol_t, 0), rank - 1))
+        recvs.append((ops.empty(shape, _np_dtype(vol_t)), rank - 1))
     if rank < world - 1:
-        above = ops.empty((1,) + tuple(vol_t.shape[1:]), _np_dtype(vol_t))
-        ops_list.append(dist.P2POp(dist.isend, ops.plane(vol_t, nxl - 1), rank + 1, group))
-        ops_list.append(dist.P2POp(dist.irecv, above, rank + 1, group))
-    if ops_list:
-        for req in dist.batch_isend_irecv(ops_list):
-            req.wait()
+        sends.append((ops.plane(vol_t, nxl - 1), rank + 1))
+        recvs.append((ops.empty(shape, _np_dtype(vol_t)), rank + 1))
+    got = comm.exchange(sends, recvs)
+    below = got.pop(0) if rank > 0 else None
+    above = got.pop(0) if rank < world - 1 else None
     return below, above
 
 
@@ -153,42 +195,45 @@ def build_pdm_set_sharded(volume: Volume, b: int, scheme: PartitionScheme,
     ``group``.  ``volume`` is this rank's slab (its x0 must be a multiple of b
     and every slab but the last must hold whole blocks); the result is this
     rank's slab of every partition's distance map, bit-identical to the
-    corresponding planes of the single-device build_pdm_set."""
+    corresponding planes of the single-device build_pdm_set.
+
+    Validation is agreed across ranks before any data moves: the slab table
+    all_gather carries each rank's error flag, so a bad slab makes EVERY rank
+    raise VolumeError instead of leaving its peers waiting in a collective."""
     import torch
-    import torch.distributed as dist
 
     _require_mode(mode)
     if scheme.intensity_span != (1 << volume.bits):
         raise VolumeError(
             f"scheme spans {scheme.intensity_span} intensities, volume needs {1 << volume.bits}")
     ops = ops or GpuOps()
-    world = dist.get_world_size(group)
-    rank = dist.get_rank(group)
+    comm = _Comm(group)
+    world, rank = comm.world, comm.rank
     vol_t = ops.voxels(volume)
     grid = BlockGrid.for_dims(volume.dims, b)
     bdims, n = grid.bdims, scheme.n
 
-    # slab table in block planes (every rank learns every slab's start)
-    mine = torch.tensor([bdims[0] if bx0 is None else bx0, bdims[0]], dtype=torch.int64)
-    if dist.get_backend(group) == "nccl":
+    # slab table in block planes (every rank learns every slab's start) + error flags
+    partial = int(volume.dims[0] % b != 0)  # legal on the last rank only
+    mine = torch.tensor([-1 if bx0 is None else bx0, bdims[0], partial], dtype=torch.int64)
+    if comm.nccl:
         mine = mine.cuda()
-    table = [torch.zeros_like(mine) for _ in range(world)]
-    dist.all_gather(table, mine, group=group)
-    sizes = [int(t[1]) for t in table]
+    table = comm.all_gather(mine).cpu().numpy()
+    sizes = table[:, 1]
     starts = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
-    if bx0 is not None and int(starts[rank]) != bx0:
-        raise VolumeError(f"rank {rank}: slab starts at block {bx0}, expected {starts[rank]}")
+    for r in range(world):
+        if table[r, 2] and r < world - 1:
+            raise VolumeError(f"rank {r}: only the last slab may end inside a block")
+        if table[r, 0] >= 0 and table[r, 0] != starts[r]:
+            raise VolumeError(f"rank {r}: slab starts at block {table[r, 0]}, "
+                              f"expected {starts[r]}")
 
     below = above = None
     if mode == "range_apron":
-        if rank < world - 1 and volume.dims[0] % b:
-            raise VolumeError("only the last slab may end inside a block")
-        below, above = _exchange_planes(vol_t, ops, rank, world, group)
+        below, above = _exchange_planes(vol_t, ops, comm)
     storage, pitch, edges = slab_phase_local(vol_t, volume.bits, b, scheme, mode, below, above,
                                              ops)
-    gathered = [torch.empty_like(edges) for _ in range(world)]
-    dist.all_gather(gathered, edges, group=group)
-    edges_all = torch.stack(gathered).contiguous()
+    edges_all = comm.all_gather(edges).contiguous()
     slab_phase_fold(storage, pitch, n, bdims, edges_all, world, rank, starts, ops)
     pset = PdmSet(grid=grid, scheme=scheme, occupancy_mode=mode, storage=storage)
     pset.slab = (int(starts[rank]), int(starts[rank + 1]), int(starts[-1]))

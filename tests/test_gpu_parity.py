@@ -261,10 +261,13 @@ def test_combine_empty_singleton_full(built16):
     assert np.all(large <= small)
 
 
-def test_combine_deferred_host_and_device_paths(built16):
-    """combine() results launch on first use: .dist writes pinned host memory
-    directly, .device() writes HBM; both orders agree, for every selection
-    kind (device flags, host indices, empty)."""
+def test_combine_is_eager_and_host_view_lazy(built16):
+    """combine() returns a finished map (the reference's contract,
+    acceleration.py:244-276): its merge has run into a fresh HBM buffer and
+    the stream is idle when it returns; .dist then makes the host view.  Every
+    selection kind (device flags, host indices, empty), both access orders."""
+    import torch
+
     scheme, pset = built16
     want = np.minimum.reduce([pset.pdms[i - 1].dist for i in (2, 7, 11)])
     lut = np.zeros((256, 4))
@@ -272,15 +275,74 @@ def test_combine_deferred_host_and_device_paths(built16):
         lo, hi = scheme.partitions[i - 1].rho_lo, scheme.partitions[i - 1].rho_hi
         lut[lo: hi + 1, 3] = 0.5
     tf = pdm.TransferFunction(lut=lut)
-    a = pdm.combine(pset, pdm.select_partitions(tf, scheme))  # device flags, host first
+    sel = pdm.select_partitions(tf, scheme)
+    assert torch.cuda.current_stream().query()  # selection complete on return
+    a = pdm.combine(pset, sel)  # device flags
+    assert a._dev is not None and a._host is None
+    assert torch.cuda.current_stream().query()  # merge complete on return
     assert np.array_equal(a.dist, want) and np.array_equal(a.device().cpu().numpy(), want)
-    b = pdm.combine(pset, pdm.select_partitions(tf, scheme))  # device first
+    b = pdm.combine(pset, pdm.select_partitions(tf, scheme))  # device view first
     assert np.array_equal(b.device().cpu().numpy(), want) and np.array_equal(b.dist, want)
     c = pdm.combine(pset, pdm.PartitionSelection(selected=frozenset({2, 7, 11}), n=16))
+    assert torch.cuda.current_stream().query()
     assert np.array_equal(c.dist, want)
     e = pdm.combine(pset, pdm.PartitionSelection(selected=frozenset(), n=16))
     assert np.all(e.dist == 255) and int(e.device().min()) == 255
     assert a.dist.ctypes.data != b.dist.ctypes.data
+    for p in pset.pdms:  # never aliases a PDM
+        assert a.device().data_ptr() != p.device().data_ptr()
+
+
+def test_select_rereads_a_mutated_lut(built16):
+    """select_partitions stages tf.lut on every call (the reference re-reads
+    it): an in-place edit of the LUT changes the next selection."""
+    scheme, _ = built16
+    lut = np.zeros((256, 4))
+    lut[3, 3] = 0.5
+    tf = pdm.TransferFunction(lut=lut)
+    assert pdm.select_partitions(tf, scheme).sorted == [1]
+    tf.lut[3, 3] = 0.0
+    tf.lut[255, 3] = 0.25
+    assert pdm.select_partitions(tf, scheme).sorted == [16]
+
+
+@pytest.mark.parametrize("fmt", [1, 2, 3])
+def test_dprime_to_host_formats_and_pieces(fmt):
+    """pdm_dprime_to_host through the C ABI: a finished D' in HBM re-encoded
+    in the nibble, delta and sparse delta forms, 1-7 pieces, 1-Lipschitz maps
+    with zero plateaus, flat runs and slopes, sizes with a partial last item;
+    bytes past map_bytes are never written."""
+    import torch
+
+    from paper_2407_21552_b200 import _lib
+
+    L = _lib.lib()
+    rng = np.random.default_rng(10 + fmt)
+    st = _lib.stream_handle()
+    for map_bytes in (70000, 4096 * 3 + 5, 31, 1):
+        steps = rng.choice([-1, 0, 0, 0, 1], size=map_bytes)
+        d = np.clip(int(rng.integers(0, 40)) + np.cumsum(steps), 0, 255)
+        d[: map_bytes // 5] = 0
+        d[map_bytes // 5:] = np.minimum(d[map_bytes // 5:],
+                                         np.arange(1, map_bytes - map_bytes // 5 + 1))
+        d = d.astype(np.uint8)
+        assert map_bytes < 2 or np.abs(np.diff(d.astype(np.int16))).max() <= 1
+        dev = torch.from_numpy(d).cuda()
+        chunks = int(L.pdm_packed_chunks(map_bytes))
+        stage = torch.empty(max(chunks * 8, -(-chunks // 64) * 336), dtype=torch.uint8,
+                            pin_memory=True)
+        stage_b = torch.empty(chunks, dtype=torch.uint8, pin_memory=True)
+        for pieces in (1, 3, 7):
+            out = np.full(map_bytes + 32, 0xCD, np.uint8)
+            _lib.check(L.pdm_dprime_to_host(_lib.ptr(dev), map_bytes, stage.data_ptr(),
+                                            stage_b.data_ptr(), out.ctypes.data, pieces, fmt,
+                                            st), "dprime_to_host")
+            assert np.array_equal(out[:map_bytes], d), (map_bytes, pieces)
+            assert (out[map_bytes:] == 0xCD).all()
+    out = np.empty(64, np.uint8)
+    with pytest.raises(ValueError):
+        _lib.check(L.pdm_dprime_to_host(_lib.ptr(dev), 1, stage.data_ptr(), stage_b.data_ptr(),
+                                        out.ctypes.data, 1, 4, st), "bad format")
 
 
 def test_combine_more_than_one_param_batch():

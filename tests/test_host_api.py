@@ -267,19 +267,27 @@ def test_distance_map_dump_format(tmp_path):
 def test_host_buffer_recycles_only_unreferenced_buffers():
     from paper_2407_21552_b200 import device
 
+    import gc
+
     a = device.host_buffer((3, 7))
     a[:] = 5
     b = device.host_buffer((3, 7))
     assert not np.shares_memory(a, b)  # a is alive: a second buffer
-    base_a = a.base
+    addrs = {a.ctypes.data, b.ctypes.data}
     view = a[1:]
     del a
+    gc.collect()
     c = device.host_buffer((3, 7))
     assert not np.shares_memory(c, view)  # a slice keeps its buffer in use
+    assert (view == 5).all()
+    addrs.add(c.ctypes.data)
     del view, b, c
+    gc.collect()
     d = device.host_buffer((3, 7))
-    assert d.base is base_a or d.base is not None  # some pooled buffer is reused
-    assert d.shape == (3, 7) and d.dtype == np.uint8
+    e = device.host_buffer((3, 7))
+    f = device.host_buffer((3, 7))
+    assert {d.ctypes.data, e.ctypes.data, f.ctypes.data} == addrs  # released buffers reused
+    assert d.shape == (3, 7) and d.dtype == np.uint8 and d.ctypes.data % 64 == 0
 
 
 @pytest.mark.parametrize("avx512", [True, False])

@@ -135,3 +135,30 @@ def test_synth_slab_matches_full():
     part = oracle.synth_volume(16, dims, boxes, seed=5, x_range=(7, 19))
     assert np.array_equal(full[7:19], part)
     assert full.max() > 0 and (full == 0).any()
+
+
+@pytest.mark.parametrize("mode", ["voxel", "range_apron"])
+@pytest.mark.parametrize("dims,bits,b,slab", [((37, 9, 11), 16, 4, 8), ((30, 7, 12), 8, 3, 9),
+                                               ((16, 5, 6), 8, 2, 2)])
+def test_slabwise_synth_build_matches_whole_volume(mode, dims, bits, b, slab):
+    """oracle.build_pdm_set_synth (slab-by-slab occupancy, used for the
+    2048^3 parity checks) == build_pdm_set on the whole generated volume."""
+    from paper_2407_21552_b200.synth import synth_boxes
+
+    boxes = synth_boxes(dims, bits, 5, 6)
+    vox = oracle.synth_volume(bits, dims, boxes, 5)
+    bounds = [(lo, hi) for lo, hi in _uniform_bounds(5, bits)]
+    want = oracle.build_pdm_set(vox, b, bounds, mode)
+    got = oracle.build_pdm_set_synth(bits, dims, boxes, 5, b, bounds, mode, slab_voxels=slab)
+    assert np.array_equal(got, want)
+
+
+def _uniform_bounds(n, bits):
+    span = 1 << bits
+    q, r = divmod(span, n)
+    out, lo = [], 0
+    for i in range(n):
+        w = q + (i < r)
+        out.append((lo, lo + w - 1))
+        lo += w
+    return out

@@ -1,0 +1,77 @@
+"""The reference's OWN test suite, unmodified, run through the drop-in overlay
+on the GPU (the strongest drop-in check).
+
+`integration/pdmrender` executes the reference package's ``__init__`` but
+binds ``pdmrender.acceleration`` / ``.volume`` / ``.transfer`` / ``.raycast``
+to this repo's CUDA implementation; every other module (``bench``, ``cli``,
+``service``, ``_kernels``) and every test file comes from the reference as
+shipped.  The reference tree is read from /root/reference in this container
+or from ``baseline/_ref`` (staged by tools/stage_reference.sh: a pip install
+of the package plus its ``tests/`` directory, git-ignored, travels with the
+repo to the GPU box).  The summary (pass/fail/skip counts per file) is
+written to $PDM_REF_SUITE_REPORT when set.
+"""
+
+from __future__ import annotations
+
+import json
+import os
+import subprocess
+import sys
+import xml.etree.ElementTree as ET
+from pathlib import Path
+
+import pytest
+
+ROOT = Path(__file__).resolve().parents[1]
+FILES = ("test_acceleration.py", "test_volume.py", "test_transfer.py", "test_acceptance.py",
+         "test_bench.py", "test_service.py", "test_raycast.py", "test_cli.py")
+
+
+def _reference_tree():
+    staged = ROOT / "baseline" / "_ref"
+    if (staged / "pdmrender").is_dir() and (staged / "pkg_tests").is_dir():
+        return staged / "pdmrender", staged / "pkg_tests", staged / "pkg_pyproject.toml"
+    src = Path("/root/reference/pkg")
+    if src.is_dir():
+        return src / "src" / "pdmrender", src / "tests", src / "pyproject.toml"
+    return None
+
+
+@pytest.mark.gpu
+def test_reference_suite_through_overlay(tmp_path):
+    tree = _reference_tree()
+    if tree is None:
+        pytest.skip("reference package not staged (tools/stage_reference.sh)")
+    pkg, tests, pyproject = tree
+    junit = tmp_path / "junit.xml"
+    env = dict(os.environ, PYTHONPATH=f"{ROOT / 'integration'}:{ROOT}", PDMRENDER_REF=str(pkg),
+               NUMBA_CACHE_DIR=str(tmp_path / "numba"), PYTHONDONTWRITEBYTECODE="1")
+    cmd = [sys.executable, "-m", "pytest", *[str(tests / f) for f in FILES], "-q",
+           "-p", "no:cacheprovider", f"--rootdir={tests.parent}", "-c", str(pyproject),
+           f"--junitxml={junit}", "-x" if os.environ.get("PDM_REF_SUITE_X") else "-ra"]
+    r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=3000,
+                       cwd=str(tmp_path))
+    per_file: dict = {}
+    failed = []
+    for case in ET.parse(junit).getroot().iter("testcase"):
+        f = case.get("classname", "").split(".")[0] + ".py"
+        row = per_file.setdefault(f, {"passed": 0, "failed": 0, "skipped": 0})
+        if case.find("failure") is not None or case.find("error") is not None:
+            row["failed"] += 1
+            failed.append(f"{case.get('classname')}::{case.get('name')}")
+        elif case.find("skipped") is not None:
+            row["skipped"] += 1
+        else:
+            row["passed"] += 1
+    summary = {"files": per_file,
+               "passed": sum(v["passed"] for v in per_file.values()),
+               "failed": len(failed), "skipped": sum(v["skipped"] for v in per_file.values()),
+               "failures": failed, "tail": r.stdout[-3000:]}
+    out = os.environ.get("PDM_REF_SUITE_REPORT")
+    if out:
+        Path(out).parent.mkdir(parents=True, exist_ok=True)
+        Path(out).write_text(json.dumps(summary, indent=1))
+    print(json.dumps({k: summary[k] for k in ("passed", "failed", "skipped")}))
+    assert summary["passed"] > 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert not failed, "\n".join(failed[:40]) + "\n" + r.stdout[-4000:]

@@ -172,3 +172,84 @@ def test_sharded_emulated_on_one_gpu(mode, dims, bits, b, n, planes):
         nb = int(np.prod(bd))
         got = storage[:, :nb].cpu().numpy().reshape((n,) + bd)
         assert np.array_equal(got, want[:, starts[r]:starts[r + 1]]), r
+
+
+def _bad_slab_worker(rank, world, port, mode, q):
+    """Rank 0's slab ends inside a block (illegal except on the last rank):
+    every rank must raise VolumeError, none may hang in a collective."""
+    from sharded_host_ops import HostOps
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        rng = np.random.default_rng(3)
+        vox = random_structured_volume(rng, (18, 6, 8), 8)
+        x0, x1 = (0, 9) if rank == 0 else (9, 18)  # b=4: 9 is inside a block
+        slab = pdm.Volume.from_array(vox[x0:x1])
+        try:
+            sharded.build_pdm_set_sharded(slab, 4, pdm.scheme_uniform(4, 8), mode, ops=HostOps())
+            q.put((rank, "no error"))
+        except pdm.VolumeError as exc:
+            q.put((rank, f"VolumeError: {exc}"))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("mode", ["voxel", "range_apron"])
+def test_sharded_bad_slab_raises_on_every_rank(mode):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_bad_slab_worker, args=(r, 2, port, mode, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0, "a rank hung or crashed"
+    got = dict(q.get(timeout=5) for _ in range(2))
+    assert all(v.startswith("VolumeError: rank 0: only the last slab") for v in got.values()), got
+
+
+def _gpu_gloo_worker(rank, world, port, mode, q):
+    """One rank of a 2-process sharded build on the SAME GPU: real GpuOps
+    kernels per slab, collectives over gloo with the CUDA tensors staged
+    through host memory (no kernel waits on another rank's kernel)."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        rng = np.random.default_rng(91)
+        dims, bits, b, n = (40, 24, 32), 16, 4, 12
+        vox = random_structured_volume(rng, dims, bits)
+        scheme = pdm.scheme_uniform(n, bits)
+        xs = sharded.slab_bounds(dims[0], b, world)
+        slab = pdm.Volume.from_array(vox[xs[rank]:xs[rank + 1]])
+        pset = sharded.build_pdm_set_sharded(slab, b, scheme, mode, bx0=xs[rank] // b)
+        assert isinstance(pset.storage, torch.Tensor) and pset.storage.is_cuda
+        nb = pset.grid.num_blocks
+        got = pset.storage[:, :nb].cpu().numpy().reshape((n,) + pset.grid.bdims)
+        want = oracle.build_pdm_set(vox, b, scheme.bounds(), mode)[:, pset.slab[0]:pset.slab[1]]
+        ok = np.array_equal(got, want)
+        sel = pdm.PartitionSelection(selected=frozenset({2, 5, 11}), n=n)
+        ok = ok and np.array_equal(pdm.combine(pset, sel).dist, oracle.combine(want, [2, 5, 11]))
+        q.put((rank, bool(ok)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("mode", ["voxel", "range_apron"])
+def test_sharded_two_processes_one_gpu_gloo(mode):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gpu_gloo_worker, args=(r, 2, port, mode, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=300)
+        assert p.exitcode == 0
+    got = dict(q.get(timeout=5) for _ in range(2))
+    assert got == {0: True, 1: True}, got
