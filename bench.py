@@ -353,7 +353,8 @@ def run_b200(args, rank, world, local_rank):
         flush_r.sum()
 
     stream = torch.cuda.current_stream()
-    for i in range(warm):
+    for i in range(warm):  # (the flush's torch kernels load lazily: warm them too)
+        flush_l2(i)
         pdm.update_from_tf(pset, alphas_w[i], out=outs[0], flags=flags)
 
     def timed_pass(merge_only):

@@ -44,6 +44,12 @@ enum pdm_status {
 int pdm_version(void);              /* ABI version, currently 1 */
 const char *pdm_last_error(void);   /* message of the last failing call (thread-local) */
 int pdm_device_sm_count(int device);
+/* Wait for all work enqueued on `stream` (the public API's completion point:
+ * the reference's functions return finished results). */
+int pdm_stream_synchronize(pdm_stream_t stream);
+/* dst[0..bytes) = value, stream-ordered (a constant map: the all-255 D of an
+ * empty TF support, the all-0 D of a full one). */
+int pdm_fill_u8(uint8_t *dst, int64_t bytes, int32_t value, pdm_stream_t stream);
 
 /* volume.py:86-90 intensity_range of a device-resident volume: out[0] = min,
  * out[1] = max over count voxels (out: device uint32[2]). */
@@ -65,6 +71,16 @@ int pdm_count_value(const uint8_t *data, int64_t bytes, uint32_t value,
  * a CTA or a warp per partition).  flags: device uint8[n]. */
 int pdm_select(const double *alpha, int64_t span, int64_t alpha_stride, const int32_t *starts,
                int32_t n, int32_t max_width, uint8_t *flags, pdm_stream_t stream);
+
+/* select_partitions(tf, scheme) end to end (transfer.py:250-259): gathers
+ * alpha = lut_alpha[i * lut_stride] (host memory, e.g. &lut[0][3] with
+ * lut_stride 4) into pinned stage_host, copies it to stage_dev (f64[span]),
+ * runs pdm_select into flags_dev (uint8[n]), copies the flags to pinned
+ * flags_host and synchronises `stream`: returns with the finished selection
+ * on the host. */
+int pdm_select_tf(const double *lut_alpha, int64_t span, int64_t lut_stride, double *stage_host,
+                  double *stage_dev, const int32_t *starts, int32_t n, int32_t max_width,
+                  uint8_t *flags_dev, uint8_t *flags_host, pdm_stream_t stream);
 
 /* transfer.py:250-259 on the LUT alone: nz[v] = alpha[v] > 0.0 and, when
  * prefix != NULL, prefix[v+1] = #{u <= v : alpha[u] > 0} with prefix[0] = 0
@@ -99,6 +115,14 @@ int pdm_packed_chunks(int64_t map_bytes);
 int pdm_pack_pdms(const uint8_t *pdms, int64_t plane_pitch, int64_t map_bytes, int32_t n,
                   uint8_t *nib, int64_t nib_pitch, uint8_t *base, int64_t base_pitch,
                   uint32_t *violations, pdm_stream_t stream);
+
+/* *count = number of 16-block chunks (linear order, per plane; the last one
+ * partial) of planes pdms[p * plane_pitch ..][0..map_bytes) whose
+ * consecutive bytes differ by more than 1 -- 0 means the D' of any selection
+ * may cross PCIe in the delta forms (a set loaded from a dump,
+ * acceleration.py:279-354, is checked before they are used). */
+int pdm_count_nonlipschitz_chunks(const uint8_t *pdms, int64_t plane_pitch, int64_t map_bytes,
+                                  int32_t n, uint32_t *count, pdm_stream_t stream);
 
 /* pdm_distance_transform_mask followed by pdm_pack_pdms, with the packing
  * fused into the last (z) pass when bz is 128, 256 or 512 (the rows are

@@ -27,11 +27,15 @@ _SIGNATURES = {
     "pdm_version": [],
     "pdm_last_error": [],
     "pdm_device_sm_count": [_INT],
+    "pdm_stream_synchronize": [_P],
+    "pdm_fill_u8": [_P, _I64, _I32, _P],
     "pdm_select": [_P, _I64, _I64, _P, _I32, _I32, _P, _P],
+    "pdm_select_tf": [_P, _I64, _I64, _P, _P, _P, _I32, _I32, _P, _P, _P],
     "pdm_alpha_support": [_P, _I64, _I64, _P, _P, _P],
     "pdm_combine": [_P, _I64, _I64, _I32, _P, _I32, _P, _P],
     "pdm_combine_flags": [_P, _I64, _I64, _I32, _P, _P, _P],
     "pdm_packed_chunks": [_I64],
+    "pdm_count_nonlipschitz_chunks": [_P, _I64, _I64, _I32, _P, _P],
     "pdm_pack_pdms": [_P, _I64, _I64, _I32, _P, _I64, _P, _I64, _P, _P],
     "pdm_distance_transform_mask_packed": [_P, _I32, _I32, _I64, _I64, _I64, _P, _I64, _P, _I64,
                                            _P, _I64, _P, _P],
@@ -120,10 +124,13 @@ def check(status: int, what: str) -> None:
 
 
 def stream_handle(stream=None) -> int:
+    """Raw cudaStream_t of `stream` (default: torch's current stream on the
+    current device; the direct accessor avoids building a Stream object)."""
     import torch
 
-    s = torch.cuda.current_stream() if stream is None else stream
-    return int(s.cuda_stream)
+    if stream is not None:
+        return int(stream.cuda_stream)
+    return torch._C._cuda_getCurrentRawStream(torch._C._cuda_getDevice())
 
 
 def ptr(t) -> int:

@@ -325,10 +325,11 @@ def _minmax_device(volume, grid, minmax):
     return mins.contiguous(), maxs.contiguous()
 
 
-def _tf_support(volume: Volume, grid: BlockGrid, tf: TransferFunction, mode: str):
+def _tf_support(volume: Volume, grid: BlockGrid, tf: TransferFunction, mode: str,
+                prefix_too: bool = False):
     """Validation shared by occupancy_for_tf / standard_distance_map
-    (acceleration.py:158-163), then the TF's nz LUT and, for range_apron, its
-    prefix count (pdm_alpha_support) on the device."""
+    (acceleration.py:158-163), then the TF's nz LUT and, for range_apron (or
+    prefix_too), its prefix count (pdm_alpha_support) on the device."""
     _require_mode(mode)
     check_pair(volume, grid)
     if tf.lut.shape[0] != (1 << volume.bits):
@@ -338,7 +339,8 @@ def _tf_support(volume: Volume, grid: BlockGrid, tf: TransferFunction, mode: str
     span = 1 << volume.bits
     alpha = alpha_to_device(tf)
     nz = device.empty((span,), np.uint8)
-    prefix = device.empty((span + 1,), np.int32) if mode == "range_apron" else None
+    prefix = device.empty((span + 1,), np.int32) if (mode == "range_apron" or prefix_too) \
+        else None
     _lib.check(L.pdm_alpha_support(_lib.ptr(alpha), span, 1, _lib.ptr(nz),
                                    _lib.ptr(prefix) if prefix is not None else None,
                                    _lib.stream_handle()), "pdm_alpha_support")
@@ -385,12 +387,23 @@ def standard_distance_map(volume: Volume, grid: BlockGrid, tf: TransferFunction,
     """Full recompute for one TF: occupancy scan + distance transform
     (acceleration.py:184-196, the Deakin & Knackstedt baseline), fused: the
     occupancy kernel writes the transform's {0, 255} seed into D directly
-    (pdm_standard_distance_map_voxel / _minmax), the passes run in place."""
-    nz, prefix = _tf_support(volume, grid, tf, mode)
+    (pdm_standard_distance_map_voxel / _minmax), the passes run in place.
+
+    A TF whose support is every intensity or none makes every block occupied
+    (each block holds a voxel, and its apron range meets the support) or none:
+    D is then all 0 / all 255 without a volume pass -- the reference's block
+    scans exit at the first voxel or find nothing (_kernels.py:113-134).  The
+    support size comes back from the device (4 bytes) to pick the path."""
+    nz, prefix = _tf_support(volume, grid, tf, mode, prefix_too=True)
     L = _lib.lib()
     st = _lib.stream_handle()
     out = device.empty(grid.bdims, np.uint8)
-    if mode == "voxel":
+    span = 1 << volume.bits
+    support = int(prefix[span].item())  # waits for the support kernels only
+    if support == 0 or support == span:
+        _lib.check(L.pdm_fill_u8(_lib.ptr(out), out.numel(), 255 if support == 0 else 0, st),
+                   "pdm_fill_u8")
+    elif mode == "voxel":
         vox = volume.device_voxels()
         _lib.check(L.pdm_standard_distance_map_voxel(_lib.ptr(vox), volume.bits, *volume.dims,
                                                      grid.b, _lib.ptr(nz), _lib.ptr(out), st),
@@ -479,7 +492,7 @@ def combine(pdm_set: PdmSet, selection: PartitionSelection,
     flags = selection.device_flags()
     if (flags is not None and selection._selected is None and max_maps_per_pass is None
             and pdm_set.n <= _MAX_FLAGS):
-        # selection still on the device (select_partitions): no host round trip
+        # selection held on the device (select_partitions_device, the session)
         out = device.empty(grid.bdims, np.uint8)
         combine_flags_into(pdm_set, flags, out)
     else:
@@ -607,21 +620,57 @@ def load_distance_map(path) -> DistanceMap:
     return DistanceMap(b=b, bdims=(bx, by, bz), dist=payload.reshape((bx, by, bz)).copy())
 
 
-def save_pdm_set(pdm_set: PdmSet, path) -> None:
-    """'PDMS' + <9I (b, dims, bdims, n, mode) + n x <2I bounds + n raw maps."""
+_IO_CHUNK = 32 << 20  # bytes per pinned staging buffer (two in flight)
+
+
+def _stage_buffers():
+    t = device.torch()
+    return ([t.empty(_IO_CHUNK, dtype=t.uint8, pin_memory=True) for _ in range(2)],
+            [t.cuda.Event() for _ in range(2)])
+
+
+def _set_header(pdm_set: PdmSet) -> bytes:
     g = pdm_set.grid
     head = _SET_MAGIC + struct.pack("<9I", g.b, *g.dims, *g.bdims, pdm_set.n,
                                     0 if pdm_set.occupancy_mode == "voxel" else 1)
-    bounds = b"".join(struct.pack("<2I", lo, hi) for lo, hi in pdm_set.scheme.bounds())
-    nb = g.num_blocks
-    maps = device.to_host(pdm_set.storage[:, :nb], np.uint8).tobytes()
-    Path(path).write_bytes(head + bounds + maps)
+    return head + b"".join(struct.pack("<2I", lo, hi) for lo, hi in pdm_set.scheme.bounds())
 
 
-def load_pdm_set(path) -> PdmSet:
-    """Reads a 'PDMS' dump straight into one device allocation."""
-    raw = Path(path).read_bytes()
-    if raw[:4] != _SET_MAGIC:
+def save_pdm_set(pdm_set: PdmSet, path) -> None:
+    """'PDMS' + <9I (b, dims, bdims, n, mode) + n x <2I bounds + n raw maps
+    (acceleration.py:297-315 byte format).  Device-resident planes stream to
+    the file through two pinned buffers (the D2H of chunk i+1 overlaps the
+    write of chunk i); a set of host maps is written as is (no device)."""
+    nb = pdm_set.grid.num_blocks
+    with open(path, "wb") as f:
+        f.write(_set_header(pdm_set))
+        if pdm_set._storage is None:
+            for dm in pdm_set.pdms:
+                f.write(np.ascontiguousarray(dm.dist, dtype=np.uint8).tobytes())
+            return
+        st = pdm_set.storage
+        bufs, evs = _stage_buffers()
+        jobs = [(p, o, min(_IO_CHUNK, nb - o)) for p in range(pdm_set.n)
+                for o in range(0, nb, _IO_CHUNK)]
+        pending = None
+        for i, (p, o, ln) in enumerate(jobs):
+            k = i % 2
+            bufs[k][:ln].copy_(st[p, o:o + ln], non_blocking=True)
+            evs[k].record()
+            if pending is not None:
+                evs[pending[0]].synchronize()
+                f.write(memoryview(bufs[pending[0]][:pending[1]].numpy()))
+            pending = (k, ln)
+        if pending is not None:
+            evs[pending[0]].synchronize()
+            f.write(memoryview(bufs[pending[0]][:pending[1]].numpy()))
+
+
+def _read_set_header(f, path):
+    """(grid, scheme, mode, payload offset) of a 'PDMS' dump, validated like
+    the reference's load_pdm_set (acceleration.py:318-354)."""
+    raw = f.read(40)
+    if raw[:4] != _SET_MAGIC or len(raw) < 40:
         raise VolumeError(f"{path} is not a partition set dump")
     vals = struct.unpack_from("<9I", raw, 4)
     b, dims, bdims, n = vals[0], vals[1:4], tuple(vals[4:7]), vals[7]
@@ -629,16 +678,61 @@ def load_pdm_set(path) -> PdmSet:
     grid = BlockGrid.for_dims(dims, b)
     if grid.bdims != bdims:
         raise VolumeError(f"{path} header block dims are inconsistent")
-    off = 40
-    bounds = [struct.unpack_from("<2I", raw, off + 8 * i) for i in range(n)]
-    off += 8 * n
-    nb = grid.num_blocks
-    if len(raw) - off != n * nb:
+    braw = f.read(8 * n)
+    if len(braw) != 8 * n:
+        raise VolumeError(f"{path} payload size does not match header")
+    bounds = [struct.unpack_from("<2I", braw, 8 * i) for i in range(n)]
+    off = 40 + 8 * n
+    if os.fstat(f.fileno()).st_size - off != n * grid.num_blocks:
         raise VolumeError(f"{path} payload size does not match header")
     scheme = PartitionScheme(tuple(Partition(lo, hi) for lo, hi in bounds))
-    maps = np.frombuffer(raw, dtype=np.uint8, count=n * nb, offset=off).reshape(n, nb)
-    pitch = device.plane_pitch(nb)
-    storage = device.empty((n, pitch), np.uint8)
-    storage[:, :nb].copy_(device.torch().from_numpy(maps.copy()))
-    return PdmSet(grid=grid, scheme=scheme, occupancy_mode=mode, init_seconds=0.0,
+    return grid, scheme, mode, off
+
+
+def _read_pdm_set_host(path):
+    """Host-side parse of a 'PDMS' dump: (grid, scheme, mode, maps uint8
+    [n, num_blocks] memory-mapped) -- no device."""
+    with open(path, "rb") as f:
+        grid, scheme, mode, off = _read_set_header(f, path)
+    maps = np.memmap(path, dtype=np.uint8, mode="r", offset=off,
+                     shape=(scheme.n, grid.num_blocks))
+    return grid, scheme, mode, maps
+
+
+def load_pdm_set(path) -> PdmSet:
+    """Reads a 'PDMS' dump straight into one [n][plane_pitch] device
+    allocation: the payload streams through two pinned buffers (the read of
+    chunk i+1 overlaps the DMA of chunk i), then the merge's packed planes are
+    built on the device.  The PCIe delta forms of D' are enabled only if every
+    chunk of every loaded map is 1-Lipschitz (pdm_count_nonlipschitz_chunks)."""
+    with open(path, "rb") as f:
+        grid, scheme, mode, off = _read_set_header(f, path)
+        n, nb = scheme.n, grid.num_blocks
+        storage = device.empty((n, device.plane_pitch(nb)), np.uint8)
+        bufs, evs = _stage_buffers()
+        used = [False, False]
+        i = 0
+        for p in range(n):
+            for o in range(0, nb, _IO_CHUNK):
+                ln = min(_IO_CHUNK, nb - o)
+                k = i % 2
+                if used[k]:
+                    evs[k].synchronize()  # the DMA out of this buffer has finished
+                view = bufs[k][:ln].numpy()
+                if f.readinto(memoryview(view)) != ln:
+                    raise VolumeError(f"{path} payload size does not match header")
+                storage[p, o:o + ln].copy_(bufs[k][:ln], non_blocking=True)
+                evs[k].record()
+                used[k] = True
+                i += 1
+    pset = PdmSet(grid=grid, scheme=scheme, occupancy_mode=mode, init_seconds=0.0,
                   storage=storage)
+    L = _lib.lib()
+    bad = device.empty((1,), np.int32)
+    _lib.check(L.pdm_count_nonlipschitz_chunks(_lib.ptr(storage), pset.plane_pitch, nb, n,
+                                               _lib.ptr(bad), _lib.stream_handle()),
+               "pdm_count_nonlipschitz_chunks")
+    pset.packed()  # pack at load, not in the first merge
+    pset._delta_ok = int(bad.item()) == 0
+    device.complete()
+    return pset

@@ -489,6 +489,17 @@ extern "C" int pdm_version(void) { return 1; }
 
 extern "C" const char *pdm_last_error(void) { return g_last_error; }
 
+extern "C" int pdm_fill_u8(uint8_t *dst, int64_t bytes, int32_t value, pdm_stream_t stream) {
+    PDM_REQUIRE(dst && bytes >= 0 && value >= 0 && value <= 255, "pdm_fill_u8: bad arguments");
+    PDM_CUDA_TRY(cudaMemsetAsync(dst, value, (size_t)bytes, as_stream(stream)));
+    return PDM_OK;
+}
+
+extern "C" int pdm_stream_synchronize(pdm_stream_t stream) {
+    PDM_CUDA_TRY(cudaStreamSynchronize(as_stream(stream)));
+    return PDM_OK;
+}
+
 extern "C" int pdm_device_sm_count(int device) {
     int n = 0;
     if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) {
@@ -547,6 +558,29 @@ extern "C" int pdm_select(const double *alpha, int64_t span, int64_t alpha_strid
                                                                     flags);
     }
     return cuda_status("select_kernel");
+}
+
+// select_partitions(tf, scheme) in one call (transfer.py:250-259): gather the
+// TF's alpha column from host memory into pinned staging, DMA it into HBM,
+// run the f64 `> 0.0` selection, DMA the n flags back and wait -- the
+// reference returns a finished host selection, and so does this.  One C call
+// instead of a chain of framework calls keeps the per-TF-change host cost at
+// a few microseconds.
+extern "C" int pdm_select_tf(const double *lut_alpha, int64_t span, int64_t lut_stride,
+                             double *stage_host, double *stage_dev, const int32_t *starts,
+                             int32_t n, int32_t max_width, uint8_t *flags_dev, uint8_t *flags_host,
+                             pdm_stream_t stream) {
+    PDM_REQUIRE(lut_alpha && stage_host && stage_dev && flags_host,
+                "pdm_select_tf: null pointer");
+    int st = pdm_gather_f64_host(lut_alpha, span, lut_stride, stage_host);
+    if (st) return st;
+    cudaStream_t s = as_stream(stream);
+    PDM_CUDA_TRY(cudaMemcpyAsync(stage_dev, stage_host, (size_t)span * sizeof(double),
+                                 cudaMemcpyHostToDevice, s));
+    if ((st = pdm_select(stage_dev, span, 1, starts, n, max_width, flags_dev, stream))) return st;
+    PDM_CUDA_TRY(cudaMemcpyAsync(flags_host, flags_dev, (size_t)n, cudaMemcpyDeviceToHost, s));
+    PDM_CUDA_TRY(cudaStreamSynchronize(s));
+    return PDM_OK;
 }
 
 extern "C" int pdm_alpha_support(const double *alpha, int64_t span, int64_t alpha_stride,

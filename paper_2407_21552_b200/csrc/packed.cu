@@ -955,3 +955,53 @@ extern "C" int pdm_dprime_to_host(const uint8_t *d, int64_t map_bytes, uint8_t *
     }
     return PDM_OK;
 }
+
+namespace pdm {
+// ---- chunk Lipschitz check (maps loaded from elsewhere) -------------------
+// The delta forms of D' on PCIe (formats 2/3) need every 16-block chunk of
+// every selected map to change by at most 1 from block to block.  Sets built
+// here satisfy it by construction (distance fields with bz % 16 == 0); for a
+// set loaded from a dump (acceleration.py:279-354) this kernel counts the
+// chunks that do not, so the loader can pick the delta forms only when they
+// are exact.  Thread = one chunk of one plane (16 bytes); the partial last
+// chunk checks its in-map bytes only.
+__global__ void __launch_bounds__(256)
+    lipschitz_chunks_kernel(const uint8_t *__restrict__ pdms, int64_t pitch, int64_t map_bytes,
+                            int n, int64_t nchunks, unsigned int *bad) {
+    const int64_t total = (int64_t)n * nchunks;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    unsigned int nbad = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += stride) {
+        const int64_t p = i / nchunks, c = i - p * nchunks;
+        const uint8_t *src = pdms + p * pitch + c * 16;
+        const int m = (int)min((int64_t)16, map_bytes - c * 16);
+        int prev = src[0], worst = 0;
+        for (int j = 1; j < m; ++j) {
+            const int v = src[j];
+            worst = max(worst, abs(v - prev));
+            prev = v;
+        }
+        nbad += worst > 1;
+    }
+    if (nbad) atomicAdd(bad, nbad);
+}
+
+}  // namespace pdm
+
+extern "C" int pdm_count_nonlipschitz_chunks(const uint8_t *pdms, int64_t plane_pitch,
+                                             int64_t map_bytes, int32_t n, uint32_t *count,
+                                             pdm_stream_t stream) {
+    PDM_REQUIRE(pdms && count, "pdm_count_nonlipschitz_chunks: null pointer");
+    PDM_REQUIRE(map_bytes >= 1 && plane_pitch >= map_bytes && n >= 1,
+                "pdm_count_nonlipschitz_chunks: bad sizes");
+    cudaStream_t s = as_stream(stream);
+    PDM_CUDA_TRY(cudaMemsetAsync(count, 0, sizeof(uint32_t), s));
+    const int64_t nchunks = ceil_div(map_bytes, 16);
+    int64_t grid = ceil_div((int64_t)n * nchunks, 256);
+    const int64_t cap =
+        (int64_t)sm_count() * resident_ctas((const void *)lipschitz_chunks_kernel, 256, 0);
+    if (grid > cap) grid = cap;
+    lipschitz_chunks_kernel<<<(unsigned)grid, 256, 0, s>>>(pdms, plane_pitch, map_bytes, n,
+                                                           nchunks, count);
+    return cuda_status("lipschitz_chunks_kernel");
+}

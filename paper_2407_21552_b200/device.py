@@ -16,10 +16,16 @@ PLANE_ALIGN = 256  # bytes between partition planes are a multiple of this
 _PINNED_MIN = 1 << 16  # below this a plain pageable copy is cheaper
 
 
-def torch():
-    import torch as _torch
+_TORCH = None
 
-    return _torch
+
+def torch():
+    global _TORCH
+    if _TORCH is None:
+        import torch as _torch
+
+        _TORCH = _torch
+    return _TORCH
 
 
 def device():
@@ -43,8 +49,14 @@ _VIEW_AS = {np.dtype(np.bool_): np.uint8, np.dtype(np.uint16): np.int16,
             np.dtype(np.uint32): np.int32}
 
 
+_DT_CACHE: dict = {}
+
+
 def _torch_dtype(dt):
-    return getattr(torch(), _TORCH_DTYPE[np.dtype(dt)])
+    got = _DT_CACHE.get(dt)
+    if got is None:
+        got = _DT_CACHE[dt] = getattr(torch(), _TORCH_DTYPE[np.dtype(dt)])
+    return got
 
 
 def to_device(a: np.ndarray):
@@ -85,12 +97,19 @@ def complete() -> None:
     """Wait for the current stream: the public API returns completed results,
     as the reference's synchronous numpy/numba functions do, so a caller's own
     timer (bench.measure_ms, SessionStore.set_tf) measures the device work."""
-    torch().cuda.current_stream().synchronize()
+    from . import _lib
+
+    _lib.check(_lib.lib().pdm_stream_synchronize(_lib.stream_handle()), "stream synchronize")
 
 
 def empty(shape, np_dtype):
+    """Uninitialised tensor on the current CUDA device (raises without one)."""
+    from . import _lib
+
+    if _lib._lib is None:
+        _lib.lib()  # no CUDA device / library: there is no CPU fallback
     return torch().empty(tuple(int(s) for s in shape), dtype=_torch_dtype(np_dtype),
-                         device=device())
+                         device="cuda")
 
 
 def plane_pitch(num_blocks: int) -> int:

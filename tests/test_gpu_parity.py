@@ -277,12 +277,16 @@ def test_combine_is_eager_and_host_view_lazy(built16):
     tf = pdm.TransferFunction(lut=lut)
     sel = pdm.select_partitions(tf, scheme)
     assert torch.cuda.current_stream().query()  # selection complete on return
-    a = pdm.combine(pset, sel)  # device flags
+    a = pdm.combine(pset, sel)  # host selection (select_partitions)
     assert a._dev is not None and a._host is None
     assert torch.cuda.current_stream().query()  # merge complete on return
     assert np.array_equal(a.dist, want) and np.array_equal(a.device().cpu().numpy(), want)
     b = pdm.combine(pset, pdm.select_partitions(tf, scheme))  # device view first
     assert np.array_equal(b.device().cpu().numpy(), want) and np.array_equal(b.dist, want)
+    flags = pdm.select_partitions_device(pdm.transfer.alpha_to_device(tf), scheme)
+    f = pdm.combine(pset, pdm.PartitionSelection(n=16, flags_dev=flags))  # device flags
+    assert torch.cuda.current_stream().query()
+    assert np.array_equal(f.dist, want) and f.dist.ctypes.data != b.dist.ctypes.data
     c = pdm.combine(pset, pdm.PartitionSelection(selected=frozenset({2, 7, 11}), n=16))
     assert torch.cuda.current_stream().query()
     assert np.array_equal(c.dist, want)
@@ -735,3 +739,26 @@ def test_volume_range_kernel(bits):
                                               _lib.stream_handle()), "range")
                 got = tuple(int(v) for v in out.cpu().numpy().view(np.uint32))
                 assert got == (int(h.min()), int(h.max())), (count, where, off)
+
+
+@pytest.mark.parametrize("bits", [8, 16])
+@pytest.mark.parametrize("mode", ["voxel", "range_apron"])
+def test_standard_distance_map_full_and_empty_support(bits, mode):
+    """The constant-D shortcut of the full recompute (support = every
+    intensity or none) against the oracle, next to a one-intensity-short TF
+    that takes the scan + transform path; partial blocks included."""
+    rng = np.random.default_rng(bits)
+    dims, b = (21, 18, 35), 4
+    vox = random_structured_volume(rng, dims, bits)
+    vol = pdm.Volume.from_array(vox)
+    grid = pdm.BlockGrid.for_dims(dims, b)
+    span = 1 << bits
+    for fill in ("full", "empty", "all_but_one"):
+        lut = np.zeros((span, 4))
+        if fill == "full":
+            lut[:, 3] = 0.25
+        elif fill == "all_but_one":
+            lut[:, 3] = 0.25
+            lut[int(vox.flat[0]), 3] = 0.0
+        got = pdm.standard_distance_map(vol, grid, pdm.TransferFunction(lut=lut), mode).dist
+        assert np.array_equal(got, oracle.standard_distance_map(vox, b, lut, mode)), fill

@@ -55,7 +55,7 @@ def test_reference_suite_through_overlay(tmp_path):
     per_file: dict = {}
     failed = []
     for case in ET.parse(junit).getroot().iter("testcase"):
-        f = case.get("classname", "").split(".")[0] + ".py"
+        f = case.get("classname", "").split(".")[-1] + ".py"
         row = per_file.setdefault(f, {"passed": 0, "failed": 0, "skipped": 0})
         if case.find("failure") is not None or case.find("error") is not None:
             row["failed"] += 1
