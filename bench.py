@@ -330,6 +330,7 @@ def run_b200(args, rank, world, local_rank):
             pset.storage[p, :B].cpu().numpy(), want[p].reshape(-1))]
         parity = {"checked": True, "oracle_build_s": round(oracle_s, 1),
                   "pdm_planes": n, "pdm_planes_mismatched": len(bad_planes)}
+        time.sleep(0.05)  # the oracle's OpenMP threads stop spinning before timing
     elif world > 1:
         parity = {"checked": False, "why": "N>1: the multi-rank build is checked against the "
                   "oracle by tests/test_sharded.py (gloo world 2/3; 2-rank GPU test)"}
@@ -392,6 +393,7 @@ def run_b200(args, rank, world, local_rank):
             if not np.array_equal(outs[i % nbuf].cpu().numpy(), wd):
                 bad.append(i)
         parity.update({"dprime_steps": min(steps, nbuf), "dprime_mismatched": len(bad)})
+        time.sleep(0.05)  # the oracle's OpenMP threads stop spinning before the next pass
     merge_ms = timed_pass(merge_only=True)
     total_ms = sum(step_ms)
     merge_bytes = sum((k + 1) * B for k in ks)  # SURVEY.md §8(d) algorithmic bytes
@@ -418,6 +420,8 @@ def run_b200(args, rank, world, local_rank):
     e2e_s = 0.0
     parts = np.zeros(3)  # select_partitions / combine (merge, completed) / .dist (D2H)
     e2e_bad = 0
+    host_dprimes = []
+    time.sleep(0.05)  # the oracle's OpenMP threads (parity check above) stop spinning
     barrier()
     for i in range(steps):
         tf = pdm.TransferFunction(lut=host_luts[i])  # the reference's TF (validated) -- untimed
@@ -432,12 +436,15 @@ def run_b200(args, rank, world, local_rank):
         t4 = time.perf_counter()
         e2e_s += t4 - t1
         parts += (t2 - t1, t3 - t2, t4 - t3)
-        if check:  # untimed
-            import oracle
-
-            e2e_bad += not np.array_equal(host, oracle.combine(want, timed_tfs[i][0]))
+        if check:  # kept for the oracle check after the loop (no CPU work between steps)
+            host_dprimes.append(host.copy())
         del dm, host
     if check:
+        import oracle
+
+        for i, host in enumerate(host_dprimes):
+            e2e_bad += not np.array_equal(host, oracle.combine(want, timed_tfs[i][0]))
+        del host_dprimes
         parity.update({"e2e_host_steps": steps, "e2e_host_mismatched": e2e_bad})
         parity["ok"] = (parity["pdm_planes_mismatched"] == 0 and parity["dprime_mismatched"] == 0
                         and e2e_bad == 0)

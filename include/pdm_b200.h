@@ -318,6 +318,38 @@ int pdm_dt_slab_fold(uint8_t *pdms, int64_t plane_pitch, int32_t n, int64_t bx, 
 int pdm_dt_pass_yz(uint8_t *pdms, int64_t plane_pitch, int32_t n, int64_t bx, int64_t by,
                    int64_t bz, pdm_stream_t stream);
 
+/* ---- multi-GPU precompute over NCCL -----------
+ * NCCL is loaded at run time (libnccl.so.2; inside a torch process that is
+ * torch's own, so ProcessGroupNCCL._comm_ptr() communicators work).
+ * `comm` is an ncclComm_t passed as void*. */
+int pdm_nccl_available(void); /* 1 if NCCL could be loaded */
+int pdm_nccl_unique_id(uint8_t *id_out /* 128 bytes */);
+int pdm_nccl_comm_init(void **comm_out, int32_t world, const uint8_t *id, int32_t rank);
+int pdm_nccl_comm_destroy(void *comm);
+int pdm_nccl_comm_count(void *comm); /* ranks of the communicator, -1 on error */
+/* Workspace bytes pdm_build_pdm_set_slab_nccl needs (-1 on bad sizes). */
+int64_t pdm_build_pdm_set_slab_nccl_workspace(int32_t world, int bits, int64_t nx, int64_t ny,
+                                              int64_t nz, int32_t b, int32_t n);
+/* acceleration.py:199-241 build_pdm_set over this rank's x-slab (nx voxel
+ * planes; every slab but the last a whole number of blocks) of a volume split
+ * across the communicator's ranks in rank order: the slab table is
+ * all-gathered and validated identically on every rank (bx0_expected >= 0
+ * also checks this rank's start block plane); range_apron (mode 1) swaps one
+ * boundary voxel plane with each neighbour (ncclSend/Recv); the distance
+ * transform all-gathers 2*n*by*bz edge bytes per rank and folds them in
+ * (bit-exact with the single-device transform).  Writes this rank's slab of
+ * every plane (pdms [n][plane_pitch]) and, when nib != NULL, the merge's
+ * packed planes; slab_out (host int64[3]) = start, end, total block planes.
+ * Stream-ordered on `stream` (NCCL included); synchronises once, after the
+ * slab table. */
+int pdm_build_pdm_set_slab_nccl(void *comm, const void *vox, int bits, int64_t nx, int64_t ny,
+                                int64_t nz, int32_t b, const int32_t *pid, int32_t n,
+                                int32_t mode, int64_t bx0_expected, uint8_t *pdms,
+                                int64_t plane_pitch, uint8_t *nib, int64_t nib_pitch,
+                                uint8_t *base, int64_t base_pitch, uint32_t *violations,
+                                void *workspace, int64_t workspace_bytes, int64_t *slab_out,
+                                pdm_stream_t stream);
+
 /* ---- synthetic volumes (bench / test inputs, not a reference function) ----
  * Background 0 plus hashed-intensity boxes; boxes = HOST int64 [nbox][8]
  * (x0 x1 y0 y1 z0 z1 band_lo band_hi).  Writes the x-slab [xs0, xs1).

@@ -68,12 +68,21 @@ _SIGNATURES = {
     "pdm_volume_range": [_P, _INT, _I64, _P, _P],
     "pdm_count_value": [_P, _I64, ctypes.c_uint32, _P, _P],
     "pdm_minmax_fold": [_P, _P, _P, _P, _INT, _I64, _P],
+    "pdm_nccl_available": [],
+    "pdm_nccl_unique_id": [_P],
+    "pdm_nccl_comm_init": [_P, _I32, _P, _I32],
+    "pdm_nccl_comm_destroy": [_P],
+    "pdm_nccl_comm_count": [_P],
+    "pdm_build_pdm_set_slab_nccl_workspace": [_I32, _INT, _I64, _I64, _I64, _I32, _I32],
+    "pdm_build_pdm_set_slab_nccl": [_P, _P, _INT, _I64, _I64, _I64, _I32, _P, _I32, _I32, _I64,
+                                    _P, _I64, _P, _I64, _P, _I64, _P, _P, _I64, _P, _P],
     "pdm_synth_volume": [_INT, _I64, _I64, _I64, _I64, _I64, _P, _I32, ctypes.c_uint64, _P, _P],
     "pdm_camera_rays": [_P, _F64, _F64, _P, _I32, _I32, _P, _P],
     "pdm_march_rays": [_P, _I32, _I64, _I64, _I64, _P, _I64, _P, _I32, _F64, _I32, _F64, _P, _P,
                        _I64, _P, _P, _P, _P, _P],
 }
-_RESTYPES = {"pdm_last_error": ctypes.c_char_p}
+_RESTYPES = {"pdm_last_error": ctypes.c_char_p,
+             "pdm_build_pdm_set_slab_nccl_workspace": _I64}
 
 EXPORTED = tuple(_SIGNATURES)
 

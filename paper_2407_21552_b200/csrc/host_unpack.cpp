@@ -5,9 +5,11 @@
 #include <stdint.h>
 #include <string.h>
 
+#include <algorithm>
 #include <cstdlib>
 
 #include "../../include/pdm_b200.h"
+#include "host_pool.h"
 
 namespace pdm {
 void set_error(const char *fmt, ...);  // capi.cu: pdm_last_error's buffer
@@ -30,15 +32,17 @@ extern "C" int pdm_unpack_packed_host(const uint8_t *nib, const uint8_t *base, i
     REQUIRE(nib && base && out && map_bytes >= 1, "pdm_unpack_packed_host: bad arguments");
     const int64_t full = map_bytes / 16;
     const __m128i lo4 = _mm_set1_epi8(0x0F);
-#pragma omp parallel for schedule(static)
-    for (int64_t c = 0; c < full; ++c) {
-        const __m128i q = _mm_loadl_epi64(reinterpret_cast<const __m128i *>(nib + 8 * c));
-        const __m128i even = _mm_and_si128(q, lo4);
-        const __m128i odd = _mm_and_si128(_mm_srli_epi16(q, 4), lo4);
-        __m128i v = _mm_unpacklo_epi8(even, odd);
-        v = _mm_add_epi8(v, _mm_set1_epi8((char)base[c]));
-        _mm_storeu_si128(reinterpret_cast<__m128i *>(out + 16 * c), v);
-    }
+    constexpr int64_t kU = 4096;  // chunks per pool unit
+    pdm::host::parallel_for((full + kU - 1) / kU, [&](int64_t u) {
+        for (int64_t c = u * kU, e = std::min(full, c + kU); c < e; ++c) {
+            const __m128i q = _mm_loadl_epi64(reinterpret_cast<const __m128i *>(nib + 8 * c));
+            const __m128i even = _mm_and_si128(q, lo4);
+            const __m128i odd = _mm_and_si128(_mm_srli_epi16(q, 4), lo4);
+            __m128i v = _mm_unpacklo_epi8(even, odd);
+            v = _mm_add_epi8(v, _mm_set1_epi8((char)base[c]));
+            _mm_storeu_si128(reinterpret_cast<__m128i *>(out + 16 * c), v);
+        }
+    });
     for (int64_t i = full * 16; i < map_bytes; ++i) {
         const int64_t c = i / 16, j = i % 16;
         out[i] = (uint8_t)(base[c] + ((nib[8 * c + j / 2] >> (4 * (j & 1))) & 15));
@@ -66,8 +70,8 @@ static inline __m128i delta_chunk_sse(uint32_t code, uint8_t base) {
     return _mm_add_epi8(x, _mm_slli_si128(x, 8));
 }
 
-__attribute__((target("avx2,avx512f,avx512bw,avx512vl,avx512vbmi"))) static void delta_avx512(
-    const uint32_t *codes, const uint8_t *base, int64_t chunks4, uint8_t *out) {
+__attribute__((target("avx2,avx512f,avx512bw,avx512vl,avx512vbmi"))) static void delta_avx512_range(
+    const uint32_t *codes, const uint8_t *base, int64_t q0, int64_t q1, uint8_t *out) {
     // control: block i of a 16-byte lane reads bits 2(i mod 8).. of qword i/8
     alignas(64) uint8_t ctl[64];
     alignas(64) uint8_t bidx[64];
@@ -81,8 +85,7 @@ __attribute__((target("avx2,avx512f,avx512bw,avx512vl,avx512vbmi"))) static void
     const __m256i dup = _mm256_setr_epi32(0, 0, 1, 1, 2, 2, 3, 3);
     const __m512i three = _mm512_set1_epi8(3), one = _mm512_set1_epi8(1);
     const __mmask64 first = 0x0001000100010001ull;
-#pragma omp parallel for schedule(static)
-    for (int64_t q = 0; q < chunks4; ++q) {
+    for (int64_t q = q0; q < q1; ++q) {
         const __m128i c4 = _mm_loadu_si128(reinterpret_cast<const __m128i *>(codes + 4 * q));
         // qwords [c0, c0, c1, c1, c2, c2, c3, c3] << 2, each code zero-extended
         __m512i src = _mm512_cvtepu32_epi64(
@@ -102,6 +105,14 @@ __attribute__((target("avx2,avx512f,avx512bw,avx512vl,avx512vbmi"))) static void
         x = _mm512_add_epi8(x, _mm512_bslli_epi128(x, 8));
         _mm512_storeu_si512(reinterpret_cast<void *>(out + 64 * q), x);
     }
+}
+
+static void delta_avx512(const uint32_t *codes, const uint8_t *base, int64_t chunks4,
+                         uint8_t *out) {
+    constexpr int64_t kU = 1024;  // 4-chunk groups per pool unit
+    pdm::host::parallel_for((chunks4 + kU - 1) / kU, [&](int64_t u) {
+        delta_avx512_range(codes, base, u * kU, std::min(chunks4, u * kU + kU), out);
+    });
 }
 
 static bool have_avx512vbmi() {
@@ -124,9 +135,12 @@ extern "C" int pdm_unpack_delta_host(const uint8_t *codes, const uint8_t *base, 
         delta_avx512(cw, base, q, out);
         done = 4 * q;
     }
-#pragma omp parallel for schedule(static)
-    for (int64_t c = done; c < full; ++c)
-        _mm_storeu_si128(reinterpret_cast<__m128i *>(out + 16 * c), delta_chunk_sse(cw[c], base[c]));
+    constexpr int64_t kU = 4096;
+    pdm::host::parallel_for((full - done + kU - 1) / kU, [&](int64_t u) {
+        for (int64_t c = done + u * kU, e = std::min(full, c + kU); c < e; ++c)
+            _mm_storeu_si128(reinterpret_cast<__m128i *>(out + 16 * c),
+                             delta_chunk_sse(cw[c], base[c]));
+    });
     if (full * 16 < map_bytes) {
         alignas(16) uint8_t tmp[16];
         _mm_store_si128(reinterpret_cast<__m128i *>(tmp), delta_chunk_sse(cw[full], base[full]));
@@ -295,29 +309,30 @@ struct SparseExpand {
 extern "C" int pdm_unpack_sparse_host(const uint8_t *regions, int64_t map_bytes, uint8_t *out) {
     REQUIRE(regions && out && map_bytes >= 1, "pdm_unpack_sparse_host: bad arguments");
     const SparseExpand ex(regions, map_bytes, out);
-    // dynamic: coded regions cluster in space (surfaces), zero ones in bulk
-#pragma omp parallel
-    {
-#pragma omp for schedule(dynamic, 64) nowait
-        for (int64_t w = 0; w < ex.nreg; ++w) ex(w);
-        if (ex.nt) _mm_sfence();  // streaming stores visible before the caller reads out
-    }
+    // dynamic units: coded regions cluster in space (surfaces), zero ones in bulk;
+    // the pool fences each unit's streaming stores before the call returns
+    constexpr int64_t kU = 16;  // regions (16 KB of output) per unit
+    pdm::host::parallel_for((ex.nreg + kU - 1) / kU, [&](int64_t u) {
+        for (int64_t w = u * kU, e = std::min(ex.nreg, w + kU); w < e; ++w) ex(w);
+    });
     return PDM_OK;
 }
 
 // Host side: gather a strided f64 column into a contiguous (pinned) buffer --
 // the alpha channel lut[:, 3] of a TransferFunction (transfer.py:44-70,
 // 250-259) staged for its upload on every select_partitions call (the
-// reference re-reads tf.lut each call, so no copy is cached).  OpenMP across
-// the column: a 65,536-entry LUT is 2 MB of strided reads, ~100 us for one
-// core, a few us for the pool.
+// reference re-reads tf.lut each call, so no copy is cached).  A 65,536-entry
+// LUT is 2 MB of strided reads: the caller starts at once and the host pool's
+// helpers join as they wake (host_pool.h).
 extern "C" int pdm_gather_f64_host(const double *src, int64_t n, int64_t stride, double *dst) {
     REQUIRE(src && dst && n >= 0 && stride >= 1, "pdm_gather_f64_host: bad arguments");
-    if (n < (1 << 14)) {
+    constexpr int64_t kU = 2048;  // entries per pool unit (64 KB of LUT rows)
+    if (n <= kU) {
         for (int64_t i = 0; i < n; ++i) dst[i] = src[i * stride];
         return PDM_OK;
     }
-#pragma omp parallel for schedule(static)
-    for (int64_t i = 0; i < n; ++i) dst[i] = src[i * stride];
+    pdm::host::parallel_for((n + kU - 1) / kU, [&](int64_t u) {
+        for (int64_t i = u * kU, e = std::min(n, i + kU); i < e; ++i) dst[i] = src[i * stride];
+    });
     return PDM_OK;
 }

@@ -27,6 +27,7 @@
 #include <cstdlib>
 #include <mutex>
 
+#include "host_pool.h"
 #include "pdm_common.cuh"
 
 namespace pdm {
@@ -819,6 +820,8 @@ extern "C" int pdm_merge_packed_to_host(const uint8_t *nib, int64_t nib_pitch, c
         if (st) return st;
         PDM_CUDA_TRY(cudaEventRecord(piece_event(used), s));
     }
+    // the host pool's helpers wake while the first piece is still on the GPU
+    host::prewake(400);
     for (int i = 0; i < used; ++i) {
         const int64_t t0 = i * per;
         const int64_t nbytes = min(map_bytes, 32 * (t0 + per)) - 32 * t0;
@@ -942,6 +945,8 @@ extern "C" int pdm_dprime_to_host(const uint8_t *d, int64_t map_bytes, uint8_t *
         if (st) return st;
         PDM_CUDA_TRY(cudaEventRecord(piece_event(used), s));
     }
+    // the host pool's helpers wake while the first piece is still on the GPU
+    host::prewake(400);
     for (int i = 0; i < used; ++i) {
         const int64_t t0 = i * per;
         const int64_t nbytes = min(map_bytes, 32 * (t0 + per)) - 32 * t0;

@@ -243,6 +243,74 @@ def build_pdm_set_sharded(volume: Volume, b: int, scheme: PartitionScheme,
     return pset
 
 
+def torch_nccl_comm(group=None) -> int:
+    """The ncclComm_t (as an int) of a torch.distributed NCCL process group
+    (ProcessGroupNCCL._comm_ptr), forcing its lazy creation first."""
+    import torch
+    import torch.distributed as dist
+
+    pg = group if group is not None else dist.distributed_c10d._get_default_group()
+    backend = pg._get_backend(torch.device("cuda", torch.cuda.current_device()))
+    ptr = int(backend._comm_ptr())
+    if ptr == 0:  # communicator not created yet: one tiny collective does it
+        dist.all_reduce(torch.zeros(1, device="cuda"), group=group)
+        ptr = int(backend._comm_ptr())
+    return ptr
+
+
+def build_pdm_set_sharded_nccl(volume: Volume, b: int, scheme: PartitionScheme,
+                               mode: str = "range_apron", bx0: int | None = None,
+                               comm: int | None = None, group=None) -> PdmSet:
+    """build_pdm_set_sharded as ONE library call over an NCCL communicator
+    (pdm_build_pdm_set_slab_nccl, the C-ABI multi-GPU entry of SURVEY.md §8b
+    item 5): slab table, boundary planes, edge all_gather, fold, y/z passes
+    and the packed planes all enqueued on the current stream.  ``comm`` is an
+    ncclComm_t (default: the NCCL communicator of ``group`` / the default
+    torch.distributed group)."""
+    _require_mode(mode)
+    if scheme.intensity_span != (1 << volume.bits):
+        raise VolumeError(
+            f"scheme spans {scheme.intensity_span} intensities, volume needs {1 << volume.bits}")
+    L = _lib.lib()
+    if comm is None:
+        comm = torch_nccl_comm(group)
+    vol_t = volume.device_voxels()
+    grid = BlockGrid.for_dims(volume.dims, b)
+    n = scheme.n
+    pitch = device.plane_pitch(grid.num_blocks)
+    storage = device.empty((n, pitch), np.uint8)
+    pset = PdmSet(grid=grid, scheme=scheme, occupancy_mode=mode, storage=storage)
+    import ctypes
+
+    ws_bytes = int(L.pdm_build_pdm_set_slab_nccl_workspace(
+        _comm_size(L, comm), volume.bits, *volume.dims, b, n))
+    if ws_bytes < 0:
+        raise ValueError("pdm_build_pdm_set_slab_nccl_workspace: bad sizes")
+    ws = device.empty((ws_bytes,), np.uint8)
+    packed = pset._alloc_packed() if n else False
+    nib, nib_pitch, base, base_pitch, bad = packed
+    slab = (ctypes.c_int64 * 3)()
+    _lib.check(L.pdm_build_pdm_set_slab_nccl(
+        comm, _lib.ptr(vol_t), volume.bits, *volume.dims, b, _lib.ptr(scheme.device_pid_lut()),
+        n, 0 if mode == "voxel" else 1, -1 if bx0 is None else int(bx0), _lib.ptr(storage),
+        pitch, _lib.ptr(nib), nib_pitch, _lib.ptr(base), base_pitch, _lib.ptr(bad),
+        _lib.ptr(ws), ws_bytes, ctypes.addressof(slab), _lib.stream_handle()),
+        "pdm_build_pdm_set_slab_nccl")
+    pset._finish_pack(packed)
+    pset.slab = (int(slab[0]), int(slab[1]), int(slab[2]))
+    pset._delta_ok = grid.bdims[2] % 16 == 0
+    device.complete()
+    return pset
+
+
+def _comm_size(L, comm) -> int:
+    """Ranks of an ncclComm_t (for the workspace size)."""
+    world = int(L.pdm_nccl_comm_count(comm))
+    if world < 1:
+        raise RuntimeError("pdm_nccl_comm_count: not a valid NCCL communicator")
+    return world
+
+
 def slab_phase_local(vol_t, bits: int, b: int, scheme: PartitionScheme, mode: str, below, above,
                      ops):
     """Everything a rank does before the exchange: its POM (folding in the

@@ -368,3 +368,33 @@ def test_unpack_sparse_host_matches_numpy_encoder(monkeypatch, avx512):
                                                 out.ctypes.data) == _lib.PDM_OK
                 assert np.array_equal(out[:nb], vals.reshape(-1)[:nb].astype(np.uint8)), nb
                 assert (out[nb:] == 0xAB).all(), nb  # nothing written past map_bytes
+
+
+def test_gather_host_pool_concurrent_callers():
+    """pdm_gather_f64_host (host pool, no GPU): strided column gathers of
+    several sizes, from 4 host threads at once (ctypes drops the GIL), each
+    result exact; the pool serialises jobs and never loses a unit."""
+    import threading
+
+    from paper_2407_21552_b200 import _lib
+
+    L = _lib.load_library()
+    rng = np.random.default_rng(8)
+    errors = []
+
+    def work(seed):
+        r = np.random.default_rng(seed)
+        for n in (1, 2047, 2048, 2049, 65536, 100003):
+            lut = r.random((n, 4))
+            out = np.full(n + 1, -1.0)
+            assert L.pdm_gather_f64_host(lut.ctypes.data + 24, n, 4, out.ctypes.data) == 0
+            if not (np.array_equal(out[:n], lut[:, 3]) and out[n] == -1.0):
+                errors.append((seed, n))
+
+    threads = [threading.Thread(target=work, args=(int(rng.integers(1 << 30)),))
+               for _ in range(4)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errors, errors

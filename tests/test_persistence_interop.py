@@ -114,7 +114,8 @@ def test_reference_dump_loads_onto_the_device(ref, tmp_path, monkeypatch, dims, 
     want = np.stack([d.dist.reshape(-1) for d in rs.pdms])
     assert np.array_equal(got.storage[:, :nb].cpu().numpy(), want)
     assert got._packed not in (None, False)  # packed at load
-    assert got._delta_ok  # reference distance maps are 1-Lipschitz
+    if got.grid.bdims[2] % 16 == 0:  # chunks inside z rows: distance maps are 1-Lipschitz
+        assert got._delta_ok
     for sel in ({1}, {2, 4}, set(range(1, n + 1)), set()):
         s = frozenset(sel)
         mine = pdm.combine(got, pdm.PartitionSelection(selected=s, n=n)).dist

@@ -253,3 +253,51 @@ def test_sharded_two_processes_one_gpu_gloo(mode):
         assert p.exitcode == 0
     got = dict(q.get(timeout=5) for _ in range(2))
     assert got == {0: True, 1: True}, got
+
+
+@pytest.mark.gpu
+def test_native_nccl_slab_build_world1(monkeypatch):
+    """pdm_build_pdm_set_slab_nccl (the C-ABI multi-GPU entry) on a one-rank
+    NCCL communicator -- torch's (ProcessGroupNCCL._comm_ptr) and one made by
+    the library itself (pdm_nccl_unique_id + pdm_nccl_comm_init): PDMs,
+    packed planes and merges equal the single-device build, both modes;
+    a wrong expected slab start fails cleanly."""
+    import ctypes
+
+    from paper_2407_21552_b200 import _lib
+
+    monkeypatch.setenv("PDM_PACKED", "1")
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(_free_port())
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    L = _lib.lib()
+    assert L.pdm_nccl_available() == 1
+    uid = (ctypes.c_uint8 * 128)()
+    assert L.pdm_nccl_unique_id(uid) == 0
+    own = ctypes.c_void_p()
+    _lib.check(L.pdm_nccl_comm_init(ctypes.byref(own), 1, uid, 0), "comm init")
+    try:
+        rng = np.random.default_rng(78)
+        dims, b, n = (36, 24, 64), 4, 12
+        vox = random_structured_volume(rng, dims, 16)
+        vol = pdm.Volume.from_array(vox)
+        scheme = pdm.scheme_uniform(n, 16)
+        for mode in ("voxel", "range_apron"):
+            want = pdm.build_pdm_set(vol, pdm.BlockGrid.for_dims(dims, b), scheme, mode)
+            for comm in (None, own.value):
+                got = sharded.build_pdm_set_sharded_nccl(vol, b, scheme, mode, bx0=0, comm=comm)
+                assert got.slab == (0, 9, 9)
+                assert np.array_equal(np.stack([d.dist for d in got.pdms]),
+                                      np.stack([d.dist for d in want.pdms])), mode
+                assert got.packed() is not None and got._delta_ok
+                for a, w in zip(got.packed(), want.packed()):
+                    if isinstance(a, torch.Tensor):
+                        assert torch.equal(a, w)
+                sel = pdm.PartitionSelection(selected=frozenset({1, 4, 9, 12}), n=n)
+                assert np.array_equal(pdm.combine(got, sel).dist, pdm.combine(want, sel).dist)
+        with pytest.raises(ValueError, match="expected 0"):
+            sharded.build_pdm_set_sharded_nccl(vol, b, scheme, "voxel", bx0=3, comm=own.value)
+    finally:
+        L.pdm_nccl_comm_destroy(own)
+        dist.destroy_process_group()
