@@ -324,15 +324,48 @@ extern "C" int pdm_unpack_sparse_host(const uint8_t *regions, int64_t map_bytes,
 // reference re-reads tf.lut each call, so no copy is cached).  A 65,536-entry
 // LUT is 2 MB of strided reads: the caller starts at once and the host pool's
 // helpers join as they wake (host_pool.h).
+namespace {
+// dst[i] = src[4 i] for i in [i0, i1) with whole 64-byte loads: 8 outputs
+// from 4 loads and two 2-source permutes (the LUT rows are (r, g, b, a)).
+// The last load of a group reads 3 doubles past element 4 (i + 7): the loop
+// stops one group early at the end of the column (i + 9 <= n).
+__attribute__((target("avx512f"))) static void gather_stride4_avx512(const double *src,
+                                                                     int64_t i0, int64_t i1,
+                                                                     int64_t n, double *dst) {
+    const __m512i lo = _mm512_setr_epi64(0, 4, 8, 12, 0, 0, 0, 0);
+    int64_t i = i0;
+    for (; i + 8 <= i1 && i + 9 <= n; i += 8) {
+        const double *p = src + 4 * i;
+        const __m512d a = _mm512_loadu_pd(p), b = _mm512_loadu_pd(p + 8);
+        const __m512d c = _mm512_loadu_pd(p + 16), d = _mm512_loadu_pd(p + 24);
+        const __m512d ab = _mm512_permutex2var_pd(a, lo, b);  // a0 a4 b0 b4
+        const __m512d cd = _mm512_permutex2var_pd(c, lo, d);
+        _mm512_storeu_pd(dst + i, _mm512_shuffle_f64x2(ab, cd, 0x44));
+    }
+    for (; i < i1; ++i) dst[i] = src[4 * i];
+}
+
+static bool have_avx512f() {
+    static const bool ok = __builtin_cpu_supports("avx512f") && getenv("PDM_NO_AVX512") == nullptr;
+    return ok;
+}
+}  // namespace
+
 extern "C" int pdm_gather_f64_host(const double *src, int64_t n, int64_t stride, double *dst) {
     REQUIRE(src && dst && n >= 0 && stride >= 1, "pdm_gather_f64_host: bad arguments");
-    constexpr int64_t kU = 2048;  // entries per pool unit (64 KB of LUT rows)
+    constexpr int64_t kU = 4096;  // entries per pool unit (128 KB of LUT rows)
+    const bool vec = stride == 4 && have_avx512f();
+    auto unit = [&](int64_t i0, int64_t i1) {
+        if (vec)
+            gather_stride4_avx512(src, i0, i1, n, dst);
+        else
+            for (int64_t i = i0; i < i1; ++i) dst[i] = src[i * stride];
+    };
     if (n <= kU) {
-        for (int64_t i = 0; i < n; ++i) dst[i] = src[i * stride];
+        unit(0, n);
         return PDM_OK;
     }
-    pdm::host::parallel_for((n + kU - 1) / kU, [&](int64_t u) {
-        for (int64_t i = u * kU, e = std::min(n, i + kU); i < e; ++i) dst[i] = src[i * stride];
-    });
+    pdm::host::parallel_for((n + kU - 1) / kU,
+                            [&](int64_t u) { unit(u * kU, std::min(n, u * kU + kU)); });
     return PDM_OK;
 }

@@ -22,7 +22,7 @@ ROOT = Path(__file__).resolve().parents[1]
 
 def _header_symbols() -> set[str]:
     text = (ROOT / "include" / "pdm_b200.h").read_text()
-    return set(re.findall(r"^\s*(?:int|const char \*)\s*(pdm_\w+)\s*\(", text, re.M))
+    return set(re.findall(r"^\s*(?:int|int64_t|const char \*)\s*(pdm_\w+)\s*\(", text, re.M))
 
 
 def test_library_exports_every_header_symbol():
