@@ -74,10 +74,12 @@ int pdm_select(const double *alpha, int64_t span, int64_t alpha_stride, const in
 
 /* select_partitions(tf, scheme) end to end (transfer.py:250-259): gathers
  * alpha = lut_alpha[i * lut_stride] (host memory, e.g. &lut[0][3] with
- * lut_stride 4) into pinned stage_host, copies it to stage_dev (f64[span]),
- * runs pdm_select into flags_dev (uint8[n]), copies the flags to pinned
- * flags_host and synchronises `stream`: returns with the finished selection
- * on the host. */
+ * lut_stride 4) into pinned stage_host, runs pdm_select on it with the kernel
+ * reading stage_host and writing pinned flags_host (uint8[n]) directly
+ * (zero-copy over PCIe: one launch, one wait), and synchronises `stream`:
+ * returns with the finished selection on the host.  stage_dev (f64[span]) and
+ * flags_dev (uint8[n]) are only used, and then required, with
+ * PDM_SELECT_DMA=1 (H2D alpha, select in HBM, D2H flags). */
 int pdm_select_tf(const double *lut_alpha, int64_t span, int64_t lut_stride, double *stage_host,
                   double *stage_dev, const int32_t *starts, int32_t n, int32_t max_width,
                   uint8_t *flags_dev, uint8_t *flags_host, pdm_stream_t stream);
@@ -195,6 +197,19 @@ int pdm_merge_packed_to_host(const uint8_t *nib, int64_t nib_pitch, const uint8_
                              const uint8_t *flags, const int32_t *sel, int32_t k,
                              uint8_t *stage_nib, uint8_t *stage_base, uint8_t *out,
                              int32_t pieces, int32_t format, pdm_stream_t stream);
+
+/* combine() for a caller that reads the host view (acceleration.py:244-276 +
+ * DistanceMap.dist, :65-75), in one pass: the packed merge writes D' as plain
+ * bytes into dprime_dev (HBM, map_bytes, 16-byte aligned) AND in the sparse
+ * delta form (format 3 of pdm_merge_packed_to_host) into pinned `stage`; the
+ * host expands piece i into `out` while later pieces are merged.  Returns
+ * once both D' copies are complete.  Same selection and Lipschitz
+ * requirements as pdm_merge_packed_to_host format 3. */
+int pdm_combine_packed_host(const uint8_t *nib, int64_t nib_pitch, const uint8_t *base,
+                            int64_t base_pitch, int64_t map_bytes, int32_t n,
+                            const uint8_t *flags, const int32_t *sel, int32_t k,
+                            uint8_t *dprime_dev, uint8_t *stage, uint8_t *out, int32_t pieces,
+                            pdm_stream_t stream);
 
 /* DistanceMap.dist for a finished D' in HBM (acceleration.py:71-79 host view;
  * combine() itself completes D' on the device, acceleration.py:244-276): D'

@@ -46,6 +46,8 @@ _SIGNATURES = {
     "pdm_unpack_packed_host": [_P, _P, _I64, _P],
     "pdm_merge_packed_to_host": [_P, _I64, _P, _I64, _I64, _I32, _P, _P, _I32, _P, _P, _P, _I32,
                                  _I32, _P],
+    "pdm_combine_packed_host": [_P, _I64, _P, _I64, _I64, _I32, _P, _P, _I32, _P, _P, _P, _I32,
+                                _P],
     "pdm_gather_f64_host": [_P, _I64, _I64, _P],
     "pdm_dprime_to_host": [_P, _I64, _P, _P, _P, _I32, _I32, _P],
     "pdm_unpack_delta_host": [_P, _P, _I64, _P],

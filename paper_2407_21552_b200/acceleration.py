@@ -131,6 +131,9 @@ class DistanceMap(_BlockArray):
 
     @property
     def dist(self) -> np.ndarray:
+        probe = self.__dict__.get("_probe")
+        if probe is not None:
+            probe.read = True
         return self._host_array()
 
     @property
@@ -501,11 +504,67 @@ def combine(pdm_set: PdmSet, selection: PartitionSelection,
             raise ValueError(f"max_maps_per_pass must be >= 1, got {max_maps_per_pass}")
         sel = np.ascontiguousarray([i - 1 for i in indices], dtype=np.int32)
         out = device.empty(grid.bdims, np.uint8)
+        if 0 < sel.size <= _MAX_PACKED_SEL and _host_reader(pdm_set):
+            return _combine_with_host_view(pdm_set, sel, out)
         _combine_indices(pdm_set, sel, out)
     device.complete()
     dm = DistanceMap(b=grid.b, bdims=grid.bdims, dist=out)
     if _host_packed_pays(pdm_set):
+        probe = _HostReadProbe()
+        pdm_set._last_probe = probe
+        dm._probe = probe
         dm._host_fill = lambda host: _dprime_to_host(pdm_set, out, host)
+    return dm
+
+
+class _HostReadProbe:
+    """Whether the host view of one combine() result was read."""
+
+    __slots__ = ("read", "dual")
+
+    def __init__(self, dual: bool = False):
+        self.read = False
+        self.dual = dual
+
+
+def _host_reader(pdm_set: PdmSet) -> bool:
+    """Should this combine() also stream D''s host view?  Yes while the
+    caller keeps reading ``.dist`` of its results (a CLI / service / script
+    that consumes D' on the host): the last result of this set had its host
+    view read.  A device consumer (the ray marcher, the reference's
+    measure_ms(combine)) never reads it, so it never pays for PCIe.
+    PDM_HOST_SPECULATE=0 turns this off (A/B)."""
+    probe = getattr(pdm_set, "_last_probe", None)
+    if probe is None or not probe.read or not _SPECULATE:
+        return False
+    return _host_packed_pays(pdm_set) and _host_format(pdm_set) == 3
+
+
+_SPECULATE = os.environ.get("PDM_HOST_SPECULATE", "1") != "0"
+
+
+def _combine_with_host_view(pdm_set: PdmSet, sel: np.ndarray, out) -> DistanceMap:
+    """combine() for a host reader, one pass (pdm_combine_packed_host): the
+    merge writes D' into ``out`` (HBM) and its sparse delta form into pinned
+    staging; the host expands each piece while the next is merged.  Returns
+    with both copies complete, so ``.dist`` is free."""
+    L = _lib.lib()
+    grid = pdm_set.grid
+    nib, nib_pitch, base, base_pitch = pdm_set.packed()
+    stage, _ = pdm_set._host_stage()
+    host = device.host_buffer(grid.bdims)
+    nb = grid.num_blocks
+    pieces = max(1, min(16, (-(-nb // 32)) // _HOST_PIECE_ITEMS))
+    _lib.check(L.pdm_combine_packed_host(_lib.ptr(nib), nib_pitch, _lib.ptr(base), base_pitch,
+                                         nb, pdm_set.n, None, sel.ctypes.data, int(sel.size),
+                                         _lib.ptr(out), _lib.ptr(stage), host.ctypes.data,
+                                         pieces, _lib.stream_handle()),
+               "pdm_combine_packed_host")
+    dm = DistanceMap(b=grid.b, bdims=grid.bdims, dist=out)
+    dm._host = host
+    probe = _HostReadProbe(dual=True)
+    pdm_set._last_probe = probe
+    dm._probe = probe
     return dm
 
 

@@ -562,7 +562,8 @@ extern "C" int pdm_select(const double *alpha, int64_t span, int64_t alpha_strid
 
 // select_partitions(tf, scheme) in one call (transfer.py:250-259): gather the
 // TF's alpha column from host memory into pinned staging, DMA it into HBM,
-// run the f64 `> 0.0` selection, DMA the n flags back and wait -- the
+// run the f64 `> 0.0` selection on it (zero-copy, below), store the n flags
+// into pinned host memory and wait -- the
 // reference returns a finished host selection, and so does this.  One C call
 // instead of a chain of framework calls keeps the per-TF-change host cost at
 // a few microseconds.
@@ -570,15 +571,30 @@ extern "C" int pdm_select_tf(const double *lut_alpha, int64_t span, int64_t lut_
                              double *stage_host, double *stage_dev, const int32_t *starts,
                              int32_t n, int32_t max_width, uint8_t *flags_dev, uint8_t *flags_host,
                              pdm_stream_t stream) {
-    PDM_REQUIRE(lut_alpha && stage_host && stage_dev && flags_host,
-                "pdm_select_tf: null pointer");
+    PDM_REQUIRE(lut_alpha && stage_host && flags_host, "pdm_select_tf: null pointer");
+    cudaStream_t s = as_stream(stream);
     int st = pdm_gather_f64_host(lut_alpha, span, lut_stride, stage_host);
     if (st) return st;
-    cudaStream_t s = as_stream(stream);
-    PDM_CUDA_TRY(cudaMemcpyAsync(stage_dev, stage_host, (size_t)span * sizeof(double),
-                                 cudaMemcpyHostToDevice, s));
-    if ((st = pdm_select(stage_dev, span, 1, starts, n, max_width, flags_dev, stream))) return st;
-    PDM_CUDA_TRY(cudaMemcpyAsync(flags_host, flags_dev, (size_t)n, cudaMemcpyDeviceToHost, s));
+    // Zero-copy (default): the select kernel reads the gathered alpha straight
+    // from pinned host memory over PCIe and stores the n flags into pinned
+    // host memory, so the call is one launch and one wait -- the two DMA
+    // round trips (H2D alpha, D2H flags) each added a copy-engine latency.
+    // PDM_SELECT_DMA=1 keeps the DMA chain (A/B).  (Alpha of 8-bit TFs in the
+    // kernel parameters instead measured slower: 5.9 vs 3.9 us of kernel time,
+    // the CTA's staging of a 2 KB parameter block through the constant cache
+    // serialises.)
+    static const bool dma = getenv("PDM_SELECT_DMA") && getenv("PDM_SELECT_DMA")[0] == '1';
+    if (dma) {
+        PDM_REQUIRE(stage_dev && flags_dev, "pdm_select_tf: null device staging");
+        PDM_CUDA_TRY(cudaMemcpyAsync(stage_dev, stage_host, (size_t)span * sizeof(double),
+                                     cudaMemcpyHostToDevice, s));
+        if ((st = pdm_select(stage_dev, span, 1, starts, n, max_width, flags_dev, stream)))
+            return st;
+        PDM_CUDA_TRY(
+            cudaMemcpyAsync(flags_host, flags_dev, (size_t)n, cudaMemcpyDeviceToHost, s));
+    } else if ((st = pdm_select(stage_host, span, 1, starts, n, max_width, flags_host, stream))) {
+        return st;
+    }
     PDM_CUDA_TRY(cudaStreamSynchronize(s));
     return PDM_OK;
 }

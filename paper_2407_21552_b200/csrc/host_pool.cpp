@@ -44,7 +44,18 @@ inline void run(Job *j) {
     }
 }
 
-constexpr int64_t kLingerUs = 40;  // a helper spins this long after a job (next piece)
+// A helper keeps spinning this long after a job before it sleeps, so the next
+// piece of a D' expansion and the next TF change's alpha gather find it
+// awake (a futex wake-up costs ~50 us, longer than a whole 2 MB gather):
+// the same trade as OpenMP runtimes' spin-before-sleep (GOMP_SPINCOUNT,
+// KMP_BLOCKTIME).  PDM_HOST_LINGER_US overrides (0: sleep at once).
+int64_t linger_us() {
+    static const int64_t v = [] {
+        const char *e = getenv("PDM_HOST_LINGER_US");
+        return e ? (int64_t)atoll(e) : (int64_t)1000;
+    }();
+    return v;
+}
 
 class Pool {
   public:
@@ -138,7 +149,7 @@ class Pool {
             if (j) {
                 run(j);
                 holders_.fetch_sub(1, std::memory_order_acq_rel);
-                linger = now_us() + kLingerUs;
+                linger = now_us() + linger_us();
             }
         }
     }

@@ -36,10 +36,17 @@ constexpr int kPackedThreads = 256;
 constexpr int kPackedMaxSel = 240;       // indices in kernel parameters
 constexpr int kPackedMaxFlags = 4096;
 
-struct PackedSel {
+// Host index lists travel in the kernel parameters.  A launch copies its
+// whole parameter block, so selections of up to kPackedSmallSel planes (every
+// k <= 31: one cache line of parameters) use the small form.
+template <int N>
+struct PackedSelN {
     int32_t k;
-    int32_t idx[kPackedMaxSel];
+    int32_t idx[N];
 };
+constexpr int kPackedSmallSel = 31;
+using PackedSel = PackedSelN<kPackedMaxSel>;
+using PackedSelSmall = PackedSelN<kPackedSmallSel>;
 
 // ---- packing ---------------------------------------------------------------
 // Thread = one chunk of one plane: 16 raw bytes in, 8 nibble bytes + 1 base
@@ -255,6 +262,9 @@ __device__ __forceinline__ uint32_t ld_stream_u16(const void *p) {
 // A flat chunk (16 equal values) is just its base, an all-zero chunk nothing:
 // in D' most chunks are one or the other (occupied regions, far field), so a
 // TF change sends 1.3-2.9 bytes per 16 blocks instead of 5.
+// kOut 3 with out_base != nullptr: the merge ALSO writes D' as plain bytes to
+// out_base (HBM) -- one pass serves a caller that wants the device map and its
+// host view (combine() when the host view is being read, pdm_combine_packed_host).
 // zeros != nullptr (D' bytes only): also count D''s zero blocks -- the
 // occupied fraction the live session reports (service/app.py:129,
 // acceleration.py:77-79) -- without a second pass over D'.
@@ -380,6 +390,19 @@ __device__ __forceinline__ void emit_item(const PackedAcc &acc, int64_t t, bool 
         uint32_t bases = 0;
         if (live) acc.encode_delta(codes, bases);
         store_sparse(out + (t >> 5) * kSparseRegion, warp_stage, codes, bases);
+        if (out_base != nullptr && live) {  // dual epilogue: plain D' into HBM as well
+            uint4 lo, hi;
+            acc.result(lo, hi);
+            uint8_t *dst = out_base + t * 32;
+            if (t * 32 + 32 <= map_bytes) {
+                st_stream_u4(dst, lo);
+                st_stream_u4(dst + 16, hi);
+            } else {
+                const uint32_t o[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
+                for (int i = 0; t * 32 + i < map_bytes; ++i)
+                    dst[i] = (uint8_t)(o[i >> 2] >> (8 * (i & 3)));
+            }
+        }
     } else if (kOut == 2) {
         uint2 codes;
         uint32_t bases;
@@ -475,11 +498,11 @@ __device__ __forceinline__ void fill_table(const uint8_t *nib, int64_t nib_pitch
     }
 }
 
-template <int kOut, bool kCount>
+template <int kOut, bool kCount, class Sel>
 __global__ void __launch_bounds__(kPackedThreads, kPackedCtas)
     combine_packed_kernel(const uint8_t *__restrict__ nib, int64_t nib_pitch,
                           const uint8_t *__restrict__ base, int64_t base_pitch, int64_t map_bytes,
-                          const __grid_constant__ PackedSel sel, uint8_t *__restrict__ out,
+                          const __grid_constant__ Sel sel, uint8_t *__restrict__ out,
                           uint8_t *__restrict__ out_base, unsigned long long *zeros) {
     __shared__ const uint8_t *s_nib[kPackedMaxSel];
     __shared__ const uint8_t *s_base[kPackedMaxSel];
@@ -612,14 +635,24 @@ static int launch_packed(const uint8_t *nib, int64_t nib_pitch, const uint8_t *b
                          unsigned long long *zeros = nullptr, int out_mode = -1) {
     if (zeros) PDM_CUDA_TRY(cudaMemsetAsync(zeros, 0, sizeof(unsigned long long), s));
     if (out_mode < 0) out_mode = out_base ? 1 : 0;
-    auto kern = out_mode == 3 ? combine_packed_kernel<3, false>
-                : out_mode == 2 ? combine_packed_kernel<2, false>
-                : out_mode == 1 ? combine_packed_kernel<1, false>
-                : zeros   ? combine_packed_kernel<0, true>
-                          : combine_packed_kernel<0, false>;
-    kern<<<packed_grid(kern, map_bytes), kPackedThreads, 0, s>>>(nib, nib_pitch, base,
-                                                                  base_pitch, map_bytes, p, out,
-                                                                  out_base, zeros);
+    auto go = [&](auto sel) {
+        using Sel = decltype(sel);
+        auto kern = out_mode == 3 ? combine_packed_kernel<3, false, Sel>
+                    : out_mode == 2 ? combine_packed_kernel<2, false, Sel>
+                    : out_mode == 1 ? combine_packed_kernel<1, false, Sel>
+                    : zeros   ? combine_packed_kernel<0, true, Sel>
+                              : combine_packed_kernel<0, false, Sel>;
+        kern<<<packed_grid(kern, map_bytes), kPackedThreads, 0, s>>>(
+            nib, nib_pitch, base, base_pitch, map_bytes, sel, out, out_base, zeros);
+    };
+    if (p.k <= kPackedSmallSel) {
+        PackedSelSmall small;
+        small.k = p.k;
+        for (int i = 0; i < p.k; ++i) small.idx[i] = p.idx[i];
+        go(small);
+    } else {
+        go(p);
+    }
     return cuda_status("combine_packed_kernel");
 }
 
@@ -782,14 +815,20 @@ static cudaEvent_t piece_event(int i) {
 }
 }  // namespace pdm
 
-extern "C" int pdm_merge_packed_to_host(const uint8_t *nib, int64_t nib_pitch, const uint8_t *base,
-                                        int64_t base_pitch, int64_t map_bytes, int32_t n,
-                                        const uint8_t *flags, const int32_t *sel, int32_t k,
-                                        uint8_t *stage_nib, uint8_t *stage_base, uint8_t *out,
-                                        int32_t pieces, int32_t format, pdm_stream_t stream) {
-    const char *fn = "pdm_merge_packed_to_host";
+namespace pdm {
+// Shared body of pdm_merge_packed_to_host / pdm_combine_packed_host.
+// dprime_dev != nullptr (format 3 only): the same launches also write D' as
+// plain bytes into HBM (dual epilogue).
+static int merge_packed_host_impl(const char *fn, const uint8_t *nib, int64_t nib_pitch,
+                                  const uint8_t *base, int64_t base_pitch, int64_t map_bytes,
+                                  int32_t n, const uint8_t *flags, const int32_t *sel, int32_t k,
+                                  uint8_t *stage_nib, uint8_t *stage_base, uint8_t *dprime_dev,
+                                  uint8_t *out, int32_t pieces, int32_t format,
+                                  pdm_stream_t stream) {
     PDM_REQUIRE(format >= 1 && format <= 3,
                 "%s: format must be 1 (nibble), 2 (delta) or 3 (sparse delta)", fn);
+    PDM_REQUIRE(!dprime_dev || (format == 3 && (uintptr_t)dprime_dev % 16 == 0),
+                "%s: a device D' needs format 3 and 16-byte alignment", fn);
     const int64_t per_item = format == 1 ? 16 : 8;  // staged code bytes per 32 blocks
     int st = check_packed(fn, nib, nib_pitch, base, base_pitch, map_bytes, n, stage_nib,
                           stage_base, format != 3);  // format 3 uses stage_nib only
@@ -809,14 +848,19 @@ extern "C" int pdm_merge_packed_to_host(const uint8_t *nib, int64_t nib_pitch, c
     auto stage_at = [&](int64_t t0) {
         return format == 3 ? stage_nib + (t0 / 32) * kSparseRegion : stage_nib + per_item * t0;
     };
+    // second output of a launch: bases (formats 1, 2) or the device D' (format 3)
+    auto second_at = [&](int64_t t0) -> uint8_t * {
+        if (format == 3) return dprime_dev ? dprime_dev + 32 * t0 : nullptr;
+        return stage_base + 2 * t0;
+    };
     int used = 0;
     for (int64_t t0 = 0; t0 < items; t0 += per, ++used) {
         const int64_t nbytes = min(map_bytes, 32 * (t0 + per)) - 32 * t0;
         st = flags ? launch_packed_flags(nib + 16 * t0, nib_pitch, base + 2 * t0, base_pitch,
-                                         nbytes, n, flags, stage_at(t0), stage_base + 2 * t0, s,
+                                         nbytes, n, flags, stage_at(t0), second_at(t0), s,
                                          nullptr, format)
                    : launch_packed(nib + 16 * t0, nib_pitch, base + 2 * t0, base_pitch, nbytes, p,
-                                   stage_at(t0), stage_base + 2 * t0, s, nullptr, format);
+                                   stage_at(t0), second_at(t0), s, nullptr, format);
         if (st) return st;
         PDM_CUDA_TRY(cudaEventRecord(piece_event(used), s));
     }
@@ -834,6 +878,28 @@ extern "C" int pdm_merge_packed_to_host(const uint8_t *nib, int64_t nib_pitch, c
         if (st) return st;
     }
     return PDM_OK;
+}
+}  // namespace pdm
+
+extern "C" int pdm_merge_packed_to_host(const uint8_t *nib, int64_t nib_pitch, const uint8_t *base,
+                                        int64_t base_pitch, int64_t map_bytes, int32_t n,
+                                        const uint8_t *flags, const int32_t *sel, int32_t k,
+                                        uint8_t *stage_nib, uint8_t *stage_base, uint8_t *out,
+                                        int32_t pieces, int32_t format, pdm_stream_t stream) {
+    return merge_packed_host_impl("pdm_merge_packed_to_host", nib, nib_pitch, base, base_pitch,
+                                  map_bytes, n, flags, sel, k, stage_nib, stage_base, nullptr, out,
+                                  pieces, format, stream);
+}
+
+extern "C" int pdm_combine_packed_host(const uint8_t *nib, int64_t nib_pitch, const uint8_t *base,
+                                       int64_t base_pitch, int64_t map_bytes, int32_t n,
+                                       const uint8_t *flags, const int32_t *sel, int32_t k,
+                                       uint8_t *dprime_dev, uint8_t *stage, uint8_t *out,
+                                       int32_t pieces, pdm_stream_t stream) {
+    const char *fn = "pdm_combine_packed_host";
+    PDM_REQUIRE(dprime_dev, "%s: null device D'", fn);
+    return merge_packed_host_impl(fn, nib, nib_pitch, base, base_pitch, map_bytes, n, flags, sel,
+                                  k, stage, nullptr, dprime_dev, out, pieces, 3, stream);
 }
 
 // ---- a finished D' (plain bytes in HBM) to a host array ---------------------

@@ -108,8 +108,7 @@ def empty(shape, np_dtype):
 
     if _lib._lib is None:
         _lib.lib()  # no CUDA device / library: there is no CPU fallback
-    return torch().empty(tuple(int(s) for s in shape), dtype=_torch_dtype(np_dtype),
-                         device="cuda")
+    return torch().empty(shape, dtype=_torch_dtype(np_dtype), device="cuda")
 
 
 def plane_pitch(num_blocks: int) -> int:

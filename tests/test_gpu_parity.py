@@ -635,6 +635,36 @@ def test_packed_dprime_to_host(monkeypatch, min_blocks, fmt):
             assert np.array_equal(idx_path.device().cpu().numpy(), want), (dims, s)
 
 
+def test_combine_streams_host_view_while_it_is_read(monkeypatch):
+    """combine() switches to the one-pass merge that also streams D''s host
+    view (pdm_combine_packed_host) only while the caller reads .dist of its
+    results, and back when it stops; every result is complete on return and
+    equal to the oracle on both sides (HBM and host)."""
+    import torch
+
+    monkeypatch.setattr(pdm.acceleration, "_HOST_PACKED_MIN_BLOCKS", 0)
+    monkeypatch.setattr(pdm.acceleration, "_HOST_PIECE_ITEMS", 8)  # several pieces
+    monkeypatch.setenv("PDM_HOST_FORMAT", "3")
+    rng = np.random.default_rng(33)
+    dims, b = (64, 48, 128), 2
+    vox = random_structured_volume(rng, dims, 8)
+    scheme = pdm.scheme_uniform(8, 8)
+    pset = pdm.build_pdm_set(pdm.Volume.from_array(vox), pdm.BlockGrid.for_dims(dims, b), scheme)
+    assert pset.packed() is not None and pset._delta_ok
+    maps = oracle.build_pdm_set(vox, b, scheme.bounds(), "range_apron")
+    sels = ([2], [1, 3, 8], [4, 5, 6, 7], list(range(1, 9)), [6])
+    dual = []
+    for i, s in enumerate(sels * 2):
+        want = oracle.combine(maps, s)
+        dm = pdm.combine(pset, pdm.PartitionSelection(selected=frozenset(s), n=8))
+        assert torch.cuda.current_stream().query()
+        dual.append(dm._probe.dual)
+        assert np.array_equal(dm.device().cpu().numpy(), want), (i, s)
+        if i < 7:  # a host reader for the first 7 results, then a device-only one
+            assert np.array_equal(dm.dist, want), (i, s)
+    assert dual == [False] + [True] * 7 + [False, False]
+
+
 def test_packed_disabled_by_env_and_dropped(monkeypatch):
     """PDM_PACKED=0 keeps sets raw; drop_packed() forgets a packed copy; both
     merge paths agree."""

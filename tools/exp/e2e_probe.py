@@ -78,6 +78,27 @@ def main():
         flags = pdm.select_partitions_device(pdm.transfer.alpha_to_device(tfs[0]), scheme)
         r["merge_packed_to_host_old"] = timed(lambda: pdm.acceleration._host_packed_pays(pset) and
             L.pdm_merge_packed_to_host(*_old_args(pset, flags, out, L)))
+        sel_idx = np.ascontiguousarray([i - 1 for i in sel.sorted], dtype=np.int32)
+        nib, nib_pitch, base, base_pitch = pset.packed()
+        dprime = device.empty(grid.bdims, np.uint8)
+        pieces = max(1, min(16, (-(-nb // 32)) // pdm.acceleration._HOST_PIECE_ITEMS))
+        r["combine_dual_c"] = timed(lambda: L.pdm_combine_packed_host(
+            _lib.ptr(nib), nib_pitch, _lib.ptr(base), base_pitch, nb, pset.n, None,
+            sel_idx.ctypes.data, int(sel_idx.size), _lib.ptr(dprime), _lib.ptr(stage_n),
+            out.ctypes.data, pieces, _lib.stream_handle()))
+        r["merge_to_host_idx_c"] = timed(lambda: L.pdm_merge_packed_to_host(
+            _lib.ptr(nib), nib_pitch, _lib.ptr(base), base_pitch, nb, pset.n, None,
+            sel_idx.ctypes.data, int(sel_idx.size), _lib.ptr(stage_n), _lib.ptr(stage_b),
+            out.ctypes.data, pieces, 3, _lib.stream_handle()))
+
+        def reader_combine():
+            pset._last_probe = pdm.acceleration._HostReadProbe()
+            pset._last_probe.read = True
+            return pdm.combine(pset, sel).dist
+
+        r["combine_dual_py_dist"] = timed(reader_combine)
+        r["step_total_reader"] = timed(lambda: pdm.combine(pset, pdm.select_partitions(
+            tfs[next(it) % 40], scheme)).dist)
         res[f"{dims[0]}^3_n{n}"] = r
         del pset, vol
     print(json.dumps(res, indent=1))
