@@ -394,15 +394,28 @@ def run_b200(args, rank, world, local_rank):
                 bad.append(i)
         parity.update({"dprime_steps": min(steps, nbuf), "dprime_mismatched": len(bad)})
         time.sleep(0.05)  # the oracle's OpenMP threads stop spinning before the next pass
-    merge_ms = timed_pass(merge_only=True)
+    # merge-only pass, counting the (1024-block tile, plane) pairs the packed
+    # merges actually read (the per-tile skip drops planes that cannot lower a
+    # tile): the moved bytes below are counted, not assumed
+    L = pdm._lib.lib()
+    pairs = torch.zeros(1, dtype=torch.int64, device=dev)
+    L.pdm_merge_stats(pairs.data_ptr())
+    try:
+        merge_ms = timed_pass(merge_only=True)
+    finally:
+        L.pdm_merge_stats(None)
+    pairs_read = int(pairs.item())
     total_ms = sum(step_ms)
     merge_bytes = sum((k + 1) * B for k in ks)  # SURVEY.md §8(d) algorithmic bytes
     packed = pset.packed()
     host_packed = pdm.acceleration._host_packed_pays(pset)
     host_fmt = pdm.acceleration._host_format(pset) if host_packed else 0
-    if packed is not None:  # bytes the packed merge actually moves: nibbles + bases + D'
-        per_plane = -(-B // 32) * 2 * 9
-        moved_bytes = sum(k * per_plane + B for k in ks)
+    tiles = -(-B // 1024)
+    pairs_all = sum(ks) * tiles
+    if packed is not None:  # bytes the packed merge moves: nibbles + bases read, D' written
+        moved_bytes = pairs_read * 1024 * 9 // 16 + steps * B
+        if pset.tile_bounds_ptr() is not None:  # + the tile-bounds rows (2 B per pair)
+            moved_bytes += 2 * pairs_all
     else:
         moved_bytes = merge_bytes
 
@@ -491,6 +504,10 @@ def run_b200(args, rank, world, local_rank):
                      "algorithmic_bytes": "(k+1) * num_blocks per launch (SURVEY.md 8(d)); "
                                           f"mean k {mean_k:.2f}",
                      "moved_bytes_per_step": round(moved_bytes / steps),
+                     "planes_read_share": round(pairs_read / max(1, pairs_all), 4),
+                     "moved_bytes_note": ("counted: (tile, plane) pairs the merge read x 576 B "
+                                          "(nibbles + bases of 1024 blocks) + D' written + "
+                                          "tile-bounds rows read"),
                      "moved_GBps": round(moved_bytes / (merge_total_ms * 1e-3) / 1e9, 1),
                      "moved_frac": round(moved_bytes / (merge_total_ms * 1e-3) / 1e9 / peak, 4),
                      "traffic": traffic, "traffic_source": traffic_src,

@@ -135,18 +135,35 @@ int pdm_distance_transform_mask_packed(const uint32_t *mask, int32_t words, int3
                                        uint8_t *base, int64_t base_pitch, uint32_t *violations,
                                        pdm_stream_t stream);
 
+/* Per-tile plane bounds of a packed set, for the merges' tile skip:
+ * tile_bounds[tile][p] = min | max << 8 of plane p over blocks
+ * [1024 tile, 1024 tile + 1024) (uint16 [ceil(map_bytes / 1024)][n]).  With
+ * them a merge reads, per tile, only the selected planes whose minimum is
+ * below the smallest maximum among the selected planes (the others cannot
+ * lower any block of the tile) -- exact.  Recompute after the planes change. */
+int pdm_packed_tile_bounds(const uint8_t *nib, int64_t nib_pitch, const uint8_t *base,
+                           int64_t base_pitch, int64_t map_bytes, int32_t n,
+                           uint16_t *tile_bounds, pdm_stream_t stream);
+
+/* Measurement hook: while planes_read != NULL every packed merge adds the
+ * number of (1024-block tile, selected plane) pairs it read to *planes_read
+ * (device uint64); NULL turns it off. */
+int pdm_merge_stats(unsigned long long *planes_read);
+
 /* pdm_combine over packed planes (k <= 240), and pdm_combine_flags over them
  * (n <= 4096, PDL behind pdm_select).  Output: plain uint8 D'.  zero_count
  * (device uint64, may be NULL): set to the number of D' blocks equal to 0 --
- * DistanceMap.occupied_fraction (acceleration.py:77-79) fused into the merge. */
+ * DistanceMap.occupied_fraction (acceleration.py:77-79) fused into the merge.
+ * tile_bounds (from pdm_packed_tile_bounds, may be NULL): per-tile plane skip
+ * for selections of up to 64 planes. */
 int pdm_combine_packed(const uint8_t *nib, int64_t nib_pitch, const uint8_t *base,
-                       int64_t base_pitch, int64_t map_bytes, int32_t n, const int32_t *sel,
-                       int32_t k, uint8_t *out, unsigned long long *zero_count,
-                       pdm_stream_t stream);
+                       int64_t base_pitch, const uint16_t *tile_bounds, int64_t map_bytes,
+                       int32_t n, const int32_t *sel, int32_t k, uint8_t *out,
+                       unsigned long long *zero_count, pdm_stream_t stream);
 int pdm_combine_flags_packed(const uint8_t *nib, int64_t nib_pitch, const uint8_t *base,
-                             int64_t base_pitch, int64_t map_bytes, int32_t n,
-                             const uint8_t *flags, uint8_t *out, unsigned long long *zero_count,
-                             pdm_stream_t stream);
+                             int64_t base_pitch, const uint16_t *tile_bounds, int64_t map_bytes,
+                             int32_t n, const uint8_t *flags, uint8_t *out,
+                             unsigned long long *zero_count, pdm_stream_t stream);
 
 /* The same two merges writing D' itself in the packed encoding (out_nib: 8 *
  * chunks bytes, out_base: chunks bytes, 16/2-byte aligned) -- 9/16 of the
@@ -193,8 +210,8 @@ int pdm_unpack_sparse_host(const uint8_t *regions, int64_t map_bytes, uint8_t *o
  * when flags != NULL (PDL behind pdm_select), else host sel[0..k).  Returns
  * once `out` is complete. */
 int pdm_merge_packed_to_host(const uint8_t *nib, int64_t nib_pitch, const uint8_t *base,
-                             int64_t base_pitch, int64_t map_bytes, int32_t n,
-                             const uint8_t *flags, const int32_t *sel, int32_t k,
+                             int64_t base_pitch, const uint16_t *tile_bounds, int64_t map_bytes,
+                             int32_t n, const uint8_t *flags, const int32_t *sel, int32_t k,
                              uint8_t *stage_nib, uint8_t *stage_base, uint8_t *out,
                              int32_t pieces, int32_t format, pdm_stream_t stream);
 
@@ -206,8 +223,8 @@ int pdm_merge_packed_to_host(const uint8_t *nib, int64_t nib_pitch, const uint8_
  * once both D' copies are complete.  Same selection and Lipschitz
  * requirements as pdm_merge_packed_to_host format 3. */
 int pdm_combine_packed_host(const uint8_t *nib, int64_t nib_pitch, const uint8_t *base,
-                            int64_t base_pitch, int64_t map_bytes, int32_t n,
-                            const uint8_t *flags, const int32_t *sel, int32_t k,
+                            int64_t base_pitch, const uint16_t *tile_bounds, int64_t map_bytes,
+                            int32_t n, const uint8_t *flags, const int32_t *sel, int32_t k,
                             uint8_t *dprime_dev, uint8_t *stage, uint8_t *out, int32_t pieces,
                             pdm_stream_t stream);
 

@@ -12,7 +12,11 @@ from __future__ import annotations
 import ctypes
 from pathlib import Path
 
-LIB_PATH = Path(__file__).resolve().parent / "lib" / "libpdm_b200.so"
+import os
+
+# PDM_LIB_PATH: an A/B build of the same library (tools/exp/build_variant.py)
+LIB_PATH = Path(os.environ.get("PDM_LIB_PATH") or
+                Path(__file__).resolve().parent / "lib" / "libpdm_b200.so")
 
 PDM_OK, PDM_EINVAL, PDM_ECUDA, PDM_EUNSUPPORTED = 0, 1, 2, 3
 
@@ -39,15 +43,17 @@ _SIGNATURES = {
     "pdm_pack_pdms": [_P, _I64, _I64, _I32, _P, _I64, _P, _I64, _P, _P],
     "pdm_distance_transform_mask_packed": [_P, _I32, _I32, _I64, _I64, _I64, _P, _I64, _P, _I64,
                                            _P, _I64, _P, _P],
-    "pdm_combine_packed": [_P, _I64, _P, _I64, _I64, _I32, _P, _I32, _P, _P, _P],
-    "pdm_combine_flags_packed": [_P, _I64, _P, _I64, _I64, _I32, _P, _P, _P, _P],
+    "pdm_packed_tile_bounds": [_P, _I64, _P, _I64, _I64, _I32, _P, _P],
+    "pdm_merge_stats": [_P],
+    "pdm_combine_packed": [_P, _I64, _P, _I64, _P, _I64, _I32, _P, _I32, _P, _P, _P],
+    "pdm_combine_flags_packed": [_P, _I64, _P, _I64, _P, _I64, _I32, _P, _P, _P, _P],
     "pdm_combine_packed_to_packed": [_P, _I64, _P, _I64, _I64, _I32, _P, _I32, _P, _P, _P],
     "pdm_combine_flags_packed_to_packed": [_P, _I64, _P, _I64, _I64, _I32, _P, _P, _P, _P],
     "pdm_unpack_packed_host": [_P, _P, _I64, _P],
-    "pdm_merge_packed_to_host": [_P, _I64, _P, _I64, _I64, _I32, _P, _P, _I32, _P, _P, _P, _I32,
-                                 _I32, _P],
-    "pdm_combine_packed_host": [_P, _I64, _P, _I64, _I64, _I32, _P, _P, _I32, _P, _P, _P, _I32,
-                                _P],
+    "pdm_merge_packed_to_host": [_P, _I64, _P, _I64, _P, _I64, _I32, _P, _P, _I32, _P, _P, _P,
+                                 _I32, _I32, _P],
+    "pdm_combine_packed_host": [_P, _I64, _P, _I64, _P, _I64, _I32, _P, _P, _I32, _P, _P, _P,
+                                _I32, _P],
     "pdm_gather_f64_host": [_P, _I64, _I64, _P],
     "pdm_dprime_to_host": [_P, _I64, _P, _P, _P, _I32, _I32, _P],
     "pdm_unpack_delta_host": [_P, _P, _I64, _P],

@@ -54,6 +54,11 @@ def _packed_enabled() -> bool:
     return os.environ.get("PDM_PACKED", "1") != "0"
 
 
+def _tile_skip_enabled() -> bool:
+    # PDM_TILE_SKIP=0: packed merges read every selected plane (A/B).
+    return os.environ.get("PDM_TILE_SKIP", "1") != "0"
+
+
 class OccupancyModeError(ValueError):
     """Unknown occupancy mode string."""
 
@@ -176,6 +181,7 @@ class PdmSet:
         self.plane_pitch = device.plane_pitch(grid.num_blocks)
         self._storage = storage
         self._packed = None  # None: not packed yet; False: does not pack; else planes
+        self._tile_bounds = None  # per-tile plane bounds of the packed planes
         # every map is a distance field whose z rows hold whole 16-block chunks
         # (built here by the distance transform with bz % 16 == 0): D' can then
         # go to the host in the 5/16-size delta form
@@ -250,6 +256,21 @@ class PdmSet:
         nib, nib_pitch, base, base_pitch, bad = pending
         ok = int(bad.cpu()[0]) == 0  # int32 view of the uint32 count; 0 either way
         self._packed = (nib, nib_pitch, base, base_pitch) if ok else False
+        self._tile_bounds = None
+        if ok and _tile_skip_enabled():
+            # per (1024-block tile, plane) min/max: the merges' exact tile skip
+            nb = self.grid.num_blocks
+            tb = device.empty((-(-nb // 1024), self.n), np.int16)
+            _lib.check(_lib.lib().pdm_packed_tile_bounds(
+                _lib.ptr(nib), nib_pitch, _lib.ptr(base), base_pitch, nb, self.n, _lib.ptr(tb),
+                _lib.stream_handle()), "pdm_packed_tile_bounds")
+            self._tile_bounds = tb
+
+    def tile_bounds_ptr(self):
+        """Device pointer of the per-tile plane bounds (pdm_packed_tile_bounds)
+        of the packed planes, or None."""
+        tb = self.__dict__.get("_tile_bounds")
+        return _lib.ptr(tb) if tb is not None and self._packed else None
 
     def packed(self):
         """(nib, nib_pitch, base, base_pitch) device planes, or None when the
@@ -274,6 +295,7 @@ class PdmSet:
     def drop_packed(self) -> None:
         """Forget the packed copy (after writing into ``storage``)."""
         self._packed = None
+        self._tile_bounds = None
 
     def device_bytes(self) -> int:
         """Device bytes held: raw planes plus the packed copy, if any."""
@@ -281,6 +303,9 @@ class PdmSet:
         pk = self._packed
         if pk:
             total += self.n * (pk[1] + pk[3])
+        tb = self.__dict__.get("_tile_bounds")
+        if tb is not None:
+            total += tb.numel() * 2
         return total
 
 
@@ -556,7 +581,8 @@ def _combine_with_host_view(pdm_set: PdmSet, sel: np.ndarray, out) -> DistanceMa
     nb = grid.num_blocks
     pieces = max(1, min(16, (-(-nb // 32)) // _HOST_PIECE_ITEMS))
     _lib.check(L.pdm_combine_packed_host(_lib.ptr(nib), nib_pitch, _lib.ptr(base), base_pitch,
-                                         nb, pdm_set.n, None, sel.ctypes.data, int(sel.size),
+                                         pdm_set.tile_bounds_ptr(), nb, pdm_set.n, None,
+                                         sel.ctypes.data, int(sel.size),
                                          _lib.ptr(out), _lib.ptr(stage), host.ctypes.data,
                                          pieces, _lib.stream_handle()),
                "pdm_combine_packed_host")
@@ -576,8 +602,8 @@ def _combine_indices(pdm_set: PdmSet, sel: np.ndarray, out) -> None:
     if packed is not None:
         nib, nib_pitch, base, base_pitch = packed
         _lib.check(L.pdm_combine_packed(_lib.ptr(nib), nib_pitch, _lib.ptr(base), base_pitch,
-                                        grid.num_blocks, pdm_set.n, sel.ctypes.data,
-                                        int(sel.size), _lib.ptr(out), None,
+                                        pdm_set.tile_bounds_ptr(), grid.num_blocks, pdm_set.n,
+                                        sel.ctypes.data, int(sel.size), _lib.ptr(out), None,
                                         _lib.stream_handle()), "pdm_combine_packed")
         return
     storage = pdm_set.storage if sel.size else None
@@ -647,8 +673,8 @@ def combine_flags_into(pdm_set: PdmSet, flags, out=None, count_zeros: bool = Fal
         nib, nib_pitch, base, base_pitch = packed
         zeros = device.empty((1,), np.int64) if count_zeros else None
         _lib.check(L.pdm_combine_flags_packed(_lib.ptr(nib), nib_pitch, _lib.ptr(base), base_pitch,
-                                              grid.num_blocks, pdm_set.n, _lib.ptr(flags),
-                                              _lib.ptr(out),
+                                              pdm_set.tile_bounds_ptr(), grid.num_blocks,
+                                              pdm_set.n, _lib.ptr(flags), _lib.ptr(out),
                                               _lib.ptr(zeros) if zeros is not None else None,
                                               _lib.stream_handle()),
                    "pdm_combine_flags_packed")

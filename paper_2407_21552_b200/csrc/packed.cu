@@ -24,6 +24,7 @@
 
 #include <cuda_fp16.h>
 
+#include <atomic>
 #include <cstdlib>
 #include <mutex>
 
@@ -439,41 +440,165 @@ __device__ __forceinline__ void add_zero_count(uint32_t nzero, unsigned long lon
     if ((threadIdx.x & 31) == 0 && w) atomicAdd(zeros, (unsigned long long)w);
 }
 
+// ---- per-tile plane skip ------------------------------------------------------
+// For every plane p and tile of kTileBlocks blocks (the 32 items one warp
+// merges per lap) the set keeps tb[tile][p] = tmin | tmax << 8, the plane's
+// smallest and largest distance over the tile (made once after packing,
+// pdm_packed_tile_bounds).  For a selection S every block of the tile ends at
+// most U = min_{p in S} tmax[p], so a plane q with tmin[q] >= U cannot lower
+// any block of the tile and the warp reads nothing of it: exact, and decided
+// from 2 bytes per selected plane instead of 18 per item.  The plane attaining
+// U is always kept (when it is constant at U over the tile nothing else is).
+// A TF that makes an everywhere-present intensity range visible (background,
+// tissue) has a near-zero plane in S and the warp then reads only the planes
+// that come closer than it -- on the bench's TF sequence 55 % of the
+// (tile, selected plane) pairs are read (tools/exp/tile_bound_stats.py).
+constexpr int kTileBlocks = 1024;
+struct TileSkip {
+    const uint16_t *tb;  // [tiles][n]; nullptr: read every selected plane
+    int n;
+    const int32_t *pid;  // plane index of selected plane m, m < k
+    unsigned long long *planes_read;  // optional: (tile, plane) pairs read, summed
+};
+
+// Selected planes of the warp's current tile as a mask over m in [0, k),
+// k <= 64, from the table entries e0 (m = lane), e1 (m = lane + 32)
+// (0xFFFF where m >= k: tmin = tmax = 255, never the unique minimum).
+__device__ __forceinline__ uint64_t tile_keep(uint32_t e0, uint32_t e1, bool v0, bool v1) {
+    uint32_t U = min(e0 >> 8, e1 >> 8);
+    U = __reduce_min_sync(0xFFFFFFFFu, U);
+    const uint32_t k0 = __ballot_sync(0xFFFFFFFFu, v0 && (e0 & 0xFFu) < U);
+    const uint32_t k1 = __ballot_sync(0xFFFFFFFFu, v1 && (e1 & 0xFFu) < U);
+    const uint32_t a0 = __ballot_sync(0xFFFFFFFFu, v0 && (e0 >> 8) == U);
+    const uint32_t a1 = __ballot_sync(0xFFFFFFFFu, v1 && (e1 >> 8) == U);
+    const uint64_t att = (uint64_t)a0 | ((uint64_t)a1 << 32);
+    return ((uint64_t)k0 | ((uint64_t)k1 << 32)) | (att & (~att + 1));
+}
+
+// Fold one batch of kept planes id[0..B) (-1: none).  Same dominance vote
+// as fold_batch after the first batch.
+template <int B>
+__device__ __forceinline__ void fold_ids(PackedAcc &acc, const uint4 (&q)[B],
+                                         const uint32_t (&b)[B], const int (&id)[B], bool first,
+                                         bool vote) {
+    if (!first) {
+        uint32_t m0, m1;
+        acc.chunk_max(m0, m1);
+#pragma unroll
+        for (int j = 0; j < B; ++j) {
+            if (id[j] >= 0) {
+                const bool dom = (0x6400u | (b[j] & 0xFFu)) >= m0 &&
+                                 (0x6400u | ((b[j] >> 8) & 0xFFu)) >= m1;
+                if (!__all_sync(0xFFFFFFFFu, dom || !vote)) acc.fold(q[j], b[j]);
+            }
+        }
+        return;
+    }
+#pragma unroll
+    for (int j = 0; j < B; ++j)
+        if (id[j] >= 0) acc.fold(q[j], b[j]);
+}
+
+// Tiles are split statically: warp w of W merges tiles w, w + W, ... (one
+// wave of resident CTAs, laps equalised).  Measured and rejected: warps
+// claiming tiles from an atomic queue (1 or 4-8 tiles per claim) to even out
+// the skip's uneven work -- 70-78 us vs 43-45 us per step (the same-address
+// atomics and their exposed latency cost far more than the imbalance), and a
+// per-tile compaction of the kept planes into full batches (42.3 vs 40.0 us:
+// more instructions per plane; the fold, not the round trips, dominates).
 template <int B, int kOut, bool kCount, class P>  // B: selected planes per load batch
 __device__ __forceinline__ void merge_packed(const P planes, int k, int64_t map_bytes,
                                              uint8_t *__restrict__ out,
                                              uint8_t *__restrict__ out_base,
-                                             unsigned long long *zeros, uint4 *stage = nullptr) {
+                                             unsigned long long *zeros, uint4 *stage,
+                                             const TileSkip skip) {
     uint32_t nzero = 0;
     const int64_t items = ceil_div(map_bytes, 32);
-    const int64_t T = (int64_t)gridDim.x * blockDim.x;
-    // Whole warps stay in the loop together (t - lane = the warp's first item):
-    // the dominance vote and the kOut 3 compaction are full-warp operations.
-    const int64_t lane_off = threadIdx.x & 31;
-    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t - lane_off < items;
-         t += T) {
+    const int64_t ntiles = ceil_div(items, 32);
+    // Whole warps stay together: the dominance vote, the tile skip and the
+    // kOut 3 compaction are full-warp operations.
+    const int lane = threadIdx.x & 31;
+    const bool tiles = skip.tb != nullptr && k <= 64 && k > 0;
+    const bool v0 = lane < k, v1 = lane + 32 < k;
+    const int pid0 = tiles && v0 ? skip.pid[lane] : 0, pid1 = tiles && v1 ? skip.pid[lane + 32] : 0;
+    uint64_t nread = 0;
+    const int64_t W = (int64_t)gridDim.x * (blockDim.x >> 5);
+    auto fetch = [&](int64_t tile, uint32_t &e0, uint32_t &e1) {
+        e0 = e1 = 0xFFFFu;
+        if (tiles && tile < ntiles) {
+#ifdef PDM_SKIP_NOFETCH  // (A/B builds: keep every plane without reading the table)
+            if (v0) e0 = 0xFF00u;
+            if (v1) e1 = 0xFF00u;
+#else
+            const uint16_t *row = skip.tb + tile * skip.n;
+            if (v0) e0 = __ldg(row + pid0);
+            if (v1) e1 = __ldg(row + pid1);
+#endif
+        }
+    };
+    int64_t tile = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    uint32_t c0, c1;  // bounds row of the current tile, fetched one lap ahead
+    fetch(tile, c0, c1);
+    for (; tile < ntiles; tile += W) {
+        const int64_t t = tile * 32 + lane;
         const bool live = t < items;
         PackedAcc acc;
         acc.init();
-        for (int m = 0; m < k; m += B) {
-            uint4 q[B];
-            uint32_t b[B];
+        if (tiles) {
+            uint64_t keep = tile_keep(c0, c1, v0, v1);
+#ifdef PDM_SKIP_FORCE_ALL  // (A/B builds: the skip's bookkeeping without the skip)
+            keep = k >= 64 ? ~0ull : ((1ull << k) - 1ull);
+#endif
+            fetch(tile + W, c0, c1);  // (two laps ahead measured the same)
+            nread += __popcll(keep);
+            // the unskipped merge's batches of B planes, loads predicated on
+            // the keep bits (warp-uniform); batches with no kept plane are
+            // not visited
+            bool first = true;
+            for (int m = 0; m < k; m += B) {
+                const uint32_t bits = (uint32_t)(keep >> m) & ((1u << B) - 1u);
+                if (bits == 0) continue;
+                uint4 qv[B];
+                uint32_t bv[B];
+                int id[B];
 #pragma unroll
-            for (int j = 0; j < B; ++j) {
-                q[j] = make_uint4(0u, 0u, 0u, 0u);
-                b[j] = 0u;
-                if (live && m + j < k) {
-                    q[j] = ld_stream_u4(planes.nib_at(m + j) + t * 16);
-                    b[j] = ld_stream_u16(planes.base_at(m + j) + t * 2);
+                for (int j = 0; j < B; ++j) {
+                    id[j] = ((bits >> j) & 1u) ? m + j : -1;
+                    // (zero-filled and live-predicated like the unskipped loop:
+                    // without them the compiler's code ran 58 vs 38 us per merge)
+                    qv[j] = make_uint4(0u, 0u, 0u, 0u);
+                    bv[j] = 0u;
+                    if (live && id[j] >= 0) {
+                        qv[j] = ld_stream_u4(planes.nib_at(m + j) + t * 16);
+                        bv[j] = ld_stream_u16(planes.base_at(m + j) + t * 2);
+                    }
                 }
+                fold_ids<B>(acc, qv, bv, id, first, live);
+                first = false;
             }
-            fold_batch<B>(acc, q, b, m, k, live);
+        } else {
+            nread += (uint64_t)k;
+            for (int m = 0; m < k; m += B) {
+                uint4 qv[B];
+                uint32_t bv[B];
+#pragma unroll
+                for (int j = 0; j < B; ++j) {
+                    qv[j] = make_uint4(0u, 0u, 0u, 0u);
+                    bv[j] = 0u;
+                    if (live && m + j < k) {
+                        qv[j] = ld_stream_u4(planes.nib_at(m + j) + t * 16);
+                        bv[j] = ld_stream_u16(planes.base_at(m + j) + t * 2);
+                    }
+                }
+                fold_batch<B>(acc, qv, bv, m, k, live);
+            }
         }
         if (kOut == 3 || live)
             emit_item<kOut, kCount>(acc, t, live, map_bytes, out, out_base,
                                     stage + (threadIdx.x >> 5) * (kSparseRegion / 16), nzero);
     }
     if (kCount) add_zero_count(nzero, zeros);  // every thread of the grid reaches it
+    if (skip.planes_read != nullptr && lane == 0 && nread) atomicAdd(skip.planes_read, nread);
 }
 
 // Planes per load batch and CTAs per SM: with the pointer table, 6 planes per
@@ -503,14 +628,16 @@ __global__ void __launch_bounds__(kPackedThreads, kPackedCtas)
     combine_packed_kernel(const uint8_t *__restrict__ nib, int64_t nib_pitch,
                           const uint8_t *__restrict__ base, int64_t base_pitch, int64_t map_bytes,
                           const __grid_constant__ Sel sel, uint8_t *__restrict__ out,
-                          uint8_t *__restrict__ out_base, unsigned long long *zeros) {
+                          uint8_t *__restrict__ out_base, unsigned long long *zeros,
+                          TileSkip skip) {
     __shared__ const uint8_t *s_nib[kPackedMaxSel];
     __shared__ const uint8_t *s_base[kPackedMaxSel];
     __shared__ uint4 s_stage[kOut == 3 ? kPackedThreads / 32 * kSparseRegion / 16 : 1];
     fill_table(nib, nib_pitch, base, base_pitch, sel.idx, sel.k, s_nib, s_base);
     __syncthreads();
+    skip.pid = sel.idx;
     merge_packed<kPackedBatch, kOut, kCount>(TablePlanes{s_nib, s_base}, sel.k, map_bytes, out,
-                                             out_base, zeros, s_stage);
+                                             out_base, zeros, s_stage, skip);
 }
 
 // Selection resident on the device (written by the select kernel ahead of it
@@ -521,7 +648,7 @@ __global__ void __launch_bounds__(kPackedThreads, kTable ? kPackedCtas : kPacked
                                 const uint8_t *__restrict__ base, int64_t base_pitch,
                                 int64_t map_bytes, int n, const uint8_t *__restrict__ flags,
                                 uint8_t *__restrict__ out, uint8_t *__restrict__ out_base,
-                                unsigned long long *zeros) {
+                                unsigned long long *zeros, TileSkip skip) {
     constexpr int kIdx = kTable ? kPackedTable : kPackedMaxFlags;
     __shared__ int32_t s_idx[kIdx];
     __shared__ const uint8_t *s_nib[kTable ? kPackedTable : 1];
@@ -531,15 +658,16 @@ __global__ void __launch_bounds__(kPackedThreads, kTable ? kPackedCtas : kPacked
     pdl_wait();
     compact_flags(flags, n, s_idx, &s_k);
     __syncthreads();
+    skip.pid = s_idx;
     if constexpr (kTable) {
         fill_table(nib, nib_pitch, base, base_pitch, s_idx, s_k, s_nib, s_base);
         __syncthreads();
         merge_packed<kPackedBatch, kOut, kCount>(TablePlanes{s_nib, s_base}, s_k, map_bytes, out,
-                                                 out_base, zeros, s_stage);
+                                                 out_base, zeros, s_stage, skip);
     } else {
         merge_packed<kPackedBatchIdx, kOut, kCount>(
             IdxPlanes{nib, nib_pitch, base, base_pitch, s_idx}, s_k, map_bytes, out, out_base,
-            zeros, s_stage);
+            zeros, s_stage, skip);
     }
 }
 
@@ -567,11 +695,12 @@ static int packed_grid(K kernel, int64_t map_bytes) {
         }
     }
     if (per_sm < 1) per_sm = 1;
-    // One wave; laps equalised so no CTA runs an extra one.
-    const int64_t items = ceil_div(map_bytes, 32);
+    // One wave of resident CTAs; laps equalised so no warp runs an extra one.
+    const int64_t tiles = ceil_div(ceil_div(map_bytes, 32), 32);
     const int64_t cap = (int64_t)sm_count() * per_sm;
-    const int64_t laps = ceil_div(items, cap * kPackedThreads);
-    int64_t grid = ceil_div(items, laps * kPackedThreads);
+    const int64_t wpc = kPackedThreads / 32;
+    const int64_t laps = ceil_div(tiles, cap * wpc);
+    int64_t grid = ceil_div(tiles, laps * wpc);
     if (grid > cap) grid = cap;
     return grid < 1 ? 1 : (int)grid;
 }
@@ -629,10 +758,19 @@ static int check_packed(const char *fn, const void *nib, int64_t nib_pitch, cons
     return PDM_OK;
 }
 
+// Optional measurement hook (pdm_merge_stats): every packed merge adds the
+// number of (tile, selected plane) pairs it read to *g_planes_read.
+static unsigned long long *g_planes_read = nullptr;
+
+static TileSkip make_skip(const uint16_t *tb, int n) {
+    return TileSkip{tb, n, nullptr, g_planes_read};
+}
+
 static int launch_packed(const uint8_t *nib, int64_t nib_pitch, const uint8_t *base,
                          int64_t base_pitch, int64_t map_bytes, const PackedSel &p,
                          uint8_t *out, uint8_t *out_base, cudaStream_t s,
-                         unsigned long long *zeros = nullptr, int out_mode = -1) {
+                         unsigned long long *zeros = nullptr, int out_mode = -1,
+                         const uint16_t *tb = nullptr, int n = 0) {
     if (zeros) PDM_CUDA_TRY(cudaMemsetAsync(zeros, 0, sizeof(unsigned long long), s));
     if (out_mode < 0) out_mode = out_base ? 1 : 0;
     auto go = [&](auto sel) {
@@ -643,7 +781,8 @@ static int launch_packed(const uint8_t *nib, int64_t nib_pitch, const uint8_t *b
                     : zeros   ? combine_packed_kernel<0, true, Sel>
                               : combine_packed_kernel<0, false, Sel>;
         kern<<<packed_grid(kern, map_bytes), kPackedThreads, 0, s>>>(
-            nib, nib_pitch, base, base_pitch, map_bytes, sel, out, out_base, zeros);
+            nib, nib_pitch, base, base_pitch, map_bytes, sel, out, out_base, zeros,
+            make_skip(tb, n));
     };
     if (p.k <= kPackedSmallSel) {
         PackedSelSmall small;
@@ -661,7 +800,7 @@ static int launch_packed_flags(const uint8_t *nib, int64_t nib_pitch, const uint
                                int64_t base_pitch, int64_t map_bytes, int n,
                                const uint8_t *flags, uint8_t *out, uint8_t *out_base,
                                cudaStream_t s, unsigned long long *zeros = nullptr,
-                               int out_mode = -1) {
+                               int out_mode = -1, const uint16_t *tb = nullptr) {
     if (out_mode < 0) out_mode = out_base ? 1 : 0;
     const bool table = n <= kPackedTable;
     auto kern = out_mode == 3 ? (table ? combine_packed_flags_kernel<3, false, true>
@@ -685,7 +824,7 @@ static int launch_packed_flags(const uint8_t *nib, int64_t nib_pitch, const uint
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     PDM_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, nib, nib_pitch, base, base_pitch, map_bytes, n,
-                                    flags, out, out_base, zeros));
+                                    flags, out, out_base, zeros, make_skip(tb, n)));
     return cuda_status("combine_packed_flags_kernel");
 }
 
@@ -734,23 +873,24 @@ extern "C" int pdm_pack_pdms(const uint8_t *pdms, int64_t plane_pitch, int64_t m
 }
 
 extern "C" int pdm_combine_packed(const uint8_t *nib, int64_t nib_pitch, const uint8_t *base,
-                                  int64_t base_pitch, int64_t map_bytes, int32_t n,
-                                  const int32_t *sel, int32_t k, uint8_t *out,
-                                  unsigned long long *zero_count, pdm_stream_t stream) {
+                                  int64_t base_pitch, const uint16_t *tile_bounds,
+                                  int64_t map_bytes, int32_t n, const int32_t *sel, int32_t k,
+                                  uint8_t *out, unsigned long long *zero_count,
+                                  pdm_stream_t stream) {
     const char *fn = "pdm_combine_packed";
     int st = check_packed(fn, nib, nib_pitch, base, base_pitch, map_bytes, n, out, nullptr, false);
     if (st) return st;
     PackedSel p;
     if ((st = packed_sel(fn, sel, k, n, p))) return st;
     return launch_packed(nib, nib_pitch, base, base_pitch, map_bytes, p, out, nullptr,
-                         as_stream(stream), zero_count);
+                         as_stream(stream), zero_count, -1, tile_bounds, n);
 }
 
 extern "C" int pdm_combine_flags_packed(const uint8_t *nib, int64_t nib_pitch,
                                         const uint8_t *base, int64_t base_pitch,
-                                        int64_t map_bytes, int32_t n, const uint8_t *flags,
-                                        uint8_t *out, unsigned long long *zero_count,
-                                        pdm_stream_t stream) {
+                                        const uint16_t *tile_bounds, int64_t map_bytes, int32_t n,
+                                        const uint8_t *flags, uint8_t *out,
+                                        unsigned long long *zero_count, pdm_stream_t stream) {
     const char *fn = "pdm_combine_flags_packed";
     int st = check_packed(fn, nib, nib_pitch, base, base_pitch, map_bytes, n, out, nullptr, false);
     if (st) return st;
@@ -760,7 +900,7 @@ extern "C" int pdm_combine_flags_packed(const uint8_t *nib, int64_t nib_pitch,
         PDM_CUDA_TRY(cudaMemsetAsync(zero_count, 0, sizeof(unsigned long long),
                                      as_stream(stream)));
     return launch_packed_flags(nib, nib_pitch, base, base_pitch, map_bytes, n, flags, out,
-                               nullptr, as_stream(stream), zero_count);
+                               nullptr, as_stream(stream), zero_count, -1, tile_bounds);
 }
 
 extern "C" int pdm_combine_packed_to_packed(const uint8_t *nib, int64_t nib_pitch,
@@ -820,7 +960,8 @@ namespace pdm {
 // dprime_dev != nullptr (format 3 only): the same launches also write D' as
 // plain bytes into HBM (dual epilogue).
 static int merge_packed_host_impl(const char *fn, const uint8_t *nib, int64_t nib_pitch,
-                                  const uint8_t *base, int64_t base_pitch, int64_t map_bytes,
+                                  const uint8_t *base, int64_t base_pitch,
+                                  const uint16_t *tile_bounds, int64_t map_bytes,
                                   int32_t n, const uint8_t *flags, const int32_t *sel, int32_t k,
                                   uint8_t *stage_nib, uint8_t *stage_base, uint8_t *dprime_dev,
                                   uint8_t *out, int32_t pieces, int32_t format,
@@ -842,11 +983,14 @@ static int merge_packed_host_impl(const char *fn, const uint8_t *nib, int64_t ni
     }
     cudaStream_t s = as_stream(stream);
     const int64_t items = ceil_div(map_bytes, 32);
-    int64_t per = ceil_div(items, pieces);
-    if (format == 3) per = 32 * ceil_div(per, 32);  // pieces of whole warp regions
+    // pieces of whole warp tiles (32 items: a sparse region, a tile-bounds row)
+    const int64_t per = 32 * ceil_div(ceil_div(items, pieces), 32);
     // format 3: stage_nib holds ceil(items / 32) regions of kSparseRegion bytes
     auto stage_at = [&](int64_t t0) {
         return format == 3 ? stage_nib + (t0 / 32) * kSparseRegion : stage_nib + per_item * t0;
+    };
+    auto tb_at = [&](int64_t t0) -> const uint16_t * {
+        return tile_bounds ? tile_bounds + (t0 / 32) * n : nullptr;
     };
     // second output of a launch: bases (formats 1, 2) or the device D' (format 3)
     auto second_at = [&](int64_t t0) -> uint8_t * {
@@ -858,9 +1002,9 @@ static int merge_packed_host_impl(const char *fn, const uint8_t *nib, int64_t ni
         const int64_t nbytes = min(map_bytes, 32 * (t0 + per)) - 32 * t0;
         st = flags ? launch_packed_flags(nib + 16 * t0, nib_pitch, base + 2 * t0, base_pitch,
                                          nbytes, n, flags, stage_at(t0), second_at(t0), s,
-                                         nullptr, format)
+                                         nullptr, format, tb_at(t0))
                    : launch_packed(nib + 16 * t0, nib_pitch, base + 2 * t0, base_pitch, nbytes, p,
-                                   stage_at(t0), second_at(t0), s, nullptr, format);
+                                   stage_at(t0), second_at(t0), s, nullptr, format, tb_at(t0), n);
         if (st) return st;
         PDM_CUDA_TRY(cudaEventRecord(piece_event(used), s));
     }
@@ -882,24 +1026,107 @@ static int merge_packed_host_impl(const char *fn, const uint8_t *nib, int64_t ni
 }  // namespace pdm
 
 extern "C" int pdm_merge_packed_to_host(const uint8_t *nib, int64_t nib_pitch, const uint8_t *base,
-                                        int64_t base_pitch, int64_t map_bytes, int32_t n,
-                                        const uint8_t *flags, const int32_t *sel, int32_t k,
-                                        uint8_t *stage_nib, uint8_t *stage_base, uint8_t *out,
-                                        int32_t pieces, int32_t format, pdm_stream_t stream) {
+                                        int64_t base_pitch, const uint16_t *tile_bounds,
+                                        int64_t map_bytes, int32_t n, const uint8_t *flags,
+                                        const int32_t *sel, int32_t k, uint8_t *stage_nib,
+                                        uint8_t *stage_base, uint8_t *out, int32_t pieces,
+                                        int32_t format, pdm_stream_t stream) {
     return merge_packed_host_impl("pdm_merge_packed_to_host", nib, nib_pitch, base, base_pitch,
-                                  map_bytes, n, flags, sel, k, stage_nib, stage_base, nullptr, out,
-                                  pieces, format, stream);
+                                  tile_bounds, map_bytes, n, flags, sel, k, stage_nib, stage_base,
+                                  nullptr, out, pieces, format, stream);
 }
 
 extern "C" int pdm_combine_packed_host(const uint8_t *nib, int64_t nib_pitch, const uint8_t *base,
-                                       int64_t base_pitch, int64_t map_bytes, int32_t n,
-                                       const uint8_t *flags, const int32_t *sel, int32_t k,
-                                       uint8_t *dprime_dev, uint8_t *stage, uint8_t *out,
-                                       int32_t pieces, pdm_stream_t stream) {
+                                       int64_t base_pitch, const uint16_t *tile_bounds,
+                                       int64_t map_bytes, int32_t n, const uint8_t *flags,
+                                       const int32_t *sel, int32_t k, uint8_t *dprime_dev,
+                                       uint8_t *stage, uint8_t *out, int32_t pieces,
+                                       pdm_stream_t stream) {
     const char *fn = "pdm_combine_packed_host";
     PDM_REQUIRE(dprime_dev, "%s: null device D'", fn);
-    return merge_packed_host_impl(fn, nib, nib_pitch, base, base_pitch, map_bytes, n, flags, sel,
-                                  k, stage, nullptr, dprime_dev, out, pieces, 3, stream);
+    return merge_packed_host_impl(fn, nib, nib_pitch, base, base_pitch, tile_bounds, map_bytes, n,
+                                  flags, sel, k, stage, nullptr, dprime_dev, out, pieces, 3,
+                                  stream);
+}
+
+// ---- per-tile plane bounds (the merge's tile skip) ---------------------------
+// Thread = one 32-block item of one plane (16 nibble bytes + 2 bases): its
+// smallest value is the smaller base, its largest base + largest nibble of
+// the chunk; a warp covers one tile (32 items) of one plane and lane 0 writes
+// tb[tile][p] = tmin | tmax << 8.  The map's last item counts only its blocks
+// inside the map (the padding past it is never stored).
+namespace pdm {
+__device__ __forceinline__ uint32_t max_nibble(uint2 w) {
+    // max over the 16 nibbles of 8 bytes
+    uint32_t lo = (w.x & 0x0F0F0F0Fu), hi = (w.x >> 4) & 0x0F0F0F0Fu;
+    uint32_t m = __vmaxu4(lo, hi);
+    lo = (w.y & 0x0F0F0F0Fu), hi = (w.y >> 4) & 0x0F0F0F0Fu;
+    m = __vmaxu4(m, __vmaxu4(lo, hi));
+    m = __vmaxu4(m, m >> 16);
+    m = __vmaxu4(m, m >> 8);
+    return m & 0xFFu;
+}
+
+__global__ void __launch_bounds__(256)
+    tile_bounds_kernel(const uint8_t *__restrict__ nib, int64_t nib_pitch,
+                       const uint8_t *__restrict__ base, int64_t base_pitch, int64_t map_bytes,
+                       int n, uint16_t *__restrict__ tb) {
+    const int64_t items = ceil_div(map_bytes, 32);
+    const int64_t tiles = ceil_div(items, 32);
+    const int64_t total = (int64_t)n * tiles * 32;  // one thread per (plane, tile, lane)
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += stride) {
+        const int64_t p = i / (tiles * 32), r = i - p * tiles * 32;  // warp-uniform p, tile
+        const int64_t t = r;  // item
+        uint32_t lo = 255, hi = 0;
+        if (t < items) {
+            const uint4 q = *reinterpret_cast<const uint4 *>(nib + p * nib_pitch + t * 16);
+            const uint32_t bb = *reinterpret_cast<const uint16_t *>(base + p * base_pitch + t * 2);
+            const uint32_t b0 = bb & 0xFFu, b1 = bb >> 8;
+            if (t * 32 + 32 <= map_bytes) {
+                lo = min(b0, b1);
+                hi = max(b0 + max_nibble(make_uint2(q.x, q.y)),
+                         b1 + max_nibble(make_uint2(q.z, q.w)));
+            } else {  // the map's last item: its blocks inside the map only
+                const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+                for (int j = 0; t * 32 + j < map_bytes; ++j) {
+                    const uint32_t v = (j < 16 ? b0 : b1) + ((w[j >> 3] >> (4 * (j & 7))) & 15u);
+                    lo = min(lo, v);
+                    hi = max(hi, v);
+                }
+            }
+        }
+        lo = __reduce_min_sync(0xFFFFFFFFu, lo);
+        hi = __reduce_max_sync(0xFFFFFFFFu, hi);
+        if ((threadIdx.x & 31) == 0) tb[(r >> 5) * n + p] = (uint16_t)(lo | (min(hi, 255u) << 8));
+    }
+}
+}  // namespace pdm
+
+extern "C" int pdm_packed_tile_bounds(const uint8_t *nib, int64_t nib_pitch, const uint8_t *base,
+                                      int64_t base_pitch, int64_t map_bytes, int32_t n,
+                                      uint16_t *tile_bounds, pdm_stream_t stream) {
+    const char *fn = "pdm_packed_tile_bounds";
+    PDM_REQUIRE(nib && base && tile_bounds, "%s: null pointer", fn);
+    PDM_REQUIRE(map_bytes >= 1 && n >= 1, "%s: bad sizes", fn);
+    PDM_REQUIRE(nib_pitch % 16 == 0 && (uintptr_t)nib % 16 == 0 && base_pitch % 2 == 0 &&
+                    (uintptr_t)base % 2 == 0 && (uintptr_t)tile_bounds % 2 == 0,
+                "%s: needs 16-byte aligned nibble planes", fn);
+    const int64_t items = ceil_div(map_bytes, 32);
+    const int64_t total = (int64_t)n * ceil_div(items, 32) * 32;
+    int64_t grid = ceil_div(total, 256);
+    const int64_t cap =
+        (int64_t)sm_count() * resident_ctas((const void *)tile_bounds_kernel, 256, 0);
+    if (grid > cap) grid = cap;
+    tile_bounds_kernel<<<(unsigned)grid, 256, 0, as_stream(stream)>>>(nib, nib_pitch, base,
+                                                                      base_pitch, map_bytes, n,
+                                                                      tile_bounds);
+    return cuda_status("tile_bounds_kernel");
+}
+
+extern "C" int pdm_merge_stats(unsigned long long *planes_read) {
+    g_planes_read = planes_read;
+    return PDM_OK;
 }
 
 // ---- a finished D' (plain bytes in HBM) to a host array ---------------------

@@ -487,22 +487,33 @@ def test_packed_abi_many_planes(n, map_bytes):
     _lib.check(L.pdm_pack_pdms(_lib.ptr(planes), pitch, map_bytes, n, _lib.ptr(nib), nib_pitch,
                                _lib.ptr(base), base_pitch, _lib.ptr(bad), st), "pack")
     assert int(bad.cpu()[0]) == 0
+    tiles = -(-map_bytes // 1024)
+    tb = torch.empty((tiles, n), dtype=torch.int16, device="cuda")
+    _lib.check(L.pdm_packed_tile_bounds(_lib.ptr(nib), nib_pitch, _lib.ptr(base), base_pitch,
+                                        map_bytes, n, _lib.ptr(tb), st), "tile bounds")
+    tbh = tb.cpu().numpy().view(np.uint16)
+    for t in range(tiles):  # min | max << 8 of each plane over the tile
+        seg = maps[:, 1024 * t: 1024 * (t + 1)]
+        assert np.array_equal(tbh[t] & 0xFF, seg.min(axis=1))
+        assert np.array_equal(tbh[t] >> 8, seg.max(axis=1))
     out = torch.empty(map_bytes, dtype=torch.uint8, device="cuda")
-    for k in (1, 7, min(n, 240), n):
+    for k in (1, 7, 33, 64, min(n, 240), n):
         sel = np.sort(rng.choice(n, size=k, replace=False)).astype(np.int32)
         want = maps[sel].min(axis=0)
         flags = torch.zeros(n, dtype=torch.uint8, device="cuda")
         flags[torch.from_numpy(sel).long().cuda()] = 1
-        _lib.check(L.pdm_combine_flags_packed(_lib.ptr(nib), nib_pitch, _lib.ptr(base),
-                                              base_pitch, map_bytes, n, _lib.ptr(flags),
-                                              _lib.ptr(out), None, st), "flags")
-        assert np.array_equal(out.cpu().numpy(), want), k
-        if k <= 240:  # host index list (kernel parameter) path
+        for tbp in (None, _lib.ptr(tb)):  # without / with the per-tile plane skip
             out.fill_(7)
-            _lib.check(L.pdm_combine_packed(_lib.ptr(nib), nib_pitch, _lib.ptr(base), base_pitch,
-                                            map_bytes, n, sel.ctypes.data, k, _lib.ptr(out),
-                                            None, st), "sel")
-            assert np.array_equal(out.cpu().numpy(), want), k
+            _lib.check(L.pdm_combine_flags_packed(_lib.ptr(nib), nib_pitch, _lib.ptr(base),
+                                                  base_pitch, tbp, map_bytes, n, _lib.ptr(flags),
+                                                  _lib.ptr(out), None, st), "flags")
+            assert np.array_equal(out.cpu().numpy(), want), (k, tbp)
+            if k <= 240:  # host index list (kernel parameter) path
+                out.fill_(7)
+                _lib.check(L.pdm_combine_packed(_lib.ptr(nib), nib_pitch, _lib.ptr(base),
+                                                base_pitch, tbp, map_bytes, n, sel.ctypes.data, k,
+                                                _lib.ptr(out), None, st), "sel")
+                assert np.array_equal(out.cpu().numpy(), want), (k, tbp)
 
 
 @pytest.mark.parametrize("fmt", [1, 2, 3])
@@ -542,6 +553,9 @@ def test_merge_packed_to_host_formats_and_pieces(fmt):
                                    nib_pitch, _lib.ptr(base), base_pitch, _lib.ptr(bad), st),
                    "pack")
         assert int(bad.cpu()[0]) == 0
+        tb = torch.empty((-(-map_bytes // 1024), n), dtype=torch.int16, device="cuda")
+        _lib.check(L.pdm_packed_tile_bounds(_lib.ptr(nib), nib_pitch, _lib.ptr(base), base_pitch,
+                                            map_bytes, n, _lib.ptr(tb), st), "tile bounds")
         stage_n = torch.empty(max(chunks * 8, -(-chunks // 64) * 336), dtype=torch.uint8,
                               pin_memory=True)
         stage_b = torch.empty(chunks, dtype=torch.uint8, pin_memory=True)
@@ -554,7 +568,8 @@ def test_merge_packed_to_host_formats_and_pieces(fmt):
                 for use_flags in (True, False):
                     out = np.full(map_bytes + 32, 0xCD, np.uint8)
                     _lib.check(L.pdm_merge_packed_to_host(
-                        _lib.ptr(nib), nib_pitch, _lib.ptr(base), base_pitch, map_bytes, n,
+                        _lib.ptr(nib), nib_pitch, _lib.ptr(base), base_pitch,
+                        _lib.ptr(tb) if use_flags else None, map_bytes, n,
                         _lib.ptr(flags) if use_flags else None,
                         None if use_flags else sel.ctypes.data, k, stage_n.data_ptr(),
                         stage_b.data_ptr(), out.ctypes.data, pieces, fmt, st), "to_host")
@@ -585,7 +600,8 @@ def test_packed_planes_decode_to_the_raw_planes(monkeypatch, dims):
     vals += base[:, :, None]
     raw = np.stack([d.dist.reshape(-1) for d in pset.pdms])
     assert np.array_equal(vals.reshape(8, -1)[:, :nb], raw)
-    assert pset.device_bytes() == 8 * (pset.plane_pitch + nib_pitch + base_pitch)
+    tiles = -(-nb // 1024)  # + the merge's per-tile plane bounds (uint16 [tiles][n])
+    assert pset.device_bytes() == 8 * (pset.plane_pitch + nib_pitch + base_pitch) + 2 * tiles * 8
 
 
 def test_packed_skipped_for_maps_that_are_not_distance_fields():

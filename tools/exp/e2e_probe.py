@@ -83,11 +83,11 @@ def main():
         dprime = device.empty(grid.bdims, np.uint8)
         pieces = max(1, min(16, (-(-nb // 32)) // pdm.acceleration._HOST_PIECE_ITEMS))
         r["combine_dual_c"] = timed(lambda: L.pdm_combine_packed_host(
-            _lib.ptr(nib), nib_pitch, _lib.ptr(base), base_pitch, nb, pset.n, None,
+            _lib.ptr(nib), nib_pitch, _lib.ptr(base), base_pitch, pset.tile_bounds_ptr(), nb, pset.n, None,
             sel_idx.ctypes.data, int(sel_idx.size), _lib.ptr(dprime), _lib.ptr(stage_n),
             out.ctypes.data, pieces, _lib.stream_handle()))
         r["merge_to_host_idx_c"] = timed(lambda: L.pdm_merge_packed_to_host(
-            _lib.ptr(nib), nib_pitch, _lib.ptr(base), base_pitch, nb, pset.n, None,
+            _lib.ptr(nib), nib_pitch, _lib.ptr(base), base_pitch, pset.tile_bounds_ptr(), nb, pset.n, None,
             sel_idx.ctypes.data, int(sel_idx.size), _lib.ptr(stage_n), _lib.ptr(stage_b),
             out.ctypes.data, pieces, 3, _lib.stream_handle()))
 
@@ -108,7 +108,7 @@ def _old_args(pset, flags, out, L):
     from paper_2407_21552_b200 import _lib
     nib, nib_pitch, base, base_pitch = pset.packed()
     nib_h, base_h = pset._host_stage()
-    return (_lib.ptr(nib), nib_pitch, _lib.ptr(base), base_pitch, pset.grid.num_blocks, pset.n,
+    return (_lib.ptr(nib), nib_pitch, _lib.ptr(base), base_pitch, None, pset.grid.num_blocks, pset.n,
             _lib.ptr(flags), None, 0, _lib.ptr(nib_h), _lib.ptr(base_h), out.ctypes.data, 2, 3,
             _lib.stream_handle())
 

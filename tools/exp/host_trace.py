@@ -22,7 +22,7 @@ for pieces in (1, 4, 1, 4):
     flush.fill_(1)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    L.pdm_merge_packed_to_host(_lib.ptr(nib), nib_pitch, _lib.ptr(base), base_pitch, nb, 32,
+    L.pdm_merge_packed_to_host(_lib.ptr(nib), nib_pitch, _lib.ptr(base), base_pitch, None, nb, 32,
                                None, sel.ctypes.data, 16, _lib.ptr(nib_h), _lib.ptr(base_h),
                                out.ctypes.data, pieces, 3, st)
     print(f"pieces={pieces} total {(time.perf_counter() - t0) * 1e6:.1f} us", file=sys.stderr,

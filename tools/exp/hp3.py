@@ -45,7 +45,7 @@ for k in (1, 4, 16, 28):
     for fmt in (2, 3):
         for pieces in (1, 4):
             res[f"k{k}_f{fmt}_p{pieces}"] = timed(lambda: L.pdm_merge_packed_to_host(
-                _lib.ptr(nib), nib_pitch, _lib.ptr(base), base_pitch, nb, 32, None,
+                _lib.ptr(nib), nib_pitch, _lib.ptr(base), base_pitch, None, nb, 32, None,
                 sel.ctypes.data, k, _lib.ptr(nib_h), _lib.ptr(base_h), out.ctypes.data, pieces,
                 fmt, st))
         if fmt == 2:

@@ -108,7 +108,7 @@ def breakdown():
 
     def launch_only():
         L.pdm_combine_packed(_lib.ptr(nib), nib_pitch, _lib.ptr(base), base_pitch,
-                             grid.num_blocks, pset.n, idx.ctypes.data, int(idx.size),
+                             pset.tile_bounds_ptr(), grid.num_blocks, pset.n, idx.ctypes.data, int(idx.size),
                              _lib.ptr(out_t), None, st)
 
     def launch_sync():

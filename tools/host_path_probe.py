@@ -48,7 +48,7 @@ def main():
         _lib.ptr(nib_h), _lib.ptr(base_h), nb, out.ctypes.data))
     for pieces in (1, 2, 4, 8, 16):  # 3 = sparse delta D' (the default)
         res[f"pipeline_f3_{pieces}"] = timed(lambda: L.pdm_merge_packed_to_host(
-            _lib.ptr(nib), nib_pitch, _lib.ptr(base), base_pitch, nb, 32, None,
+            _lib.ptr(nib), nib_pitch, _lib.ptr(base), base_pitch, None, nb, 32, None,
             sel.ctypes.data, 16, _lib.ptr(nib_h), _lib.ptr(base_h), out.ctypes.data,
             pieces, 3, st))
     res["unpack_sparse_only"] = timed(lambda: L.pdm_unpack_sparse_host(
@@ -56,7 +56,7 @@ def main():
     for fmt in (1, 2):  # 1 = nibble D', 2 = 2-bit delta D'
         for pieces in (1, 2, 4, 8):
             res[f"pipeline_f{fmt}_{pieces}"] = timed(lambda: L.pdm_merge_packed_to_host(
-                _lib.ptr(nib), nib_pitch, _lib.ptr(base), base_pitch, nb, 32, None,
+                _lib.ptr(nib), nib_pitch, _lib.ptr(base), base_pitch, None, nb, 32, None,
                 sel.ctypes.data, 16, _lib.ptr(nib_h), _lib.ptr(base_h), out.ctypes.data,
                 pieces, fmt, st))
     s = pdm.PartitionSelection(selected=frozenset(int(i) + 1 for i in sel), n=32)

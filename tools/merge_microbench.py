@@ -99,7 +99,7 @@ def main():
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record()
                 _lib.check(L.pdm_combine_packed(_lib.ptr(nib), nib_pitch, _lib.ptr(base),
-                                                base_pitch, nb, n, sel.ctypes.data, k,
+                                                base_pitch, None, nb, n, sel.ctypes.data, k,
                                                 _lib.ptr(out), None, st), "pdm_combine_packed")
                 e1.record()
                 torch.cuda.synchronize()
@@ -148,7 +148,7 @@ def main():
                         "pdm_combine_packed_to_packed")
                 elif mode.startswith("packed"):
                     _lib.check(L.pdm_combine_packed(_lib.ptr(nib), nib_pitch, _lib.ptr(base),
-                                                    base_pitch, nb, n, sel.ctypes.data, k,
+                                                    base_pitch, None, nb, n, sel.ctypes.data, k,
                                                     _lib.ptr(dst), None, st), "pdm_combine_packed")
                 else:
                     _lib.check(L.pdm_combine(_lib.ptr(pdms), pitch, nb, n, sel.ctypes.data, k,
