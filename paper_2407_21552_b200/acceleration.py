@@ -494,9 +494,9 @@ def build_pdm_set(volume: Volume, grid: BlockGrid, scheme: PartitionScheme,
                                                  *grid.bdims, _lib.ptr(storage), pitch,
                                                  _lib.stream_handle()),
                    "pdm_distance_transform_mask")
+    pset._finish_pack(pending)  # (+ the merge's tile bounds)
     torch.cuda.synchronize()
     pset.init_seconds = time.perf_counter() - start
-    pset._finish_pack(pending)
     return pset
 
 
