@@ -128,12 +128,14 @@ int pdm_count_nonlipschitz_chunks(const uint8_t *pdms, int64_t plane_pitch, int6
 
 /* pdm_distance_transform_mask followed by pdm_pack_pdms, with the packing
  * fused into the last (z) pass when bz is 128, 256 or 512 (the rows are
- * packed while still in shared memory); base_pitch % 4 == 0. */
+ * packed while still in shared memory); base_pitch % 4 == 0.  tile_bounds
+ * (may be NULL): also the merge's per-tile plane bounds (as
+ * pdm_packed_tile_bounds), taken from the same rows in the fused case. */
 int pdm_distance_transform_mask_packed(const uint32_t *mask, int32_t words, int32_t n, int64_t bx,
                                        int64_t by, int64_t bz, uint8_t *pdms,
                                        int64_t plane_pitch, uint8_t *nib, int64_t nib_pitch,
                                        uint8_t *base, int64_t base_pitch, uint32_t *violations,
-                                       pdm_stream_t stream);
+                                       uint16_t *tile_bounds, pdm_stream_t stream);
 
 /* Per-tile plane bounds of a packed set, for the merges' tile skip:
  * tile_bounds[tile][p] = min | max << 8 of plane p over blocks

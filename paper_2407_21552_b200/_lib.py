@@ -42,7 +42,7 @@ _SIGNATURES = {
     "pdm_count_nonlipschitz_chunks": [_P, _I64, _I64, _I32, _P, _P],
     "pdm_pack_pdms": [_P, _I64, _I64, _I32, _P, _I64, _P, _I64, _P, _P],
     "pdm_distance_transform_mask_packed": [_P, _I32, _I32, _I64, _I64, _I64, _P, _I64, _P, _I64,
-                                           _P, _I64, _P, _P],
+                                           _P, _I64, _P, _P, _P],
     "pdm_packed_tile_bounds": [_P, _I64, _P, _I64, _I64, _I32, _P, _P],
     "pdm_merge_stats": [_P],
     "pdm_combine_packed": [_P, _I64, _P, _I64, _P, _I64, _I32, _P, _I32, _P, _P, _P],

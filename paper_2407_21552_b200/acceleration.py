@@ -249,7 +249,17 @@ class PdmSet:
                                    _lib.stream_handle()), "pdm_pack_pdms")
         return planes
 
-    def _finish_pack(self, pending) -> None:
+    def _alloc_tile_bounds(self):
+        """uint16 [tiles][n] device table for the merge's per-tile plane skip,
+        or None when the skip is off (PDM_TILE_SKIP=0)."""
+        if not _tile_skip_enabled():
+            return None
+        return device.empty((-(-self.grid.num_blocks // 1024), self.n), np.int16)
+
+    def _finish_pack(self, pending, tile_bounds=None) -> None:
+        """Adopt the packed planes if they packed; tile_bounds: the per-tile
+        plane bounds already made with them (the fused z pass), else they are
+        computed here (pdm_packed_tile_bounds)."""
         if pending is False:
             self._packed = False
             return
@@ -257,10 +267,12 @@ class PdmSet:
         ok = int(bad.cpu()[0]) == 0  # int32 view of the uint32 count; 0 either way
         self._packed = (nib, nib_pitch, base, base_pitch) if ok else False
         self._tile_bounds = None
-        if ok and _tile_skip_enabled():
+        if ok and tile_bounds is not None:
+            self._tile_bounds = tile_bounds
+        elif ok and _tile_skip_enabled():
             # per (1024-block tile, plane) min/max: the merges' exact tile skip
             nb = self.grid.num_blocks
-            tb = device.empty((-(-nb // 1024), self.n), np.int16)
+            tb = self._alloc_tile_bounds()
             _lib.check(_lib.lib().pdm_packed_tile_bounds(
                 _lib.ptr(nib), nib_pitch, _lib.ptr(base), base_pitch, nb, self.n, _lib.ptr(tb),
                 _lib.stream_handle()), "pdm_packed_tile_bounds")
@@ -484,17 +496,19 @@ def build_pdm_set(volume: Volume, grid: BlockGrid, scheme: PartitionScheme,
         # writes them itself when it can (pdm_distance_transform_mask_packed)
         pending = pset._alloc_packed()
         nib, nib_pitch, base, base_pitch, bad = pending
+        tb = pset._alloc_tile_bounds()
         _lib.check(L.pdm_distance_transform_mask_packed(
             _lib.ptr(mask), mask.shape[1], scheme.n, *grid.bdims, _lib.ptr(storage), pitch,
             _lib.ptr(nib), nib_pitch, _lib.ptr(base), base_pitch, _lib.ptr(bad),
-            _lib.stream_handle()), "pdm_distance_transform_mask_packed")
+            _lib.ptr(tb) if tb is not None else None, _lib.stream_handle()),
+            "pdm_distance_transform_mask_packed")
     else:
-        pending = False
+        pending, tb = False, None
         _lib.check(L.pdm_distance_transform_mask(_lib.ptr(mask), mask.shape[1], scheme.n,
                                                  *grid.bdims, _lib.ptr(storage), pitch,
                                                  _lib.stream_handle()),
                    "pdm_distance_transform_mask")
-    pset._finish_pack(pending)  # (+ the merge's tile bounds)
+    pset._finish_pack(pending, tb)  # (+ the merge's tile bounds)
     torch.cuda.synchronize()
     pset.init_seconds = time.perf_counter() - start
     return pset

@@ -407,6 +407,8 @@ struct PackDst {
     uint8_t *base;
     int64_t base_pitch;
     unsigned int *bad;  // chunks spanning > 15 values (none for distance fields)
+    uint16_t *tb;       // the merge's per-tile plane bounds [tiles][n] (may be null)
+    int n;
 };
 
 __device__ __forceinline__ uint32_t hmin2_u(uint32_t a, uint32_t b) {
@@ -423,7 +425,8 @@ __device__ __forceinline__ uint32_t hmax2_u(uint32_t a, uint32_t b) {
 // Pack one 16-byte chunk: bytes as fp16 1024 + v in 16-bit lanes (HMNMX2 on
 // the FMA pipe) for min/max, offsets v - min (< 16, no borrow between bytes),
 // then two nibble bytes per byte pair via shift/or and one PRMT per 8 blocks.
-__device__ __forceinline__ uint2 pack_chunk(uint4 q, uint32_t &mn, unsigned int &nbad) {
+__device__ __forceinline__ uint2 pack_chunk(uint4 q, uint32_t &mn, uint32_t &mx,
+                                            unsigned int &nbad) {
     const uint32_t w[4] = {q.x, q.y, q.z, q.w};
     uint32_t lo = 0x64FF64FFu, hi = 0x64006400u;
 #pragma unroll
@@ -436,7 +439,8 @@ __device__ __forceinline__ uint2 pack_chunk(uint4 q, uint32_t &mn, unsigned int 
     lo = hmin2_u(lo, __byte_perm(lo, 0u, 0x1032));
     hi = hmax2_u(hi, __byte_perm(hi, 0u, 0x1032));
     mn = lo & 0xFFu;
-    nbad += (hi & 0xFFu) - mn > 15u;
+    mx = hi & 0xFFu;
+    nbad += mx - mn > 15u;
     const uint32_t mb = mn * 0x01010101u;
     uint32_t t[4];
 #pragma unroll
@@ -581,13 +585,16 @@ __global__ void __launch_bounds__(256)
                 const int nst = L / 2 + 8, bst = L / 16 + 4;
                 uint8_t *sn = tab_warp, *sb = tab_warp + 32 * nst;
                 unsigned int nbad = 0;
+                uint32_t rlo = 255, rhi = 0;  // the row's min / max
                 if (lane < nlines) {
                     const TileLine<kRowSwz> tl{line, lane};
                     for (int c = 0; c < cpr; ++c) {
-                        uint32_t mn;
-                        const uint2 pw = pack_chunk(*tl.chunk(c), mn, nbad);
+                        uint32_t mn, mx;
+                        const uint2 pw = pack_chunk(*tl.chunk(c), mn, mx, nbad);
                         *reinterpret_cast<uint2 *>(sn + lane * nst + 8 * c) = pw;
                         sb[lane * bst + c] = (uint8_t)mn;
+                        rlo = min(rlo, mn);
+                        rhi = max(rhi, mx);
                     }
                 }
                 if (nbad) atomicAdd(pk.bad, nbad);
@@ -595,6 +602,17 @@ __global__ void __launch_bounds__(256)
                 // rows r0.. of plane p are contiguous in the packed planes too
                 const int64_t rows = bx * by, per_p = ceil_div(rows, 32);
                 const int64_t p = t / per_p, r0 = (t % per_p) * 32;
+                if (pk.tb != nullptr) {
+                    // the merge's tile bounds: a 1024-block tile is rpt = 1024 / L
+                    // whole rows (r0 is a multiple of 32 >= rpt), reduced over lanes
+                    const int rpt = 1024 / L;
+                    for (int o = 1; o < rpt; o <<= 1) {
+                        rlo = min(rlo, __shfl_xor_sync(0xFFFFFFFFu, rlo, o));
+                        rhi = max(rhi, __shfl_xor_sync(0xFFFFFFFFu, rhi, o));
+                    }
+                    if ((lane & (rpt - 1)) == 0 && lane < nlines)
+                        pk.tb[((r0 + lane) / rpt) * pk.n + p] = (uint16_t)(rlo | (rhi << 8));
+                }
                 uint8_t *gn = pk.nib + p * pk.nib_pitch + r0 * (L / 2);
                 uint8_t *gb = pk.base + p * pk.base_pitch + r0 * (L / 16);
                 const int nu = L / 16;  // 8-byte nibble units (= chunks) per row
@@ -955,7 +973,7 @@ extern "C" int pdm_distance_transform_mask_packed(const uint32_t *mask, int32_t 
                                                   uint8_t *pdms, int64_t plane_pitch,
                                                   uint8_t *nib, int64_t nib_pitch, uint8_t *base,
                                                   int64_t base_pitch, uint32_t *violations,
-                                                  pdm_stream_t stream) {
+                                                  uint16_t *tile_bounds, pdm_stream_t stream) {
     const char *fn = "pdm_distance_transform_mask_packed";
     PDM_REQUIRE(mask && pdms && nib && base && violations, "%s: null pointer", fn);
     PDM_REQUIRE(words == (n + 31) / 32, "%s: words", fn);
@@ -969,14 +987,20 @@ extern "C" int pdm_distance_transform_mask_packed(const uint32_t *mask, int32_t 
     if (!dt_fused_pack_ok(bz)) {  // separate packing pass
         st = pdm_distance_transform_mask(mask, words, n, bx, by, bz, pdms, plane_pitch, stream);
         if (st) return st;
-        return pdm_pack_pdms(pdms, plane_pitch, nb, n, nib, nib_pitch, base, base_pitch,
-                             violations, stream);
+        st = pdm_pack_pdms(pdms, plane_pitch, nb, n, nib, nib_pitch, base, base_pitch,
+                           violations, stream);
+        if (st || !tile_bounds) return st;
+        return pdm_packed_tile_bounds(nib, nib_pitch, base, base_pitch, nb, n, tile_bounds,
+                                      stream);
     }
     PDM_CUDA_TRY(cudaMemsetAsync(violations, 0, sizeof(uint32_t), s));
     st = pass_x_mask(mask, words, n, bx, by, bz, pdms, plane_pitch, s);
     if (st) return st;
+    // (the last tile of a plane whose rows do not fill it: its missing rows
+    // are simply absent from the reduction; a partial last warp tile of 32
+    // rows likewise)
     st = pass_yz(n, bx, by, bz, pdms, plane_pitch, s,
-                 PackDst{nib, nib_pitch, base, base_pitch, violations});
+                 PackDst{nib, nib_pitch, base, base_pitch, violations, tile_bounds, n});
     if (st) return st;
     if (nchunks * 16 > nb) {  // the even-count padding chunk: all 255
         PDM_CUDA_TRY(cudaMemset2DAsync(nib + (nchunks - 1) * 8, nib_pitch, 0, 8, n, s));

@@ -1057,27 +1057,28 @@ extern "C" int pdm_combine_packed_host(const uint8_t *nib, int64_t nib_pitch, co
 // inside the map (the padding past it is never stored).
 namespace pdm {
 __device__ __forceinline__ uint32_t max_nibble(uint2 w) {
-    // max over the 16 nibbles of 8 bytes
-    uint32_t lo = (w.x & 0x0F0F0F0Fu), hi = (w.x >> 4) & 0x0F0F0F0Fu;
-    uint32_t m = __vmaxu4(lo, hi);
-    lo = (w.y & 0x0F0F0F0Fu), hi = (w.y >> 4) & 0x0F0F0F0Fu;
-    m = __vmaxu4(m, __vmaxu4(lo, hi));
-    m = __vmaxu4(m, m >> 16);
-    m = __vmaxu4(m, m >> 8);
-    return m & 0xFFu;
+    // max over the 16 nibbles of 8 bytes, as u16x2 lanes (VIMNMX.U16x2)
+    const uint32_t m4 = 0x000F000Fu;
+    uint32_t m = __vmaxu2(__vmaxu2(w.x & m4, (w.x >> 4) & m4), __vmaxu2((w.x >> 8) & m4, (w.x >> 12) & m4));
+    m = __vmaxu2(m, __vmaxu2(__vmaxu2(w.y & m4, (w.y >> 4) & m4), __vmaxu2((w.y >> 8) & m4, (w.y >> 12) & m4)));
+    return max(m & 0xFFFFu, m >> 16);
 }
 
 __global__ void __launch_bounds__(256)
     tile_bounds_kernel(const uint8_t *__restrict__ nib, int64_t nib_pitch,
                        const uint8_t *__restrict__ base, int64_t base_pitch, int64_t map_bytes,
                        int n, uint16_t *__restrict__ tb) {
+    // warp = one tile of one plane; warps walk (plane, tile) pairs tile-major
     const int64_t items = ceil_div(map_bytes, 32);
     const int64_t tiles = ceil_div(items, 32);
-    const int64_t total = (int64_t)n * tiles * 32;  // one thread per (plane, tile, lane)
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += stride) {
-        const int64_t p = i / (tiles * 32), r = i - p * tiles * 32;  // warp-uniform p, tile
-        const int64_t t = r;  // item
+    const int lane = threadIdx.x & 31;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int64_t total = tiles * n;
+    for (int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < total;
+         w += nwarps) {
+        const int64_t tile = w / n;
+        const int p = (int)(w - tile * n);
+        const int64_t t = tile * 32 + lane;  // item
         uint32_t lo = 255, hi = 0;
         if (t < items) {
             const uint4 q = *reinterpret_cast<const uint4 *>(nib + p * nib_pitch + t * 16);
@@ -1088,9 +1089,9 @@ __global__ void __launch_bounds__(256)
                 hi = max(b0 + max_nibble(make_uint2(q.x, q.y)),
                          b1 + max_nibble(make_uint2(q.z, q.w)));
             } else {  // the map's last item: its blocks inside the map only
-                const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+                const uint32_t wd[4] = {q.x, q.y, q.z, q.w};
                 for (int j = 0; t * 32 + j < map_bytes; ++j) {
-                    const uint32_t v = (j < 16 ? b0 : b1) + ((w[j >> 3] >> (4 * (j & 7))) & 15u);
+                    const uint32_t v = (j < 16 ? b0 : b1) + ((wd[j >> 3] >> (4 * (j & 7))) & 15u);
                     lo = min(lo, v);
                     hi = max(hi, v);
                 }
@@ -1098,7 +1099,7 @@ __global__ void __launch_bounds__(256)
         }
         lo = __reduce_min_sync(0xFFFFFFFFu, lo);
         hi = __reduce_max_sync(0xFFFFFFFFu, hi);
-        if ((threadIdx.x & 31) == 0) tb[(r >> 5) * n + p] = (uint16_t)(lo | (min(hi, 255u) << 8));
+        if (lane == 0) tb[tile * n + p] = (uint16_t)(lo | (min(hi, 255u) << 8));
     }
 }
 }  // namespace pdm
@@ -1113,7 +1114,7 @@ extern "C" int pdm_packed_tile_bounds(const uint8_t *nib, int64_t nib_pitch, con
                     (uintptr_t)base % 2 == 0 && (uintptr_t)tile_bounds % 2 == 0,
                 "%s: needs 16-byte aligned nibble planes", fn);
     const int64_t items = ceil_div(map_bytes, 32);
-    const int64_t total = (int64_t)n * ceil_div(items, 32) * 32;
+    const int64_t total = (int64_t)n * ceil_div(items, 32) * 32;  // threads: a warp per pair
     int64_t grid = ceil_div(total, 256);
     const int64_t cap =
         (int64_t)sm_count() * resident_ctas((const void *)tile_bounds_kernel, 256, 0);

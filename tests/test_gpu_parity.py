@@ -681,6 +681,32 @@ def test_combine_streams_host_view_while_it_is_read(monkeypatch):
     assert dual == [False] + [True] * 7 + [False, False]
 
 
+@pytest.mark.parametrize("dims,b", [
+    ((48, 32, 64), 4),      # bz = 16: separate packing pass + pdm_packed_tile_bounds
+    ((12, 8, 512), 4),      # bz = 128: bounds taken in the fused z-pass epilogue (8 rows/tile)
+    ((9, 6, 1024), 4),      # bz = 256: fused, 4 rows per tile, rows % 4 != 0 at the end
+    ((6, 5, 1024), 2),      # bz = 512: fused, 2 rows per tile, odd row count
+])
+def test_tile_bounds_match_the_planes(monkeypatch, dims, b):
+    """The merge's per-tile plane bounds (min | max << 8 over each 1024-block
+    tile of every plane), however they were made, equal numpy's over the raw
+    planes (partial last tiles included)."""
+    monkeypatch.setenv("PDM_PACKED", "1")
+    monkeypatch.setenv("PDM_TILE_SKIP", "1")
+    rng = np.random.default_rng(17)
+    vox = random_structured_volume(rng, dims, 16)
+    scheme = pdm.scheme_uniform(8, 16)
+    pset = pdm.build_pdm_set(pdm.Volume.from_array(vox), pdm.BlockGrid.for_dims(dims, b), scheme)
+    assert pset.packed() is not None and pset._tile_bounds is not None
+    nb = pset.grid.num_blocks
+    raw = np.stack([d.dist.reshape(-1) for d in pset.pdms])
+    tb = pset._tile_bounds.cpu().numpy().view(np.uint16)
+    for t in range(-(-nb // 1024)):
+        seg = raw[:, 1024 * t: 1024 * (t + 1)]
+        assert np.array_equal(tb[t] & 0xFF, seg.min(axis=1)), t
+        assert np.array_equal(tb[t] >> 8, seg.max(axis=1)), t
+
+
 def test_packed_disabled_by_env_and_dropped(monkeypatch):
     """PDM_PACKED=0 keeps sets raw; drop_packed() forgets a packed copy; both
     merge paths agree."""
