@@ -248,27 +248,29 @@ def oracle_pdms(cfg, gdims, x_range):
                                       cfg["mode"])
 
 
-def merge_traffic(mean_k: float):
-    """ncu dram bytes per merge launch (profiles/merge_traffic.json: --set full
-    captures of this kernel at several k), fit linearly in k and evaluated at
-    the run's mean k -- from committed captures, not this run."""
+def merge_traffic(ks):
+    """ncu dram bytes (read + write) per merge launch for the run's TF sequence,
+    from profiles/merge_traffic.json -- per-k values measured by
+    `ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum` over the same
+    k = 1..32 sequence (tools/evidence.sh), averaged over this run's ks; a
+    committed capture, not this run."""
     p = ROOT / "profiles" / "merge_traffic.json"
     if not p.exists():
         return None, None
     d = json.loads(p.read_text())
+    per_k = {int(k): v for k, v in (d.get("per_k") or {}).items()}
+    if per_k and all(k in per_k for k in ks):
+        return round(float(np.mean([per_k[k] for k in ks]))), d.get("source")
     pts = d.get("points") or [{"k": d["k"], "traffic_bytes_per_launch":
                               d["traffic_bytes_per_launch"]}]
-    ks = np.array([q["k"] for q in pts], float)
+    kk = np.array([q["k"] for q in pts], float)
     tr = np.array([q["traffic_bytes_per_launch"] for q in pts], float)
+    mean_k = float(np.mean(ks))
     if len(pts) >= 2:
-        slope, icpt = np.polyfit(ks, tr, 1)
+        slope, icpt = np.polyfit(kk, tr, 1)
         return round(float(icpt + slope * mean_k)), d.get("source")
-    return round(float(tr[0] * (mean_k + 1) / (ks[0] + 1))), d.get("source")
+    return round(float(tr[0] * (mean_k + 1) / (kk[0] + 1))), d.get("source")
 
-
-# ---------------------------------------------------------------------------------
-# B200 arm
-# ---------------------------------------------------------------------------------
 
 def run_b200(args, rank, world, local_rank):
     import torch
@@ -483,7 +485,7 @@ def run_b200(args, rank, world, local_rank):
     peak, peak_kind = peaks()
     achieved = merge_bytes / (merge_total_ms * 1e-3) / 1e9
     mean_k = float(np.mean(ks))
-    traffic, traffic_src = merge_traffic(mean_k)
+    traffic, traffic_src = merge_traffic(ks)
     by, bz = grid.bdims[1], grid.bdims[2]
     line = {
         "metric": METRIC,

@@ -159,7 +159,9 @@ def main():
                 r_half = update_row(pset, vol, grid, scheme,
                                     tf_of(aligned_alpha(scheme, max(1, n // 2), rng)),
                                     f"aligned k={max(1, n // 2)}")
-                rows.append({"n": n, "pdm_bytes": pset.memory_bytes(), "precompute_ms": pre,
+                rows.append({"n": n, "pdm_bytes": pset.memory_bytes(),
+                             "device_bytes": pset.device_bytes(),  # raw + packed + tile bounds
+                             "precompute_ms": pre,
                              "update_ms_k_n": r_all["update_ms"],
                              "update_GBps_k_n": r_all["update_GBps"],
                              "update_ms_k_half": r_half["update_ms"],
