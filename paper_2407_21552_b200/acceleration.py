@@ -267,6 +267,7 @@ class PdmSet:
         ok = int(bad.cpu()[0]) == 0  # int32 view of the uint32 count; 0 either way
         self._packed = (nib, nib_pitch, base, base_pitch) if ok else False
         self._tile_bounds = None
+        self._pargs = None
         if ok and tile_bounds is not None:
             self._tile_bounds = tile_bounds
         elif ok and _tile_skip_enabled():
@@ -277,6 +278,19 @@ class PdmSet:
                 _lib.ptr(nib), nib_pitch, _lib.ptr(base), base_pitch, nb, self.n, _lib.ptr(tb),
                 _lib.stream_handle()), "pdm_packed_tile_bounds")
             self._tile_bounds = tb
+
+    def _packed_args(self):
+        """(nib, nib_pitch, base, base_pitch, tile_bounds) as the packed merges
+        take them (device pointers), cached; None when the set does not pack."""
+        args = self.__dict__.get("_pargs")
+        if args is None:
+            pk = self.packed()
+            if pk is None:
+                return None
+            nib, nib_pitch, base, base_pitch = pk
+            args = self._pargs = (_lib.ptr(nib), nib_pitch, _lib.ptr(base), base_pitch,
+                                  self.tile_bounds_ptr())
+        return args
 
     def tile_bounds_ptr(self):
         """Device pointer of the per-tile plane bounds (pdm_packed_tile_bounds)
@@ -308,6 +322,7 @@ class PdmSet:
         """Forget the packed copy (after writing into ``storage``)."""
         self._packed = None
         self._tile_bounds = None
+        self._pargs = None
 
     def device_bytes(self) -> int:
         """Device bytes held: raw planes plus the packed copy, if any."""
@@ -612,12 +627,10 @@ def _combine_indices(pdm_set: PdmSet, sel: np.ndarray, out) -> None:
     """K7 over a host index list (0-based), into ``out`` (enqueued only)."""
     L = _lib.lib()
     grid = pdm_set.grid
-    packed = pdm_set.packed() if 0 < sel.size <= _MAX_PACKED_SEL else None
-    if packed is not None:
-        nib, nib_pitch, base, base_pitch = packed
-        _lib.check(L.pdm_combine_packed(_lib.ptr(nib), nib_pitch, _lib.ptr(base), base_pitch,
-                                        pdm_set.tile_bounds_ptr(), grid.num_blocks, pdm_set.n,
-                                        sel.ctypes.data, int(sel.size), _lib.ptr(out), None,
+    ptrs = pdm_set._packed_args() if 0 < sel.size <= _MAX_PACKED_SEL else None
+    if ptrs is not None:
+        _lib.check(L.pdm_combine_packed(*ptrs, grid.num_blocks, pdm_set.n, sel.ctypes.data,
+                                        int(sel.size), out.data_ptr(), None,
                                         _lib.stream_handle()), "pdm_combine_packed")
         return
     storage = pdm_set.storage if sel.size else None

@@ -579,10 +579,10 @@ extern "C" int pdm_select_tf(const double *lut_alpha, int64_t span, int64_t lut_
     // from pinned host memory over PCIe and stores the n flags into pinned
     // host memory, so the call is one launch and one wait -- the two DMA
     // round trips (H2D alpha, D2H flags) each added a copy-engine latency.
-    // PDM_SELECT_DMA=1 keeps the DMA chain (A/B).  (Alpha of 8-bit TFs in the
-    // kernel parameters instead measured slower: 5.9 vs 3.9 us of kernel time,
-    // the CTA's staging of a 2 KB parameter block through the constant cache
-    // serialises.)
+    // PDM_SELECT_DMA=1 keeps the DMA chain (A/B).  Measured and rejected for
+    // 8-bit TFs: alpha in the kernel parameters (2 KB), read from the
+    // parameter bank -- 18.6 vs 16.0 us per call (the larger launch costs more
+    // than the one PCIe round trip it saves).
     static const bool dma = getenv("PDM_SELECT_DMA") && getenv("PDM_SELECT_DMA")[0] == '1';
     if (dma) {
         PDM_REQUIRE(stage_dev && flags_dev, "pdm_select_tf: null device staging");

@@ -554,7 +554,6 @@ __device__ __forceinline__ void merge_packed(const P planes, int k, int64_t map_
             // the unskipped merge's batches of B planes, loads predicated on
             // the keep bits (warp-uniform); batches with no kept plane are
             // not visited
-            bool first = true;
             for (int m = 0; m < k; m += B) {
                 const uint32_t bits = (uint32_t)(keep >> m) & ((1u << B) - 1u);
                 if (bits == 0) continue;
@@ -573,8 +572,11 @@ __device__ __forceinline__ void merge_packed(const P planes, int k, int64_t map_
                         bv[j] = ld_stream_u16(planes.base_at(m + j) + t * 2);
                     }
                 }
-                fold_ids<B>(acc, qv, bv, id, first, live);
-                first = false;
+                // no dominance vote here: the tile skip has already dropped the
+                // planes that cannot lower the warp's blocks (the vote's
+                // chunk maxima cost more than the folds it still saved:
+                // 41.0 -> 39.2 us per bench step without it)
+                fold_ids<B>(acc, qv, bv, id, true, live);
             }
         } else {
             nread += (uint64_t)k;

@@ -102,13 +102,18 @@ def complete() -> None:
     _lib.check(_lib.lib().pdm_stream_synchronize(_lib.stream_handle()), "stream synchronize")
 
 
+_EMPTY = None
+
+
 def empty(shape, np_dtype):
     """Uninitialised tensor on the current CUDA device (raises without one)."""
-    from . import _lib
+    global _EMPTY
+    if _EMPTY is None:
+        from . import _lib
 
-    if _lib._lib is None:
         _lib.lib()  # no CUDA device / library: there is no CPU fallback
-    return torch().empty(shape, dtype=_torch_dtype(np_dtype), device="cuda")
+        _EMPTY = torch().empty
+    return _EMPTY(shape, dtype=_torch_dtype(np_dtype), device="cuda")
 
 
 def plane_pitch(num_blocks: int) -> int:

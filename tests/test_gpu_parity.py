@@ -761,6 +761,75 @@ def test_merge_writes_stay_inside_the_map(monkeypatch, packed):
         assert np.array_equal(host, oracle.combine(maps, s)), s
 
 
+@pytest.mark.parametrize("dims,b,bits", [
+    ((20, 12, 64), 4, 16),    # apron fast path (16-byte chunks), DT with separate packing
+    ((9, 10, 512), 4, 16),    # fused z-pass packing + tile bounds (bz = 128), partial y block
+    ((7, 5, 96), 2, 8),       # 8-bit apron fast path, b = 2, partial strip
+    ((6, 7, 13), 1, 8),       # generic kernels (nz not a chunk multiple)
+])
+def test_precompute_kernels_write_inside_their_outputs(dims, b, bits):
+    """Canary bytes around every precompute output survive (compute-sanitizer
+    is closed on this pool; this is the bounds check that replaces it): apron
+    min/max and the range_apron mask, the DT planes with the fused packing and
+    tile bounds.  Results equal the oracle, so the writes inside are right."""
+    import torch
+
+    from paper_2407_21552_b200 import _lib
+
+    L = _lib.lib()
+    st = _lib.stream_handle()
+    rng = np.random.default_rng(sum(dims) + b)
+    vox = random_structured_volume(rng, dims, bits)
+    n = 12
+    scheme = pdm.scheme_uniform(n, bits)
+    grid = pdm.BlockGrid.for_dims(dims, b)
+    nb = grid.num_blocks
+    vt = pdm.device.to_device(vox)
+    G = 256  # canary bytes on each side
+    dt = torch.int16 if bits == 16 else torch.uint8
+    esz = 2 if bits == 16 else 1
+
+    def guarded(nbytes):
+        buf = torch.full((nbytes + 2 * G,), 0xA5, dtype=torch.uint8, device="cuda")
+        return buf, buf[G:G + nbytes]
+
+    def intact(buf, nbytes):
+        return int((buf[:G] != 0xA5).sum()) == 0 and int((buf[G + nbytes:] != 0xA5).sum()) == 0
+
+    bmn, mn = guarded(nb * esz)
+    bmx, mx = guarded(nb * esz)
+    _lib.check(L.pdm_block_min_max(_lib.ptr(vt), bits, *dims, b, _lib.ptr(mn), _lib.ptr(mx), st),
+               "minmax")
+    want_mn, want_mx = oracle.block_min_max(vox, b)
+    assert np.array_equal(mn.view(dt).cpu().numpy().view(want_mn.dtype), want_mn.reshape(-1))
+    assert np.array_equal(mx.view(dt).cpu().numpy().view(want_mx.dtype), want_mx.reshape(-1))
+    assert intact(bmn, nb * esz) and intact(bmx, nb * esz)
+    pid = pdm.device.to_device(scheme.pid_lut())
+    words = (n + 31) // 32
+    bmask, mask = guarded(nb * words * 4)
+    _lib.check(L.pdm_partition_mask_range_apron(_lib.ptr(vt), bits, *dims, b, _lib.ptr(pid), n,
+                                                _lib.ptr(mask), words, st), "mask")
+    assert intact(bmask, nb * words * 4)
+    pitch = pdm.device.plane_pitch(nb)
+    chunks = int(L.pdm_packed_chunks(nb))
+    nib_pitch, base_pitch = -(-chunks * 8 // 256) * 256, -(-chunks // 256) * 256
+    tiles = -(-nb // 1024)
+    bst, storage = guarded(n * pitch)
+    bnib, nib = guarded(n * nib_pitch)
+    bbase, base = guarded(n * base_pitch)
+    btb, tb = guarded(tiles * n * 2)
+    bad = torch.zeros(1, dtype=torch.int32, device="cuda")
+    _lib.check(L.pdm_distance_transform_mask_packed(
+        _lib.ptr(mask), words, n, *grid.bdims, _lib.ptr(storage), pitch, _lib.ptr(nib), nib_pitch,
+        _lib.ptr(base), base_pitch, _lib.ptr(bad), _lib.ptr(tb), st), "dt packed")
+    want = oracle.build_pdm_set(vox, b, scheme.bounds(), "range_apron")
+    got = storage.view(n, pitch)[:, :nb].cpu().numpy()
+    assert np.array_equal(got, np.stack([w.reshape(-1) for w in want]))
+    for buf, nbytes in ((bst, n * pitch), (bnib, n * nib_pitch), (bbase, n * base_pitch),
+                        (btb, tiles * n * 2)):
+        assert intact(buf, nbytes)
+
+
 def test_merge_fused_zero_count(monkeypatch):
     """combine_flags_into(count_zeros=True): the packed merge counts D''s zero
     blocks itself; occupied_fraction equals the host count (map size not a
