@@ -441,7 +441,7 @@ __device__ __forceinline__ void add_zero_count(uint32_t nzero, unsigned long lon
 }
 
 // ---- per-tile plane skip ------------------------------------------------------
-// For every plane p and tile of kTileBlocks blocks (the 32 items one warp
+// For every plane p and tile of 1024 blocks (the 32 items one warp
 // merges per lap) the set keeps tb[tile][p] = tmin | tmax << 8, the plane's
 // smallest and largest distance over the tile (made once after packing,
 // pdm_packed_tile_bounds).  For a selection S every block of the tile ends at
@@ -453,7 +453,6 @@ __device__ __forceinline__ void add_zero_count(uint32_t nzero, unsigned long lon
 // tissue) has a near-zero plane in S and the warp then reads only the planes
 // that come closer than it -- on the bench's TF sequence 55 % of the
 // (tile, selected plane) pairs are read (tools/exp/tile_bound_stats.py).
-constexpr int kTileBlocks = 1024;
 struct TileSkip {
     const uint16_t *tb;  // [tiles][n]; nullptr: read every selected plane
     int n;
@@ -503,9 +502,12 @@ __device__ __forceinline__ void fold_ids(PackedAcc &acc, const uint4 (&q)[B],
 // wave of resident CTAs, laps equalised).  Measured and rejected: warps
 // claiming tiles from an atomic queue (1 or 4-8 tiles per claim) to even out
 // the skip's uneven work -- 70-78 us vs 43-45 us per step (the same-address
-// atomics and their exposed latency cost far more than the imbalance), and a
+// atomics and their exposed latency cost far more than the imbalance), a
 // per-tile compaction of the kept planes into full batches (42.3 vs 40.0 us:
-// more instructions per plane; the fold, not the round trips, dominates).
+// more instructions per plane; the fold, not the round trips, dominates), and
+// an L2 prefetch of the next tile's kept planes a lap ahead (48.0 vs 39.0 us:
+// the kernel is issue-bound, ncu 42-55 % issue active with 20 of 24 warps
+// resident, and every extra instruction shows).
 template <int B, int kOut, bool kCount, class P>  // B: selected planes per load batch
 __device__ __forceinline__ void merge_packed(const P planes, int k, int64_t map_bytes,
                                              uint8_t *__restrict__ out,
