@@ -33,6 +33,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdlib>
+#include <mutex>
 
 #include "pdm_common.cuh"
 
@@ -672,6 +673,277 @@ __global__ void __launch_bounds__(256)
     }
 }
 
+// ---- sweep passes with the lines held in tensor memory -------------------------
+// dt_tile_kernel keeps every warp's tile (8 KB) AND its sweep table (8 KB) in
+// shared memory, so an SM holds 14 sweeping warps -- and the sweep is bound
+// by the latency of its table lookup chain (ncu: 54-66 % issue active,
+// short-scoreboard and wait stalls).  Here a warp's 32 lines live in TMEM
+// (the tensor cores' 256 KB per SM, idle in this pass): each lane's line is
+// 64 private 32-bit columns of its TMEM lane (tcgen05.st / tcgen05.ld of 16
+// columns = 64 elements at a time), so the warp needs only one 8 KB
+// shared-memory buffer -- the cp.async staging of its tile, then the table
+// of each sweep, then the staging of the write-back -- and 24 warps sweep per
+// SM.  Lines of exactly 256 blocks in full 32-line tiles (config c's 256^3
+// block grid); everything else runs dt_tile_kernel.
+namespace tmem {
+
+__device__ __forceinline__ void alloc(uint32_t *dst, uint32_t cols) {  // whole warp
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_addr(dst)),
+                 "r"(cols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void dealloc(uint32_t taddr, uint32_t cols) {  // whole warp
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(cols)
+                 : "memory");
+}
+__device__ __forceinline__ void fence_before() {
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void fence_after() {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+// 16 consecutive columns of the thread's lane <- w[0..16)
+__device__ __forceinline__ void st16(uint32_t taddr, const uint32_t (&w)[16]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
+        "%11, %12, %13, %14, %15, %16};" ::"r"(taddr),
+        "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7]),
+        "r"(w[8]), "r"(w[9]), "r"(w[10]), "r"(w[11]), "r"(w[12]), "r"(w[13]), "r"(w[14]),
+        "r"(w[15])
+        : "memory");
+}
+// w[0..16) <- 16 consecutive columns; waits for this thread's earlier stores
+// first and for the load itself before returning (one asm block, so no use
+// of w can be scheduled ahead of the wait).
+__device__ __forceinline__ void ld16(uint32_t taddr, uint32_t (&w)[16]) {
+    asm volatile(
+        "tcgen05.wait::st.sync.aligned;\n\t"
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
+        "%11, %12, %13, %14, %15}, [%16];\n\t"
+        "tcgen05.wait::ld.sync.aligned;"
+        : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]), "=r"(w[4]), "=r"(w[5]), "=r"(w[6]),
+          "=r"(w[7]), "=r"(w[8]), "=r"(w[9]), "=r"(w[10]), "=r"(w[11]), "=r"(w[12]),
+          "=r"(w[13]), "=r"(w[14]), "=r"(w[15])
+        : "r"(taddr)
+        : "memory");
+}
+__device__ __forceinline__ void wait_st() {
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+
+}  // namespace tmem
+
+constexpr int kTmemWarps = 4;      // one warp per TMEM lane quarter
+constexpr int kTmemL = 256;        // line length served
+constexpr int kTmemCols = 64;      // 256 bytes per lane
+
+template <int AXIS>
+__global__ void __launch_bounds__(32 * kTmemWarps, 6)
+    dt_tmem_kernel(int n, int64_t bx, int64_t by, int64_t bz, uint8_t *__restrict__ pdms,
+                   int64_t pitch, int64_t tiles, PackDst pk, unsigned long long *next) {
+    constexpr int L = kTmemL, NC = L / 64;  // TMEM chunks of 16 columns
+    constexpr bool kRows = AXIS == kAxisZ;
+    __shared__ __align__(16) uint8_t s_buf[kTmemWarps][32 * L];
+    __shared__ uint32_t s_taddr;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (warp == 0) tmem::alloc(&s_taddr, kTmemCols);
+    tmem::fence_before();
+    __syncthreads();
+    tmem::fence_after();
+    const uint32_t tbase = s_taddr;
+    const uint32_t taddr = tbase + ((uint32_t)(32 * (warp & 3)) << 16);
+    uint8_t *s = s_buf[warp];
+    const uint32_t tab = smem_addr(s + lane);  // the sweep table's lane column
+    const int64_t S = bz;                      // y lines: element stride
+    const int64_t zblocks = bz / 32;
+    // Tiles are handed out by an atomic counter, claimed one tile ahead: a
+    // tile is ~16k chain steps per lane and flat tiles are skipped, so a
+    // static split left a warp's CTA-mates idle at the end (ncu: barrier
+    // stalls at the dealloc sync).
+    auto claim = [&]() -> int64_t {
+        unsigned long long v = 0;
+        if (lane == 0) v = atomicAdd(next, 1ull);
+        return (int64_t)__shfl_sync(0xFFFFFFFFu, v, 0);
+    };
+    int64_t t_next = claim();
+    for (;;) {
+        const int64_t t = t_next;
+        if (t >= tiles) break;
+        t_next = claim();
+        uint8_t *g;
+        if (kRows) {
+            const int64_t per_p = bx * by / 32;
+            g = pdms + (t / per_p) * pitch + (t % per_p) * 32 * bz;
+        } else {
+            const int64_t po = t / zblocks, z0 = (t % zblocks) * 32;
+            g = pdms + (po / bx) * pitch + (po % bx) * by * bz + z0;
+        }
+        // stage the tile (rows: 16-byte chunks swizzled by row; y lines: [u][32])
+        if (kRows) {
+            for (int i = lane; i < 32 * (L / 16); i += 32) {
+                const int r = i >> 4, c = i & 15;
+                cpa::copy16(s + r * L + ((c ^ (r & 7)) << 4), g + (int64_t)r * bz + 16 * c);
+            }
+        } else {
+            for (int i = lane; i < L * 2; i += 32) {
+                const int u = i >> 1, w = i & 1;
+                cpa::copy16(s + u * 32 + 16 * w, g + (int64_t)u * S + 16 * w);
+            }
+        }
+        cpa::commit();
+        cpa::wait<0>();
+        __syncwarp();
+        const bool flat = tile_is_flat(s, 32 * L, lane);
+        if (!kRows && flat) {  // no change, nothing to pack
+            __syncwarp();
+            continue;
+        }
+        // the lane's line -> TMEM (words of 4 consecutive elements)
+#pragma unroll
+        for (int cc = 0; cc < NC; ++cc) {
+            uint32_t w[16];
+            if (kRows) {
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const int c = 4 * cc + q;
+                    const uint4 v = *reinterpret_cast<const uint4 *>(
+                        s + lane * L + ((c ^ (lane & 7)) << 4));
+                    w[4 * q] = v.x, w[4 * q + 1] = v.y, w[4 * q + 2] = v.z, w[4 * q + 3] = v.w;
+                }
+            } else {
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                    const int u = 64 * cc + 4 * i;
+                    const uint32_t b0 = s[u * 32 + lane], b1 = s[(u + 1) * 32 + lane],
+                                   b2 = s[(u + 2) * 32 + lane], b3 = s[(u + 3) * 32 + lane];
+                    w[i] = __byte_perm(b0 | (b1 << 8), b2 | (b3 << 8), 0x5410);
+                }
+            }
+            tmem::st16(taddr + 16 * cc, w);
+        }
+        tmem::wait_st();
+        __syncwarp();  // the staged tile is consumed: the buffer becomes the table
+        if (!flat) {
+            // forward sweep: L[u] = min_{i<=u} max(u - i, g[i])
+            clear_table<1>(s, lane);
+            __syncwarp();
+            {
+                uint32_t M = tab + SweepTable<1>::kRow * kDistClamp;
+#pragma unroll 1
+                for (int cc = 0; cc < NC; ++cc) {
+                    uint32_t w[16];
+                    tmem::ld16(taddr + 16 * cc, w);
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) w[i] = sweep_word<1, false>(M, w[i], 64 * cc + 4 * i, tab);
+                    tmem::st16(taddr + 16 * cc, w);
+                }
+            }
+            __syncwarp();
+            clear_table<1>(s, lane);
+            __syncwarp();
+            {   // backward sweep over L gives the envelope, in place
+                uint32_t M = tab + SweepTable<1>::kRow * kDistClamp;
+#pragma unroll 1
+                for (int cc = NC - 1; cc >= 0; --cc) {
+                    uint32_t w[16];
+                    tmem::ld16(taddr + 16 * cc, w);
+#pragma unroll
+                    for (int i = 15; i >= 0; --i)
+                        w[i] = sweep_word<1, true>(M, w[i], L - 4 - (64 * cc + 4 * i), tab);
+                    tmem::st16(taddr + 16 * cc, w);
+                }
+            }
+            __syncwarp();
+        }
+        if (!kRows) {
+            // transpose back through the buffer, then coalesced 16-byte stores
+#pragma unroll 1
+            for (int cc = 0; cc < NC; ++cc) {
+                uint32_t w[16];
+                tmem::ld16(taddr + 16 * cc, w);
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                    const int u = 64 * cc + 4 * i;
+                    s[u * 32 + lane] = (uint8_t)w[i];
+                    s[(u + 1) * 32 + lane] = (uint8_t)(w[i] >> 8);
+                    s[(u + 2) * 32 + lane] = (uint8_t)(w[i] >> 16);
+                    s[(u + 3) * 32 + lane] = (uint8_t)(w[i] >> 24);
+                }
+            }
+            __syncwarp();
+            for (int i = lane; i < L * 2; i += 32) {
+                const int u = i >> 1, w = i & 1;
+                *reinterpret_cast<uint4 *>(g + (int64_t)u * S + 16 * w) =
+                    *reinterpret_cast<const uint4 *>(s + u * 32 + 16 * w);
+            }
+            __syncwarp();
+            continue;
+        }
+        // rows: write back (unless flat) and pack (staging in the buffer)
+        const int nst = L / 2 + 8, bst = L / 16 + 4;
+        uint8_t *sn = s, *sb = s + 32 * nst;
+        unsigned int nbad = 0;
+        uint32_t rlo = 255, rhi = 0;
+        uint8_t *grow = g + (int64_t)lane * bz;
+#pragma unroll 1
+        for (int cc = 0; cc < NC; ++cc) {
+            uint32_t w[16];
+            tmem::ld16(taddr + 16 * cc, w);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const uint4 v = make_uint4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
+                const int c = 4 * cc + q;
+                if (!flat) *reinterpret_cast<uint4 *>(grow + 16 * c) = v;
+                if (pk.nib != nullptr) {
+                    uint32_t mn, mx;
+                    const uint2 pw = pack_chunk(v, mn, mx, nbad);
+                    *reinterpret_cast<uint2 *>(sn + lane * nst + 8 * c) = pw;
+                    sb[lane * bst + c] = (uint8_t)mn;
+                    rlo = min(rlo, mn);
+                    rhi = max(rhi, mx);
+                }
+            }
+        }
+        if (pk.nib != nullptr) {
+            if (nbad) atomicAdd(pk.bad, nbad);
+            __syncwarp();
+            const int64_t rows = bx * by, per_p = rows / 32;
+            const int64_t p = t / per_p, r0 = (t % per_p) * 32;
+            if (pk.tb != nullptr) {  // 1024-block tile = 4 rows of 256
+                constexpr int rpt = 1024 / L;
+#pragma unroll
+                for (int o = 1; o < rpt; o <<= 1) {
+                    rlo = min(rlo, __shfl_xor_sync(0xFFFFFFFFu, rlo, o));
+                    rhi = max(rhi, __shfl_xor_sync(0xFFFFFFFFu, rhi, o));
+                }
+                if ((lane & (rpt - 1)) == 0)
+                    pk.tb[((r0 + lane) / rpt) * pk.n + p] = (uint16_t)(rlo | (rhi << 8));
+            }
+            uint8_t *gn = pk.nib + p * pk.nib_pitch + r0 * (L / 2);
+            uint8_t *gb = pk.base + p * pk.base_pitch + r0 * (L / 16);
+            constexpr int nu = L / 16;
+            for (int i = lane; i < 32 * nu; i += 32) {
+                const int r = i / nu, c = i - r * nu;
+                *reinterpret_cast<uint2 *>(gn + 8 * (int64_t)i) =
+                    *reinterpret_cast<const uint2 *>(sn + r * nst + 8 * c);
+            }
+            constexpr int bu = L / 64;
+            for (int i = lane; i < 32 * bu; i += 32) {
+                const int r = i / bu, c = i - r * bu;
+                *reinterpret_cast<uint32_t *>(gb + 4 * (int64_t)i) =
+                    *reinterpret_cast<const uint32_t *>(sb + r * bst + 4 * c);
+            }
+        }
+        __syncwarp();
+    }
+    tmem::fence_before();
+    __syncthreads();
+    tmem::fence_after();
+    if (warp == 0) tmem::dealloc(tbase, kTmemCols);
+}
+
 // Lines longer than 1024 blocks: one thread per line straight from global
 // memory (correct for any length up to 4095, slower).
 template <int AXIS, bool kDist1D>
@@ -897,6 +1169,65 @@ static int wide_x_pass(int n, int64_t bx, int64_t by, int64_t bz, uint8_t *pdms,
     return cuda_status("dt_dist1d_wide_kernel");
 }
 
+// A zeroed tile counter for one launch on stream s: a ring of 64 per device
+// (never freed), zeroed in stream order, so launches in flight on different
+// streams do not share one.
+static int tile_counter(cudaStream_t s, unsigned long long **out) {
+    constexpr int kSlots = 64;
+    static std::mutex mu;
+    static unsigned long long *ring[64] = {nullptr};
+    static unsigned next_slot[64] = {0};
+    int dev = 0;
+    PDM_CUDA_TRY(cudaGetDevice(&dev));
+    PDM_REQUIRE(dev >= 0 && dev < 64, "tile_counter: device %d", dev);
+    unsigned long long *p;
+    {
+        std::lock_guard<std::mutex> lock(mu);
+        if (ring[dev] == nullptr)
+            PDM_CUDA_TRY(cudaMalloc(&ring[dev], kSlots * sizeof(unsigned long long)));
+        p = ring[dev] + (next_slot[dev]++ % kSlots);
+    }
+    PDM_CUDA_TRY(cudaMemsetAsync(p, 0, sizeof(unsigned long long), s));
+    *out = p;
+    return PDM_OK;
+}
+
+// The TMEM sweep serves 256-long lines in full 32-line tiles with 16-byte
+// aligned rows; PDM_DT_TMEM=0 keeps dt_tile_kernel (A/B).
+template <int AXIS>
+static bool tmem_pass_ok(int64_t bx, int64_t by, int64_t bz) {
+    static const bool off = getenv("PDM_DT_TMEM") && getenv("PDM_DT_TMEM")[0] == '0';
+    if (off || AXIS == kAxisX) return false;
+    if (AXIS == kAxisY) return by == kTmemL && bz % 32 == 0;
+    return bz == kTmemL && (bx * by) % 32 == 0;
+}
+
+template <int AXIS>
+static int tmem_pass(int n, int64_t bx, int64_t by, int64_t bz, uint8_t *pdms, int64_t pitch,
+                     cudaStream_t s, PackDst pk) {
+    auto kern = dt_tmem_kernel<AXIS>;
+    const int64_t tiles = AXIS == kAxisZ ? (int64_t)n * (bx * by / 32)
+                                         : (int64_t)n * bx * (bz / 32);
+    // 6 CTAs of 4 warps per SM (33 KB of shared memory each, 80 registers,
+    // 6 x 64 TMEM columns); the carveout must be the maximum for that
+    static bool attr_set = false;
+    if (!attr_set) {
+        PDM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                          (int)cudaSharedmemCarveoutMaxShared));
+        attr_set = true;
+    }
+    // (the occupancy API answers 1 for this kernel; the limits are as above)
+    const int per_sm = 6;
+    int64_t grid = ceil_div(tiles, kTmemWarps);
+    const int64_t cap = (int64_t)sm_count() * per_sm;
+    if (grid > cap) grid = cap;
+    unsigned long long *ctr = nullptr;
+    int st = tile_counter(s, &ctr);
+    if (st) return st;
+    kern<<<(unsigned)grid, 32 * kTmemWarps, 0, s>>>(n, bx, by, bz, pdms, pitch, tiles, pk, ctr);
+    return cuda_status("dt_tmem_kernel");
+}
+
 // pk (z pass only): fused packing epilogue; honoured when the z pass runs the
 // swizzled sweep (dt_fused_pack_ok), ignored otherwise.
 template <int AXIS, bool kDist1D>
@@ -910,6 +1241,8 @@ static int axis_pass(int n, int64_t bx, int64_t by, int64_t bz, uint8_t *pdms, i
         if (L <= 1024) return tile_pass<64, AXIS, true>(n, bx, by, bz, pdms, pitch, s);
     } else {
         // lines <= 512: stack-free sweep envelope; longer: Meijster's scan
+        if (tmem_pass_ok<AXIS>(bx, by, bz))
+            return tmem_pass<AXIS>(n, bx, by, bz, pdms, pitch, s, pk);
         if (L <= 256) return tile_pass<256, AXIS, false, true>(n, bx, by, bz, pdms, pitch, s, pk);
         if (L <= 512) return tile_pass<512, AXIS, false, true>(n, bx, by, bz, pdms, pitch, s, pk);
         if (L <= 1024) return tile_pass<1024, AXIS, false>(n, bx, by, bz, pdms, pitch, s);
