@@ -15,6 +15,8 @@
 // HBM (y-apron rows are re-read from L2 by the neighbouring warp).
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "pdm_common.cuh"
 
 namespace pdm {
@@ -42,10 +44,23 @@ __device__ __forceinline__ void write_range_bits(uint32_t *mask, int64_t c, int 
 #define PDM_APRON_RING 2
 #endif
 constexpr int kApronRing = PDM_APRON_RING;
-template <int B>
+template <int B, int RB>
 constexpr size_t apron_smem_per_warp() {
-    return (size_t)kApronRing * (B + 2) * (32 * 16 + 2 * 4);
+    return (size_t)kApronRing * (RB * B + 2) * (32 * 16 + 2 * 4);
 }
+// Block rows per warp.  Two (16-bit volumes, b = 4: a warp reads 2b + 2 rows
+// for 2b instead of 2b + 4, the two shared apron rows reduce once) measured
+// 0.445 vs 0.438 ms at config c: the register cost (96 vs 72, 5 vs 6 CTAs per
+// SM) outweighs the rows saved (ncu: DRAM read 2.35 vs 2.46 GB).  One is the
+// default; PDM_APRON_RB=2 selects two (A/B; same results, tested).
+template <int BITS, int B>
+constexpr bool apron_two_rows() {
+    return BITS == 16 && B == 4;
+}
+#ifndef PDM_APRON_MINCTAS  // (overridable for A/B builds)
+#define PDM_APRON_MINCTAS 6
+#endif
+constexpr int kApronMinCtas = PDM_APRON_MINCTAS;  // 16-bit, b = 4, one block row
 constexpr int kApronWarps = 4;
 
 // Voxels as unsigned 16-bit lanes: a 16-byte chunk is NW = VPC / 2 words of
@@ -77,8 +92,9 @@ __device__ __forceinline__ void chunk_words(uint4 q, uint32_t (&w)[16 / (BITS / 
 // neighbours; the plane then folds into the current block row (and into the
 // previous one at r = 0, the next one at r = B - 1), all decided at compile
 // time by unrolling the B planes of a block.
-template <int BITS, int B, int OUTS>
-__global__ void __launch_bounds__(32 * kApronWarps)
+template <int BITS, int B, int OUTS, int RB>
+__global__ void __launch_bounds__(32 * kApronWarps,
+                                  (BITS == 16 && B == 4) ? (RB == 1 ? kApronMinCtas : 5) : 1)
     apron_fast_kernel(const typename VoxT<BITS>::type *__restrict__ vox, int64_t nx, int64_t ny,
                       int64_t nz, int64_t bx, int64_t by, int64_t bz, int XB,
                       typename VoxT<BITS>::type *__restrict__ mins,
@@ -88,7 +104,7 @@ __global__ void __launch_bounds__(32 * kApronWarps)
     constexpr int VPC = 16 / (BITS / 8);  // voxels per lane chunk
     constexpr int NW = VPC / 2;           // u16x2 words per chunk
     constexpr int ZB = VPC / B;           // z-blocks per lane
-    constexpr int kRows = B + 2;
+    constexpr int kRows = RB * B + 2;     // RB block rows and their two apron rows
     constexpr int WV = 4 / (BITS / 8);  // voxels per 4-byte edge word
     const unsigned FULL = 0xFFFFFFFFu;
     const int lane = threadIdx.x & 31;
@@ -102,14 +118,15 @@ __global__ void __launch_bounds__(32 * kApronWarps)
     const int64_t strip = 32 * VPC;
     const int64_t nstrips = ceil_div(nz, strip);
     const int64_t xchunks = ceil_div(bx, XB);
-    const int64_t items = by * nstrips * xchunks;
+    const int64_t groups = ceil_div(by, RB);
+    const int64_t items = groups * nstrips * xchunks;
     const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     const int64_t plane_elems = ny * nz;
     for (int64_t it = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; it < items;
          it += warps) {
         const int64_t s = it % nstrips;
         const int64_t rest = it / nstrips;
-        const int64_t xc = rest % xchunks, j = rest / xchunks;
+        const int64_t xc = rest % xchunks, jg = rest / xchunks;
         const int64_t zs = s * strip;
         const int64_t zl = zs + (int64_t)lane * VPC;
         const bool active = zl < nz;
@@ -130,11 +147,13 @@ __global__ void __launch_bounds__(32 * kApronWarps)
             eoff = has_right ? zs + strip : last;
             esel = has_right ? 0 : WV - 1;
         }
-        int64_t roff[kRows];
+        // rows y = clamp(jg RB B - 1 + r); a block row past the volume (odd by
+        // with RB = 2) reads clamped rows and is never emitted
+        uint32_t roffb[kRows];  // (a plane is < 2 GB: apron_fast_launch checks)
 #pragma unroll
         for (int r = 0; r < kRows; ++r) {
-            const int64_t y = min(max(j * B - 1 + r, (int64_t)0), ny - 1);
-            roff[r] = y * nz;
+            const int64_t y = min(max(jg * RB * B - 1 + r, (int64_t)0), ny - 1);
+            roffb[r] = (uint32_t)(y * nz * (int64_t)sizeof(T));
         }
         const int64_t xa = i0 * B - 1;                      // first plane of the run
         const int nplanes = (int)((i1 - i0) * B + 2);  // + leading and trailing apron planes
@@ -143,9 +162,6 @@ __global__ void __launch_bounds__(32 * kApronWarps)
         const char *lane0 = reinterpret_cast<const char *>(vox + zcol);
         const int64_t edelta = (eoff - zcol) * (int64_t)sizeof(T);
         const int64_t plane_bytes = plane_elems * (int64_t)sizeof(T);
-        int64_t roffb[kRows];
-#pragma unroll
-        for (int r = 0; r < kRows; ++r) roffb[r] = roff[r] * (int64_t)sizeof(T);
         auto issue = [&](int q) {  // plane q of the run into ring slot q % kApronRing
             if (q < nplanes) {
                 const int64_t x = min(max(xa + q, (int64_t)0), nx - 1);
@@ -162,25 +178,17 @@ __global__ void __launch_bounds__(32 * kApronWarps)
             }
             cpa::commit();
         };
-        // z-block min/max of plane q (after its copies landed)
-        auto plane_mm = [&](int q, uint32_t (&mn)[ZB], uint32_t (&mx)[ZB]) {
-            const int slot = q % kApronRing;
-            uint32_t wmn[NW], wmx[NW];
-            {
-                uint32_t w0[NW], w1[NW];
-                chunk_words<BITS>(ring_main[(slot * kRows + 0) * 32 + lane], w0);
-                chunk_words<BITS>(ring_main[(slot * kRows + 1) * 32 + lane], w1);
+        // u16x2 min/max over rows [a, b) of ring slot `slot` (3-input forms)
+        auto rows_mm = [&](int slot, int a, int b, uint32_t (&wmn)[NW], uint32_t (&wmx)[NW]) {
+            uint32_t w0[NW];
+            chunk_words<BITS>(ring_main[(slot * kRows + a) * 32 + lane], w0);
 #pragma unroll
-                for (int i = 0; i < NW; ++i) {
-                    wmn[i] = __vminu2(w0[i], w1[i]);
-                    wmx[i] = __vmaxu2(w0[i], w1[i]);
-                }
-            }
+            for (int i = 0; i < NW; ++i) wmn[i] = wmx[i] = w0[i];
 #pragma unroll
-            for (int r = 2; r < kRows; r += 2) {
+            for (int r = a + 1; r < b; r += 2) {
                 uint32_t wa[NW], wb[NW];
                 chunk_words<BITS>(ring_main[(slot * kRows + r) * 32 + lane], wa);
-                if (r + 1 < kRows) {
+                if (r + 1 < b) {
                     chunk_words<BITS>(ring_main[(slot * kRows + r + 1) * 32 + lane], wb);
 #pragma unroll
                     for (int i = 0; i < NW; ++i) {
@@ -195,11 +203,16 @@ __global__ void __launch_bounds__(32 * kApronWarps)
                     }
                 }
             }
+        };
+        // z-block min/max of block row k of plane q (after its copies landed),
+        // given the row reduction of its B + 2 rows
+        auto zblocks = [&](int slot, int k, const uint32_t (&wmn)[NW], const uint32_t (&wmx)[NW],
+                           uint32_t (&mn)[ZB], uint32_t (&mx)[ZB]) {
             // strip-edge voxel (lanes 0 and 31): reduce its rows
             uint32_t emn = 0xFFFFFFFFu, emx = 0;
             if (lane == 0 || lane == 31) {
 #pragma unroll
-                for (int r = 0; r < kRows; ++r) {
+                for (int r = k * B; r < k * B + B + 2; ++r) {
                     const uint32_t w = ring_edge[(slot * kRows + r) * 2 + (lane == 31)];
                     const uint32_t e = BITS == 8 ? (w >> (8 * esel)) & 0xFFu
                                                  : (w >> (16 * esel)) & 0xFFFFu;
@@ -238,8 +251,35 @@ __global__ void __launch_bounds__(32 * kApronWarps)
                 mx[t] = max(b2, t == ZB - 1 ? rmx : vmx[t * B + B]);
             }
         };
-        auto emit = [&](int64_t i, const uint32_t(&mn)[ZB], const uint32_t(&mx)[ZB]) {
-            if (!active) return;
+        auto plane_mm = [&](int q, uint32_t (&mn)[RB][ZB], uint32_t (&mx)[RB][ZB]) {
+            const int slot = q % kApronRing;
+            if (RB == 1) {
+                uint32_t wmn[NW], wmx[NW];
+                rows_mm(slot, 0, kRows, wmn, wmx);
+                zblocks(slot, 0, wmn, wmx, mn[0], mx[0]);
+            } else {
+                // block rows 0 and 1 share their two middle rows B, B + 1
+                uint32_t smn[NW], smx[NW], amn[NW], amx[NW];
+                rows_mm(slot, B, B + 2, smn, smx);
+                rows_mm(slot, 0, B, amn, amx);
+#pragma unroll
+                for (int i = 0; i < NW; ++i) {
+                    amn[i] = __vminu2(amn[i], smn[i]);
+                    amx[i] = __vmaxu2(amx[i], smx[i]);
+                }
+                zblocks(slot, 0, amn, amx, mn[0], mx[0]);
+                rows_mm(slot, B + 2, 2 * B + 2, amn, amx);
+#pragma unroll
+                for (int i = 0; i < NW; ++i) {
+                    amn[i] = __vminu2(amn[i], smn[i]);
+                    amx[i] = __vmaxu2(amx[i], smx[i]);
+                }
+                zblocks(slot, 1, amn, amx, mn[RB - 1], mx[RB - 1]);
+            }
+        };
+        auto emit = [&](int64_t i, int k, const uint32_t(&mn)[ZB], const uint32_t(&mx)[ZB]) {
+            const int64_t j = jg * RB + k;
+            if (!active || j >= by) return;
             const int64_t c0 = (i * by + j) * bz + zl / B;
 #pragma unroll
             for (int t = 0; t < ZB; ++t) {
@@ -252,12 +292,14 @@ __global__ void __launch_bounds__(32 * kApronWarps)
         };
 #pragma unroll
         for (int d = 0; d < kApronRing; ++d) issue(d);
-        uint32_t pmn[ZB], pmx[ZB], cmn[ZB], cmx[ZB], nmn[ZB], nmx[ZB];
+        uint32_t pmn[RB][ZB], pmx[RB][ZB], cmn[RB][ZB], cmx[RB][ZB], nmn[RB][ZB], nmx[RB][ZB];
 #pragma unroll
-        for (int t = 0; t < ZB; ++t) {
-            pmn[t] = nmn[t] = 0xFFFFFFFFu;
-            pmx[t] = nmx[t] = 0u;
-        }
+        for (int k = 0; k < RB; ++k)
+#pragma unroll
+            for (int t = 0; t < ZB; ++t) {
+                pmn[k][t] = nmn[k][t] = 0xFFFFFFFFu;
+                pmx[k][t] = nmx[k][t] = 0u;
+            }
         // plane 0: the leading apron plane of block i0 starts its accumulator
         cpa::wait<kApronRing - 1>();
         __syncwarp();
@@ -270,46 +312,55 @@ __global__ void __launch_bounds__(32 * kApronWarps)
             for (int r = 0; r < B; ++r, ++q) {
                 cpa::wait<kApronRing - 1>();
                 __syncwarp();
-                uint32_t mn[ZB], mx[ZB];
+                uint32_t mn[RB][ZB], mx[RB][ZB];
                 plane_mm(q, mn, mx);
                 __syncwarp();
                 issue(q + kApronRing);  // refill the slot just read
 #pragma unroll
-                for (int t = 0; t < ZB; ++t) {
-                    cmn[t] = min(cmn[t], mn[t]);
-                    cmx[t] = max(cmx[t], mx[t]);
-                    if (r == 0) {  // trailing apron plane of block i - 1
-                        pmn[t] = min(pmn[t], mn[t]);
-                        pmx[t] = max(pmx[t], mx[t]);
+                for (int k = 0; k < RB; ++k)
+#pragma unroll
+                    for (int t = 0; t < ZB; ++t) {
+                        cmn[k][t] = min(cmn[k][t], mn[k][t]);
+                        cmx[k][t] = max(cmx[k][t], mx[k][t]);
+                        if (r == 0) {  // trailing apron plane of block i - 1
+                            pmn[k][t] = min(pmn[k][t], mn[k][t]);
+                            pmx[k][t] = max(pmx[k][t], mx[k][t]);
+                        }
+                        if (r == B - 1) {  // leading apron plane of block i + 1
+                            nmn[k][t] = mn[k][t];
+                            nmx[k][t] = mx[k][t];
+                        }
                     }
-                    if (r == B - 1) {  // leading apron plane of block i + 1
-                        nmn[t] = mn[t];
-                        nmx[t] = mx[t];
-                    }
-                }
-                if (r == 0 && i > i0) emit(i - 1, pmn, pmx);
+                if (r == 0 && i > i0)
+#pragma unroll
+                    for (int k = 0; k < RB; ++k) emit(i - 1, k, pmn[k], pmx[k]);
             }
 #pragma unroll
-            for (int t = 0; t < ZB; ++t) {
-                pmn[t] = cmn[t];
-                pmx[t] = cmx[t];
-                cmn[t] = nmn[t];
-                cmx[t] = nmx[t];
-            }
+            for (int k = 0; k < RB; ++k)
+#pragma unroll
+                for (int t = 0; t < ZB; ++t) {
+                    pmn[k][t] = cmn[k][t];
+                    pmx[k][t] = cmx[k][t];
+                    cmn[k][t] = nmn[k][t];
+                    cmx[k][t] = nmx[k][t];
+                }
         }
         // trailing apron plane of the run's last block
         cpa::wait<kApronRing - 1>();
         __syncwarp();
         {
-            uint32_t mn[ZB], mx[ZB];
+            uint32_t mn[RB][ZB], mx[RB][ZB];
             plane_mm(q, mn, mx);
 #pragma unroll
-            for (int t = 0; t < ZB; ++t) {
-                pmn[t] = min(pmn[t], mn[t]);
-                pmx[t] = max(pmx[t], mx[t]);
-            }
+            for (int k = 0; k < RB; ++k)
+#pragma unroll
+                for (int t = 0; t < ZB; ++t) {
+                    pmn[k][t] = min(pmn[k][t], mn[k][t]);
+                    pmx[k][t] = max(pmx[k][t], mx[k][t]);
+                }
         }
-        emit(i1 - 1, pmn, pmx);
+#pragma unroll
+        for (int k = 0; k < RB; ++k) emit(i1 - 1, k, pmn[k], pmx[k]);
         cpa::wait<0>();  // the ring is reused by the next item
         __syncwarp();
     }
@@ -322,13 +373,22 @@ static int launch_b(const void *vox, int64_t nx, int64_t ny, int64_t nz, int64_t
     using T = typename VoxT<BITS>::type;
     constexpr int VPC = 16 / (BITS / 8);
     const int XB = 32;
-    const int64_t items = by * ceil_div(nz, 32 * VPC) * ceil_div(bx, XB);
-    const size_t smem = kApronWarps * apron_smem_per_warp<B>();
+    static const bool two = getenv("PDM_APRON_RB") && getenv("PDM_APRON_RB")[0] == '2';
+    constexpr int RB2 = apron_two_rows<BITS, B>() ? 2 : 1;
+    const int RB = two ? RB2 : 1;
+    const int64_t items = ceil_div(by, RB) * ceil_div(nz, 32 * VPC) * ceil_div(bx, XB);
+    const size_t smem = kApronWarps * (RB == 1 ? apron_smem_per_warp<B, 1>()
+                                               : apron_smem_per_warp<B, RB2>());
     const int threads = 32 * kApronWarps;
     auto pick = [&]() {
-        if (outs == kOutMinMax) return apron_fast_kernel<BITS, B, kOutMinMax>;
-        if (outs == kOutMask) return apron_fast_kernel<BITS, B, kOutMask>;
-        return apron_fast_kernel<BITS, B, kOutMinMax | kOutMask>;
+        if (RB == 1) {
+            if (outs == kOutMinMax) return apron_fast_kernel<BITS, B, kOutMinMax, 1>;
+            if (outs == kOutMask) return apron_fast_kernel<BITS, B, kOutMask, 1>;
+            return apron_fast_kernel<BITS, B, kOutMinMax | kOutMask, 1>;
+        }
+        if (outs == kOutMinMax) return apron_fast_kernel<BITS, B, kOutMinMax, RB2>;
+        if (outs == kOutMask) return apron_fast_kernel<BITS, B, kOutMask, RB2>;
+        return apron_fast_kernel<BITS, B, kOutMinMax | kOutMask, RB2>;
     };
     auto kern = pick();
     PDM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -352,7 +412,9 @@ int apron_fast_launch(const void *vox, int bits, int64_t nx, int64_t ny, int64_t
                       int outs, void *mins, void *maxs, const int32_t *pid, uint32_t *mask,
                       int words, cudaStream_t s) {
     const int vpc = bits == 8 ? 16 : 8;
-    if ((nz % vpc) != 0 || (vpc % b) != 0 || ((uintptr_t)vox % 16) != 0) return PDM_EUNSUPPORTED;
+    if ((nz % vpc) != 0 || (vpc % b) != 0 || ((uintptr_t)vox % 16) != 0 ||
+        ny * nz * (bits / 8) >= ((int64_t)1 << 31))
+        return PDM_EUNSUPPORTED;
     const int64_t bx = ceil_div(nx, b), by = ceil_div(ny, b), bz = ceil_div(nz, b);
     if (bits == 8) {
         switch (b) {
