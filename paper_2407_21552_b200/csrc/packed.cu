@@ -513,6 +513,17 @@ __device__ __forceinline__ void fold_ids(PackedAcc &acc, const uint4 (&q)[B],
 // current one is folded (two register buffers: B=2/3/4/6 at 4/3/3/2 CTAs per
 // SM, 52.4/41.0/43.9/40.4 vs 35.7 us -- although ncu puts 42 % of this
 // loop's stall samples on the first use of a batch's loads), and
+// a per-warp cp.async ring walking the (tile, kept plane) pairs of its tiles
+// 8 slots ahead across tile boundaries, 4 CTAs per SM, no register staging
+// (61.4 vs 36.1 us per merge over the bench sweep), the same pair stream cut
+// into compacted batches with the next batch's loads issued before the
+// current one is folded (two register buffers: B=2/3/4/6 at 4/3/3/2 CTAs per
+// SM, 52.4/41.0/43.9/40.4 vs 35.7 us -- although ncu puts 42 % of this
+// loop's stall samples on the first use of a batch's loads), tiles claimed
+// one ahead from a self-resetting counter (40.4 vs 36.4 us), the add and
+// the min fused as VIADDMNMX.U16x2 (36.2 vs 36.2 us), and -- timing probes
+// with wrong results -- nibbles or bases read from an L2-resident 64 KB /
+// 4 KB instead of HBM (34.8 / 35.0 vs 35.5 us: DRAM is not what bounds it),
 // an L2 prefetch of the next tile's kept planes a lap ahead (48.0 vs 39.0 us:
 // the kernel is issue-bound, ncu 42-55 % issue active with 20 of 24 warps
 // resident, and every extra instruction shows).
