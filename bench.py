@@ -413,9 +413,15 @@ def run_b200(args, rank, world, local_rank):
     host_packed = pdm.acceleration._host_packed_pays(pset)
     host_fmt = pdm.acceleration._host_format(pset) if host_packed else 0
     tiles = -(-B // 1024)
-    pairs_all = sum(ks) * tiles
+    # selections of up to raw_k planes merge the raw planes (pdm_combine_flags_auto):
+    # (k + 1) bytes per block; the others the packed planes with the tile skip
+    raw_k = int(L.pdm_combine_raw_max_k()) if packed is not None else 0
+    ks_raw = [k for k in ks if 1 <= k <= raw_k]
+    ks_packed = [k for k in ks if k > raw_k]
+    pairs_all = sum(ks_packed) * tiles
     if packed is not None:  # bytes the packed merge moves: nibbles + bases read, D' written
-        moved_bytes = pairs_read * 1024 * 9 // 16 + steps * B
+        moved_bytes = (pairs_read * 1024 * 9 // 16 + len(ks_packed) * B
+                       + sum((k + 1) * B for k in ks_raw))
         if pset.tile_bounds_ptr() is not None:  # + the tile-bounds rows (2 B per pair)
             moved_bytes += 2 * pairs_all
     else:

@@ -167,6 +167,20 @@ int pdm_combine_flags_packed(const uint8_t *nib, int64_t nib_pitch, const uint8_
                              int32_t n, const uint8_t *flags, uint8_t *out,
                              unsigned long long *zero_count, pdm_stream_t stream);
 
+/* pdm_combine_flags_packed with the set's raw planes beside the packed ones
+ * (pdms[n][plane_pitch], the pdm_combine_flags layout): the kernel compacts
+ * the flags on the device and, for selections of up to 4 planes (the
+ * latency-bound end of the packed merge; PDM_RAW_MAX_K overrides, 0 = never)
+ * and no zero count, merges the raw planes instead.  Same D' either way.
+ * Replaces acceleration.py:244-276 combine for a device-resident selection. */
+int pdm_combine_flags_auto(const uint8_t *pdms, int64_t plane_pitch, const uint8_t *nib,
+                           int64_t nib_pitch, const uint8_t *base, int64_t base_pitch,
+                           const uint16_t *tile_bounds, int64_t map_bytes, int32_t n,
+                           const uint8_t *flags, uint8_t *out, unsigned long long *zero_count,
+                           pdm_stream_t stream);
+/* The largest selection pdm_combine_flags_auto merges from the raw planes. */
+int pdm_combine_raw_max_k(void);
+
 /* The same two merges writing D' itself in the packed encoding (out_nib: 8 *
  * chunks bytes, out_base: chunks bytes, 16/2-byte aligned) -- 9/16 of the
  * bytes, for a D' headed to host memory over PCIe (combine(...).dist), where

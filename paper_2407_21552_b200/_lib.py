@@ -47,6 +47,8 @@ _SIGNATURES = {
     "pdm_merge_stats": [_P],
     "pdm_combine_packed": [_P, _I64, _P, _I64, _P, _I64, _I32, _P, _I32, _P, _P, _P],
     "pdm_combine_flags_packed": [_P, _I64, _P, _I64, _P, _I64, _I32, _P, _P, _P, _P],
+    "pdm_combine_flags_auto": [_P, _I64, _P, _I64, _P, _I64, _P, _I64, _I32, _P, _P, _P, _P],
+    "pdm_combine_raw_max_k": [],
     "pdm_combine_packed_to_packed": [_P, _I64, _P, _I64, _I64, _I32, _P, _I32, _P, _P, _P],
     "pdm_combine_flags_packed_to_packed": [_P, _I64, _P, _I64, _I64, _I32, _P, _P, _P, _P],
     "pdm_unpack_packed_host": [_P, _P, _I64, _P],

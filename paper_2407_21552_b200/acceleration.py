@@ -623,11 +623,24 @@ def _combine_with_host_view(pdm_set: PdmSet, sel: np.ndarray, out) -> DistanceMa
     return dm
 
 
+_RAW_MAX_K = None
+
+
+def _raw_max_k() -> int:
+    """Largest selection merged from the raw planes (pdm_combine_raw_max_k)."""
+    global _RAW_MAX_K
+    if _RAW_MAX_K is None:
+        _RAW_MAX_K = int(_lib.lib().pdm_combine_raw_max_k())
+    return _RAW_MAX_K
+
+
 def _combine_indices(pdm_set: PdmSet, sel: np.ndarray, out) -> None:
     """K7 over a host index list (0-based), into ``out`` (enqueued only)."""
     L = _lib.lib()
     grid = pdm_set.grid
-    ptrs = pdm_set._packed_args() if 0 < sel.size <= _MAX_PACKED_SEL else None
+    # small selections: the raw planes (the packed merge is latency-bound there,
+    # pdm_combine_flags_auto)
+    ptrs = (pdm_set._packed_args() if _raw_max_k() < sel.size <= _MAX_PACKED_SEL else None)
     if ptrs is not None:
         _lib.check(L.pdm_combine_packed(*ptrs, grid.num_blocks, pdm_set.n, sel.ctypes.data,
                                         int(sel.size), out.data_ptr(), None,
@@ -699,12 +712,14 @@ def combine_flags_into(pdm_set: PdmSet, flags, out=None, count_zeros: bool = Fal
     if packed is not None:
         nib, nib_pitch, base, base_pitch = packed
         zeros = device.empty((1,), np.int64) if count_zeros else None
-        _lib.check(L.pdm_combine_flags_packed(_lib.ptr(nib), nib_pitch, _lib.ptr(base), base_pitch,
-                                              pdm_set.tile_bounds_ptr(), grid.num_blocks,
-                                              pdm_set.n, _lib.ptr(flags), _lib.ptr(out),
-                                              _lib.ptr(zeros) if zeros is not None else None,
-                                              _lib.stream_handle()),
-                   "pdm_combine_flags_packed")
+        # raw planes beside the packed ones: small selections merge those
+        _lib.check(L.pdm_combine_flags_auto(_lib.ptr(pdm_set.storage), pdm_set.plane_pitch,
+                                            _lib.ptr(nib), nib_pitch, _lib.ptr(base), base_pitch,
+                                            pdm_set.tile_bounds_ptr(), grid.num_blocks,
+                                            pdm_set.n, _lib.ptr(flags), _lib.ptr(out),
+                                            _lib.ptr(zeros) if zeros is not None else None,
+                                            _lib.stream_handle()),
+                   "pdm_combine_flags_auto")
         dm = DistanceMap(b=grid.b, bdims=grid.bdims, dist=out)
         dm._zero_count = zeros
         return dm

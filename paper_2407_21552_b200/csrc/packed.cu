@@ -29,6 +29,7 @@
 #include <mutex>
 
 #include "host_pool.h"
+#include "merge_raw.cuh"
 #include "pdm_common.cuh"
 
 namespace pdm {
@@ -663,6 +664,18 @@ __global__ void __launch_bounds__(kPackedThreads, kPackedCtas)
                                              out_base, zeros, s_stage, skip);
 }
 
+// The raw planes of the set, for the flags merge's small-selection path:
+// with k <= max_k selected the packed merge's laps are latency-bound (one
+// tile of one to a few planes per warp per lap: k = 1 took 17.5 us against a
+// 4 us copy floor), while the raw small-k loop keeps 8 independent 16-byte
+// loads in flight per thread and runs at the copy rate on (k + 1) bytes per
+// block.  pdms == nullptr: always packed.
+struct RawPlanes {
+    const uint8_t *pdms;
+    int64_t pitch;
+    int max_k;
+};
+
 // Selection resident on the device (written by the select kernel ahead of it
 // in the stream, PDL): every CTA compacts the flags, then merges.
 template <int kOut, bool kCount, bool kTable>
@@ -671,7 +684,7 @@ __global__ void __launch_bounds__(kPackedThreads, kTable ? kPackedCtas : kPacked
                                 const uint8_t *__restrict__ base, int64_t base_pitch,
                                 int64_t map_bytes, int n, const uint8_t *__restrict__ flags,
                                 uint8_t *__restrict__ out, uint8_t *__restrict__ out_base,
-                                unsigned long long *zeros, TileSkip skip) {
+                                unsigned long long *zeros, TileSkip skip, RawPlanes raw) {
     constexpr int kIdx = kTable ? kPackedTable : kPackedMaxFlags;
     __shared__ int32_t s_idx[kIdx];
     __shared__ const uint8_t *s_nib[kTable ? kPackedTable : 1];
@@ -681,6 +694,16 @@ __global__ void __launch_bounds__(kPackedThreads, kTable ? kPackedCtas : kPacked
     pdl_wait();
     compact_flags(flags, n, s_idx, &s_k);
     __syncthreads();
+    if (kOut == 0 && !kCount && raw.pdms != nullptr && s_k >= 1 && s_k <= raw.max_k) {
+        // a small selection: the raw planes, 8 loads in flight per thread
+        const int64_t nvec = map_bytes / 16;
+        if (s_k <= 2)
+            merge_small_k<4, 2, false>(raw.pdms, raw.pitch, nvec, s_idx, s_k, out);
+        else
+            merge_small_k<2, 4, false>(raw.pdms, raw.pitch, nvec, s_idx, s_k, out);
+        merge_tail(raw.pdms, raw.pitch, nvec * 16, map_bytes, s_idx, s_k, false, out);
+        return;
+    }
     skip.pid = s_idx;
     if constexpr (kTable) {
         fill_table(nib, nib_pitch, base, base_pitch, s_idx, s_k, s_nib, s_base);
@@ -823,7 +846,8 @@ static int launch_packed_flags(const uint8_t *nib, int64_t nib_pitch, const uint
                                int64_t base_pitch, int64_t map_bytes, int n,
                                const uint8_t *flags, uint8_t *out, uint8_t *out_base,
                                cudaStream_t s, unsigned long long *zeros = nullptr,
-                               int out_mode = -1, const uint16_t *tb = nullptr) {
+                               int out_mode = -1, const uint16_t *tb = nullptr,
+                               RawPlanes raw = RawPlanes{nullptr, 0, 0}) {
     if (out_mode < 0) out_mode = out_base ? 1 : 0;
     const bool table = n <= kPackedTable;
     auto kern = out_mode == 3 ? (table ? combine_packed_flags_kernel<3, false, true>
@@ -847,7 +871,7 @@ static int launch_packed_flags(const uint8_t *nib, int64_t nib_pitch, const uint
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     PDM_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, nib, nib_pitch, base, base_pitch, map_bytes, n,
-                                    flags, out, out_base, zeros, make_skip(tb, n)));
+                                    flags, out, out_base, zeros, make_skip(tb, n), raw));
     return cuda_status("combine_packed_flags_kernel");
 }
 
@@ -924,6 +948,40 @@ extern "C" int pdm_combine_flags_packed(const uint8_t *nib, int64_t nib_pitch,
                                      as_stream(stream)));
     return launch_packed_flags(nib, nib_pitch, base, base_pitch, map_bytes, n, flags, out,
                                nullptr, as_stream(stream), zero_count, -1, tile_bounds);
+}
+
+// Raw planes beside the packed ones: selections of up to PDM_RAW_MAX_K
+// planes (default 4; 0 = never) merge the raw planes (see RawPlanes).
+static int raw_max_k() {
+    static const int v = [] {
+        const char *e = getenv("PDM_RAW_MAX_K");
+        return e ? atoi(e) : 4;
+    }();
+    return v;
+}
+
+extern "C" int pdm_combine_raw_max_k(void) { return raw_max_k(); }
+
+extern "C" int pdm_combine_flags_auto(const uint8_t *pdms, int64_t plane_pitch,
+                                      const uint8_t *nib, int64_t nib_pitch, const uint8_t *base,
+                                      int64_t base_pitch, const uint16_t *tile_bounds,
+                                      int64_t map_bytes, int32_t n, const uint8_t *flags,
+                                      uint8_t *out, unsigned long long *zero_count,
+                                      pdm_stream_t stream) {
+    const char *fn = "pdm_combine_flags_auto";
+    int st = check_packed(fn, nib, nib_pitch, base, base_pitch, map_bytes, n, out, nullptr, false);
+    if (st) return st;
+    PDM_REQUIRE(pdms && flags && n <= kPackedMaxFlags, "%s: null planes/flags or n=%d above %d",
+                fn, n, kPackedMaxFlags);
+    PDM_REQUIRE(plane_pitch >= map_bytes, "%s: plane_pitch below map_bytes", fn);
+    if (zero_count)  // (sits between the select kernel and the merge: no PDL overlap then)
+        PDM_CUDA_TRY(cudaMemsetAsync(zero_count, 0, sizeof(unsigned long long),
+                                     as_stream(stream)));
+    // the raw loop reads 16-byte vectors: aligned planes only
+    const bool aligned = plane_pitch % 16 == 0 && (uintptr_t)pdms % 16 == 0;
+    const RawPlanes raw{aligned ? pdms : nullptr, plane_pitch, raw_max_k()};
+    return launch_packed_flags(nib, nib_pitch, base, base_pitch, map_bytes, n, flags, out,
+                               nullptr, as_stream(stream), zero_count, -1, tile_bounds, raw);
 }
 
 extern "C" int pdm_combine_packed_to_packed(const uint8_t *nib, int64_t nib_pitch,
