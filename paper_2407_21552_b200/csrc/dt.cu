@@ -1044,6 +1044,134 @@ __global__ void __launch_bounds__(256)
     }
 }
 
+// ---- expand + x pass in one kernel, from the partition mask --------------------
+// dt_expand_mask_kernel writes every {0, 255} plane (n B bytes) and the x pass
+// reads them back: ~1 GB of DRAM traffic at config c for what is a function
+// of the 4 B mask word per block.  Here a CTA stages the mask words of one
+// (y, 32-z) column of x lines, [x][32 z] (32 KB, every partition's bits),
+// ORs/ANDs them to find the partitions whose lines are all empty / all
+// occupied (written as constant rows by the whole CTA, no sweep), and its 8
+// warps claim the other partitions one at a time (a shared counter: a static
+// split left warps waiting at the column barrier) and run their lines' 1-D
+// distance from the mask bits: lane l line z0 + l, forward run into a [x][32]
+// byte tile, backward run min'ed into it, then 16-byte row stores.  Config c:
+// 0.29 / 0.37 ms (voxel / range_apron masks) vs 0.30 / 0.45 ms for expand +
+// pass x, 0.58 instead of ~1.6 GB of DRAM traffic.  Masks of one word per
+// block (n <= 32), lines <= 256, bz % 32 == 0; PDM_DT_XMASK=0: expand + x.
+constexpr int kXMaskWarps = 8;
+
+__global__ void __launch_bounds__(32 * kXMaskWarps, 2)
+    dt_x_mask_kernel(const uint32_t *__restrict__ mask, int n, int64_t bx, int64_t by,
+                     int64_t bz, uint8_t *__restrict__ pdms, int64_t pitch, int64_t tiles) {
+    extern __shared__ __align__(16) uint8_t s_xm[];
+    const int L = (int)bx;
+    uint32_t *sm = reinterpret_cast<uint32_t *>(s_xm);                 // [L][32] mask words
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint8_t *so = s_xm + (size_t)L * 128 + (size_t)warp * L * 32;     // [L][32] this warp's lines
+    __shared__ uint32_t s_red[2][kXMaskWarps];
+    __shared__ int s_next;  // next mixed partition of the column to claim
+    const int64_t zq = bz / 32, S = by * bz;
+    for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+        const int64_t y = t / zq, z0 = (t % zq) * 32;
+        const uint32_t *src = mask + y * bz + z0;
+        for (int i = threadIdx.x; i < L * 8; i += blockDim.x) {
+            const int x = i >> 3, c = i & 7;
+            cpa::copy16(sm + x * 32 + 4 * c, src + (int64_t)x * S + 4 * c);
+        }
+        cpa::commit();
+        if (threadIdx.x == 0) s_next = 0;
+        cpa::wait<0>();
+        __syncthreads();
+        uint32_t any = 0, all = 0xFFFFFFFFu;
+        for (int i = threadIdx.x; i < L * 32; i += blockDim.x) {
+            any |= sm[i];
+            all &= sm[i];
+        }
+        any = __reduce_or_sync(0xFFFFFFFFu, any);
+        all = __reduce_and_sync(0xFFFFFFFFu, all);
+        if (lane == 0) s_red[0][warp] = any, s_red[1][warp] = all;
+        __syncthreads();
+        any = 0, all = 0xFFFFFFFFu;
+#pragma unroll
+        for (int w = 0; w < kXMaskWarps; ++w) any |= s_red[0][w], all &= s_red[1][w];
+        const uint32_t nmask = n >= 32 ? 0xFFFFFFFFu : ((1u << n) - 1u);
+        const uint32_t mixed = any & ~all & nmask;  // partitions whose lines need the sweep
+        // constant partitions (every line 255 / 0): row stores split over the warps
+        const uint32_t flat = nmask & ~mixed;
+        for (int i = threadIdx.x; i < __popc(flat) * L * 2; i += blockDim.x) {
+            const int q = i / (L * 2), rr = i - q * L * 2;
+            uint32_t fm = flat;
+            for (int j = 0; j < q; ++j) fm &= fm - 1;
+            const int p = __ffs(fm) - 1;
+            const uint32_t v = ((any >> p) & 1u) ? 0u : 0xFFFFFFFFu;
+            *reinterpret_cast<uint4 *>(pdms + (int64_t)p * pitch + y * bz + z0 +
+                                       (int64_t)(rr >> 1) * S + 16 * (rr & 1)) =
+                make_uint4(v, v, v, v);
+        }
+        // mixed partitions: claimed by the warps one at a time
+        for (;;) {
+            int j = 0;
+            if (lane == 0) j = atomicAdd(&s_next, 1);
+            j = __shfl_sync(0xFFFFFFFFu, j, 0);
+            if (j >= __popc(mixed)) break;
+            uint32_t mm = mixed;
+            for (int i = 0; i < j; ++i) mm &= mm - 1;
+            const int p = __ffs(mm) - 1;
+            uint8_t *dst = pdms + (int64_t)p * pitch + y * bz + z0;
+            const uint32_t *col = sm + lane;
+            uint8_t *oc = so + lane;
+            const uint32_t bit = 1u << p;
+            // batches of 8 rows: the shared loads of a batch are issued before
+            // its stores (the compiler cannot tell the two tiles apart)
+            constexpr int kB = 8;
+            const int L8 = L & ~(kB - 1);
+            uint32_t r = kDistClamp;  // "no occupied block yet"
+            for (int x0 = 0; x0 < L8; x0 += kB) {
+                uint32_t w[kB];
+#pragma unroll
+                for (int j = 0; j < kB; ++j) w[j] = col[32 * (x0 + j)];
+#pragma unroll
+                for (int j = 0; j < kB; ++j) {
+                    r = (w[j] & bit) ? 0u : min(r + 1u, (uint32_t)kDistClamp);
+                    w[j] = r;
+                }
+#pragma unroll
+                for (int j = 0; j < kB; ++j) oc[32 * (x0 + j)] = (uint8_t)w[j];
+            }
+            for (int x = L8; x < L; ++x) {
+                r = (col[32 * x] & bit) ? 0u : min(r + 1u, (uint32_t)kDistClamp);
+                oc[32 * x] = (uint8_t)r;
+            }
+            r = kDistClamp;
+            for (int x = L - 1; x >= L8; --x) {
+                r = (col[32 * x] & bit) ? 0u : min(r + 1u, (uint32_t)kDistClamp);
+                oc[32 * x] = (uint8_t)min(r, (uint32_t)oc[32 * x]);
+            }
+            for (int x0 = L8 - kB; x0 >= 0; x0 -= kB) {
+                uint32_t w[kB], f[kB];
+#pragma unroll
+                for (int j = 0; j < kB; ++j) {
+                    w[j] = col[32 * (x0 + j)];
+                    f[j] = oc[32 * (x0 + j)];
+                }
+#pragma unroll
+                for (int j = kB - 1; j >= 0; --j) {
+                    r = (w[j] & bit) ? 0u : min(r + 1u, (uint32_t)kDistClamp);
+                    f[j] = min(r, f[j]);
+                }
+#pragma unroll
+                for (int j = 0; j < kB; ++j) oc[32 * (x0 + j)] = (uint8_t)f[j];
+            }
+            __syncwarp();
+            for (int i = lane; i < L * 2; i += 32)
+                *reinterpret_cast<uint4 *>(dst + (int64_t)(i >> 1) * S + 16 * (i & 1)) =
+                    *reinterpret_cast<const uint4 *>(so + (i >> 1) * 32 + 16 * (i & 1));
+            __syncwarp();
+        }
+        __syncthreads();  // the mask tile is restaged for the next column
+    }
+}
+
 // ---- slab pieces --------------------------------------------------------------------
 __global__ void slab_edges_kernel(const uint8_t *__restrict__ pdms, int64_t pitch, int n,
                                   int64_t bx, int64_t plane, uint8_t *__restrict__ edges) {
@@ -1253,9 +1381,27 @@ static int axis_pass(int n, int64_t bx, int64_t by, int64_t bz, uint8_t *pdms, i
     return cuda_status("dt_line_kernel");
 }
 
+static bool x_mask_ok(int words, int64_t bx, int64_t bz, const uint32_t *mask) {
+    static const bool off = getenv("PDM_DT_XMASK") && getenv("PDM_DT_XMASK")[0] == '0';
+    return !off && words == 1 && bx >= 2 && bx <= 256 && bz % 32 == 0 &&
+           (uintptr_t)mask % 16 == 0;
+}
+
 static int pass_x_mask(const uint32_t *mask, int words, int n, int64_t bx, int64_t by,
                        int64_t bz, uint8_t *pdms, int64_t pitch, cudaStream_t s) {
     const int64_t nb = bx * by * bz;
+    if (x_mask_ok(words, bx, bz, mask) && pitch % 16 == 0 && (uintptr_t)pdms % 16 == 0) {
+        auto kern = dt_x_mask_kernel;
+        const size_t smem = (size_t)bx * 128 + (size_t)kXMaskWarps * bx * 32;
+        PDM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)smem));
+        const int64_t tiles = by * (bz / 32);
+        int64_t grid = (int64_t)sm_count() * 2;
+        if (grid > tiles) grid = tiles;
+        kern<<<(unsigned)grid, 32 * kXMaskWarps, smem, s>>>(mask, n, bx, by, bz, pdms, pitch,
+                                                            tiles);
+        return cuda_status("dt_x_mask_kernel");
+    }
     dt_expand_mask_kernel<<<grid_for(ceil_div(nb, 16), 256, 8), 256, 0, s>>>(
         MaskSrc{mask, words}, n, nb, pdms, pitch);
     int st = cuda_status("dt_expand_mask_kernel");

@@ -50,13 +50,16 @@ def main():
         return round(min(ts), 4)
 
     res = {"dims": args.dims, "bits": args.bits, "b": args.b, "n": args.n, "blocks": nb}
+    pitch = device.plane_pitch(nb)
+    storage = device.empty((args.n, pitch), np.uint8)
     for mode in ("voxel", "range_apron"):
         mask = pdm.partition_mask(vol, grid, scheme, mode)
         ms = timed(lambda: pdm.partition_mask(vol, grid, scheme, mode))
         res[f"mask_{mode}_ms"] = ms
         res[f"mask_{mode}_GBps"] = round((vbytes + nb * 4) / ms / 1e6, 1)
-    pitch = device.plane_pitch(nb)
-    storage = device.empty((args.n, pitch), np.uint8)
+        res[f"dt_pass_x_{mode}_ms"] = timed(lambda: _lib.check(L.pdm_dt_pass_x_mask(
+            _lib.ptr(mask), mask.shape[1], args.n, *grid.bdims, _lib.ptr(storage), pitch, st),
+            "pass_x"))
     words = mask.shape[1]
 
     def pass_x():
