@@ -34,7 +34,7 @@ python tools/exp/merge_once.py 8 16 32 > "$o/merge3_plain.log" 2>&1 && \
 # full capture of the precompute kernels (apron POM, expand, DT passes)
 python tools/exp/precompute_once.py 1 > "$o/pre_plain.log" 2>&1 && \
   ncu --set full --clock-control none --import-source on \
-      -k "regex:apron_fast|dt_tile|dt_dist1d|dt_expand|tile_bounds" -c 6 \
+      -k "regex:apron_fast|dt_tmem|dt_x_mask|dt_tile|tile_bounds" -c 6 \
       -o "$o/precompute_full" python tools/exp/precompute_once.py 1 \
       > "$o/ncu_pre.log" 2>&1; echo "ncu pre rc=$?" >> "$o/status.txt"
 # launch list of a short bench run (cold-cache, serialised)

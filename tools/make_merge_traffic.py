@@ -22,7 +22,7 @@ def main(src, dst):
                                                          r["Metric Unit"])
     scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ns": 1e-3, "us": 1, "ms": 1e3}
     launches = [per[i] for i in sorted(per, key=int)]
-    out = {"kernel": "combine_packed_flags_kernel<0, 0, 1> (tile skip on)", "per_k": {},
+    out = {"kernel": "combine_packed_flags_kernel<0, 0, 1> (tile skip on; k <= 4: its raw-plane path)", "per_k": {},
            "duration_us_per_k": {},
            "source": ("ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,"
                       "gpu__time_duration.sum --clock-control none on tools/exp/merge_once.py "
