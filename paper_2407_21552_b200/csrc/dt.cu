@@ -801,7 +801,7 @@ __global__ void __launch_bounds__(32 * kTmemWarps, 6)
             continue;
         }
         // the lane's line -> TMEM (words of 4 consecutive elements)
-#pragma unroll
+#pragma unroll 1
         for (int cc = 0; cc < NC; ++cc) {
             uint32_t w[16];
             if (kRows) {

@@ -521,7 +521,11 @@ __device__ __forceinline__ void fold_ids(PackedAcc &acc, const uint4 (&q)[B],
 // current one is folded (two register buffers: B=2/3/4/6 at 4/3/3/2 CTAs per
 // SM, 52.4/41.0/43.9/40.4 vs 35.7 us -- although ncu puts 42 % of this
 // loop's stall samples on the first use of a batch's loads), tiles claimed
-// one ahead from a self-resetting counter (40.4 vs 36.4 us), the add and
+// one ahead from a self-resetting counter (40.4 vs 36.4 us; chunks of 1/2/4
+// consecutive tiles, the first chunk static so only ~5k atomics remain: 40.3 /
+// 41.2 / 49.6 vs 36.1 us -- the larger the chunk the slower, i.e. what the
+// static split buys is the compact window of tiles all warps read at once),
+// the add and
 // the min fused as VIADDMNMX.U16x2 (36.2 vs 36.2 us), and -- timing probes
 // with wrong results -- nibbles or bases read from an L2-resident 64 KB /
 // 4 KB instead of HBM (34.8 / 35.0 vs 35.5 us: DRAM is not what bounds it),
