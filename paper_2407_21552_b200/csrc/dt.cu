@@ -1058,6 +1058,10 @@ __global__ void __launch_bounds__(256)
 // 0.29 / 0.37 ms (voxel / range_apron masks) vs 0.30 / 0.45 ms for expand +
 // pass x, 0.58 instead of ~1.6 GB of DRAM traffic.  Masks of one word per
 // block (n <= 32), lines <= 256, bz % 32 == 0; PDM_DT_XMASK=0: expand + x.
+// Measured and rejected: the forward runs parked in TMEM instead of the byte
+// tile, backward results stored straight to HBM (one 32-byte sector per warp
+// store), 24-32 warps per SM: 0.34 / 0.47 ms -- the byte-wide global stores
+// cost more than the occupancy bought.
 constexpr int kXMaskWarps = 8;
 
 __global__ void __launch_bounds__(32 * kXMaskWarps, 2)
