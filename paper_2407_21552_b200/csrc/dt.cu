@@ -881,22 +881,43 @@ __global__ void __launch_bounds__(32 * kTmemWarps, 6)
             __syncwarp();
             continue;
         }
-        // rows: write back (unless flat) and pack (staging in the buffer)
+        // rows: write back (unless flat) through the buffer, swizzled like the
+        // load, so the tile's 32 contiguous rows leave as 512-byte warp stores
+        // (lane-per-row 16-byte stores kept L1 80 % busy), then pack (staging
+        // in the buffer too)
+        if (!flat) {
+#pragma unroll 1
+            for (int cc = 0; cc < NC; ++cc) {
+                uint32_t w[16];
+                tmem::ld16(taddr + 16 * cc, w);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const int c = 4 * cc + q;
+                    *reinterpret_cast<uint4 *>(s + lane * L + ((c ^ (lane & 7)) << 4)) =
+                        make_uint4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
+                }
+            }
+            __syncwarp();
+            for (int i = lane; i < 32 * (L / 16); i += 32) {
+                const int r = i >> 4, c = i & 15;
+                *reinterpret_cast<uint4 *>(g + (int64_t)r * bz + 16 * c) =
+                    *reinterpret_cast<const uint4 *>(s + r * L + ((c ^ (r & 7)) << 4));
+            }
+            __syncwarp();
+        }
         const int nst = L / 2 + 8, bst = L / 16 + 4;
         uint8_t *sn = s, *sb = s + 32 * nst;
         unsigned int nbad = 0;
         uint32_t rlo = 255, rhi = 0;
-        uint8_t *grow = g + (int64_t)lane * bz;
 #pragma unroll 1
-        for (int cc = 0; cc < NC; ++cc) {
+        for (int cc = 0; cc < NC && pk.nib != nullptr; ++cc) {
             uint32_t w[16];
             tmem::ld16(taddr + 16 * cc, w);
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
                 const uint4 v = make_uint4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
                 const int c = 4 * cc + q;
-                if (!flat) *reinterpret_cast<uint4 *>(grow + 16 * c) = v;
-                if (pk.nib != nullptr) {
+                {
                     uint32_t mn, mx;
                     const uint2 pw = pack_chunk(v, mn, mx, nbad);
                     *reinterpret_cast<uint2 *>(sn + lane * nst + 8 * c) = pw;

@@ -907,3 +907,41 @@ def test_standard_distance_map_full_and_empty_support(bits, mode):
             lut[int(vox.flat[0]), 3] = 0.0
         got = pdm.standard_distance_map(vol, grid, pdm.TransferFunction(lut=lut), mode).dist
         assert np.array_equal(got, oracle.standard_distance_map(vox, b, lut, mode)), fill
+
+
+@pytest.mark.parametrize("dims", [(17, 12, 64), (5, 7, 48), (3, 5, 16)])
+def test_flags_merge_small_selections_take_the_raw_planes(monkeypatch, dims):
+    """pdm_combine_flags_auto: selections of up to pdm_combine_raw_max_k() planes
+    merge the raw planes on the device (after the flag compaction), larger ones
+    the packed planes; both equal the oracle for k = 0..8, including map sizes
+    that leave a byte tail past the last 16-byte chunk."""
+    monkeypatch.setenv("PDM_PACKED", "1")
+    import torch
+
+    from paper_2407_21552_b200 import _lib
+
+    L = _lib.lib()
+    assert L.pdm_combine_raw_max_k() >= 1
+    rng = np.random.default_rng(sum(dims))
+    vox = random_structured_volume(rng, dims, 8)
+    scheme = pdm.scheme_uniform(10, 8)
+    pset = pdm.build_pdm_set(pdm.Volume.from_array(vox), pdm.BlockGrid.for_dims(dims, 1), scheme)
+    assert pset.packed() is not None
+    maps = np.stack([d.dist for d in pset.pdms])
+    nb = pset.grid.num_blocks
+    nib, nib_pitch, base, base_pitch = pset.packed()
+    for k in range(0, 9):
+        s = sorted(rng.choice(np.arange(1, 11), size=k, replace=False).tolist())
+        flags = torch.zeros(10, dtype=torch.uint8, device="cuda")
+        if s:
+            flags[[i - 1 for i in s]] = 1
+        out = torch.full((nb + 64,), 7, dtype=torch.uint8, device="cuda")
+        _lib.check(L.pdm_combine_flags_auto(
+            _lib.ptr(pset.storage), pset.plane_pitch, _lib.ptr(nib), nib_pitch, _lib.ptr(base),
+            base_pitch, pset.tile_bounds_ptr(), nb, 10, _lib.ptr(flags), _lib.ptr(out), None,
+            _lib.stream_handle()), "pdm_combine_flags_auto")
+        got = out.cpu().numpy()
+        assert np.array_equal(got[:nb].reshape(pset.grid.bdims), oracle.combine(maps, s)), (k, s)
+        assert (got[nb:] == 7).all(), k  # nothing written past the map
+        dm = pdm.acceleration.combine_flags_into(pset, flags)
+        assert np.array_equal(dm.dist, oracle.combine(maps, s)), (k, s)
