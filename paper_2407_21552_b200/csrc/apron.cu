@@ -16,10 +16,62 @@
 #include <cuda_runtime.h>
 
 #include <cstdlib>
+#include <cstring>
+
+#include <cuda.h>
+#include <cudaTypedefs.h>
 
 #include "pdm_common.cuh"
 
 namespace pdm {
+
+// ---- TMA plane loads (16-bit volumes, b = 4) ----------------------------------------
+// One warp's plane of a run is a box of the volume seen as a 3-D tensor
+// (z innermost): 6 rows x 256 voxels (its strip) plus two 6 x 8 boxes holding
+// the strip-edge voxels -- three cp.async.bulk.tensor issued by lane 0 onto an
+// mbarrier per ring slot, instead of 6 x 32 16-byte cp.async + 12 edge words
+// per plane (the cp.async version was MIO-throttle and long-scoreboard bound).
+// Coordinates are chosen so every voxel the kernel uses lies inside the
+// volume (TMA would fill out-of-range voxels with zeros; the kernel needs the
+// clamped, replicated voxels): rows start at clamp(jB - 1, 0, ny - 6) and the
+// kernel maps its clamped rows into the box.
+struct ApronMaps {
+    CUtensorMap main;  // box {256, 6, 1}
+    CUtensorMap edge;  // box {8, 6, 1}
+};
+constexpr int kTmaMain = 6 * 256 * 2, kTmaEdge = 6 * 8 * 2;
+constexpr int kTmaSlot = kTmaMain + 2 * 128;  // edge boxes at 128-byte offsets
+constexpr uint32_t kTmaBytes = kTmaMain + 2 * kTmaEdge;
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    uint32_t ok = 0;
+    do {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(ok)
+            : "r"(smem_addr(bar)), "r"(parity)
+            : "memory");
+    } while (!ok);
+}
+__device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, int z, int y,
+                                            int x, uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
+        "[%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_addr(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(z), "r"(y), "r"(x), "r"(smem_addr(bar))
+        : "memory");
+}
 
 enum ApronOuts { kOutMinMax = 1, kOutMask = 2 };
 
@@ -92,14 +144,16 @@ __device__ __forceinline__ void chunk_words(uint4 q, uint32_t (&w)[16 / (BITS / 
 // neighbours; the plane then folds into the current block row (and into the
 // previous one at r = 0, the next one at r = B - 1), all decided at compile
 // time by unrolling the B planes of a block.
-template <int BITS, int B, int OUTS, int RB>
+template <int BITS, int B, int OUTS, int RB, bool kTma = false>
 __global__ void __launch_bounds__(32 * kApronWarps,
                                   (BITS == 16 && B == 4) ? (RB == 1 ? kApronMinCtas : 5) : 1)
     apron_fast_kernel(const typename VoxT<BITS>::type *__restrict__ vox, int64_t nx, int64_t ny,
                       int64_t nz, int64_t bx, int64_t by, int64_t bz, int XB,
                       typename VoxT<BITS>::type *__restrict__ mins,
                       typename VoxT<BITS>::type *__restrict__ maxs,
-                      const int32_t *__restrict__ pid, uint32_t *__restrict__ mask, int words) {
+                      const int32_t *__restrict__ pid, uint32_t *__restrict__ mask, int words,
+                      const __grid_constant__ ApronMaps maps) {
+    static_assert(!kTma || (BITS == 16 && B == 4 && RB == 1), "TMA planes: 16-bit, b = 4");
     using T = typename VoxT<BITS>::type;
     constexpr int VPC = 16 / (BITS / 8);  // voxels per lane chunk
     constexpr int NW = VPC / 2;           // u16x2 words per chunk
@@ -108,7 +162,7 @@ __global__ void __launch_bounds__(32 * kApronWarps,
     constexpr int WV = 4 / (BITS / 8);  // voxels per 4-byte edge word
     const unsigned FULL = 0xFFFFFFFFu;
     const int lane = threadIdx.x & 31;
-    extern __shared__ __align__(16) uint8_t s_apron[];
+    extern __shared__ __align__(128) uint8_t s_apron[];
     uint4 *ring_main = reinterpret_cast<uint4 *>(s_apron) +
                        (size_t)(threadIdx.x >> 5) * kApronRing * kRows * 32;
     uint32_t *ring_edge = reinterpret_cast<uint32_t *>(
@@ -122,6 +176,17 @@ __global__ void __launch_bounds__(32 * kApronWarps,
     const int64_t items = groups * nstrips * xchunks;
     const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     const int64_t plane_elems = ny * nz;
+    // TMA ring: slot i of this warp at tma_ring + i * kTmaSlot, one mbarrier each
+    __shared__ uint64_t s_bar[kTma ? kApronWarps * kApronRing : 1];
+    uint8_t *tma_ring = s_apron + (size_t)(threadIdx.x >> 5) * kApronRing * kTmaSlot;
+    uint64_t *bars = s_bar + (kTma ? (threadIdx.x >> 5) * kApronRing : 0);
+    uint32_t phase = 0;  // bit i: parity of ring slot i's next completion
+    if (kTma) {
+        if (lane == 0)
+            for (int i = 0; i < kApronRing; ++i) mbar_init(&bars[i], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        __syncwarp();
+    }
     for (int64_t it = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; it < items;
          it += warps) {
         const int64_t s = it % nstrips;
@@ -155,6 +220,16 @@ __global__ void __launch_bounds__(32 * kApronWarps,
             const int64_t y = min(max(jg * RB * B - 1 + r, (int64_t)0), ny - 1);
             roffb[r] = (uint32_t)(y * nz * (int64_t)sizeof(T));
         }
+        // TMA: the box's first row, the clamped row r's index inside it
+        // (3 bits each), the edge boxes' z and the voxel each edge lane uses
+        const int64_t y0 = min(max(jg * B - 1, (int64_t)0), ny - 6);
+        uint32_t ridx = 0;
+#pragma unroll
+        for (int r = 0; r < kRows; ++r)
+            ridx |= (uint32_t)(min(max(jg * B - 1 + r, (int64_t)0), ny - 1) - y0) << (3 * r);
+        const int zleft = (int)(has_left ? zs - 8 : zs);
+        const int zright = (int)(has_right ? zs + strip : min(zs + strip, nz) - 8);
+        const int tsel = lane == 0 ? (has_left ? 7 : 0) : (has_right ? 0 : 7);
         const int64_t xa = i0 * B - 1;                      // first plane of the run
         const int nplanes = (int)((i1 - i0) * B + 2);  // + leading and trailing apron planes
         // byte addresses: this lane's chunk of row r in plane 0, and the edge
@@ -163,6 +238,22 @@ __global__ void __launch_bounds__(32 * kApronWarps,
         const int64_t edelta = (eoff - zcol) * (int64_t)sizeof(T);
         const int64_t plane_bytes = plane_elems * (int64_t)sizeof(T);
         auto issue = [&](int q) {  // plane q of the run into ring slot q % kApronRing
+            if constexpr (kTma) {
+                if (q < nplanes && lane == 0) {
+                    const int x = (int)min(max(xa + q, (int64_t)0), nx - 1);
+                    const int slot = q % kApronRing;
+                    uint8_t *dst = tma_ring + slot * kTmaSlot;
+                    // the slot's previous contents were read through the generic
+                    // proxy (the caller's __syncwarp orders the lanes' reads)
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    mbar_expect_tx(&bars[slot], kTmaBytes);
+                    tma_load_3d(dst, &maps.main, (int)zs, (int)y0, x, &bars[slot]);
+                    tma_load_3d(dst + kTmaMain, &maps.edge, zleft, (int)y0, x, &bars[slot]);
+                    tma_load_3d(dst + kTmaMain + 128, &maps.edge, zright, (int)y0, x,
+                                &bars[slot]);
+                }
+                return;
+            }
             if (q < nplanes) {
                 const int64_t x = min(max(xa + q, (int64_t)0), nx - 1);
                 const char *plane = lane0 + x * plane_bytes;
@@ -179,17 +270,25 @@ __global__ void __launch_bounds__(32 * kApronWarps,
             cpa::commit();
         };
         // u16x2 min/max over rows [a, b) of ring slot `slot` (3-input forms)
+        // row r of ring slot `slot`: this lane's 16-byte chunk
+        auto row_chunk = [&](int slot, int r) -> uint4 {
+            if constexpr (kTma)
+                return *reinterpret_cast<const uint4 *>(tma_ring + slot * kTmaSlot +
+                                                        ((ridx >> (3 * r)) & 7u) * 512 +
+                                                        lane * 16);
+            return ring_main[(slot * kRows + r) * 32 + lane];
+        };
         auto rows_mm = [&](int slot, int a, int b, uint32_t (&wmn)[NW], uint32_t (&wmx)[NW]) {
             uint32_t w0[NW];
-            chunk_words<BITS>(ring_main[(slot * kRows + a) * 32 + lane], w0);
+            chunk_words<BITS>(row_chunk(slot, a), w0);
 #pragma unroll
             for (int i = 0; i < NW; ++i) wmn[i] = wmx[i] = w0[i];
 #pragma unroll
             for (int r = a + 1; r < b; r += 2) {
                 uint32_t wa[NW], wb[NW];
-                chunk_words<BITS>(ring_main[(slot * kRows + r) * 32 + lane], wa);
+                chunk_words<BITS>(row_chunk(slot, r), wa);
                 if (r + 1 < b) {
-                    chunk_words<BITS>(ring_main[(slot * kRows + r + 1) * 32 + lane], wb);
+                    chunk_words<BITS>(row_chunk(slot, r + 1), wb);
 #pragma unroll
                     for (int i = 0; i < NW; ++i) {
                         wmn[i] = __vimin3_u16x2(wmn[i], wa[i], wb[i]);
@@ -213,9 +312,15 @@ __global__ void __launch_bounds__(32 * kApronWarps,
             if (lane == 0 || lane == 31) {
 #pragma unroll
                 for (int r = k * B; r < k * B + B + 2; ++r) {
-                    const uint32_t w = ring_edge[(slot * kRows + r) * 2 + (lane == 31)];
-                    const uint32_t e = BITS == 8 ? (w >> (8 * esel)) & 0xFFu
-                                                 : (w >> (16 * esel)) & 0xFFFFu;
+                    uint32_t e;
+                    if constexpr (kTma) {
+                        e = reinterpret_cast<const uint16_t *>(
+                            tma_ring + slot * kTmaSlot + kTmaMain + (lane == 31) * 128)
+                            [((ridx >> (3 * r)) & 7u) * 8 + tsel];
+                    } else {
+                        const uint32_t w = ring_edge[(slot * kRows + r) * 2 + (lane == 31)];
+                        e = BITS == 8 ? (w >> (8 * esel)) & 0xFFu : (w >> (16 * esel)) & 0xFFFFu;
+                    }
                     emn = min(emn, e);
                     emx = max(emx, e);
                 }
@@ -290,6 +395,17 @@ __global__ void __launch_bounds__(32 * kApronWarps,
                 if (OUTS & kOutMask) write_range_bits(mask, c0 + t, words, pid[mn[t]], pid[mx[t]]);
             }
         };
+        // plane q's data has landed and is visible to every lane
+        auto wait_plane = [&](int q) {
+            if constexpr (kTma) {
+                const int slot = q % kApronRing;
+                mbar_wait(&bars[slot], (phase >> slot) & 1u);
+                phase ^= 1u << slot;
+            } else {
+                cpa::wait<kApronRing - 1>();
+            }
+            __syncwarp();
+        };
 #pragma unroll
         for (int d = 0; d < kApronRing; ++d) issue(d);
         uint32_t pmn[RB][ZB], pmx[RB][ZB], cmn[RB][ZB], cmx[RB][ZB], nmn[RB][ZB], nmx[RB][ZB];
@@ -301,8 +417,7 @@ __global__ void __launch_bounds__(32 * kApronWarps,
                 pmx[k][t] = nmx[k][t] = 0u;
             }
         // plane 0: the leading apron plane of block i0 starts its accumulator
-        cpa::wait<kApronRing - 1>();
-        __syncwarp();
+        wait_plane(0);
         plane_mm(0, cmn, cmx);
         __syncwarp();
         issue(kApronRing);
@@ -310,8 +425,7 @@ __global__ void __launch_bounds__(32 * kApronWarps,
         for (int64_t i = i0; i < i1; ++i) {
 #pragma unroll
             for (int r = 0; r < B; ++r, ++q) {
-                cpa::wait<kApronRing - 1>();
-                __syncwarp();
+                wait_plane(q);
                 uint32_t mn[RB][ZB], mx[RB][ZB];
                 plane_mm(q, mn, mx);
                 __syncwarp();
@@ -346,8 +460,7 @@ __global__ void __launch_bounds__(32 * kApronWarps,
                 }
         }
         // trailing apron plane of the run's last block
-        cpa::wait<kApronRing - 1>();
-        __syncwarp();
+        wait_plane(q);
         {
             uint32_t mn[RB][ZB], mx[RB][ZB];
             plane_mm(q, mn, mx);
@@ -361,9 +474,38 @@ __global__ void __launch_bounds__(32 * kApronWarps,
         }
 #pragma unroll
         for (int k = 0; k < RB; ++k) emit(i1 - 1, k, pmn[k], pmx[k]);
-        cpa::wait<0>();  // the ring is reused by the next item
+        if (!kTma) cpa::wait<0>();  // the ring is reused by the next item
         __syncwarp();
     }
+}
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
+static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) !=
+                cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            p = nullptr;
+        return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }();
+    return fn;
+}
+
+// The volume as a 3-D uint16 tensor (z innermost) with boxes of {bz_box, 6, 1}.
+static bool encode_volume_map(CUtensorMap *m, const void *vox, int64_t nx, int64_t ny,
+                              int64_t nz, uint32_t zbox) {
+    auto enc = tensor_map_encoder();
+    if (!enc) return false;
+    const cuuint64_t dims[3] = {(cuuint64_t)nz, (cuuint64_t)ny, (cuuint64_t)nx};
+    const cuuint64_t strides[2] = {(cuuint64_t)nz * 2, (cuuint64_t)(ny * nz * 2)};
+    const cuuint32_t box[3] = {zbox, 6, 1};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT16, 3, const_cast<void *>(vox), dims, strides, box,
+               estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+               CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 template <int BITS, int B>
@@ -376,11 +518,30 @@ static int launch_b(const void *vox, int64_t nx, int64_t ny, int64_t nz, int64_t
     static const bool two = getenv("PDM_APRON_RB") && getenv("PDM_APRON_RB")[0] == '2';
     constexpr int RB2 = apron_two_rows<BITS, B>() ? 2 : 1;
     const int RB = two ? RB2 : 1;
+    // TMA plane loads: 16-bit, b = 4, one block row per warp, at least 6 rows,
+    // z extent < 2^31; PDM_APRON_TMA=0 keeps the cp.async ring (A/B)
+    static const bool no_tma = getenv("PDM_APRON_TMA") && getenv("PDM_APRON_TMA")[0] == '0';
+    ApronMaps maps;
+    memset(&maps, 0, sizeof(maps));
+    bool tma = false;
+    if constexpr (BITS == 16 && B == 4) {
+        tma = !no_tma && RB == 1 && ny >= 6 && nz < ((int64_t)1 << 31) &&
+              nx < ((int64_t)1 << 31) && encode_volume_map(&maps.main, vox, nx, ny, nz, 256) &&
+              encode_volume_map(&maps.edge, vox, nx, ny, nz, 8);
+    }
     const int64_t items = ceil_div(by, RB) * ceil_div(nz, 32 * VPC) * ceil_div(bx, XB);
-    const size_t smem = kApronWarps * (RB == 1 ? apron_smem_per_warp<B, 1>()
-                                               : apron_smem_per_warp<B, RB2>());
+    const size_t smem = tma ? (size_t)kApronWarps * kApronRing * kTmaSlot
+                            : kApronWarps * (RB == 1 ? apron_smem_per_warp<B, 1>()
+                                                     : apron_smem_per_warp<B, RB2>());
     const int threads = 32 * kApronWarps;
     auto pick = [&]() {
+        if constexpr (BITS == 16 && B == 4) {
+            if (tma) {
+                if (outs == kOutMinMax) return apron_fast_kernel<BITS, B, kOutMinMax, 1, true>;
+                if (outs == kOutMask) return apron_fast_kernel<BITS, B, kOutMask, 1, true>;
+                return apron_fast_kernel<BITS, B, kOutMinMax | kOutMask, 1, true>;
+            }
+        }
         if (RB == 1) {
             if (outs == kOutMinMax) return apron_fast_kernel<BITS, B, kOutMinMax, 1>;
             if (outs == kOutMask) return apron_fast_kernel<BITS, B, kOutMask, 1>;
@@ -402,7 +563,7 @@ static int launch_b(const void *vox, int64_t nx, int64_t ny, int64_t nz, int64_t
     const int64_t cap = (int64_t)sm_count() * per_sm;
     if (grid > cap) grid = cap;
     kern<<<(unsigned)grid, threads, smem, s>>>((const T *)vox, nx, ny, nz, bx, by, bz, XB,
-                                              (T *)mins, (T *)maxs, pid, mask, words);
+                                              (T *)mins, (T *)maxs, pid, mask, words, maps);
     return cuda_status("apron_fast_kernel");
 }
 
