@@ -390,6 +390,9 @@ def test_pdm_set_round_trip(tmp_path, built16):
     ((64, 64, 128), 16, 4, 32), ((48, 40, 64), 16, 8, 16), ((40, 36, 96), 8, 4, 64),
     ((37, 29, 64), 16, 2, 33), ((31, 17, 48), 8, 16, 8), ((20, 20, 24), 16, 1, 4),
     ((65, 33, 40), 16, 4, 64),
+    # TMA apron planes (16-bit, b = 4): three strips with a partial last one
+    # (nz = 520) and a partial last block row; ny = 5 < 6 keeps the cp.async ring
+    ((13, 23, 520), 16, 4, 16), ((11, 5, 264), 16, 4, 8),
 ])
 @pytest.mark.parametrize("mode", ["voxel", "range_apron"])
 def test_random_volumes_vs_oracle(dims, bits, b, n, mode):
