@@ -735,27 +735,37 @@ __device__ __forceinline__ void wait_st() {
 
 }  // namespace tmem
 
-constexpr int kTmemWarps = 4;      // one warp per TMEM lane quarter
-constexpr int kTmemL = 256;        // line length served
-constexpr int kTmemCols = 64;      // 256 bytes per lane
+constexpr int kTmemWarps = 4;  // one warp per TMEM lane quarter
 
-template <int AXIS>
-__global__ void __launch_bounds__(32 * kTmemWarps, 6)
+// CTAs per SM: L = 256: 6 (33 KB of shared memory, 64 TMEM columns each);
+// L = 512: 3 (65 KB, 128 columns; 16-bit sweep tables).
+template <int L>
+constexpr int tmem_ctas() {
+    return L == 256 ? 6 : 3;
+}
+
+template <int AXIS, int L>
+__global__ void __launch_bounds__(32 * kTmemWarps, tmem_ctas<L>())
     dt_tmem_kernel(int n, int64_t bx, int64_t by, int64_t bz, uint8_t *__restrict__ pdms,
                    int64_t pitch, int64_t tiles, PackDst pk, unsigned long long *next) {
-    constexpr int L = kTmemL, NC = L / 64;  // TMEM chunks of 16 columns
+    static_assert(L == 256 || L == 512, "TMEM sweep: lines of 256 or 512");
+    constexpr int NC = L / 64;            // TMEM chunks of 16 columns
+    constexpr int kCols = L / 4;          // a lane's line: L bytes
+    constexpr int TB = L > 256 ? 2 : 1;   // sweep table entry bytes
+    constexpr int CPR = L / 16, CSH = L == 256 ? 4 : 5;  // 16-byte chunks per row
     constexpr bool kRows = AXIS == kAxisZ;
-    __shared__ __align__(16) uint8_t s_buf[kTmemWarps][32 * L];
+    static_assert(SweepTable<TB>::kBytes == 32 * L, "table and tile share the buffer");
+    extern __shared__ __align__(16) uint8_t s_dyn[];
     __shared__ uint32_t s_taddr;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    if (warp == 0) tmem::alloc(&s_taddr, kTmemCols);
+    if (warp == 0) tmem::alloc(&s_taddr, kCols);
     tmem::fence_before();
     __syncthreads();
     tmem::fence_after();
     const uint32_t tbase = s_taddr;
     const uint32_t taddr = tbase + ((uint32_t)(32 * (warp & 3)) << 16);
-    uint8_t *s = s_buf[warp];
-    const uint32_t tab = smem_addr(s + lane);  // the sweep table's lane column
+    uint8_t *s = s_dyn + (size_t)warp * 32 * L;
+    const uint32_t tab = smem_addr(s + TB * lane);  // the sweep table's lane column
     const int64_t S = bz;                      // y lines: element stride
     const int64_t zblocks = bz / 32;
     // Tiles are handed out by an atomic counter, claimed one tile ahead: a
@@ -782,8 +792,8 @@ __global__ void __launch_bounds__(32 * kTmemWarps, 6)
         }
         // stage the tile (rows: 16-byte chunks swizzled by row; y lines: [u][32])
         if (kRows) {
-            for (int i = lane; i < 32 * (L / 16); i += 32) {
-                const int r = i >> 4, c = i & 15;
+            for (int i = lane; i < 32 * CPR; i += 32) {
+                const int r = i >> CSH, c = i & (CPR - 1);
                 cpa::copy16(s + r * L + ((c ^ (r & 7)) << 4), g + (int64_t)r * bz + 16 * c);
             }
         } else {
@@ -827,31 +837,32 @@ __global__ void __launch_bounds__(32 * kTmemWarps, 6)
         __syncwarp();  // the staged tile is consumed: the buffer becomes the table
         if (!flat) {
             // forward sweep: L[u] = min_{i<=u} max(u - i, g[i])
-            clear_table<1>(s, lane);
+            clear_table<TB>(s, lane);
             __syncwarp();
             {
-                uint32_t M = tab + SweepTable<1>::kRow * kDistClamp;
+                uint32_t M = tab + SweepTable<TB>::kRow * kDistClamp;
 #pragma unroll 1
                 for (int cc = 0; cc < NC; ++cc) {
                     uint32_t w[16];
                     tmem::ld16(taddr + 16 * cc, w);
 #pragma unroll
-                    for (int i = 0; i < 16; ++i) w[i] = sweep_word<1, false>(M, w[i], 64 * cc + 4 * i, tab);
+                    for (int i = 0; i < 16; ++i)
+                        w[i] = sweep_word<TB, false>(M, w[i], 64 * cc + 4 * i, tab);
                     tmem::st16(taddr + 16 * cc, w);
                 }
             }
             __syncwarp();
-            clear_table<1>(s, lane);
+            clear_table<TB>(s, lane);
             __syncwarp();
             {   // backward sweep over L gives the envelope, in place
-                uint32_t M = tab + SweepTable<1>::kRow * kDistClamp;
+                uint32_t M = tab + SweepTable<TB>::kRow * kDistClamp;
 #pragma unroll 1
                 for (int cc = NC - 1; cc >= 0; --cc) {
                     uint32_t w[16];
                     tmem::ld16(taddr + 16 * cc, w);
 #pragma unroll
                     for (int i = 15; i >= 0; --i)
-                        w[i] = sweep_word<1, true>(M, w[i], L - 4 - (64 * cc + 4 * i), tab);
+                        w[i] = sweep_word<TB, true>(M, w[i], L - 4 - (64 * cc + 4 * i), tab);
                     tmem::st16(taddr + 16 * cc, w);
                 }
             }
@@ -898,8 +909,8 @@ __global__ void __launch_bounds__(32 * kTmemWarps, 6)
                 }
             }
             __syncwarp();
-            for (int i = lane; i < 32 * (L / 16); i += 32) {
-                const int r = i >> 4, c = i & 15;
+            for (int i = lane; i < 32 * CPR; i += 32) {
+                const int r = i >> CSH, c = i & (CPR - 1);
                 *reinterpret_cast<uint4 *>(g + (int64_t)r * bz + 16 * c) =
                     *reinterpret_cast<const uint4 *>(s + r * L + ((c ^ (r & 7)) << 4));
             }
@@ -962,7 +973,7 @@ __global__ void __launch_bounds__(32 * kTmemWarps, 6)
     tmem::fence_before();
     __syncthreads();
     tmem::fence_after();
-    if (warp == 0) tmem::dealloc(tbase, kTmemCols);
+    if (warp == 0) tmem::dealloc(tbase, kCols);
 }
 
 // Lines longer than 1024 blocks: one thread per line straight from global
@@ -1345,40 +1356,51 @@ static int tile_counter(cudaStream_t s, unsigned long long **out) {
     return PDM_OK;
 }
 
-// The TMEM sweep serves 256-long lines in full 32-line tiles with 16-byte
-// aligned rows; PDM_DT_TMEM=0 keeps dt_tile_kernel (A/B).
+// The TMEM sweep serves lines of 256 or 512 blocks in full 32-line tiles
+// with 16-byte aligned rows; PDM_DT_TMEM=0 keeps dt_tile_kernel (A/B).
 template <int AXIS>
 static bool tmem_pass_ok(int64_t bx, int64_t by, int64_t bz) {
     static const bool off = getenv("PDM_DT_TMEM") && getenv("PDM_DT_TMEM")[0] == '0';
     if (off || AXIS == kAxisX) return false;
-    if (AXIS == kAxisY) return by == kTmemL && bz % 32 == 0;
-    return bz == kTmemL && (bx * by) % 32 == 0;
+    if (AXIS == kAxisY) return (by == 256 || by == 512) && bz % 32 == 0;
+    return (bz == 256 || bz == 512) && (bx * by) % 32 == 0;
 }
 
-template <int AXIS>
-static int tmem_pass(int n, int64_t bx, int64_t by, int64_t bz, uint8_t *pdms, int64_t pitch,
-                     cudaStream_t s, PackDst pk) {
-    auto kern = dt_tmem_kernel<AXIS>;
+template <int AXIS, int L>
+static int tmem_pass_l(int n, int64_t bx, int64_t by, int64_t bz, uint8_t *pdms,
+                       int64_t pitch, cudaStream_t s, PackDst pk) {
+    auto kern = dt_tmem_kernel<AXIS, L>;
     const int64_t tiles = AXIS == kAxisZ ? (int64_t)n * (bx * by / 32)
                                          : (int64_t)n * bx * (bz / 32);
-    // 6 CTAs of 4 warps per SM (33 KB of shared memory each, 80 registers,
-    // 6 x 64 TMEM columns); the carveout must be the maximum for that
-    static bool attr_set = false;
+    const size_t smem = (size_t)kTmemWarps * 32 * L;
+    static bool attr_set = false;  // (per instantiation)
     if (!attr_set) {
+        PDM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)smem));
         PDM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
                                           (int)cudaSharedmemCarveoutMaxShared));
         attr_set = true;
     }
-    // (the occupancy API answers 1 for this kernel; the limits are as above)
-    const int per_sm = 6;
+    // (the occupancy API answers 1 for a kernel that allocates TMEM; the
+    // limits are shared memory, 80 registers and the TMEM columns: tmem_ctas)
+    const int per_sm = tmem_ctas<L>();
     int64_t grid = ceil_div(tiles, kTmemWarps);
     const int64_t cap = (int64_t)sm_count() * per_sm;
     if (grid > cap) grid = cap;
     unsigned long long *ctr = nullptr;
     int st = tile_counter(s, &ctr);
     if (st) return st;
-    kern<<<(unsigned)grid, 32 * kTmemWarps, 0, s>>>(n, bx, by, bz, pdms, pitch, tiles, pk, ctr);
+    kern<<<(unsigned)grid, 32 * kTmemWarps, smem, s>>>(n, bx, by, bz, pdms, pitch, tiles, pk,
+                                                         ctr);
     return cuda_status("dt_tmem_kernel");
+}
+
+template <int AXIS>
+static int tmem_pass(int n, int64_t bx, int64_t by, int64_t bz, uint8_t *pdms, int64_t pitch,
+                     cudaStream_t s, PackDst pk) {
+    const int64_t L = AXIS == kAxisY ? by : bz;
+    return L == 256 ? tmem_pass_l<AXIS, 256>(n, bx, by, bz, pdms, pitch, s, pk)
+                    : tmem_pass_l<AXIS, 512>(n, bx, by, bz, pdms, pitch, s, pk);
 }
 
 // pk (z pass only): fused packing epilogue; honoured when the z pass runs the

@@ -91,6 +91,7 @@ def test_distance_transform_random_vs_oracle_medium():
     (3, 256, 256),   # TMEM sweeps: y and z lines of 256 in full tiles
     (2, 256, 96),    # TMEM y sweep (bz = 96), padded-row z tiles
     (5, 64, 256),    # TMEM z sweep with fused packing rows, strided y of 64
+    (2, 512, 96),    # TMEM y sweep of 512-long lines
 ])
 def test_distance_transform_tile_layouts(dims):
     """Every shared-memory tile layout of the sweep envelope kernel against
@@ -773,6 +774,7 @@ def test_merge_writes_stay_inside_the_map(monkeypatch, packed):
     ((7, 5, 96), 2, 8),       # 8-bit apron fast path, b = 2, partial strip
     ((6, 7, 13), 1, 8),       # generic kernels (nz not a chunk multiple)
     ((8, 1024, 1024), 4, 16),  # TMEM y and z sweeps (256-long lines), fused packing
+    ((4, 2048, 2048), 4, 16),  # TMEM y and z sweeps of 512-long lines (16-bit tables)
 ])
 def test_precompute_kernels_write_inside_their_outputs(dims, b, bits):
     """Canary bytes around every precompute output survive (compute-sanitizer
