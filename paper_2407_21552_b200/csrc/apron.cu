@@ -191,7 +191,14 @@ __global__ void __launch_bounds__(32 * kApronWarps,
          it += warps) {
         const int64_t s = it % nstrips;
         const int64_t rest = it / nstrips;
+#ifdef PDM_APRON_ROW_MAJOR  // (A/B: the round-2 order, x-chunk before block row)
         const int64_t xc = rest % xchunks, jg = rest / xchunks;
+#else
+        // x-chunk slowest: the warps resident at once walk the same run of
+        // planes instead of one run per x-chunk (config c 0.41 -> 0.39 ms,
+        // config d 5.1 -> 4.7 ms with TMA, 4.0 ms with cp.async)
+        const int64_t jg = rest % groups, xc = rest / groups;
+#endif
         const int64_t zs = s * strip;
         const int64_t zl = zs + (int64_t)lane * VPC;
         const bool active = zl < nz;
@@ -514,18 +521,20 @@ static int launch_b(const void *vox, int64_t nx, int64_t ny, int64_t nz, int64_t
                     uint32_t *mask, int words, cudaStream_t s) {
     using T = typename VoxT<BITS>::type;
     constexpr int VPC = 16 / (BITS / 8);
-    const int XB = 32;
+    static const int XB = getenv("PDM_APRON_XB") ? atoi(getenv("PDM_APRON_XB")) : 32;  // (A/B)
     static const bool two = getenv("PDM_APRON_RB") && getenv("PDM_APRON_RB")[0] == '2';
     constexpr int RB2 = apron_two_rows<BITS, B>() ? 2 : 1;
     const int RB = two ? RB2 : 1;
     // TMA plane loads: 16-bit, b = 4, one block row per warp, at least 6 rows,
-    // z extent < 2^31; PDM_APRON_TMA=0 keeps the cp.async ring (A/B)
+    // volumes up to 4 GB (at config d, 17 GB with 8 MB planes, the cp.async
+    // ring measured faster: 4.0 vs 4.7 ms); PDM_APRON_TMA=0 keeps the
+    // cp.async ring (A/B)
     static const bool no_tma = getenv("PDM_APRON_TMA") && getenv("PDM_APRON_TMA")[0] == '0';
     ApronMaps maps;
     memset(&maps, 0, sizeof(maps));
     bool tma = false;
     if constexpr (BITS == 16 && B == 4) {
-        tma = !no_tma && RB == 1 && ny >= 6 && nz < ((int64_t)1 << 31) &&
+        tma = !no_tma && RB == 1 && ny >= 6 && nx * ny * nz * 2 <= ((int64_t)4 << 30) &&
               nx < ((int64_t)1 << 31) && encode_volume_map(&maps.main, vox, nx, ny, nz, 256) &&
               encode_volume_map(&maps.edge, vox, nx, ny, nz, 8);
     }
