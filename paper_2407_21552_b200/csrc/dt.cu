@@ -1089,7 +1089,7 @@ __global__ void __launch_bounds__(256)
 // byte tile, backward run min'ed into it, then 16-byte row stores.  Config c:
 // 0.29 / 0.37 ms (voxel / range_apron masks) vs 0.30 / 0.45 ms for expand +
 // pass x, 0.58 instead of ~1.6 GB of DRAM traffic.  Masks of one word per
-// block (n <= 32), lines <= 256, bz % 32 == 0; PDM_DT_XMASK=0: expand + x.
+// block (n <= 32), lines <= 512, bz % 32 == 0; PDM_DT_XMASK=0: expand + x.
 // Measured and rejected: the forward runs parked in TMEM instead of the byte
 // tile, backward results stored straight to HBM (one 32-byte sector per warp
 // store), 24-32 warps per SM: 0.34 / 0.47 ms -- the byte-wide global stores
@@ -1430,7 +1430,7 @@ static int axis_pass(int n, int64_t bx, int64_t by, int64_t bz, uint8_t *pdms, i
 
 static bool x_mask_ok(int words, int64_t bx, int64_t bz, const uint32_t *mask) {
     static const bool off = getenv("PDM_DT_XMASK") && getenv("PDM_DT_XMASK")[0] == '0';
-    return !off && words == 1 && bx >= 2 && bx <= 256 && bz % 32 == 0 &&
+    return !off && words == 1 && bx >= 2 && bx <= 512 && bz % 32 == 0 &&
            (uintptr_t)mask % 16 == 0;
 }
 
@@ -1443,7 +1443,8 @@ static int pass_x_mask(const uint32_t *mask, int words, int n, int64_t bx, int64
         PDM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           (int)smem));
         const int64_t tiles = by * (bz / 32);
-        int64_t grid = (int64_t)sm_count() * 2;
+        // 2 CTAs per SM for lines <= 256 (96 KB each), 1 for longer ones
+        int64_t grid = (int64_t)sm_count() * (smem <= 113 * 1024 ? 2 : 1);
         if (grid > tiles) grid = tiles;
         kern<<<(unsigned)grid, 32 * kXMaskWarps, smem, s>>>(mask, n, bx, by, bz, pdms, pitch,
                                                             tiles);

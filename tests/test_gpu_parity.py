@@ -394,6 +394,8 @@ def test_pdm_set_round_trip(tmp_path, built16):
     # TMA apron planes (16-bit, b = 4): three strips with a partial last one
     # (nz = 520) and a partial last block row; ny = 5 < 6 keeps the cp.async ring
     ((13, 23, 520), 16, 4, 16), ((11, 5, 264), 16, 4, 8),
+    # pass x from the mask with x lines of 257..512 blocks (one CTA per SM)
+    ((1200, 8, 128), 16, 4, 16), ((2040, 4, 128), 16, 4, 32),
 ])
 @pytest.mark.parametrize("mode", ["voxel", "range_apron"])
 def test_random_volumes_vs_oracle(dims, bits, b, n, mode):
