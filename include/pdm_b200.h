@@ -67,7 +67,9 @@ int pdm_count_value(const uint8_t *data, int64_t bytes, uint32_t value,
  * partition p has alpha[v * alpha_stride] > 0.0 (f64 compare: NaN transparent,
  * denormals visible), else 0 -- every flag is written.  starts: device
  * int32[n+1], partition p = [starts[p], starts[p+1]) (contiguous, covering,
- * starts[n] = span, transfer.py:124-148); max_width = widest partition (picks
+ * starts[n] = span, transfer.py:124-148), or NULL for the uniform scheme
+ * (scheme_uniform, transfer.py:201-203: span / n wide, the first span % n
+ * partitions one wider); max_width = widest partition (picks
  * a CTA or a warp per partition).  flags: device uint8[n]. */
 int pdm_select(const double *alpha, int64_t span, int64_t alpha_stride, const int32_t *starts,
                int32_t n, int32_t max_width, uint8_t *flags, pdm_stream_t stream);

@@ -85,17 +85,30 @@ int resident_ctas(const void *kernel, int threads, size_t smem) {
 // partition: a whole CTA (256) for wide partitions, a warp for narrow ones.
 // With PDL the dependent merge launches while this runs and waits on
 // griddepcontrol before it reads the flags.
+// starts == nullptr: the uniform scheme (transfer.py:201-203 widths: span/n,
+// the first span % n partitions one wider), bounds computed in the kernel --
+// no dependent fetch of a starts table before the alpha loads (the merge
+// waits on this kernel every TF change).
 template <int kTPP>
 __global__ void __launch_bounds__(256)
     select_kernel(const double *__restrict__ alpha, int64_t stride,
-                  const int32_t *__restrict__ starts, int n, uint8_t *__restrict__ flags) {
+                  const int32_t *__restrict__ starts, int n, int span,
+                  uint8_t *__restrict__ flags) {
     pdl_launch_dependents();
     const int group = threadIdx.x / kTPP, lane = threadIdx.x % kTPP;
     const int p = blockIdx.x * (256 / kTPP) + group;
     bool any = false;
     if (p < n) {
-        const int lo = starts[p], hi = starts[p + 1];
-#pragma unroll 4
+        int lo, hi;
+        if (starts != nullptr) {
+            lo = starts[p];
+            hi = starts[p + 1];
+        } else {
+            const int q = span / n, r = span % n;
+            lo = p * q + min(p, r);
+            hi = lo + q + (p < r ? 1 : 0);
+        }
+#pragma unroll 8
         for (int v = lo + lane; v < hi; v += kTPP) any |= alpha[(int64_t)v * stride] > 0.0;
     }
     if (kTPP == 256) {
@@ -492,15 +505,15 @@ extern "C" int pdm_count_value(const uint8_t *data, int64_t bytes, uint32_t valu
 extern "C" int pdm_select(const double *alpha, int64_t span, int64_t alpha_stride,
                           const int32_t *starts, int32_t n, int32_t max_width, uint8_t *flags,
                           pdm_stream_t stream) {
-    PDM_REQUIRE(alpha && starts && flags, "pdm_select: null pointer");
+    PDM_REQUIRE(alpha && flags, "pdm_select: null pointer");
     PDM_REQUIRE(span >= 1 && span <= (1 << 16) && n >= 1 && n <= span && alpha_stride >= 1,
                 "pdm_select: bad sizes (span=%lld n=%d)", (long long)span, n);
     cudaStream_t s = as_stream(stream);
     if (max_width >= 512) {
-        select_kernel<256><<<n, 256, 0, s>>>(alpha, alpha_stride, starts, n, flags);
+        select_kernel<256><<<n, 256, 0, s>>>(alpha, alpha_stride, starts, n, (int)span, flags);
     } else {
         select_kernel<32><<<(unsigned)ceil_div(n, 8), 256, 0, s>>>(alpha, alpha_stride, starts, n,
-                                                                    flags);
+                                                                    (int)span, flags);
     }
     return cuda_status("select_kernel");
 }
