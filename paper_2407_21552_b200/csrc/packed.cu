@@ -701,7 +701,9 @@ __global__ void __launch_bounds__(kPackedThreads, kTable ? kPackedCtas : kPacked
     if (kOut == 0 && !kCount && raw.pdms != nullptr && s_k >= 1 && s_k <= raw.max_k) {
         // a small selection: the raw planes, 8 loads in flight per thread
         const int64_t nvec = map_bytes / 16;
-        if (s_k <= 2)
+        if (s_k == 1)  // a copy: 8 chunks of the one plane in flight per thread
+            merge_small_k<8, 1, false>(raw.pdms, raw.pitch, nvec, s_idx, s_k, out);
+        else if (s_k == 2)
             merge_small_k<4, 2, false>(raw.pdms, raw.pitch, nvec, s_idx, s_k, out);
         else
             merge_small_k<2, 4, false>(raw.pdms, raw.pitch, nvec, s_idx, s_k, out);
