@@ -16,7 +16,13 @@
 // distances, so g3 == min(255, chamfer_chebyshev) cell for cell (pinned
 // against the reference's golden vectors and the C oracle in tests/).
 //
-// Lower envelopes of lines <= 256 use a stack-free forward/backward sweep with
+// Kernels, by shape (config c, 256^3 blocks, takes the first of each):
+//   expand + pass x: dt_x_mask_kernel reads the partition mask itself (masks
+//     of one word, lines <= 512); else dt_expand_mask_kernel + the x pass;
+//   pass y / pass z: dt_tmem_kernel keeps each lane's line in tensor memory
+//     (lines of 256 or 512 in full 32-line tiles); else dt_tile_kernel
+//     (lines in shared memory); lines > 1024: dt_line_kernel.
+// Lower envelopes of lines <= 512 use a stack-free forward/backward sweep with
 // a per-line table indexed by value (sweep_forward / sweep_backward below);
 // longer lines use Meijster et al.'s linear-time scan with the L-infinity
 // separator (one lane per line, stack in local memory):
