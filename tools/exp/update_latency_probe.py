@@ -72,5 +72,39 @@ def main():
     print(json.dumps(r, indent=1))
 
 
-if __name__ == "__main__":
+if __name__ == "__main__" and "--c" not in sys.argv:
     main()
+
+
+def c_floor():
+    """C-level pieces of one round trip (ctypes calls, median of 300)."""
+    import torch
+
+    L = _lib.lib()
+    st = _lib.stream_handle()
+    span, n = 256, 64
+    alpha_dev = torch.zeros(span, dtype=torch.float64, device="cuda")
+    alpha_dev[128:192] = 0.5
+    flags_dev = torch.empty(n, dtype=torch.uint8, device="cuda")
+    alpha_pin = torch.zeros(span, dtype=torch.float64, pin_memory=True)
+    alpha_pin[128:192] = 0.5
+    flags_pin = torch.empty(n, dtype=torch.uint8, pin_memory=True)
+    tiny = torch.zeros(16, dtype=torch.uint8, device="cuda")
+    cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+    r = {}
+    r["count_value(16 B)+sync (floor)"] = med(lambda: (L.pdm_count_value(
+        tiny.data_ptr(), 16, 0, cnt.data_ptr(), st), L.pdm_stream_synchronize(st)), 300)
+    r["select dev alpha/dev flags +sync"] = med(lambda: (L.pdm_select(
+        alpha_dev.data_ptr(), span, 1, None, n, 4, flags_dev.data_ptr(), st),
+        L.pdm_stream_synchronize(st)), 300)
+    r["select zero-copy alpha/flags +sync"] = med(lambda: (L.pdm_select(
+        alpha_pin.data_ptr(), span, 1, None, n, 4, flags_pin.data_ptr(), st),
+        L.pdm_stream_synchronize(st)), 300)
+    r["select launch only (no sync)"] = med(lambda: L.pdm_select(
+        alpha_dev.data_ptr(), span, 1, None, n, 4, flags_dev.data_ptr(), st), 300)
+    L.pdm_stream_synchronize(st)
+    print(json.dumps(r, indent=1))
+
+
+if __name__ == "__main__" and "--c" in sys.argv:
+    c_floor()
