@@ -529,6 +529,8 @@ __device__ __forceinline__ void fold_ids(PackedAcc &acc, const uint4 (&q)[B],
 // the min fused as VIADDMNMX.U16x2 (36.2 vs 36.2 us), and -- timing probes
 // with wrong results -- nibbles or bases read from an L2-resident 64 KB /
 // 4 KB instead of HBM (34.8 / 35.0 vs 35.5 us: DRAM is not what bounds it),
+// a per-warp ring of 8 shared slots filled by lane 0 with cp.async.bulk
+// copies per (tile, kept plane) onto per-slot mbarriers (67.5 vs 35.6 us),
 // an L2 prefetch of the next tile's kept planes a lap ahead (48.0 vs 39.0 us:
 // the kernel is issue-bound, ncu 42-55 % issue active with 20 of 24 warps
 // resident, and every extra instruction shows).
