@@ -138,7 +138,11 @@ __global__ void __launch_bounds__(128)
                 int dval;
                 V c[8];
             };
-            auto load = [&](int64_t kk, Sample &S) {
+            // `prev`: the sample before (its block and cell, when valid): a
+            // sample in the same block reuses its D' byte, one in the same
+            // trilinear cell its 8 voxels (step 0.5: about every other
+            // sample), so those lanes issue no loads.
+            auto load = [&](int64_t kk, Sample &S, const Sample &prev, bool prev_ok) {
                 const double t = t_entry + kk * a.step;
                 S.px = clampd(a.ox + t * dx, hx);
                 S.py = clampd(a.oy + t * dy, hy);
@@ -148,10 +152,18 @@ __global__ void __launch_bounds__(128)
                 S.bi = bshift >= 0 ? vx >> bshift : vx / bb;
                 S.bj = bshift >= 0 ? vy >> bshift : vy / bb;
                 S.bk = bshift >= 0 ? vz >> bshift : vz / bb;
-                S.dval = dist[(S.bi * byi + S.bj) * bzi + S.bk];
+                if (prev_ok && S.bi == prev.bi && S.bj == prev.bj && S.bk == prev.bk)
+                    S.dval = prev.dval;
+                else
+                    S.dval = dist[(S.bi * byi + S.bj) * bzi + S.bk];
                 S.x0 = vx < x_hi ? vx : x_hi;
                 S.y0 = vy < y_hi ? vy : y_hi;
                 S.z0 = vz < z_hi ? vz : z_hi;
+                if (prev_ok && S.x0 == prev.x0 && S.y0 == prev.y0 && S.z0 == prev.z0) {
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) S.c[i] = prev.c[i];
+                    return;
+                }
                 const I x1 = a.nx >= 2 ? S.x0 + 1 : S.x0;
                 const I y1 = a.ny >= 2 ? S.y0 + 1 : S.y0;
                 const I z1 = a.nz >= 2 ? S.z0 + 1 : S.z0;
@@ -166,10 +178,10 @@ __global__ void __launch_bounds__(128)
             };
             int64_t k = 0;
             Sample cur, nxt;
-            load(0, cur);
+            load(0, cur, cur, false);
             while (k < total) {
                 const bool more = k + 1 < total;
-                if (more) load(k + 1, nxt);
+                if (more) load(k + 1, nxt, cur, true);
                 if (cur.dval == 0) {
                     const double fx = cur.px - cur.x0, fy = cur.py - cur.y0, fz = cur.pz - cur.z0;
                     const double c000 = cur.c[0], c100 = cur.c[1], c010 = cur.c[2],
@@ -206,7 +218,7 @@ __global__ void __launch_bounds__(128)
                     if (k_next == k + 1) {
                         cur = nxt;
                     } else if (k_next < total) {
-                        load(k_next, cur);
+                        load(k_next, cur, cur, false);
                     }
                     k = k_next;
                 }
