@@ -134,6 +134,18 @@ class DistanceMap(_BlockArray):
         if not isinstance(dist, np.ndarray) and dist.element_size() != 1:
             raise ValueError("distance tensor must be uint8")
 
+    @classmethod
+    def _of_device(cls, b: int, bdims: tuple, t) -> "DistanceMap":
+        """A map around a uint8 CUDA tensor of shape bdims that this module
+        just made (no validation: the merges' own results)."""
+        obj = cls.__new__(cls)
+        obj.b = b
+        obj.bdims = bdims
+        obj._host = None
+        obj._dev = t
+        obj._host_fill = None
+        return obj
+
     @property
     def dist(self) -> np.ndarray:
         probe = self.__dict__.get("_probe")
@@ -553,16 +565,15 @@ def combine(pdm_set: PdmSet, selection: PartitionSelection,
         out = device.empty(grid.bdims, np.uint8)
         combine_flags_into(pdm_set, flags, out)
     else:
-        indices = selection.sorted
-        if indices and max_maps_per_pass is not None and max_maps_per_pass < 1:
+        sel = selection.indices0()
+        if sel.size and max_maps_per_pass is not None and max_maps_per_pass < 1:
             raise ValueError(f"max_maps_per_pass must be >= 1, got {max_maps_per_pass}")
-        sel = np.ascontiguousarray([i - 1 for i in indices], dtype=np.int32)
         out = device.empty(grid.bdims, np.uint8)
         if 0 < sel.size <= _MAX_PACKED_SEL and _host_reader(pdm_set):
             return _combine_with_host_view(pdm_set, sel, out)
         _combine_indices(pdm_set, sel, out)
     device.complete()
-    dm = DistanceMap(b=grid.b, bdims=grid.bdims, dist=out)
+    dm = DistanceMap._of_device(grid.b, grid.bdims, out)
     if _host_packed_pays(pdm_set):
         probe = _HostReadProbe()
         pdm_set._last_probe = probe

@@ -113,7 +113,10 @@ def empty(shape, np_dtype):
 
         _lib.lib()  # no CUDA device / library: there is no CPU fallback
         _EMPTY = torch().empty
-    return _EMPTY(shape, dtype=_torch_dtype(np_dtype), device="cuda")
+    dt = _DT_CACHE.get(np_dtype)
+    if dt is None:
+        dt = _torch_dtype(np_dtype)
+    return _EMPTY(shape, dtype=dt, device="cuda")
 
 
 def plane_pitch(num_blocks: int) -> int:
