@@ -564,7 +564,16 @@ __device__ __forceinline__ void merge_packed(const P planes, int k, int64_t map_
 #endif
         }
     };
+    // A lap's W consecutive tiles are dealt round-robin over the CTAs (warp w
+    // of CTA c takes tile w * gridDim + c), so an SM's warps are spread over
+    // the lap's window instead of owning 8 neighbouring tiles of one region:
+    // the skip makes the work per tile spatially uneven (38.2 -> 37.2 us per
+    // bench step; the window itself stays compact, which matters, see below)
+#ifdef PDM_MERGE_CTA_CONTIGUOUS  // (A/B: the previous order)
     int64_t tile = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+#else
+    int64_t tile = (int64_t)(threadIdx.x >> 5) * gridDim.x + blockIdx.x;
+#endif
     uint32_t c0, c1;  // bounds row of the current tile, fetched one lap ahead
     fetch(tile, c0, c1);
     for (; tile < ntiles; tile += W) {
