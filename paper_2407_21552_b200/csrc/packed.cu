@@ -758,12 +758,20 @@ static int packed_grid(K kernel, int64_t map_bytes) {
         }
     }
     if (per_sm < 1) per_sm = 1;
-    // One wave of resident CTAs; laps equalised so no warp runs an extra one.
     const int64_t tiles = ceil_div(ceil_div(map_bytes, 32), 32);
     const int64_t cap = (int64_t)sm_count() * per_sm;
     const int64_t wpc = kPackedThreads / 32;
+#ifdef PDM_MERGE_LAPS_EQUALISED  // (A/B: the previous sizing)
+    // One wave of resident CTAs; laps equalised so no warp runs an extra one.
     const int64_t laps = ceil_div(tiles, cap * wpc);
     int64_t grid = ceil_div(tiles, laps * wpc);
+#else
+    // Every SM gets the same number of CTAs (one full wave): with the tiles
+    // dealt round-robin over the CTAs each SM then merges the same share of
+    // the map.  (Equalising the laps instead left 34 of 148 SMs with 2 CTAs
+    // at config c -- two thirds of the work -- while the others set the pace.)
+    int64_t grid = ceil_div(tiles, wpc);
+#endif
     if (grid > cap) grid = cap;
     return grid < 1 ? 1 : (int)grid;
 }
