@@ -574,9 +574,25 @@ __device__ __forceinline__ void merge_packed(const P planes, int k, int64_t map_
 #else
     int64_t tile = (int64_t)(threadIdx.x >> 5) * gridDim.x + blockIdx.x;
 #endif
+    // A CTA's tiles (j * grid + c, j = 0, 1, ...) are claimed by its warps
+    // from a shared counter, one ahead, so the CTA's warps finish together
+    // (36.9 vs 37.1 us per step; shared-memory atomics, the window unchanged)
+#ifndef PDM_MERGE_STATIC_LAPS  // (A/B: each warp its fixed laps)
+    __shared__ int s_claim;
+    if (threadIdx.x == 0) s_claim = blockDim.x >> 5;
+    __syncthreads();
+    auto next_tile = [&](int64_t) -> int64_t {
+        int j = 0;
+        if (lane == 0) j = atomicAdd(&s_claim, 1);
+        return (int64_t)__shfl_sync(0xFFFFFFFFu, j, 0) * gridDim.x + blockIdx.x;
+    };
+#else
+    auto next_tile = [&](int64_t cur) -> int64_t { return cur + W; };
+#endif
     uint32_t c0, c1;  // bounds row of the current tile, fetched one lap ahead
     fetch(tile, c0, c1);
-    for (; tile < ntiles; tile += W) {
+    for (int64_t nxt = 0; tile < ntiles; tile = nxt) {
+        nxt = next_tile(tile);
         const int64_t t = tile * 32 + lane;
         const bool live = t < items;
         PackedAcc acc;
@@ -586,7 +602,7 @@ __device__ __forceinline__ void merge_packed(const P planes, int k, int64_t map_
 #ifdef PDM_SKIP_FORCE_ALL  // (A/B builds: the skip's bookkeeping without the skip)
             keep = k >= 64 ? ~0ull : ((1ull << k) - 1ull);
 #endif
-            fetch(tile + W, c0, c1);  // (two laps ahead measured the same)
+            fetch(nxt, c0, c1);  // (two laps ahead measured the same)
             nread += __popcll(keep);
             // the unskipped merge's batches of B planes, loads predicated on
             // the keep bits (warp-uniform); batches with no kept plane are
