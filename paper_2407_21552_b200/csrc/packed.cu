@@ -34,7 +34,14 @@
 
 namespace pdm {
 
-constexpr int kPackedThreads = 256;
+// One CTA of 24 warps per SM (80 registers): the warps of an SM claim the
+// SM's tiles from one shared counter (see merge_packed), so the whole SM's
+// share of the map is balanced, not just a CTA's (3 CTAs of 8 warps: 36.96 vs
+// 36.3 us per bench step).
+#ifndef PDM_PACKED_THREADS  // (overridable for A/B builds)
+#define PDM_PACKED_THREADS 768
+#endif
+constexpr int kPackedThreads = PDM_PACKED_THREADS;
 constexpr int kPackedMaxSel = 240;       // indices in kernel parameters
 constexpr int kPackedMaxFlags = 4096;
 
@@ -656,16 +663,20 @@ __device__ __forceinline__ void merge_packed(const P planes, int k, int64_t map_
     if (skip.planes_read != nullptr && lane == 0 && nread) atomicAdd(skip.planes_read, nread);
 }
 
-// Planes per load batch and CTAs per SM: with the pointer table, 6 planes per
-// batch at 3 CTAs (bench step, 3 interleaved runs each: 46.3 us vs 47.8 for
+// Planes per load batch and CTAs per SM (now one CTA of 768 threads, see
+// kPackedThreads): with the pointer table, 6 planes per
+// batch at 3 CTAs of 256 (bench step, 3 interleaved runs each: 46.3 us vs 47.8 for
 // 8 planes / 3 CTAs and 48.2 for 4 planes / 4 CTAs); the index path keeps 4
 // planes at 5 CTAs.
 #ifndef PDM_PACKED_BATCH  // (overridable for A/B builds)
 #define PDM_PACKED_BATCH 6
-#define PDM_PACKED_CTAS 3
+#define PDM_PACKED_CTAS 1
 #endif
 constexpr int kPackedBatch = PDM_PACKED_BATCH, kPackedCtas = PDM_PACKED_CTAS;
-constexpr int kPackedBatchIdx = 4, kPackedCtasIdx = 5;
+#ifndef PDM_PACKED_CTAS_IDX
+#define PDM_PACKED_CTAS_IDX 1
+#endif
+constexpr int kPackedBatchIdx = 4, kPackedCtasIdx = PDM_PACKED_CTAS_IDX;
 constexpr int kPackedTable = 256;  // n up to this uses TablePlanes
 
 __device__ __forceinline__ void fill_table(const uint8_t *nib, int64_t nib_pitch,
