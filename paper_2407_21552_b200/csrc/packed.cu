@@ -34,12 +34,14 @@
 
 namespace pdm {
 
-// One CTA of 24 warps per SM (80 registers): the warps of an SM claim the
-// SM's tiles from one shared counter (see merge_packed), so the whole SM's
-// share of the map is balanced, not just a CTA's (3 CTAs of 8 warps: 36.96 vs
-// 36.3 us per bench step).
+// One CTA of 32 warps per SM (64 registers, 5 planes per load batch): the
+// warps of an SM claim the SM's tiles from one shared counter (see
+// merge_packed), so the whole SM's share of the map is balanced, not just a
+// CTA's (3 CTAs of 8 warps: 36.96 us per bench step; 1 of 24 warps at 80
+// registers: 36.3; 1 of 32 at 64 registers -- a few spilled values -- 35.2;
+// with 4 planes per batch 37.2).
 #ifndef PDM_PACKED_THREADS  // (overridable for A/B builds)
-#define PDM_PACKED_THREADS 768
+#define PDM_PACKED_THREADS 1024
 #endif
 constexpr int kPackedThreads = PDM_PACKED_THREADS;
 constexpr int kPackedMaxSel = 240;       // indices in kernel parameters
@@ -669,7 +671,7 @@ __device__ __forceinline__ void merge_packed(const P planes, int k, int64_t map_
 // 8 planes / 3 CTAs and 48.2 for 4 planes / 4 CTAs); the index path keeps 4
 // planes at 5 CTAs.
 #ifndef PDM_PACKED_BATCH  // (overridable for A/B builds)
-#define PDM_PACKED_BATCH 6
+#define PDM_PACKED_BATCH 5
 #define PDM_PACKED_CTAS 1
 #endif
 constexpr int kPackedBatch = PDM_PACKED_BATCH, kPackedCtas = PDM_PACKED_CTAS;
@@ -739,9 +741,11 @@ __global__ void __launch_bounds__(kPackedThreads, kTable ? kPackedCtas : kPacked
     if (kOut == 0 && !kCount && raw.pdms != nullptr && s_k >= 1 && s_k <= raw.max_k) {
         // a small selection: the raw planes, 8 loads in flight per thread
         const int64_t nvec = map_bytes / 16;
-        if (s_k == 1)  // a copy: 8 chunks of the one plane in flight per thread
+        // (k = 1 as 8 chunks of the one plane per thread needs > 64 registers:
+        // only with the narrower CTAs)
+        if (kPackedThreads < 1024 && s_k == 1)
             merge_small_k<8, 1, false>(raw.pdms, raw.pitch, nvec, s_idx, s_k, out);
-        else if (s_k == 2)
+        else if (s_k <= 2)
             merge_small_k<4, 2, false>(raw.pdms, raw.pitch, nvec, s_idx, s_k, out);
         else
             merge_small_k<2, 4, false>(raw.pdms, raw.pitch, nvec, s_idx, s_k, out);
