@@ -34,12 +34,13 @@
 
 namespace pdm {
 
-// One CTA of 32 warps per SM (64 registers, 5 planes per load batch): the
+// One CTA of 32 warps per SM (64 registers, 6 planes per load batch): the
 // warps of an SM claim the SM's tiles from one shared counter (see
 // merge_packed), so the whole SM's share of the map is balanced, not just a
 // CTA's (3 CTAs of 8 warps: 36.96 us per bench step; 1 of 24 warps at 80
-// registers: 36.3; 1 of 32 at 64 registers -- a few spilled values -- 35.2;
-// with 4 planes per batch 37.2).
+// registers: 36.3; 1 of 32 at 64 registers -- a few spilled values -- 35.2
+// with 5 planes per batch and 64-bit tile indices; with 32-bit indices 5 / 6
+// / 7 / 8 planes per batch 35.0 / 34.1 / 34.6 / 36.2, 4 planes 37.2).
 #ifndef PDM_PACKED_THREADS  // (overridable for A/B builds)
 #define PDM_PACKED_THREADS 1024
 #endif
@@ -550,17 +551,19 @@ __device__ __forceinline__ void merge_packed(const P planes, int k, int64_t map_
                                              unsigned long long *zeros, uint4 *stage,
                                              const TileSkip skip) {
     uint32_t nzero = 0;
-    const int64_t items = ceil_div(map_bytes, 32);
-    const int64_t ntiles = ceil_div(items, 32);
+    // 32-bit tile and item indices (check_packed bounds the map): registers
+    // matter at 64 per thread
+    const int items = (int)ceil_div(map_bytes, 32);
+    const int ntiles = (int)ceil_div(items, 32);
     // Whole warps stay together: the dominance vote, the tile skip and the
     // kOut 3 compaction are full-warp operations.
     const int lane = threadIdx.x & 31;
     const bool tiles = skip.tb != nullptr && k <= 64 && k > 0;
     const bool v0 = lane < k, v1 = lane + 32 < k;
     const int pid0 = tiles && v0 ? skip.pid[lane] : 0, pid1 = tiles && v1 ? skip.pid[lane + 32] : 0;
-    uint64_t nread = 0;
-    const int64_t W = (int64_t)gridDim.x * (blockDim.x >> 5);
-    auto fetch = [&](int64_t tile, uint32_t &e0, uint32_t &e1) {
+    uint32_t nread = 0;
+    const int W = (int)(gridDim.x * (blockDim.x >> 5));
+    auto fetch = [&](int tile, uint32_t &e0, uint32_t &e1) {
         e0 = e1 = 0xFFFFu;
         if (tiles && tile < ntiles) {
 #ifdef PDM_SKIP_NOFETCH  // (A/B builds: keep every plane without reading the table)
@@ -579,9 +582,9 @@ __device__ __forceinline__ void merge_packed(const P planes, int k, int64_t map_
     // the skip makes the work per tile spatially uneven (38.2 -> 37.2 us per
     // bench step; the window itself stays compact, which matters, see below)
 #ifdef PDM_MERGE_CTA_CONTIGUOUS  // (A/B: the previous order)
-    int64_t tile = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    int tile = (int)(blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5));
 #else
-    int64_t tile = (int64_t)(threadIdx.x >> 5) * gridDim.x + blockIdx.x;
+    int tile = (int)((threadIdx.x >> 5) * gridDim.x + blockIdx.x);
 #endif
     // A CTA's tiles (j * grid + c, j = 0, 1, ...) are claimed by its warps
     // from a shared counter, one ahead, so the CTA's warps finish together
@@ -590,19 +593,19 @@ __device__ __forceinline__ void merge_packed(const P planes, int k, int64_t map_
     __shared__ int s_claim;
     if (threadIdx.x == 0) s_claim = blockDim.x >> 5;
     __syncthreads();
-    auto next_tile = [&](int64_t) -> int64_t {
+    auto next_tile = [&](int) -> int {
         int j = 0;
         if (lane == 0) j = atomicAdd(&s_claim, 1);
-        return (int64_t)__shfl_sync(0xFFFFFFFFu, j, 0) * gridDim.x + blockIdx.x;
+        return __shfl_sync(0xFFFFFFFFu, j, 0) * (int)gridDim.x + (int)blockIdx.x;
     };
 #else
-    auto next_tile = [&](int64_t cur) -> int64_t { return cur + W; };
+    auto next_tile = [&](int cur) -> int { return cur + W; };
 #endif
     uint32_t c0, c1;  // bounds row of the current tile, fetched one lap ahead
     fetch(tile, c0, c1);
-    for (int64_t nxt = 0; tile < ntiles; tile = nxt) {
+    for (int nxt = 0; tile < ntiles; tile = nxt) {
         nxt = next_tile(tile);
-        const int64_t t = tile * 32 + lane;
+        const int t = tile * 32 + lane;
         const bool live = t < items;
         PackedAcc acc;
         acc.init();
@@ -630,8 +633,8 @@ __device__ __forceinline__ void merge_packed(const P planes, int k, int64_t map_
                     qv[j] = make_uint4(0u, 0u, 0u, 0u);
                     bv[j] = 0u;
                     if (live && id[j] >= 0) {
-                        qv[j] = ld_stream_u4(planes.nib_at(m + j) + t * 16);
-                        bv[j] = ld_stream_u16(planes.base_at(m + j) + t * 2);
+                        qv[j] = ld_stream_u4(planes.nib_at(m + j) + (int64_t)t * 16);
+                        bv[j] = ld_stream_u16(planes.base_at(m + j) + (int64_t)t * 2);
                     }
                 }
                 // no dominance vote here: the tile skip has already dropped the
@@ -641,7 +644,7 @@ __device__ __forceinline__ void merge_packed(const P planes, int k, int64_t map_
                 fold_ids<B>(acc, qv, bv, id, true, live);
             }
         } else {
-            nread += (uint64_t)k;
+            nread += (uint32_t)k;
             for (int m = 0; m < k; m += B) {
                 uint4 qv[B];
                 uint32_t bv[B];
@@ -650,8 +653,8 @@ __device__ __forceinline__ void merge_packed(const P planes, int k, int64_t map_
                     qv[j] = make_uint4(0u, 0u, 0u, 0u);
                     bv[j] = 0u;
                     if (live && m + j < k) {
-                        qv[j] = ld_stream_u4(planes.nib_at(m + j) + t * 16);
-                        bv[j] = ld_stream_u16(planes.base_at(m + j) + t * 2);
+                        qv[j] = ld_stream_u4(planes.nib_at(m + j) + (int64_t)t * 16);
+                        bv[j] = ld_stream_u16(planes.base_at(m + j) + (int64_t)t * 2);
                     }
                 }
                 fold_batch<B>(acc, qv, bv, m, k, live);
@@ -671,7 +674,7 @@ __device__ __forceinline__ void merge_packed(const P planes, int k, int64_t map_
 // 8 planes / 3 CTAs and 48.2 for 4 planes / 4 CTAs); the index path keeps 4
 // planes at 5 CTAs.
 #ifndef PDM_PACKED_BATCH  // (overridable for A/B builds)
-#define PDM_PACKED_BATCH 5
+#define PDM_PACKED_BATCH 6
 #define PDM_PACKED_CTAS 1
 #endif
 constexpr int kPackedBatch = PDM_PACKED_BATCH, kPackedCtas = PDM_PACKED_CTAS;
@@ -849,7 +852,8 @@ static int check_packed(const char *fn, const void *nib, int64_t nib_pitch, cons
                         int64_t base_pitch, int64_t map_bytes, int n, const void *out,
                         const void *out_base, bool pack_out) {
     PDM_REQUIRE(nib && base && out && (!pack_out || out_base), "%s: null pointer", fn);
-    PDM_REQUIRE(map_bytes >= 1 && n >= 1, "%s: bad sizes (map_bytes=%lld n=%d)", fn,
+    PDM_REQUIRE(map_bytes >= 1 && n >= 1 && map_bytes < ((int64_t)1 << 35),
+                "%s: bad sizes (map_bytes=%lld n=%d; maps below 2^35 blocks)", fn,
                 (long long)map_bytes, n);
     PDM_REQUIRE(nib_pitch >= 16 * ceil_div(map_bytes, 32) &&
                     base_pitch >= 2 * ceil_div(map_bytes, 32),
