@@ -485,30 +485,6 @@ __device__ __forceinline__ uint64_t tile_keep(uint32_t e0, uint32_t e1, bool v0,
     return ((uint64_t)k0 | ((uint64_t)k1 << 32)) | (att & (~att + 1));
 }
 
-// Fold one batch of kept planes id[0..B) (-1: none).  Same dominance vote
-// as fold_batch after the first batch.
-template <int B>
-__device__ __forceinline__ void fold_ids(PackedAcc &acc, const uint4 (&q)[B],
-                                         const uint32_t (&b)[B], const int (&id)[B], bool first,
-                                         bool vote) {
-    if (!first) {
-        uint32_t m0, m1;
-        acc.chunk_max(m0, m1);
-#pragma unroll
-        for (int j = 0; j < B; ++j) {
-            if (id[j] >= 0) {
-                const bool dom = (0x6400u | (b[j] & 0xFFu)) >= m0 &&
-                                 (0x6400u | ((b[j] >> 8) & 0xFFu)) >= m1;
-                if (!__all_sync(0xFFFFFFFFu, dom || !vote)) acc.fold(q[j], b[j]);
-            }
-        }
-        return;
-    }
-#pragma unroll
-    for (int j = 0; j < B; ++j)
-        if (id[j] >= 0) acc.fold(q[j], b[j]);
-}
-
 // Tiles are split statically: warp w of W merges tiles w, w + W, ... (one
 // wave of resident CTAs, laps equalised).  Measured and rejected: warps
 // claiming tiles from an atomic queue (1 or 4-8 tiles per claim) to even out
@@ -624,15 +600,13 @@ __device__ __forceinline__ void merge_packed(const P planes, int k, int64_t map_
                 if (bits == 0) continue;
                 uint4 qv[B];
                 uint32_t bv[B];
-                int id[B];
 #pragma unroll
                 for (int j = 0; j < B; ++j) {
-                    id[j] = ((bits >> j) & 1u) ? m + j : -1;
                     // (zero-filled and live-predicated like the unskipped loop:
                     // without them the compiler's code ran 58 vs 38 us per merge)
                     qv[j] = make_uint4(0u, 0u, 0u, 0u);
                     bv[j] = 0u;
-                    if (live && id[j] >= 0) {
+                    if (live && ((bits >> j) & 1u)) {
                         qv[j] = ld_stream_u4(planes.nib_at(m + j) + (int64_t)t * 16);
                         bv[j] = ld_stream_u16(planes.base_at(m + j) + (int64_t)t * 2);
                     }
@@ -641,7 +615,9 @@ __device__ __forceinline__ void merge_packed(const P planes, int k, int64_t map_
                 // planes that cannot lower the warp's blocks (the vote's
                 // chunk maxima cost more than the folds it still saved:
                 // 41.0 -> 39.2 us per bench step without it)
-                fold_ids<B>(acc, qv, bv, id, true, live);
+#pragma unroll
+                for (int j = 0; j < B; ++j)
+                    if ((bits >> j) & 1u) acc.fold(qv[j], bv[j]);
             }
         } else {
             nread += (uint32_t)k;
