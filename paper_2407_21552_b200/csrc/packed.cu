@@ -699,6 +699,19 @@ struct RawPlanes {
     int max_k;
 };
 
+// A small selection: the raw planes, 8 loads in flight per thread.  Not
+// inlined: its registers would otherwise be allocated against the packed
+// loop's in the same kernel, which then spilled at 64 registers.
+__device__ __noinline__ void merge_raw_small(const RawPlanes raw, int64_t map_bytes,
+                                             const int32_t *s_idx, int k, uint8_t *out) {
+    const int64_t nvec = map_bytes / 16;
+    if (k <= 2)
+        merge_small_k<4, 2, false>(raw.pdms, raw.pitch, nvec, s_idx, k, out);
+    else
+        merge_small_k<2, 4, false>(raw.pdms, raw.pitch, nvec, s_idx, k, out);
+    merge_tail(raw.pdms, raw.pitch, nvec * 16, map_bytes, s_idx, k, false, out);
+}
+
 // Selection resident on the device (written by the select kernel ahead of it
 // in the stream, PDL): every CTA compacts the flags, then merges.
 template <int kOut, bool kCount, bool kTable>
@@ -718,17 +731,7 @@ __global__ void __launch_bounds__(kPackedThreads, kTable ? kPackedCtas : kPacked
     compact_flags(flags, n, s_idx, &s_k);
     __syncthreads();
     if (kOut == 0 && !kCount && raw.pdms != nullptr && s_k >= 1 && s_k <= raw.max_k) {
-        // a small selection: the raw planes, 8 loads in flight per thread
-        const int64_t nvec = map_bytes / 16;
-        // (k = 1 as 8 chunks of the one plane per thread needs > 64 registers:
-        // only with the narrower CTAs)
-        if (kPackedThreads < 1024 && s_k == 1)
-            merge_small_k<8, 1, false>(raw.pdms, raw.pitch, nvec, s_idx, s_k, out);
-        else if (s_k <= 2)
-            merge_small_k<4, 2, false>(raw.pdms, raw.pitch, nvec, s_idx, s_k, out);
-        else
-            merge_small_k<2, 4, false>(raw.pdms, raw.pitch, nvec, s_idx, s_k, out);
-        merge_tail(raw.pdms, raw.pitch, nvec * 16, map_bytes, s_idx, s_k, false, out);
+        merge_raw_small(raw, map_bytes, s_idx, s_k, out);
         return;
     }
     skip.pid = s_idx;
