@@ -1104,7 +1104,8 @@ constexpr int kXMaskWarps = 8;
 
 __global__ void __launch_bounds__(32 * kXMaskWarps, 2)
     dt_x_mask_kernel(const uint32_t *__restrict__ mask, int n, int64_t bx, int64_t by,
-                     int64_t bz, uint8_t *__restrict__ pdms, int64_t pitch, int64_t tiles) {
+                     int64_t bz, uint8_t *__restrict__ pdms, int64_t pitch, int64_t tiles,
+                     unsigned long long *next) {
     extern __shared__ __align__(16) uint8_t s_xm[];
     const int L = (int)bx;
     uint32_t *sm = reinterpret_cast<uint32_t *>(s_xm);                 // [L][32] mask words
@@ -1113,7 +1114,17 @@ __global__ void __launch_bounds__(32 * kXMaskWarps, 2)
     __shared__ uint32_t s_red[2][kXMaskWarps];
     __shared__ int s_next;  // next mixed partition of the column to claim
     const int64_t zq = bz / 32, S = by * bz;
-    for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+    // columns claimed from a counter (the mixed partitions per column vary, so
+    // a static split left CTAs idle at the end); next == nullptr: static
+    __shared__ long long s_col;
+    auto claim = [&](int64_t cur) {
+        __syncthreads();
+        if (threadIdx.x == 0)
+            s_col = next ? (long long)atomicAdd(next, 1ull) : (long long)(cur + gridDim.x);
+        __syncthreads();
+        return (int64_t)s_col;
+    };
+    for (int64_t t = claim((int64_t)blockIdx.x - gridDim.x); t < tiles; t = claim(t)) {
         const int64_t y = t / zq, z0 = (t % zq) * 32;
         const uint32_t *src = mask + y * bz + z0;
         for (int i = threadIdx.x; i < L * 8; i += blockDim.x) {
@@ -1452,8 +1463,14 @@ static int pass_x_mask(const uint32_t *mask, int words, int n, int64_t bx, int64
         // 2 CTAs per SM for lines <= 256 (96 KB each), 1 for longer ones
         int64_t grid = (int64_t)sm_count() * (smem <= 113 * 1024 ? 2 : 1);
         if (grid > tiles) grid = tiles;
+        static const bool dyn = !(getenv("PDM_XMASK_STATIC") && getenv("PDM_XMASK_STATIC")[0] == '1');
+        unsigned long long *ctr = nullptr;
+        if (dyn) {
+            const int st = tile_counter(s, &ctr);
+            if (st) return st;
+        }
         kern<<<(unsigned)grid, 32 * kXMaskWarps, smem, s>>>(mask, n, bx, by, bz, pdms, pitch,
-                                                            tiles);
+                                                            tiles, ctr);
         return cuda_status("dt_x_mask_kernel");
     }
     dt_expand_mask_kernel<<<grid_for(ceil_div(nb, 16), 256, 8), 256, 0, s>>>(
