@@ -52,6 +52,30 @@ int sm_count() {
     return n;
 }
 
+// A zeroed work counter for one launch on stream s (kernels that hand out
+// tiles or items with atomicAdd): a ring of 64 per device, never freed,
+// zeroed in stream order, so launches in flight on different streams do not
+// share one.
+int work_counter(cudaStream_t s, unsigned long long **out) {
+    constexpr int kSlots = 64;
+    static std::mutex mu;
+    static unsigned long long *ring[64] = {nullptr};
+    static unsigned next_slot[64] = {0};
+    int dev = 0;
+    PDM_CUDA_TRY(cudaGetDevice(&dev));
+    PDM_REQUIRE(dev >= 0 && dev < 64, "work_counter: device %d", dev);
+    unsigned long long *p;
+    {
+        std::lock_guard<std::mutex> lock(mu);
+        if (ring[dev] == nullptr)
+            PDM_CUDA_TRY(cudaMalloc(&ring[dev], kSlots * sizeof(unsigned long long)));
+        p = ring[dev] + (next_slot[dev]++ % kSlots);
+    }
+    PDM_CUDA_TRY(cudaMemsetAsync(p, 0, sizeof(unsigned long long), s));
+    *out = p;
+    return PDM_OK;
+}
+
 int resident_ctas(const void *kernel, int threads, size_t smem) {
     struct Slot {
         const void *k;

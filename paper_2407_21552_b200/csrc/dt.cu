@@ -1350,29 +1350,6 @@ static int wide_x_pass(int n, int64_t bx, int64_t by, int64_t bz, uint8_t *pdms,
     return cuda_status("dt_dist1d_wide_kernel");
 }
 
-// A zeroed tile counter for one launch on stream s: a ring of 64 per device
-// (never freed), zeroed in stream order, so launches in flight on different
-// streams do not share one.
-static int tile_counter(cudaStream_t s, unsigned long long **out) {
-    constexpr int kSlots = 64;
-    static std::mutex mu;
-    static unsigned long long *ring[64] = {nullptr};
-    static unsigned next_slot[64] = {0};
-    int dev = 0;
-    PDM_CUDA_TRY(cudaGetDevice(&dev));
-    PDM_REQUIRE(dev >= 0 && dev < 64, "tile_counter: device %d", dev);
-    unsigned long long *p;
-    {
-        std::lock_guard<std::mutex> lock(mu);
-        if (ring[dev] == nullptr)
-            PDM_CUDA_TRY(cudaMalloc(&ring[dev], kSlots * sizeof(unsigned long long)));
-        p = ring[dev] + (next_slot[dev]++ % kSlots);
-    }
-    PDM_CUDA_TRY(cudaMemsetAsync(p, 0, sizeof(unsigned long long), s));
-    *out = p;
-    return PDM_OK;
-}
-
 // The TMEM sweep serves lines of 256 or 512 blocks in full 32-line tiles
 // with 16-byte aligned rows; PDM_DT_TMEM=0 keeps dt_tile_kernel (A/B).
 template <int AXIS>
@@ -1405,7 +1382,7 @@ static int tmem_pass_l(int n, int64_t bx, int64_t by, int64_t bz, uint8_t *pdms,
     const int64_t cap = (int64_t)sm_count() * per_sm;
     if (grid > cap) grid = cap;
     unsigned long long *ctr = nullptr;
-    int st = tile_counter(s, &ctr);
+    int st = work_counter(s, &ctr);
     if (st) return st;
     kern<<<(unsigned)grid, 32 * kTmemWarps, smem, s>>>(n, bx, by, bz, pdms, pitch, tiles, pk,
                                                          ctr);
@@ -1466,7 +1443,7 @@ static int pass_x_mask(const uint32_t *mask, int words, int n, int64_t bx, int64
         static const bool dyn = !(getenv("PDM_XMASK_STATIC") && getenv("PDM_XMASK_STATIC")[0] == '1');
         unsigned long long *ctr = nullptr;
         if (dyn) {
-            const int st = tile_counter(s, &ctr);
+            const int st = work_counter(s, &ctr);
             if (st) return st;
         }
         kern<<<(unsigned)grid, 32 * kXMaskWarps, smem, s>>>(mask, n, bx, by, bz, pdms, pitch,

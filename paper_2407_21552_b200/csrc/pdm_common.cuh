@@ -41,6 +41,8 @@ int sm_count();  // cached SM count of the current device
 // Resident CTAs per SM of a kernel at (threads, dynamic smem), cached per
 // (kernel, threads, smem); at least 1.
 int resident_ctas(const void *kernel, int threads, size_t smem);
+// A zeroed device counter for one launch on stream s (capi.cu).
+int work_counter(cudaStream_t s, unsigned long long **out);
 
 // dt.cu: the three Chebyshev passes in place over one {0, 255}-seeded map
 // (the tail of pdm_distance_transform, shared with the fused recompute).
