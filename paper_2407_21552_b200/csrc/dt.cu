@@ -743,6 +743,17 @@ __device__ __forceinline__ void wait_st() {
 
 constexpr int kTmemWarps = 4;  // one warp per TMEM lane quarter
 
+// 4 x 4 byte transpose inside each quad of lanes: lane 4g + j holds row j
+// (bytes = columns 0..3) on entry and column j (bytes = rows 0..3) on exit.
+__device__ __forceinline__ uint32_t quad_transpose(uint32_t a, int lane) {
+    const uint32_t p = __shfl_xor_sync(0xFFFFFFFFu, a, 1);
+    // even lanes: [a.b0, p.b0, a.b2, p.b2]; odd: [p.b1, a.b1, p.b3, a.b3]
+    const uint32_t t = __byte_perm(a, p, (lane & 1) ? 0x3715u : 0x6240u);
+    const uint32_t q = __shfl_xor_sync(0xFFFFFFFFu, t, 2);
+    // lanes 0, 1 of the quad: [t.b0, t.b1, q.b0, q.b1]; lanes 2, 3: [q.b2, q.b3, t.b2, t.b3]
+    return __byte_perm(t, q, (lane & 2) ? 0x3276u : 0x5410u);
+}
+
 // CTAs per SM: L = 256: 6 (33 KB of shared memory, 64 TMEM columns each);
 // L = 512: 3 (65 KB, 128 columns; 16-bit sweep tables).
 template <int L>
@@ -829,12 +840,16 @@ __global__ void __launch_bounds__(32 * kTmemWarps, tmem_ctas<L>())
                     w[4 * q] = v.x, w[4 * q + 1] = v.y, w[4 * q + 2] = v.z, w[4 * q + 3] = v.w;
                 }
             } else {
+                // [u][32] tile -> the lane's column: each lane loads the word of
+                // row u + (lane & 3) holding columns 4 (lane >> 2) .. +3, and a
+                // 4 x 4 byte transpose inside each lane quad (two shuffles, two
+                // byte permutes) hands lane l column l of the 4 rows
 #pragma unroll
                 for (int i = 0; i < 16; ++i) {
                     const int u = 64 * cc + 4 * i;
-                    const uint32_t b0 = s[u * 32 + lane], b1 = s[(u + 1) * 32 + lane],
-                                   b2 = s[(u + 2) * 32 + lane], b3 = s[(u + 3) * 32 + lane];
-                    w[i] = __byte_perm(b0 | (b1 << 8), b2 | (b3 << 8), 0x5410);
+                    const uint32_t a = *reinterpret_cast<const uint32_t *>(
+                        s + (u + (lane & 3)) * 32 + 4 * (lane >> 2));
+                    w[i] = quad_transpose(a, lane);
                 }
             }
             tmem::st16(taddr + 16 * cc, w);
@@ -881,12 +896,10 @@ __global__ void __launch_bounds__(32 * kTmemWarps, tmem_ctas<L>())
                 uint32_t w[16];
                 tmem::ld16(taddr + 16 * cc, w);
 #pragma unroll
-                for (int i = 0; i < 16; ++i) {
+                for (int i = 0; i < 16; ++i) {  // the same transpose, back to rows
                     const int u = 64 * cc + 4 * i;
-                    s[u * 32 + lane] = (uint8_t)w[i];
-                    s[(u + 1) * 32 + lane] = (uint8_t)(w[i] >> 8);
-                    s[(u + 2) * 32 + lane] = (uint8_t)(w[i] >> 16);
-                    s[(u + 3) * 32 + lane] = (uint8_t)(w[i] >> 24);
+                    *reinterpret_cast<uint32_t *>(s + (u + (lane & 3)) * 32 + 4 * (lane >> 2)) =
+                        quad_transpose(w[i], lane);
                 }
             }
             __syncwarp();
