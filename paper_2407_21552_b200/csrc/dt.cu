@@ -197,13 +197,20 @@ __device__ __forceinline__ uint32_t step_scaled(uint32_t &M, int g, int j, uint3
 template <int TB, bool kRev>
 __device__ __forceinline__ uint32_t sweep_word(uint32_t &M, uint32_t w, int j0, uint32_t tab) {
     constexpr int sh = SweepTable<TB>::kShift;
-    uint32_t d[4];
+    uint32_t a[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
         const int byte = kRev ? 3 - k : k;
-        d[byte] = step_scaled<TB>(M, (int)__byte_perm(w, 0u, 0x4440u + byte), j0 + k, tab);
+        step_scaled<TB>(M, (int)__byte_perm(w, 0u, 0x4440u + byte), j0 + k, tab);
+        a[byte] = M;
     }
-    return (d[0] >> sh) | (d[1] << (8 - sh)) | (d[2] << (16 - sh)) | (d[3] << (24 - sh));
+    // a[b] = tab + (m_b << sh); the word is sum_b (a[b] - tab) << (8 b - sh), and
+    // the tab terms of bytes 1..3 fold into one loop-invariant constant (three
+    // shift-adds per word instead of a subtract per byte plus shifts and ors;
+    // the fields do not overlap, so + is |)
+    constexpr uint32_t F = (1u << (8 - sh)) + (1u << (16 - sh)) + (1u << (24 - sh));
+    return ((a[0] - tab) >> sh) + a[1] * (1u << (8 - sh)) + a[2] * (1u << (16 - sh)) +
+           a[3] * (1u << (24 - sh)) - tab * F;
 }
 
 template <int TB>
