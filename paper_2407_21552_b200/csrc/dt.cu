@@ -748,7 +748,34 @@ __device__ __forceinline__ void wait_st() {
 
 }  // namespace tmem
 
-constexpr int kTmemWarps = 4;  // one warp per TMEM lane quarter
+// Warps per CTA of the TMEM sweep (warp w uses TMEM lane quarter w % 4 and
+// column group w / 4).  Two shapes: 4 warps per CTA, 6 CTAs per SM (3 for
+// L = 512) -- 24 (12) warps; or one CTA per SM filling the shared memory
+// with 28 (14) warps' tables, used for jobs that give every warp several
+// tiles (a PDM set build: config c y + z 0.964 -> 0.946 ms, config d 9.47 ->
+// 8.67 ms).  The one-CTA shape slowed single-map passes (the fused
+// recompute, 0.56 -> 0.62 ms), which keep the small CTAs.
+template <int L>
+constexpr int tmem_big_warps() {
+    return L == 256 ? 28 : 14;
+}
+// TMEM columns a CTA allocates: a lane's line is L / 4 columns, one column
+// group per 4 warps, rounded up to a power of two (>= 32).
+template <int L, int W>
+constexpr int tmem_cols() {
+    constexpr int need = ((W + 3) / 4) * (L / 4);
+    int c = 32;
+    while (c < need) c *= 2;
+    return c;
+}
+// CTAs per SM from shared memory (one 32 L-byte buffer per warp + the 1 KB
+// per-CTA reserve, 228 KB per SM) and the 512 TMEM columns.
+template <int L, int W>
+constexpr int tmem_ctas() {
+    constexpr int by_smem = (228 * 1024) / (W * 32 * L + 1024);
+    constexpr int by_tmem = 512 / tmem_cols<L, W>();
+    return by_smem < by_tmem ? by_smem : by_tmem;
+}
 
 // 4 x 4 byte transpose inside each quad of lanes: lane 4g + j holds row j
 // (bytes = columns 0..3) on entry and column j (bytes = rows 0..3) on exit.
@@ -761,15 +788,8 @@ __device__ __forceinline__ uint32_t quad_transpose(uint32_t a, int lane) {
     return __byte_perm(t, q, (lane & 2) ? 0x3276u : 0x5410u);
 }
 
-// CTAs per SM: L = 256: 6 (33 KB of shared memory, 64 TMEM columns each);
-// L = 512: 3 (65 KB, 128 columns; 16-bit sweep tables).
-template <int L>
-constexpr int tmem_ctas() {
-    return L == 256 ? 6 : 3;
-}
-
-template <int AXIS, int L>
-__global__ void __launch_bounds__(32 * kTmemWarps, tmem_ctas<L>())
+template <int AXIS, int L, int W>
+__global__ void __launch_bounds__(32 * W, tmem_ctas<L, W>())
     dt_tmem_kernel(int n, int64_t bx, int64_t by, int64_t bz, uint8_t *__restrict__ pdms,
                    int64_t pitch, int64_t tiles, PackDst pk, unsigned long long *next) {
     static_assert(L == 256 || L == 512, "TMEM sweep: lines of 256 or 512");
@@ -782,12 +802,13 @@ __global__ void __launch_bounds__(32 * kTmemWarps, tmem_ctas<L>())
     extern __shared__ __align__(16) uint8_t s_dyn[];
     __shared__ uint32_t s_taddr;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    if (warp == 0) tmem::alloc(&s_taddr, kCols);
+    if (warp == 0) tmem::alloc(&s_taddr, tmem_cols<L, W>());
     tmem::fence_before();
     __syncthreads();
     tmem::fence_after();
     const uint32_t tbase = s_taddr;
-    const uint32_t taddr = tbase + ((uint32_t)(32 * (warp & 3)) << 16);
+    const uint32_t taddr =
+        tbase + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((warp >> 2) * kCols);
     uint8_t *s = s_dyn + (size_t)warp * 32 * L;
     const uint32_t tab = smem_addr(s + TB * lane);  // the sweep table's lane column
     const int64_t S = bz;                      // y lines: element stride
@@ -999,7 +1020,7 @@ __global__ void __launch_bounds__(32 * kTmemWarps, tmem_ctas<L>())
     tmem::fence_before();
     __syncthreads();
     tmem::fence_after();
-    if (warp == 0) tmem::dealloc(tbase, kCols);
+    if (warp == 0) tmem::dealloc(tbase, tmem_cols<L, W>());
 }
 
 // Lines longer than 1024 blocks: one thread per line straight from global
@@ -1380,13 +1401,11 @@ static bool tmem_pass_ok(int64_t bx, int64_t by, int64_t bz) {
     return (bz == 256 || bz == 512) && (bx * by) % 32 == 0;
 }
 
-template <int AXIS, int L>
+template <int AXIS, int L, int W>
 static int tmem_pass_l(int n, int64_t bx, int64_t by, int64_t bz, uint8_t *pdms,
-                       int64_t pitch, cudaStream_t s, PackDst pk) {
-    auto kern = dt_tmem_kernel<AXIS, L>;
-    const int64_t tiles = AXIS == kAxisZ ? (int64_t)n * (bx * by / 32)
-                                         : (int64_t)n * bx * (bz / 32);
-    const size_t smem = (size_t)kTmemWarps * 32 * L;
+                       int64_t pitch, cudaStream_t s, PackDst pk, int64_t tiles) {
+    auto kern = dt_tmem_kernel<AXIS, L, W>;
+    const size_t smem = (size_t)W * 32 * L;
     static bool attr_set = false;  // (per instantiation)
     if (!attr_set) {
         PDM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1397,15 +1416,14 @@ static int tmem_pass_l(int n, int64_t bx, int64_t by, int64_t bz, uint8_t *pdms,
     }
     // (the occupancy API answers 1 for a kernel that allocates TMEM; the
     // limits are shared memory, 80 registers and the TMEM columns: tmem_ctas)
-    const int per_sm = tmem_ctas<L>();
-    int64_t grid = ceil_div(tiles, kTmemWarps);
+    const int per_sm = tmem_ctas<L, W>();
+    int64_t grid = ceil_div(tiles, W);
     const int64_t cap = (int64_t)sm_count() * per_sm;
     if (grid > cap) grid = cap;
     unsigned long long *ctr = nullptr;
     int st = work_counter(s, &ctr);
     if (st) return st;
-    kern<<<(unsigned)grid, 32 * kTmemWarps, smem, s>>>(n, bx, by, bz, pdms, pitch, tiles, pk,
-                                                         ctr);
+    kern<<<(unsigned)grid, 32 * W, smem, s>>>(n, bx, by, bz, pdms, pitch, tiles, pk, ctr);
     return cuda_status("dt_tmem_kernel");
 }
 
@@ -1413,8 +1431,20 @@ template <int AXIS>
 static int tmem_pass(int n, int64_t bx, int64_t by, int64_t bz, uint8_t *pdms, int64_t pitch,
                      cudaStream_t s, PackDst pk) {
     const int64_t L = AXIS == kAxisY ? by : bz;
-    return L == 256 ? tmem_pass_l<AXIS, 256>(n, bx, by, bz, pdms, pitch, s, pk)
-                    : tmem_pass_l<AXIS, 512>(n, bx, by, bz, pdms, pitch, s, pk);
+    const int64_t tiles = AXIS == kAxisZ ? (int64_t)n * (bx * by / 32)
+                                         : (int64_t)n * bx * (bz / 32);
+    // the one-CTA shape once every warp of the grid gets >= 8 tiles
+    // (PDM_DT_TMEM_BIG=0 / 1 forces the choice, A/B)
+    static const int force = getenv("PDM_DT_TMEM_BIG") ? atoi(getenv("PDM_DT_TMEM_BIG")) : -1;
+    const int64_t big_w = L == 256 ? tmem_big_warps<256>() : tmem_big_warps<512>();
+    const bool big = force >= 0 ? force != 0 : tiles >= 8 * sm_count() * big_w;
+    if (L == 256)
+        return big ? tmem_pass_l<AXIS, 256, tmem_big_warps<256>()>(n, bx, by, bz, pdms, pitch, s,
+                                                                   pk, tiles)
+                   : tmem_pass_l<AXIS, 256, 4>(n, bx, by, bz, pdms, pitch, s, pk, tiles);
+    return big ? tmem_pass_l<AXIS, 512, tmem_big_warps<512>()>(n, bx, by, bz, pdms, pitch, s, pk,
+                                                               tiles)
+               : tmem_pass_l<AXIS, 512, 4>(n, bx, by, bz, pdms, pitch, s, pk, tiles);
 }
 
 // pk (z pass only): fused packing epilogue; honoured when the z pass runs the
