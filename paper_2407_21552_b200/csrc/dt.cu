@@ -695,9 +695,10 @@ __global__ void __launch_bounds__(256)
 // 64 private 32-bit columns of its TMEM lane (tcgen05.st / tcgen05.ld of 16
 // columns = 64 elements at a time), so the warp needs only one 8 KB
 // shared-memory buffer -- the cp.async staging of its tile, then the table
-// of each sweep, then the staging of the write-back -- and 24 warps sweep per
-// SM.  Lines of exactly 256 blocks in full 32-line tiles (config c's 256^3
-// block grid); everything else runs dt_tile_kernel.
+// of each sweep, then the staging of the write-back -- and 24 to 28 warps
+// sweep per SM.  Lines of 256 or 512 blocks in full 32-line tiles (config c's
+// 256^3 and config d's 512^3 block grids); everything else runs
+// dt_tile_kernel.
 namespace tmem {
 
 __device__ __forceinline__ void alloc(uint32_t *dst, uint32_t cols) {  // whole warp
