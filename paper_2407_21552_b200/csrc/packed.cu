@@ -34,15 +34,18 @@
 
 namespace pdm {
 
-// One CTA of 32 warps per SM (64 registers, 6 planes per load batch): the
+// One CTA of 28 warps per SM (72 registers, 8 planes per load batch): the
 // warps of an SM claim the SM's tiles from one shared counter (see
 // merge_packed), so the whole SM's share of the map is balanced, not just a
 // CTA's (3 CTAs of 8 warps: 36.96 us per bench step; 1 of 24 warps at 80
 // registers: 36.3; 1 of 32 at 64 registers -- a few spilled values -- 35.2
 // with 5 planes per batch and 64-bit tile indices; with 32-bit indices 5 / 6
-// / 7 / 8 planes per batch 35.0 / 34.1 / 34.6 / 36.2, 4 planes 37.2).
+// / 7 / 8 planes per batch 35.0 / 34.1 / 34.6 / 36.2, 4 planes 37.2; 28
+// warps at 72 registers with 6 / 7 / 8 planes 35.1 / 34.2 / 33.9 vs 34.2 for
+// 32 warps with 6, and 24 / 26 warps with 8 planes 34.8 / 34.5 --
+// tools/exp/run_r05h.sh, run_r05i.sh).
 #ifndef PDM_PACKED_THREADS  // (overridable for A/B builds)
-#define PDM_PACKED_THREADS 1024
+#define PDM_PACKED_THREADS 896
 #endif
 constexpr int kPackedThreads = PDM_PACKED_THREADS;
 constexpr int kPackedMaxSel = 240;       // indices in kernel parameters
@@ -650,10 +653,16 @@ __device__ __forceinline__ void merge_packed(const P planes, int k, int64_t map_
 // 8 planes / 3 CTAs and 48.2 for 4 planes / 4 CTAs); the index path keeps 4
 // planes at 5 CTAs.
 #ifndef PDM_PACKED_BATCH  // (overridable for A/B builds)
-#define PDM_PACKED_BATCH 6
+#define PDM_PACKED_BATCH 8
 #define PDM_PACKED_CTAS 1
 #endif
 constexpr int kPackedBatch = PDM_PACKED_BATCH, kPackedCtas = PDM_PACKED_CTAS;
+// D' for the host (kOut 1..3: the encodings' extra live values) and the
+// fused zero count keep 6 planes per batch so those instances stay
+// spill-free at the same registers
+constexpr int packed_batch(int out_kind, bool count) {
+    return out_kind == 0 && !count ? kPackedBatch : 6;
+}
 #ifndef PDM_PACKED_CTAS_IDX
 #define PDM_PACKED_CTAS_IDX 1
 #endif
@@ -683,7 +692,7 @@ __global__ void __launch_bounds__(kPackedThreads, kPackedCtas)
     fill_table(nib, nib_pitch, base, base_pitch, sel.idx, sel.k, s_nib, s_base);
     __syncthreads();
     skip.pid = sel.idx;
-    merge_packed<kPackedBatch, kOut, kCount>(TablePlanes{s_nib, s_base}, sel.k, map_bytes, out,
+    merge_packed<packed_batch(kOut, kCount), kOut, kCount>(TablePlanes{s_nib, s_base}, sel.k, map_bytes, out,
                                              out_base, zeros, s_stage, skip);
 }
 
@@ -738,7 +747,7 @@ __global__ void __launch_bounds__(kPackedThreads, kTable ? kPackedCtas : kPacked
     if constexpr (kTable) {
         fill_table(nib, nib_pitch, base, base_pitch, s_idx, s_k, s_nib, s_base);
         __syncthreads();
-        merge_packed<kPackedBatch, kOut, kCount>(TablePlanes{s_nib, s_base}, s_k, map_bytes, out,
+        merge_packed<packed_batch(kOut, kCount), kOut, kCount>(TablePlanes{s_nib, s_base}, s_k, map_bytes, out,
                                                  out_base, zeros, s_stage, skip);
     } else {
         merge_packed<kPackedBatchIdx, kOut, kCount>(
